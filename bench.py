@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 IDM hot path (arXiv 2412.16750) -- one JSON line on rank 0.
+
+A "step" is one pass of the whole hot path over one batch: idm_forward(K) -> idm_loss_grad
+(Eq. 4, L1) -> idm_backward -> idm_adam_step, on config C4 of BASELINE.json (2M vehicles in
+20,000 lanes x 100, K = 300 steps of dt = 0.1 s, per-vehicle parameters, checkpoint k = 16).
+value = vehicle-steps/s over all ranks = ranks * N * K / max-over-ranks(step time).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--scaling weak|strong]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+--impl reference times the fp64 CPU oracle (oracle/, the only other program of this method
+here) on the host cores, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2412_16750_b200 import synth  # noqa: E402
+
+LANE_VEH = 100
+WORKLOAD = "C4"
+# Frozen algorithmic counts: thread-instructions (issue slots) per
+# vehicle-step that any implementation of the kernel's math must issue, and HBM bytes per
+# vehicle-step the method must move at k = 16, K = 300.
+ALG_INSTR = {"fwd": 36.0, "bwd": 114.0}
+ISSUE_PER_CLK = 148 * 4 * 32  # SMs x schedulers x lanes (thread-instr / clk)
+
+
+def alg_bytes(K: int, k: int) -> dict:
+    return {
+        "fwd": 4.0 + 8.0 / k + (4 * 4 + 24 + 1) / K,        # P record + (s,v) ckpt + loads
+        "loss": 12.0,                                       # read P, obs; write dL/dP
+        "bwd": 4.0 + 8.0 / k + (24 + 24 + 8 + 1) / K,       # dL/dP + ckpt + params/grads
+        "adam": 6 * 28.0 / K,                               # x, g, m, v in; x, m, v out
+    }
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p.get("sm_max_mhz", 1965.0)), "measured"
+    except Exception:
+        return 6650.0, 1965.0, "fallback"
+
+
+# ---------------------------------------------------------------------------- clocks
+REASONS = ["gpu_idle", "applications_clocks_setting", "sw_power_cap", "hw_slowdown",
+           "sync_boost", "sw_thermal_slowdown", "hw_thermal_slowdown", "hw_power_brake_slowdown"]
+
+
+class ClockSampler:
+    """nvidia-smi sampled every 50 ms while the timed region runs."""
+
+    def __init__(self, gpu_index: int):
+        self.samples = []
+        self.window = None
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active")
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            try:
+                self.samples.append((time.time(), float(parts[0]), float(parts[1]),
+                                     int(parts[2], 16)))
+            except Exception:
+                pass
+
+    def wait_first(self, timeout=5.0):
+        t0 = time.time()
+        while self.p is not None and not self.samples and time.time() - t0 < timeout:
+            time.sleep(0.02)
+
+    def stop(self):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=2)
+            except Exception:
+                self.p.kill()
+
+    def summary(self, t0, t1):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        inside = [s for s in self.samples if t0 <= s[0] <= t1] or \
+            sorted(self.samples, key=lambda s: abs(s[0] - (t0 + t1) / 2))[:3]
+        mask = 0
+        for s in inside:
+            mask |= s[3]
+        reasons = [n for b, n in enumerate(REASONS) if mask >> b & 1 and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(s[1] for s in inside),
+                "sm_max_mhz": max(s[2] for s in inside), "reasons": reasons,
+                "samples": len(inside)}
+
+
+# ---------------------------------------------------------------------------- workload
+def make_rank_workload(rank: int, world: int, scaling: str):
+    if scaling == "weak" or world == 1:
+        w = synth.make_workload(WORKLOAD, seed=synth.CONFIGS[WORKLOAD]["seed"] + 1000 * rank)
+    else:
+        full = synth.make_workload(WORKLOAD)
+        l0, l1 = synth.shard_lanes(full.n_lanes, world, rank)
+        w = synth.lane_subset(full, np.arange(l0, l1))
+    return w
+
+
+def cpu_baseline(lanes: int, K: int, seed: int = 99):
+    """The fp64 oracle as it stands, single-threaded, one full step (rollout, Eq. 4 L1 loss,
+    adjoint, Adam) on `lanes` lanes of the C4 workload."""
+    from oracle import oracle as O
+    w = synth.make_workload(WORKLOAD, lane_sizes=[LANE_VEH] * lanes, K=K, seed=seed)
+    obs = synth.kinematic_obs(w).astype(np.float64)
+    st = dict(leader=O.leader_from_lanes(w.lane_offsets), length=w.length, p0=w.p0, v0=w.v0,
+              params=synth.init_params(w.n).astype(np.float64), m1=np.zeros((6, w.n)),
+              m2=np.zeros((6, w.n)))
+    t0 = time.perf_counter()
+    O.fit_iteration(st, obs, 0)
+    dt = time.perf_counter() - t0
+    return w.n * K, dt
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle timed on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    K = synth.CONFIGS[WORKLOAD]["K"]
+    vs, t = cpu_baseline(4, K)
+    per_lane = t / 4
+    budget = 150.0  # seconds for the whole --warmup + --steps run
+    lanes = int(max(1, min(20000, budget / max(1, args.steps + args.warmup) / per_lane)))
+    for _ in range(args.warmup):
+        cpu_baseline(lanes, K)
+    tot_vs, tot_t = 0, 0.0
+    for i in range(args.steps):
+        vs, t = cpu_baseline(lanes, K, seed=100 + i)
+        tot_vs += vs
+        tot_t += t
+    value = tot_vs / tot_t
+    sample = (f"{lanes} lanes x {LANE_VEH} vehicles x {K} steps of {WORKLOAD} per step "
+              f"(rollout + Eq.4 L1 + adjoint + Adam, fp64, single thread)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "vehicle-steps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD_DESC, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "vehicle-steps/s", "cores": 1,
+                         "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "vehicle-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "vehicle-steps/s, forward+loss+backward+Adam (C4: 2M vehicles, K=300)"
+WORKLOAD_DESC = ("C4: 20,000 lanes x 100 vehicles = 2M, K=300 steps, dt=0.1 s, Eq.4 L1 loss "
+                 "on dense noisy observations, per-vehicle IDM params, Adam, checkpoint k=16")
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2412_16750_b200 import idm
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    w = make_rank_workload(rank, world, args.scaling)
+    K, k = w.K, args.ckpt
+    # synthetic observations: truth rollout with theta_true (our forward) + N(0, 0.3^2)
+    sim = idm.from_workload(w, w.theta_true, max_steps=K, ckpt_every=k, stage_obs=args.e2e > 0)
+    sim.forward(K)
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    obs = sim.traj.clone()
+    obs[1:].add_(torch.randn(obs[1:].shape, device=dev, generator=gen), alpha=0.3)
+    init = torch.as_tensor(synth.init_params(w.n), device=dev)
+    sim.params.copy_(init)
+    stream = sim.stream
+    torch.cuda.synchronize()
+
+    def step(it, ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        sim.forward(K)
+        if ev is not None:
+            ev[1].record(stream)
+        sim.loss_grad(obs, kind="l1", sync=False)
+        if world > 1:
+            dist.all_reduce(sim.loss_dev)  # total loss (8 B, NCCL)
+        if ev is not None:
+            ev[2].record(stream)
+        sim.backward()
+        if ev is not None:
+            ev[3].record(stream)
+        sim.adam_step(it % 500, 500, 0.1, 0.01)
+        if ev is not None:
+            ev[4].record(stream)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.wait_first()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0 = sim.launch_count
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    tw0 = time.time()
+    start.record(stream)
+    for i in range(args.steps):
+        step(args.warmup + i, evs[i])
+    stop.record(stream)
+    torch.cuda.synchronize()
+    tw1 = time.time()
+    if world > 1:
+        dist.barrier()
+    launches = sim.launch_count - n0
+    clocks.stop()
+    ms_total = start.elapsed_time(stop)
+    phase = {"fwd": 0.0, "loss": 0.0, "bwd": 0.0, "adam": 0.0}
+    for e in evs:
+        phase["fwd"] += e[0].elapsed_time(e[1])
+        phase["loss"] += e[1].elapsed_time(e[2])
+        phase["bwd"] += e[2].elapsed_time(e[3])
+        phase["adam"] += e[3].elapsed_time(e[4])
+    t = torch.tensor([ms_total] + [phase[p] for p in ("fwd", "loss", "bwd", "adam")],
+                     dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total, ms_fwd, ms_loss, ms_bwd, ms_adam = (float(x) for x in t.tolist())
+    per_step = ms_total / args.steps
+    vsteps = float(w.n) * K * world
+    value = vsteps / (per_step * 1e-3)
+
+    # ---- end to end through the C-ABI with HOST buffers (idm_step_host)
+    e2e = None
+    if args.e2e > 0:
+        obs_h = obs.cpu().pin_memory()
+        p0_h = sim.pos0.cpu().pin_memory()
+        v0_h = sim.vel0.cpu().pin_memory()
+        sim.step_host(K, obs_h, p0_h, v0_h, iteration=0)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for i in range(args.e2e):
+            sim.step_host(K, obs_h, p0_h, v0_h, iteration=1 + i)
+        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": vsteps * args.e2e / float(te.item()), "unit": "vehicle-steps/s",
+               "h2d_bytes_per_step": int(obs_h.numel() * 4 + 8 * w.n),
+               "d2h_bytes_per_step": 8, "steps": args.e2e,
+               "path": "idm_step_host: pinned host pos0/vel0/obs -> device, fwd, loss, bwd, "
+                       "adam, loss -> host (wall clock, max over ranks)"}
+
+    if rank != 0:
+        return
+    hbm_gbs, sm_mhz_max, peak_src = load_peaks()
+    ab = alg_bytes(K, k)
+    n_veh_steps = float(w.n) * K  # per rank per launch
+    ms = {"fwd": ms_fwd / args.steps, "loss": ms_loss / args.steps,
+          "bwd": ms_bwd / args.steps, "adam": ms_adam / args.steps}
+    dom = max(("fwd", "bwd"), key=lambda p: ms[p])
+    issue_peak = ISSUE_PER_CLK * sm_mhz_max * 1e6 / 1e12  # Tinstr/s
+    achieved = ALG_INSTR[dom] * n_veh_steps / (ms[dom] * 1e-3) / 1e12
+    roofline = {"bound": "alu", "kernel": f"{dom}_kernel", "achieved": achieved,
+                "peak": issue_peak, "unit": "Tinstr/s", "frac": achieved / issue_peak,
+                "traffic": args.traffic,
+                "basis": f"{ALG_INSTR[dom]:.0f} essential thread-instr per vehicle-step; peak ="
+                         f" 148 SM x 4 issue/clk x 32 lanes x {sm_mhz_max:.0f} MHz "
+                         f"(MEASURED_PEAKS sm_max, {peak_src})"}
+    bytes_step = sum(ab.values()) * n_veh_steps
+    hbm = {"bytes_per_vehicle_step": sum(ab.values()),
+           "achieved_GBps": bytes_step / (per_step * 1e-3) / 1e9, "peak_GBps": hbm_gbs,
+           "frac": bytes_step / (per_step * 1e-3) / 1e9 / hbm_gbs, "peak_source": peak_src,
+           "per_kernel_frac": {p: ab[p] * n_veh_steps / (ms[p] * 1e-3) / 1e9 / hbm_gbs
+                               for p in ab}}
+    cpu = None
+    if world == 1 and args.cpu_lanes > 0:
+        vs_c, t_c = cpu_baseline(args.cpu_lanes, K)
+        cpu = {"value": vs_c / t_c, "unit": "vehicle-steps/s", "cores": 1, "kind": "oracle",
+               "sample": f"{args.cpu_lanes} lanes x {LANE_VEH} vehicles x {K} steps of C4, one "
+                         f"full step (fp64 rollout + Eq.4 L1 + adjoint + Adam), 1 thread, "
+                         f"{t_c:.1f} s"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "vehicle-steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step,
+        "higher_is_better": True, "scaling": args.scaling if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD_DESC, "vehicles_per_rank": w.n, "K": K,
+                   "ckpt_every": k, "parallelism": f"lane-sharded x{world}",
+                   "l2": "no flush: inputs larger than L2 (2.4 GB trajectory + obs + dL/dP per "
+                         "rank per step vs 126 MB L2)"},
+        "fwd": {"value": n_veh_steps * world / (ms["fwd"] * 1e-3), "unit": "vehicle-steps/s",
+                "ms": ms["fwd"]},
+        "phase_ms": ms,
+        "roofline": roofline,
+        "hbm": hbm,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks.summary(tw0, tw1),
+        "paper_context": "< 30 ms per timestep per pass at 2M vehicles on 16-thread Xeon "
+                         "W-2255 or one RTX A5000 (PAPER.md:36, :253) = > 6.7e7 vehicle-steps/s "
+                         "per pass",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--ckpt", type=int, default=16)
+    ap.add_argument("--e2e", type=int, default=3, help="end-to-end steps (0 = skip)")
+    ap.add_argument("--cpu-lanes", type=int, default=400,
+                    help="C4 lanes in the oracle cpu_baseline sample (0 = skip)")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes per launch of the dominant kernel (from profiles/)")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,156 @@
+/*
+ * idm.h -- C-ABI of the B200-native differentiable IDM hot path (arXiv 2412.16750).
+ *
+ * One optimizer iteration of the paper's trajectory fitting is
+ *
+ *     idm_forward(h, K)            Eqs. 1-3 + Sec. III-C bounds, K synchronous Euler steps
+ *     idm_loss_grad(h, obs, ...)   Eq. 4 loss and dL/dP
+ *     idm_backward(h)              reverse-mode adjoint to the parameters and initial state
+ *     idm_adam_step(h, it, ...)    Adam + linear lr decay + box clamp
+ *
+ * Citations "PAPER.md:N" are lines of the paper's LaTeX; "R#n" are the readings of silent or
+ * ambiguous passages listed in DESIGN.md.
+ *
+ * Conventions (all calls):
+ *   - Every array pointer in idm_desc is a DEVICE pointer owned by the caller (the Python
+ *     binding keeps torch tensors alive for the handle's lifetime).  The library owns only the
+ *     opaque handle and the caller-allocated workspace it is given (idm_workspace_bytes).
+ *   - fp32 arrays; SoA layout; vehicles are LANE-SORTED: lane l owns the index range
+ *     [lane_offsets[l], lane_offsets[l+1]) in ascending position, so the leader h(i) of
+ *     vehicle i is i+1 when i+1 is in the same lane, and the lane head has no
+ *     leader (exact free road, R#8).  Lanes never change (no lane changes, R#9).
+ *   - Parameters are SoA [6][n_par] in the order
+ *         0 a_max  1 a_pref  2 s_min  3 T_pref  4 v_targ  5 delta
+ *     (delta = IDM exponent, R#1), n_par = N (IDM_PARAMS_PER_VEHICLE,
+ *     "fixed for each trajectory") or 1 (IDM_PARAMS_SHARED).
+ *   - Trajectory arrays are step-major [(steps+1)][N]: row t holds P(t) = p_i(t), absolute
+ *     positions in m (the array P of Eq. 4).
+ *   - Every call is ordered on desc->stream (a cudaStream_t); only idm_init, idm_loss_grad
+ *     with loss_host != NULL, idm_check and idm_step_host synchronize it.
+ *   - Return value: an idm_status.  On failure idm_last_error(h) holds a sticky message.
+ *     Calls out of order (e.g. idm_backward before idm_loss_grad) return IDM_ESTATE.
+ *   - No CPU fallback: without a usable sm_100a device every call returns IDM_ECUDA.
+ */
+#ifndef IDM_H
+#define IDM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct idm_handle idm_handle; /* opaque */
+
+typedef enum {
+    IDM_OK = 0,
+    IDM_EINVAL = 1,   /* invalid argument or input data (SPEC "data error", exit 1) */
+    IDM_ENUMERIC = 2, /* non-finite state or gradient (SPEC "numerical failure", exit 2) */
+    IDM_ECUDA = 3,    /* CUDA runtime error / no device */
+    IDM_ESTATE = 4    /* call-order violation */
+} idm_status;
+
+typedef enum { IDM_PARAMS_PER_VEHICLE = 0, IDM_PARAMS_SHARED = 1 } idm_param_mode;
+typedef enum { IDM_LOSS_L1 = 0 /* Eq. 4 */, IDM_LOSS_L2 = 1 /* smooth variant */ } idm_loss_kind;
+
+typedef struct {
+    int64_t n_vehicles;          /* N >= 1 */
+    int32_t n_lanes;             /* L >= 1 */
+    const int32_t* lane_offsets; /* [L+1], non-decreasing, [0] = 0, [L] = N */
+    float* pos0;                 /* [N] initial absolute position p_i(0) (m); written only by
+                                    idm_step_host (upload) */
+    float* vel0;                 /* [N] initial speed v_i(0) >= 0 (m/s); idem */
+    const float* length;         /* [N] body length of each vehicle (m) */
+    float* params;               /* [6][n_par] IDM parameters; updated by idm_adam_step */
+    float* grad_params;          /* [6][n_par] dL/dtheta written by idm_backward */
+    float* adam_m;               /* [6][n_par] Adam first moment (caller zero-initialises) */
+    float* adam_v;               /* [6][n_par] Adam second moment (caller zero-initialises) */
+    float* grad_state0;          /* [2][N] dL/dp(0), dL/dv(0) from idm_backward (nullable) */
+    float* traj;                 /* [(max_steps+1)][N] positions P(t) (required for the loss) */
+    float* vel_traj;             /* [(max_steps+1)][N] speeds v(t) (nullable; diagnostics) */
+    float* grad_traj;            /* [(max_steps+1)][N] dL/dP from idm_loss_grad */
+    float* state_out;            /* [2][N] final position and speed (nullable) */
+    float* obs_stage;            /* [(max_steps+1)][N] device staging for idm_step_host (nullable) */
+    uint8_t* mask_stage;         /* [(max_steps+1)][N] staging for the mask (nullable) */
+    int32_t max_steps;           /* K_max >= 1 */
+    int32_t ckpt_every;          /* k: backward checkpoint interval, 1..64 (multiple of 1) */
+    float dt;                    /* Delta t > 0 (0.1 s) */
+    float a_min;                 /* < 0, maximum deceleration (-10) */
+    float eps_gap;               /* > 0, gap clamp (0.1 m, R#7) */
+    int32_t param_mode;          /* idm_param_mode */
+    uint32_t opt_mask;           /* bit k set = parameter k optimized by Adam; the paper's five:
+                                    0x1F (delta frozen) */
+    void* stream;                /* cudaStream_t (NULL = legacy default stream) */
+    void* workspace;             /* device, >= idm_workspace_bytes(desc), 256-B aligned */
+    size_t workspace_bytes;
+} idm_desc;
+
+/* Bytes of device workspace idm_init needs for this descriptor (checkpoints of (gap, speed)
+   every ckpt_every steps, the lane-tile plan, leader flags, reduction partials, status word).
+   Returns 0 if the descriptor is malformed. */
+size_t idm_workspace_bytes(const idm_desc* d);
+
+/* Validate the descriptor and input data (finite, v(0) >= 0, lengths >= 0, a_max, a_pref,
+   v_targ, delta > 0, lane offsets well formed, every lane fits one lane tile of
+   idm_max_lane_vehicles() vehicles), build the lane -> CTA tile plan and leader flags in the
+   workspace.  Synchronizes the stream.  *out receives the handle (NULL on failure).
+   The desc is copied; the arrays it points to must stay valid until idm_destroy. */
+int idm_init(idm_handle** out, const idm_desc* d);
+
+/* Simulate `steps` (1..max_steps) synchronous steps from (pos0, vel0) (Eqs. 1-3, Sec. III-B/C,
+   PAPER.md:106-152): one fused launch, state in registers, gap/speed checkpoints every
+   ckpt_every steps, traj rows 0..steps (and vel_traj, state_out if given).
+   Non-finite states are detected at checkpoints and reported by the next synchronizing call. */
+int idm_forward(idm_handle* h, int32_t steps);
+
+/* Eq. 4 over rows 0..steps of traj:
+     L1: L = sum_{observed (t,i)} |obs - P|,  dL/dP = -sign(obs - P), sign(0) = 0 (R#11)
+     L2: L = sum (obs - P)^2,                 dL/dP = -2 (obs - P)
+   obs: device [(steps+1)][N]; mask: device uint8 [(steps+1)][N], nonzero = observed, or NULL
+   (all observed).  Writes grad_traj; the loss (fixed-order fp64 reduction, deterministic) to
+   *loss_dev (device double, nullable) and, if loss_host != NULL, to *loss_host (synchronizes;
+   also reports a pending non-finite status as IDM_ENUMERIC). */
+int idm_loss_grad(idm_handle* h, const float* obs, const uint8_t* mask, int32_t kind,
+                  double* loss_dev, double* loss_host);
+
+/* Reverse-mode adjoint of the last idm_forward through grad_traj: recomputes each checkpoint
+   segment on chip and sweeps it backwards.  Writes grad_params (per vehicle, or in shared
+   mode the sum over this process's vehicles -- the caller all-reduces across ranks) and
+   grad_state0.  No atomics: fixed-order reductions, bitwise deterministic. */
+int idm_backward(idm_handle* h);
+
+/* Adam step (Kingma & Ba; beta1 0.9, beta2 0.999, eps 1e-8, bias-corrected, R#14) on the
+   parameters selected by opt_mask with lr = lr0 + (lr1 - lr0) * iter / (total_iters - 1)
+   (0.1 -> 0.01 over 500), then clamp (a_max, a_pref, s_min, T_pref, v_targ) to
+   [5,10], [0.1,5], [1,10], [0.1,5], [20,60] (R#15).  iter is 0-based. */
+int idm_adam_step(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, float lr1);
+
+/* One whole optimizer iteration from HOST buffers (end-to-end path): async-copies pos0/vel0
+   (nullable = keep), obs (required) and mask (nullable = all observed) from host memory
+   (pinned for overlap) into desc->pos0/vel0/obs_stage/mask_stage, runs forward(steps) ->
+   loss_grad -> backward -> adam_step(iter, total_iters, lr0, lr1) and copies the loss back to
+   *loss_host (synchronizes).  The obs upload overlaps the forward kernel on a second stream. */
+int idm_step_host(idm_handle* h, int32_t steps, const float* pos0_host, const float* vel0_host,
+                  const float* obs_host, const uint8_t* mask_host, int32_t kind, int32_t iter,
+                  int32_t total_iters, float lr0, float lr1, double* loss_host);
+
+/* Synchronize the stream and report a pending non-finite status (IDM_ENUMERIC) or CUDA error. */
+int idm_check(idm_handle* h);
+
+/* Number of kernel launches the library issued on this handle since idm_init. */
+int64_t idm_launch_count(const idm_handle* h);
+
+/* Largest lane (vehicles) one lane tile holds. */
+int32_t idm_max_lane_vehicles(void);
+
+/* Sticky last error message of h ("" if none; a static message if h is NULL). */
+const char* idm_last_error(const idm_handle* h);
+
+/* Release the handle (not the caller's arrays).  NULL is a no-op. */
+void idm_destroy(idm_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IDM_H */

@@ -1,0 +1,476 @@
+// idm_capi.cu -- host side of the C-ABI (include/idm.h): validation, lane-tile plan,
+// workspace carving, call-order state machine and kernel launches.  No compute happens here.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/idm.h"
+#include "idm_internal.h"
+
+using namespace idm;
+
+struct idm_handle {
+    idm_desc d;
+    cudaStream_t st;
+    int64_t n, n_par;
+    int ntiles, nck;
+    // workspace carve-outs
+    int64_t* tile_start;
+    uint8_t* lead;
+    float *ckpt_s, *ckpt_v;
+    double *loss_partials, *loss_scalar, *shared_partials;
+    unsigned long long* status;
+    // host-side resources for idm_step_host / synchronous reads
+    cudaStream_t copy_st;
+    cudaEvent_t ev_obs, ev_loss_done;
+    double* pinned;  // [0] loss, [1] status (as bits)
+    int stage;       // 0 = initialised, 1 = forward done, 2 = loss done, 3 = backward done
+    int32_t steps;
+    int64_t launches;
+    char err[512];
+};
+
+namespace {
+
+const char* kNoHandle = "idm: NULL handle";
+
+int fail(idm_handle* h, int code, const char* fmt, ...) {
+    if (h) {
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(h->err, sizeof(h->err), fmt, ap);
+        va_end(ap);
+    }
+    return code;
+}
+
+#define CK(h, call)                                                                       \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail((h), IDM_ECUDA, "CUDA error %s at %s:%d (%s)", cudaGetErrorString(e_), \
+                        __FILE__, __LINE__, #call);                                       \
+    } while (0)
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Layout {
+    size_t tile_start, lead, ckpt_s, ckpt_v, loss_partials, loss_scalar, shared_partials, status,
+        total;
+};
+
+int64_t max_tiles_for(const idm_desc* d) {
+    int64_t by_size = 2 * ((d->n_vehicles + kCap - 1) / kCap) + 1;
+    return d->n_lanes < by_size ? d->n_lanes : by_size;
+}
+
+bool layout_for(const idm_desc* d, Layout* L) {
+    if (!d || d->n_vehicles < 1 || d->n_lanes < 1 || d->max_steps < 1 || d->ckpt_every < 1 ||
+        d->ckpt_every > kMaxCkpt)
+        return false;
+    int64_t n = d->n_vehicles;
+    int64_t mt = max_tiles_for(d);
+    int64_t nck = (d->max_steps + d->ckpt_every - 1) / d->ckpt_every;
+    size_t off = 0;
+    L->tile_start = off; off += align256(sizeof(int64_t) * (mt + 1));
+    L->lead = off; off += align256((size_t)n);
+    L->ckpt_s = off; off += align256(sizeof(float) * (size_t)(nck * n));
+    L->ckpt_v = off; off += align256(sizeof(float) * (size_t)(nck * n));
+    L->loss_partials = off; off += align256(sizeof(double) * kLossBlocks);
+    L->loss_scalar = off; off += align256(sizeof(double));
+    L->shared_partials = off; off += align256(sizeof(double) * 6 * (size_t)mt);
+    L->status = off; off += align256(sizeof(unsigned long long));
+    L->total = off;
+    return true;
+}
+
+Consts consts_of(const idm_desc& d) {
+    Consts k;
+    k.dt = d.dt;
+    k.inv_dt = 1.0f / d.dt;
+    k.a_min = d.a_min;
+    k.eps = d.eps_gap;
+    return k;
+}
+
+// Reads and clears the device status word; returns IDM_OK / IDM_ENUMERIC / IDM_EINVAL.
+int consume_status(idm_handle* h, unsigned long long st) {
+    if (st == ~0ull) return IDM_OK;
+    unsigned hi = (unsigned)(st >> 32), lo = (unsigned)(st & 0xffffffffu);
+    if (hi == kBadInput)
+        return fail(h, IDM_EINVAL, "invalid initial state at vehicle %u (non-finite, v < 0 or "
+                                   "length < 0)", lo);
+    if (hi == kBadParam)
+        return fail(h, IDM_EINVAL, "invalid IDM parameter %u of vehicle %lld (must be finite "
+                                   "and > 0)", (unsigned)(lo / (h->n_par)),
+                    (long long)(lo % h->n_par));
+    return fail(h, IDM_ENUMERIC, "non-finite state detected at step %u (checkpoint), vehicle %u",
+                hi, lo);
+}
+
+int sync_status(idm_handle* h) {
+    CK(h, cudaMemcpyAsync(&h->pinned[1], h->status, sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, h->st));
+    CK(h, cudaStreamSynchronize(h->st));
+    unsigned long long st;
+    std::memcpy(&st, &h->pinned[1], sizeof(st));
+    if (st != ~0ull) {
+        CK(h, cudaMemsetAsync(h->status, 0xff, sizeof(unsigned long long), h->st));
+        return consume_status(h, st);
+    }
+    return IDM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t idm_workspace_bytes(const idm_desc* d) {
+    Layout L;
+    return layout_for(d, &L) ? L.total : 0;
+}
+
+int32_t idm_max_lane_vehicles(void) { return kCap; }
+
+const char* idm_last_error(const idm_handle* h) { return h ? h->err : kNoHandle; }
+
+int64_t idm_launch_count(const idm_handle* h) { return h ? h->launches : 0; }
+
+void idm_destroy(idm_handle* h) {
+    if (!h) return;
+    if (h->st) cudaStreamSynchronize(h->st);
+    if (h->copy_st) cudaStreamDestroy(h->copy_st);
+    if (h->ev_obs) cudaEventDestroy(h->ev_obs);
+    if (h->ev_loss_done) cudaEventDestroy(h->ev_loss_done);
+    if (h->pinned) cudaFreeHost(h->pinned);
+    delete h;
+}
+
+int idm_init(idm_handle** out, const idm_desc* d) {
+    if (!out) return IDM_EINVAL;
+    *out = nullptr;
+    idm_handle* h = new idm_handle();
+    std::memset(h, 0, sizeof(*h));
+    int rc = IDM_OK;
+    auto bail = [&](int code) { rc = code; };
+    do {
+        Layout L;
+        if (!d) { bail(fail(h, IDM_EINVAL, "NULL descriptor")); break; }
+        h->d = *d;
+        if (!layout_for(d, &L)) {
+            bail(fail(h, IDM_EINVAL, "malformed descriptor (need N >= 1, L >= 1, max_steps >= 1, "
+                                     "1 <= ckpt_every <= %d)", kMaxCkpt));
+            break;
+        }
+        if (!(d->dt > 0.f) || !(d->a_min < 0.f) || !(d->eps_gap > 0.f) || !std::isfinite(d->dt) ||
+            !std::isfinite(d->a_min) || !std::isfinite(d->eps_gap)) {
+            bail(fail(h, IDM_EINVAL, "need dt > 0, a_min < 0, eps_gap > 0 (finite)"));
+            break;
+        }
+        if (d->param_mode != IDM_PARAMS_PER_VEHICLE && d->param_mode != IDM_PARAMS_SHARED) {
+            bail(fail(h, IDM_EINVAL, "bad param_mode %d", d->param_mode));
+            break;
+        }
+        if (!d->lane_offsets || !d->pos0 || !d->vel0 || !d->length || !d->params ||
+            !d->grad_params || !d->adam_m || !d->adam_v || !d->grad_traj || !d->traj) {
+            bail(fail(h, IDM_EINVAL, "required device array is NULL"));
+            break;
+        }
+        if (!d->workspace || d->workspace_bytes < L.total || ((uintptr_t)d->workspace & 255)) {
+            bail(fail(h, IDM_EINVAL, "workspace must be >= %zu bytes and 256-byte aligned",
+                      L.total));
+            break;
+        }
+        int dev = -1;
+        cudaError_t ce = cudaGetDevice(&dev);
+        cudaDeviceProp prop;
+        if (ce == cudaSuccess) ce = cudaGetDeviceProperties(&prop, dev);
+        if (ce != cudaSuccess) {
+            bail(fail(h, IDM_ECUDA, "no CUDA device: %s", cudaGetErrorString(ce)));
+            break;
+        }
+        if (prop.major != 10) {
+            bail(fail(h, IDM_ECUDA, "device %s is sm_%d%d; this library is built for sm_100a",
+                      prop.name, prop.major, prop.minor));
+            break;
+        }
+        h->st = (cudaStream_t)d->stream;
+        h->n = d->n_vehicles;
+        h->n_par = d->param_mode == IDM_PARAMS_SHARED ? 1 : d->n_vehicles;
+        char* ws = (char*)d->workspace;
+        h->tile_start = (int64_t*)(ws + L.tile_start);
+        h->lead = (uint8_t*)(ws + L.lead);
+        h->ckpt_s = (float*)(ws + L.ckpt_s);
+        h->ckpt_v = (float*)(ws + L.ckpt_v);
+        h->loss_partials = (double*)(ws + L.loss_partials);
+        h->loss_scalar = (double*)(ws + L.loss_scalar);
+        h->shared_partials = (double*)(ws + L.shared_partials);
+        h->status = (unsigned long long*)(ws + L.status);
+        h->nck = (int)((d->max_steps + d->ckpt_every - 1) / d->ckpt_every);
+
+        // ---- lane plan on the host (cold path): whole lanes per tile, <= kCap vehicles
+        std::vector<int32_t> off((size_t)d->n_lanes + 1);
+        ce = cudaMemcpyAsync(off.data(), d->lane_offsets, sizeof(int32_t) * off.size(),
+                             cudaMemcpyDeviceToHost, h->st);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(h->st);
+        if (ce != cudaSuccess) {
+            bail(fail(h, IDM_ECUDA, "reading lane_offsets: %s", cudaGetErrorString(ce)));
+            break;
+        }
+        if (off[0] != 0 || off.back() != d->n_vehicles) {
+            bail(fail(h, IDM_EINVAL, "lane_offsets must start at 0 and end at N=%lld (got %d..%d)",
+                      (long long)d->n_vehicles, off[0], off.back()));
+            break;
+        }
+        std::vector<int64_t> tiles;
+        std::vector<uint8_t> lead((size_t)d->n_vehicles, 0);
+        tiles.push_back(0);
+        int64_t cur = 0;  // vehicles in the open tile
+        bool bad = false;
+        for (int32_t l = 0; l < d->n_lanes; ++l) {
+            int64_t a = off[l], b = off[l + 1];
+            if (b < a) {
+                bail(fail(h, IDM_EINVAL, "lane_offsets decrease at lane %d", l));
+                bad = true;
+                break;
+            }
+            int64_t sz = b - a;
+            if (sz == 0) continue;
+            if (sz > kCap) {
+                bail(fail(h, IDM_EINVAL, "lane %d has %lld vehicles; at most %d per lane are "
+                                         "supported", l, (long long)sz, kCap));
+                bad = true;
+                break;
+            }
+            if (cur + sz > kCap) {
+                tiles.push_back(a);
+                cur = 0;
+            }
+            cur += sz;
+            for (int64_t i = a; i + 1 < b; ++i) lead[(size_t)i] = 1;
+        }
+        if (bad) break;
+        tiles.push_back(d->n_vehicles);
+        h->ntiles = (int)tiles.size() - 1;
+        if ((int64_t)h->ntiles > max_tiles_for(d)) {
+            bail(fail(h, IDM_EINVAL, "internal: tile plan exceeds bound"));
+            break;
+        }
+        const char* what = "upload tile plan";
+        ce = cudaMemcpyAsync(h->tile_start, tiles.data(), sizeof(int64_t) * tiles.size(),
+                             cudaMemcpyHostToDevice, h->st);
+        if (ce == cudaSuccess) {
+            what = "upload leader flags";
+            ce = cudaMemcpyAsync(h->lead, lead.data(), lead.size(), cudaMemcpyHostToDevice, h->st);
+        }
+        if (ce == cudaSuccess) { what = "memset status"; ce = cudaMemsetAsync(h->status, 0xff, 8, h->st); }
+        if (ce == cudaSuccess) { what = "memset loss"; ce = cudaMemsetAsync(h->loss_scalar, 0, 8, h->st); }
+        if (ce == cudaSuccess) { what = "bwd smem attribute"; ce = bwd_configure(d->ckpt_every); }
+        if (ce == cudaSuccess) {
+            what = "copy stream";
+            ce = cudaStreamCreateWithFlags(&h->copy_st, cudaStreamNonBlocking);
+        }
+        if (ce == cudaSuccess) {
+            what = "events";
+            ce = cudaEventCreateWithFlags(&h->ev_obs, cudaEventDisableTiming);
+        }
+        if (ce == cudaSuccess)
+            ce = cudaEventCreateWithFlags(&h->ev_loss_done, cudaEventDisableTiming);
+        if (ce == cudaSuccess) {
+            what = "pinned buffer";
+            ce = cudaMallocHost((void**)&h->pinned, 2 * sizeof(double));
+        }
+        if (ce != cudaSuccess) {
+            bail(fail(h, IDM_ECUDA, "init (%s): %s", what, cudaGetErrorString(ce)));
+            break;
+        }
+        ValidateArgs va{d->pos0, d->vel0, d->length, d->params, h->n, h->n_par, h->status};
+        ce = launch_validate(va, h->st);
+        h->launches++;
+        if (ce != cudaSuccess) {
+            bail(fail(h, IDM_ECUDA, "validate launch: %s", cudaGetErrorString(ce)));
+            break;
+        }
+        int s = sync_status(h);  // synchronizes (also keeps tiles/lead host vectors alive)
+        if (s != IDM_OK) { bail(s); break; }
+    } while (0);
+    if (rc != IDM_OK) {
+        // keep the message reachable: the caller gets no handle, so print it
+        fprintf(stderr, "idm_init: %s\n", h->err);
+        idm_destroy(h);
+        return rc;
+    }
+    *out = h;
+    return IDM_OK;
+}
+
+int idm_forward(idm_handle* h, int32_t steps) {
+    if (!h) return IDM_EINVAL;
+    if (steps < 1 || steps > h->d.max_steps)
+        return fail(h, IDM_EINVAL, "steps=%d outside [1, max_steps=%d]", steps, h->d.max_steps);
+    FwdArgs a;
+    a.tile_start = h->tile_start;
+    a.lead = h->lead;
+    a.pos0 = h->d.pos0;
+    a.vel0 = h->d.vel0;
+    a.length = h->d.length;
+    a.params = h->d.params;
+    a.n = h->n;
+    a.n_par = h->n_par;
+    a.traj = h->d.traj;
+    a.vel_traj = h->d.vel_traj;
+    a.state_out = h->d.state_out;
+    a.ckpt_s = h->ckpt_s;
+    a.ckpt_v = h->ckpt_v;
+    a.steps = steps;
+    a.ckpt_every = h->d.ckpt_every;
+    a.k = consts_of(h->d);
+    a.status = h->status;
+    bool kahan = steps > 2000;  // compensated displacement for long horizons (C3)
+    CK(h, launch_fwd(a, h->ntiles, kahan, h->st));
+    h->launches++;
+    h->steps = steps;
+    h->stage = 1;
+    return IDM_OK;
+}
+
+int idm_loss_grad(idm_handle* h, const float* obs, const uint8_t* mask, int32_t kind,
+                  double* loss_dev, double* loss_host) {
+    if (!h) return IDM_EINVAL;
+    if (h->stage < 1) return fail(h, IDM_ESTATE, "idm_loss_grad before idm_forward");
+    if (!obs) return fail(h, IDM_EINVAL, "obs is NULL");
+    if (kind != IDM_LOSS_L1 && kind != IDM_LOSS_L2)
+        return fail(h, IDM_EINVAL, "bad loss kind %d", kind);
+    LossArgs a;
+    a.traj = h->d.traj;
+    a.obs = obs;
+    a.mask = mask;
+    a.grad = h->d.grad_traj;
+    a.n_elem = (int64_t)(h->steps + 1) * h->n;
+    a.kind = kind;
+    a.partials = h->loss_partials;
+    CK(h, launch_loss(a, kLossBlocks, h->st));
+    CK(h, launch_reduce(h->loss_partials, kLossBlocks, 1, h->loss_scalar, nullptr, h->st));
+    h->launches += 2;
+    if (loss_dev)
+        CK(h, cudaMemcpyAsync(loss_dev, h->loss_scalar, sizeof(double), cudaMemcpyDeviceToDevice,
+                              h->st));
+    h->stage = 2;
+    if (loss_host) {
+        CK(h, cudaMemcpyAsync(&h->pinned[0], h->loss_scalar, sizeof(double),
+                              cudaMemcpyDeviceToHost, h->st));
+        int s = sync_status(h);
+        *loss_host = h->pinned[0];
+        if (s != IDM_OK) return s;
+    }
+    return IDM_OK;
+}
+
+int idm_backward(idm_handle* h) {
+    if (!h) return IDM_EINVAL;
+    if (h->stage < 2) return fail(h, IDM_ESTATE, "idm_backward before idm_loss_grad");
+    BwdArgs a;
+    a.tile_start = h->tile_start;
+    a.lead = h->lead;
+    a.params = h->d.params;
+    a.n = h->n;
+    a.n_par = h->n_par;
+    a.grad_traj = h->d.grad_traj;
+    a.ckpt_s = h->ckpt_s;
+    a.ckpt_v = h->ckpt_v;
+    a.grad_params = h->d.grad_params;
+    a.grad_state0 = h->d.grad_state0;
+    a.shared_partials = h->shared_partials;
+    a.steps = h->steps;
+    a.ckpt_every = h->d.ckpt_every;
+    a.k = consts_of(h->d);
+    a.status = h->status;
+    bool shared = h->d.param_mode == IDM_PARAMS_SHARED;
+    CK(h, launch_bwd(a, h->ntiles, shared, h->st));
+    h->launches++;
+    if (shared) {
+        CK(h, launch_reduce(h->shared_partials, h->ntiles, 6, nullptr, h->d.grad_params, h->st));
+        h->launches++;
+    }
+    h->stage = 3;
+    return IDM_OK;
+}
+
+int idm_adam_step(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, float lr1) {
+    if (!h) return IDM_EINVAL;
+    if (h->stage < 3) return fail(h, IDM_ESTATE, "idm_adam_step before idm_backward");
+    if (iter < 0 || total_iters < 1 || iter >= total_iters)
+        return fail(h, IDM_EINVAL, "iter=%d outside [0, total_iters=%d)", iter, total_iters);
+    const double b1 = 0.9, b2 = 0.999;
+    double lr = total_iters > 1 ? lr0 + (double)(lr1 - lr0) * iter / (double)(total_iters - 1)
+                                : lr0;
+    double bc1 = 1.0 - std::pow(b1, iter + 1);
+    double bc2 = 1.0 - std::pow(b2, iter + 1);
+    AdamArgs a;
+    a.x = h->d.params;
+    a.m = h->d.adam_m;
+    a.v = h->d.adam_v;
+    a.grad = h->d.grad_params;
+    a.n_par = h->n_par;
+    a.opt_mask = h->d.opt_mask;
+    a.step_size = (float)(lr / bc1);
+    a.sqrt_bc2 = (float)std::sqrt(bc2);
+    a.beta1 = (float)b1;
+    a.beta2 = (float)b2;
+    a.eps = 1e-8f;
+    // boxes of PAPER.md:208 in parameter order (a_max, a_pref, s_min, T_pref, v_targ)
+    const float lo[5] = {5.f, 0.1f, 1.f, 0.1f, 20.f}, hi[5] = {10.f, 5.f, 10.f, 5.f, 60.f};
+    for (int q = 0; q < 5; ++q) { a.lo[q] = lo[q]; a.hi[q] = hi[q]; }
+    CK(h, launch_adam(a, h->st));
+    h->launches++;
+    h->stage = 0;  // parameters changed: a new forward is required
+    return IDM_OK;
+}
+
+int idm_check(idm_handle* h) {
+    if (!h) return IDM_EINVAL;
+    CK(h, cudaGetLastError());
+    return sync_status(h);
+}
+
+int idm_step_host(idm_handle* h, int32_t steps, const float* pos0_host, const float* vel0_host,
+                  const float* obs_host, const uint8_t* mask_host, int32_t kind, int32_t iter,
+                  int32_t total_iters, float lr0, float lr1, double* loss_host) {
+    if (!h) return IDM_EINVAL;
+    if (!obs_host) return fail(h, IDM_EINVAL, "obs_host is NULL");
+    if (!h->d.obs_stage || (mask_host && !h->d.mask_stage))
+        return fail(h, IDM_EINVAL, "idm_step_host needs desc.obs_stage (and mask_stage)");
+    if (steps < 1 || steps > h->d.max_steps)
+        return fail(h, IDM_EINVAL, "steps=%d outside [1, max_steps=%d]", steps, h->d.max_steps);
+    size_t nb = sizeof(float) * (size_t)h->n;
+    size_t ob = sizeof(float) * (size_t)(steps + 1) * (size_t)h->n;
+    if (pos0_host) CK(h, cudaMemcpyAsync(h->d.pos0, pos0_host, nb, cudaMemcpyHostToDevice, h->st));
+    if (vel0_host) CK(h, cudaMemcpyAsync(h->d.vel0, vel0_host, nb, cudaMemcpyHostToDevice, h->st));
+    // the obs upload waits for the previous loss kernel (staging reuse), overlaps the forward
+    CK(h, cudaStreamWaitEvent(h->copy_st, h->ev_loss_done, 0));
+    CK(h, cudaMemcpyAsync(h->d.obs_stage, obs_host, ob, cudaMemcpyHostToDevice, h->copy_st));
+    if (mask_host)
+        CK(h, cudaMemcpyAsync(h->d.mask_stage, mask_host, (size_t)(steps + 1) * (size_t)h->n,
+                              cudaMemcpyHostToDevice, h->copy_st));
+    CK(h, cudaEventRecord(h->ev_obs, h->copy_st));
+    int s = idm_forward(h, steps);
+    if (s) return s;
+    CK(h, cudaStreamWaitEvent(h->st, h->ev_obs, 0));
+    s = idm_loss_grad(h, h->d.obs_stage, mask_host ? h->d.mask_stage : nullptr, kind, nullptr,
+                      nullptr);
+    if (s) return s;
+    CK(h, cudaEventRecord(h->ev_loss_done, h->st));
+    s = idm_backward(h);
+    if (s) return s;
+    s = idm_adam_step(h, iter, total_iters, lr0, lr1);
+    if (s) return s;
+    CK(h, cudaMemcpyAsync(&h->pinned[0], h->loss_scalar, sizeof(double), cudaMemcpyDeviceToHost,
+                          h->st));
+    s = sync_status(h);
+    if (loss_host) *loss_host = h->pinned[0];
+    return s;
+}
+
+}  // extern "C"

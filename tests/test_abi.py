@@ -1,0 +1,84 @@
+"""CPU-side checks of the C-ABI boundary: libidm.so builds for sm_100a, loads, exports every
+function include/idm.h declares, and refuses to run without a GPU (no CPU fallback)."""
+import ctypes as C
+import subprocess
+
+import pytest
+
+from paper_2412_16750_b200 import build as B
+
+
+@pytest.fixture(scope="module")
+def lib():
+    B.build()
+    from paper_2412_16750_b200 import idm
+    return idm.load_library()
+
+
+def test_header_declares_the_five_calls():
+    from paper_2412_16750_b200 import idm
+    syms = idm.header_symbols()
+    for name in ("idm_init", "idm_forward", "idm_loss_grad", "idm_backward", "idm_adam_step"):
+        assert name in syms
+    assert len(syms) >= 12
+
+
+def test_library_exports_every_header_symbol(lib):
+    from paper_2412_16750_b200 import idm
+    out = subprocess.run(["nm", "-D", "--defined-only", B.LIB], capture_output=True,
+                         text=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    missing = [s for s in idm.header_symbols() if s not in exported]
+    assert not missing, missing
+    for s in idm.header_symbols():
+        assert hasattr(lib, s)
+
+
+def test_library_is_sm100a_sass(lib):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", B.LIB],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_workspace_bytes_and_descriptor_checks(lib):
+    from paper_2412_16750_b200 import idm
+    d = idm.IdmDesc()
+    d.n_vehicles = 1000
+    d.n_lanes = 10
+    d.max_steps = 300
+    d.ckpt_every = 16
+    ws = lib.idm_workspace_bytes(C.byref(d))
+    # checkpoints (gap, speed) fp32 for ceil(300/16) = 19 segments dominate
+    assert ws >= 19 * 2 * 4 * 1000
+    assert ws % 256 == 0
+    d.ckpt_every = 0
+    assert lib.idm_workspace_bytes(C.byref(d)) == 0
+    d.ckpt_every = 16
+    d.n_vehicles = 0
+    assert lib.idm_workspace_bytes(C.byref(d)) == 0
+    assert lib.idm_max_lane_vehicles() >= 333  # NGSIM-shaped lanes (C3) fit one tile
+
+
+def test_init_without_gpu_fails_loudly(lib):
+    """No CPU fallback: with no usable device idm_init returns IDM_ECUDA (or EINVAL for a
+    malformed descriptor), never a handle."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2412_16750_b200 import idm
+    import numpy as np
+    keep = [np.zeros(16, np.float32) for _ in range(12)]
+    d = idm.IdmDesc()
+    d.n_vehicles, d.n_lanes, d.max_steps, d.ckpt_every = 4, 1, 10, 4
+    d.dt, d.a_min, d.eps_gap = 0.1, -10.0, 0.1
+    ptrs = [k.ctypes.data for k in keep]
+    (d.lane_offsets, d.pos0, d.vel0, d.length, d.params, d.grad_params, d.adam_m, d.adam_v,
+     d.traj, d.grad_traj, d.grad_state0, d.state_out) = ptrs
+    ws = np.zeros(lib.idm_workspace_bytes(C.byref(d)) + 512, np.uint8)
+    d.workspace = (ws.ctypes.data + 255) & ~255
+    d.workspace_bytes = lib.idm_workspace_bytes(C.byref(d))
+    h = C.c_void_p()
+    rc = lib.idm_init(C.byref(h), C.byref(d))
+    assert rc == idm.IDM_ECUDA and not h.value
+    with pytest.raises(idm.IdmError):
+        idm.IdmSim([0, 4], np.zeros(4), np.ones(4), np.full(4, 4.0), max_steps=10)

@@ -1,0 +1,350 @@
+"""GPU (sm_100a CUDA path through the C-ABI) vs fp64 oracle parity on identical seeded inputs.
+
+Sizes: C1 (every state, every step), C2 (all 10^5 vehicles, every step to 100 and step 300),
+ragged multi-tile layouts with edge cases, and the full C4 configuration bench.py times
+(2M vehicles, K = 300, k = 16) on 256 random lanes (lanes are independent units, so the
+oracle on the subset is exactly the oracle on the whole).
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2412_16750_b200 import synth
+from tests.parity_helpers import grad_check, oracle_truth_obs, state_violation
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU hosts
+    pytest.skip("needs a CUDA GPU", allow_module_level=True)
+
+
+@pytest.fixture(scope="module")
+def idm():
+    from paper_2412_16750_b200 import build, idm as I
+    build.build()
+    return I
+
+
+def run_gpu(idm, w, params, K, obs=None, kind="l1", ckpt_every=16, shared=False, backward=True):
+    sim = idm.from_workload(w, params, max_steps=K, ckpt_every=ckpt_every, record_velocity=True,
+                            shared_params=shared)
+    sim.forward(K)
+    out = {"sim": sim}
+    if obs is not None:
+        o = torch.as_tensor(obs[:K + 1], device="cuda").contiguous()
+        out["loss"] = sim.loss_grad(o, kind=kind)
+        if backward:
+            sim.backward()
+            torch.cuda.synchronize()
+            out["g_params"] = sim.grad_params.cpu().numpy().astype(np.float64)
+            out["g_state0"] = sim.grad_state0.cpu().numpy().astype(np.float64)
+            out["grad_traj"] = sim.grad_traj[:K + 1].cpu().numpy()
+    torch.cuda.synchronize()
+    out["P"] = sim.traj[:K + 1].cpu().numpy()
+    out["V"] = sim.vel_traj[:K + 1].cpu().numpy()
+    return out
+
+
+def oracle_grads(oracle, w, params, K, obs, kind, gpu_grad_traj=None):
+    h = oracle.leader_from_lanes(w.lane_offsets)
+    P, V = oracle.rollout(h, w.length, w.p0, w.v0, params, K, w.dt)
+    sign = None
+    if kind == "l1" and gpu_grad_traj is not None:
+        sign = (-gpu_grad_traj).astype(np.int8)  # GPU sign pattern (dL/dP = -sign)
+    L, gP = oracle.loss(P, obs[:K + 1], kind, sign_override=sign)
+    g = oracle.backward(h, w.length, params, P, V, gP, w.dt)
+    return P, V, L, g
+
+
+# ------------------------------------------------------------------------- forward
+def test_forward_c1_every_step(idm, oracle):
+    w = synth.make_workload("C1")
+    prm = w.theta_true
+    r = run_gpu(idm, w, prm, w.K)
+    P, V = oracle.rollout(oracle.leader_from_lanes(w.lane_offsets), w.length, w.p0, w.v0, prm,
+                          w.K, w.dt)
+    assert state_violation(r["P"], P) <= 1.0
+    assert state_violation(r["V"], V) <= 1.0
+
+
+def test_forward_c2_all_vehicles(idm, oracle):
+    """C2: 1,000 lanes x 100 vehicles, 300 steps; every step <= 100 (north_star) and 300."""
+    w = synth.make_workload("C2")
+    prm = synth.init_params(w.n)  # the fit's starting point: far from equilibrium
+    r = run_gpu(idm, w, prm, w.K)
+    P, V = oracle.rollout(oracle.leader_from_lanes(w.lane_offsets), w.length, w.p0, w.v0,
+                          prm.astype(np.float64), w.K, w.dt)
+    assert state_violation(r["P"][:101], P[:101]) <= 1.0
+    assert state_violation(r["V"][:101], V[:101]) <= 1.0
+    assert state_violation(r["P"], P) <= 1.0
+    assert state_violation(r["V"], V) <= 1.0
+
+
+@pytest.mark.parametrize("ckpt_every", [1, 7, 16, 48])
+def test_forward_ragged_tiles_and_edge_lanes(idm, oracle, ckpt_every):
+    """Ragged lanes across several tiles: single-vehicle lanes, a lane of exactly the tile
+    capacity, near-capacity lanes, and a ragged tail; steps not a multiple of k."""
+    cap = idm.load_library().idm_max_lane_vehicles()
+    sizes = [1, 2, 37, cap, 1, cap - 1, 5, 100, 100, 100, 3, 250, 1, 1, 64, 17]
+    w = synth.make_workload("C2", lane_sizes=sizes, K=83, seed=31)
+    r = run_gpu(idm, w, w.theta_true, w.K, ckpt_every=ckpt_every)
+    P, V = oracle.rollout(oracle.leader_from_lanes(w.lane_offsets), w.length, w.p0, w.v0,
+                          w.theta_true, w.K, w.dt)
+    assert state_violation(r["P"], P) <= 1.0
+    assert state_violation(r["V"], V) <= 1.0
+
+
+def test_forward_c4_full_size_subset(idm, oracle):
+    """C4 in bench.py's launch configuration (2M vehicles in 20k lanes, K = 300, k = 16),
+    256 random lanes against the oracle on those lanes."""
+    w = synth.make_workload("C4")
+    prm = synth.init_params(w.n)
+    sim = idm.from_workload(w, prm, max_steps=w.K, ckpt_every=16)
+    sim.forward(w.K)
+    torch.cuda.synchronize()
+    lanes = np.sort(np.random.default_rng(0).choice(w.n_lanes, 256, replace=False))
+    sub = synth.lane_subset(w, lanes)
+    idx = torch.as_tensor(sub.meta["vehicle_index"], device="cuda")
+    Pg = sim.traj.index_select(1, idx).cpu().numpy()
+    P, V = oracle.rollout(oracle.leader_from_lanes(sub.lane_offsets), sub.length, sub.p0,
+                          sub.v0, prm[:, sub.meta["vehicle_index"]].astype(np.float64), w.K)
+    assert state_violation(Pg, P) <= 1.0
+    fin = sim.state_out.cpu().numpy()[:, sub.meta["vehicle_index"]]
+    assert state_violation(fin[1], V[-1]) <= 1.0
+
+
+def test_forward_invariants_and_determinism(idm):
+    """v >= 0, non-decreasing positions, |a| <= 10 (+ float slack) on C2; two runs are
+    bitwise identical (no atomics, fixed-order math)."""
+    w = synth.make_workload("C2")
+    prm = synth.init_params(w.n)
+    r1 = run_gpu(idm, w, prm, w.K)
+    r2 = run_gpu(idm, w, prm, w.K)
+    assert np.array_equal(r1["P"], r2["P"]) and np.array_equal(r1["V"], r2["V"])
+    V = r1["V"].astype(np.float64)
+    assert V.min() >= 0.0
+    assert np.all(np.diff(r1["P"].astype(np.float64), axis=0) >= 0)
+    acc = np.diff(V, axis=0) / w.dt
+    assert np.abs(acc).max() <= 10.0 + 1e-3
+
+
+def test_long_horizon_c3_kahan(idm, oracle):
+    """C3-shaped (6 lanes x 333 vehicles, dt 0.1, 27,000 steps = 45 min): compensated
+    displacement keeps positions within tolerance at 100 ... 27,000 steps."""
+    w = synth.make_workload("C3")
+    r = run_gpu(idm, w, w.theta_true, w.K, ckpt_every=32)
+    P, V = oracle.rollout(oracle.leader_from_lanes(w.lane_offsets), w.length, w.p0, w.v0,
+                          w.theta_true, w.K, w.dt)
+    for t in (100, 1000, 3000, 10000, 27000):
+        assert state_violation(r["P"][t], P[t]) <= 1.0, t
+        assert state_violation(r["V"][t], V[t]) <= 1.0, t
+
+
+# ---------------------------------------------------------------------- loss
+@pytest.mark.parametrize("kind", ["l1", "l2"])
+def test_loss_kernel_exact(idm, oracle, kind):
+    """Eq. 4 on the GPU's own trajectory: dL/dP exactly -sign(obs - P) (L1) / -2(obs - P) (L2)
+    and the fp64 loss equal to the oracle's sum to rounding; masked entries contribute 0."""
+    w = synth.make_workload("C2", lane_sizes=[100] * 50 + [3], K=120, seed=41)
+    obs = synth.kinematic_obs(w)
+    sim = idm.from_workload(w, w.theta_true, max_steps=w.K)
+    sim.forward(w.K)
+    mask = (np.random.default_rng(1).random(obs.shape) < 0.7).astype(np.uint8)
+    L = sim.loss_grad(torch.as_tensor(obs, device="cuda"),
+                      torch.as_tensor(mask, device="cuda"), kind=kind)
+    P = sim.traj.cpu().numpy().astype(np.float64)
+    g = sim.grad_traj.cpu().numpy()
+    Lo, go = oracle.loss(P, obs.astype(np.float64), kind, mask=mask)
+    assert abs(L - Lo) <= 1e-6 * abs(Lo)
+    r = (obs - sim.traj.cpu().numpy())  # f32 residual as the kernel forms it
+    exp = np.where(mask != 0, -np.sign(r) if kind == "l1" else -2 * r, 0).astype(np.float32)
+    assert np.array_equal(g, exp)
+    # determinism of the fixed-order reduction
+    L2 = sim.loss_grad(torch.as_tensor(obs, device="cuda"),
+                       torch.as_tensor(mask, device="cuda"), kind=kind)
+    assert L2 == L
+
+
+# ------------------------------------------------------------------- gradients
+@pytest.mark.parametrize("kind", ["l2", "l1"])
+def test_gradients_c1(idm, oracle, kind):
+    w = synth.make_workload("C1")
+    obs = oracle_truth_obs(oracle, w)
+    prm = synth.init_params(w.n)
+    r = run_gpu(idm, w, prm, w.K, obs, kind)
+    _, _, _, g = oracle_grads(oracle, w, prm.astype(np.float64), w.K, obs, kind, r["grad_traj"])
+    worst, _ = grad_check(r["g_params"][:5], g["g_params"][:5], g["g_abs"][:5])
+    assert worst <= 1.0
+    worst_d, _ = grad_check(r["g_params"][5], g["g_params"][5], g["g_abs"][5])
+    assert worst_d <= 1.0
+    scale = np.abs(g["g_v0"]).max()
+    assert np.max(np.abs(r["g_state0"][1] - g["g_v0"])) <= 1e-3 * scale
+    scale = np.abs(g["g_p0"]).max()
+    assert np.max(np.abs(r["g_state0"][0] - g["g_p0"])) <= 1e-3 * scale
+
+
+@pytest.mark.parametrize("kind", ["l2", "l1"])
+def test_gradients_c2_subset(idm, oracle, kind):
+    """200 lanes x 100 vehicles x 100 steps (C2 geometry), noisy truth observations, paper
+    init; condition-aware tolerance on every gradient element; L1 with the sign protocol."""
+    w = synth.make_workload("C2", lane_sizes=[100] * 200, K=100, seed=2)
+    obs = oracle_truth_obs(oracle, w)
+    prm = synth.init_params(w.n)
+    r = run_gpu(idm, w, prm, w.K, obs, kind)
+    P, _, _, g = oracle_grads(oracle, w, prm.astype(np.float64), w.K, obs, kind,
+                              r["grad_traj"])
+    worst, plain = grad_check(r["g_params"], g["g_params"], g["g_abs"])
+    print(f"[{kind}] grad worst/tol = {worst:.3f}, plain-1e-3 pass = {plain:.4f}")
+    assert worst <= 1.0
+    if kind == "l1":
+        own = -np.sign(obs[:w.K + 1].astype(np.float64) - P)
+        mism = own != r["grad_traj"]
+        res = np.abs(obs[:w.K + 1].astype(np.float64) - P)[mism]
+        assert res.size == 0 or res.max() < 1e-3
+
+
+def test_gradients_shared_params(idm, oracle):
+    """Shared-parameter mode: one global parameter set; per-tile fp64 partials reduced in
+    fixed order vs the oracle's shared-mode gradient."""
+    w = synth.make_workload("C2", lane_sizes=[100] * 40 + [7, 1, 300], K=100, seed=12)
+    obs = oracle_truth_obs(oracle, w)
+    prm = np.array([8.0, 1.7, 3.0, 1.4, 33.0, 4.0], np.float32)
+    r = run_gpu(idm, w, prm, w.K, obs, "l2", shared=True)
+    _, _, _, g = oracle_grads(oracle, w, prm.astype(np.float64), w.K, obs, "l2")
+    worst, _ = grad_check(r["g_params"][:, 0], g["g_params"][:, 0], g["g_abs"][:, 0])
+    assert worst <= 1.0
+
+
+def test_gradients_c4_subset(idm, oracle):
+    """Full C4 in bench configuration (K = 300, k = 16, L1, paper init); 64 random lanes vs
+    the oracle with the sign protocol."""
+    w = synth.make_workload("C4")
+    obs = synth.kinematic_obs(w)
+    prm = synth.init_params(w.n)
+    sim = idm.from_workload(w, prm, max_steps=w.K, ckpt_every=16)
+    sim.forward(w.K)
+    sim.loss_grad(torch.as_tensor(obs, device="cuda"), kind="l1")
+    sim.backward()
+    torch.cuda.synchronize()
+    lanes = np.sort(np.random.default_rng(5).choice(w.n_lanes, 64, replace=False))
+    sub = synth.lane_subset(w, lanes)
+    vi = sub.meta["vehicle_index"]
+    gt = sim.grad_traj.cpu().numpy()[:, vi]
+    gg = sim.grad_params.cpu().numpy()[:, vi].astype(np.float64)
+    _, _, _, g = oracle_grads(oracle, sub, prm[:, vi].astype(np.float64), w.K, obs[:, vi],
+                              "l1", gt)
+    worst, plain = grad_check(gg, g["g_params"], g["g_abs"])
+    print(f"C4 subset grad worst/tol = {worst:.3f}, plain pass = {plain:.4f}")
+    assert worst <= 1.0
+
+
+# ---------------------------------------------------------------------- Adam / fit
+def test_adam_step_matches_oracle(idm, oracle):
+    w = synth.make_workload("C2", lane_sizes=[100] * 20, K=60, seed=3)
+    obs = oracle_truth_obs(oracle, w)
+    prm = synth.init_params(w.n)
+    sim = idm.from_workload(w, prm, max_steps=w.K)
+    x = prm.astype(np.float64)
+    m1 = np.zeros_like(x)
+    m2 = np.zeros_like(x)
+    pm = oracle.param_mask(0x1F, w.n)
+    for it in range(5):
+        sim.forward(w.K)
+        sim.loss_grad(torch.as_tensor(obs, device="cuda"), kind="l1")
+        sim.backward()
+        torch.cuda.synchronize()
+        g = sim.grad_params.cpu().numpy().astype(np.float64)
+        x_before = sim.params.cpu().numpy().astype(np.float64)
+        assert np.allclose(x_before, x, rtol=1e-5, atol=1e-6)
+        x = x_before.copy()
+        oracle.adam_step(x, g, m1, m2, it + 1, oracle.lr(it, 500, 0.1, 0.01), mask=pm)
+        oracle.project(x)
+        sim.adam_step(it, 500, 0.1, 0.01)
+        torch.cuda.synchronize()
+        got = sim.params.cpu().numpy().astype(np.float64)
+        assert np.allclose(got, x, rtol=2e-6, atol=2e-6)
+        assert np.all(got[5] == 4.0)  # delta frozen
+
+
+def test_fit_c1_converges_and_gradients_track(idm, oracle):
+    """The paper's 500-iteration recipe on C1: loss falls >= 20x, boxes
+    hold, and the GPU gradient at the GPU's own iterates matches the oracle's."""
+    w = synth.make_workload("C1")
+    obs = oracle_truth_obs(oracle, w, sigma=0.0)
+    sim = idm.from_workload(w, None, max_steps=w.K)
+    o = torch.as_tensor(obs, device="cuda")
+    losses = []
+    for it in range(500):
+        sim.forward(w.K)
+        losses.append(sim.loss_grad(o, kind="l1"))
+        sim.backward()
+        if it in (0, 100, 250, 499):
+            torch.cuda.synchronize()
+            prm = sim.params.cpu().numpy().astype(np.float64)
+            gt = sim.grad_traj.cpu().numpy()
+            _, _, _, g = oracle_grads(oracle, w, prm, w.K, obs, "l1", gt)
+            worst, _ = grad_check(sim.grad_params.cpu().numpy(), g["g_params"], g["g_abs"])
+            assert worst <= 1.0, (it, worst)
+        sim.adam_step(it)
+    assert losses[-1] < losses[0] / 20
+    p = sim.params.cpu().numpy()
+    for k, (lo, hi) in enumerate([(5, 10), (0.1, 5), (1, 10), (0.1, 5), (20, 60)]):
+        assert p[k].min() >= lo and p[k].max() <= hi
+
+
+def test_step_host_matches_device_path(idm, oracle):
+    """idm_step_host (host buffers, copies inside) == the device-resident call sequence."""
+    w = synth.make_workload("C2", lane_sizes=[100] * 30, K=50, seed=8)
+    obs = synth.kinematic_obs(w)
+    a = idm.from_workload(w, None, max_steps=w.K)
+    b = idm.from_workload(w, None, max_steps=w.K, stage_obs=True)
+    o_dev = torch.as_tensor(obs, device="cuda")
+    o_host = torch.as_tensor(obs).pin_memory()
+    for it in range(3):
+        a.forward(w.K)
+        La = a.loss_grad(o_dev)
+        a.backward()
+        a.adam_step(it)
+        Lb = b.step_host(w.K, o_host, iteration=it)
+        assert La == Lb
+    torch.cuda.synchronize()
+    assert torch.equal(a.params, b.params)
+
+
+# ------------------------------------------------------------------- error paths
+def test_error_paths(idm):
+    w = synth.make_workload("C1")
+    sim = idm.from_workload(w, None, max_steps=w.K)
+    with pytest.raises(idm.IdmError) as e:
+        sim.backward()
+    assert e.value.code == idm.IDM_ESTATE
+    with pytest.raises(idm.IdmError) as e:
+        sim.forward(w.K + 1)
+    assert e.value.code == idm.IDM_EINVAL
+    bad = synth.init_params(w.n)
+    bad[0, 3] = np.nan
+    with pytest.raises(idm.IdmError) as e:
+        idm.from_workload(w, bad, max_steps=w.K)
+    assert e.value.code == idm.IDM_EINVAL
+    cap = idm.load_library().idm_max_lane_vehicles()
+    w2 = synth.make_workload("C1", lane_sizes=[cap + 1], K=5)
+    with pytest.raises(idm.IdmError) as e:
+        idm.from_workload(w2, None, max_steps=5)
+    assert e.value.code == idm.IDM_EINVAL
+    # a non-finite parameter injected after init surfaces as IDM_ENUMERIC at the sync point
+    sim.params[4, 2] = float("inf") * 0
+    sim.forward(w.K)
+    with pytest.raises(idm.IdmError) as e:
+        sim.loss_grad(torch.zeros(w.K + 1, w.n, device="cuda"))
+    assert e.value.code == idm.IDM_ENUMERIC
+
+
+def test_launch_count(idm):
+    w = synth.make_workload("C1")
+    sim = idm.from_workload(w, None, max_steps=w.K)
+    n0 = sim.launch_count
+    sim.forward(w.K)
+    sim.loss_grad(torch.zeros(w.K + 1, w.n, device="cuda"))
+    sim.backward()
+    sim.adam_step(0)
+    assert sim.launch_count - n0 == 5  # fwd, loss, loss-reduce, bwd, adam
