@@ -28,7 +28,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_2412_16750_b200 import synth  # noqa: E402
+from paper_2412_16750_b200 import parallel, synth  # noqa: E402
 
 LANE_VEH = 100
 WORKLOAD = "C4"
@@ -121,7 +121,7 @@ def make_rank_workload(rank: int, world: int, scaling: str):
         w = synth.make_workload(WORKLOAD, seed=synth.CONFIGS[WORKLOAD]["seed"] + 1000 * rank)
     else:
         full = synth.make_workload(WORKLOAD)
-        l0, l1 = synth.shard_lanes(full.n_lanes, world, rank)
+        l0, l1 = parallel.shard_lanes(full.n_lanes, world, rank)
         w = synth.lane_subset(full, np.arange(l0, l1))
     return w
 
@@ -207,8 +207,7 @@ def run_ours(args, rank, world, local_rank):
         if ev is not None:
             ev[1].record(stream)
         sim.loss_grad(obs, kind="l1", sync=False)
-        if world > 1:
-            dist.all_reduce(sim.loss_dev)  # total loss (8 B, NCCL)
+        parallel.reduce_step(sim.loss_dev)  # total loss: one 8-byte NCCL all-reduce
         if ev is not None:
             ev[2].record(stream)
         sim.backward()
@@ -343,7 +342,7 @@ def main():
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--ckpt", type=int, default=16)
     ap.add_argument("--e2e", type=int, default=3, help="end-to-end steps (0 = skip)")
-    ap.add_argument("--cpu-lanes", type=int, default=400,
+    ap.add_argument("--cpu-lanes", type=int, default=2000,
                     help="C4 lanes in the oracle cpu_baseline sample (0 = skip)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the dominant kernel (from profiles/)")

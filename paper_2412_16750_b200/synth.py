@@ -157,12 +157,3 @@ def lane_subset(w: Workload, lanes) -> Workload:
                     length=w.length[idx].copy(), p0=w.p0[idx].copy(), v0=w.v0[idx].copy(),
                     theta_true=w.theta_true[:, idx].copy(), K=w.K, dt=w.dt, seed=w.seed,
                     meta={"vehicle_index": idx, "lanes": lanes})
-
-
-def shard_lanes(n_lanes: int, world: int, rank: int, align: int = 1):
-    """Contiguous whole-lane shard [l0, l1) of rank `rank`; shard boundaries
-    are multiples of `align` lanes except the last."""
-    chunks = (n_lanes + align - 1) // align
-    c0 = chunks * rank // world
-    c1 = chunks * (rank + 1) // world
-    return min(n_lanes, c0 * align), min(n_lanes, c1 * align)

@@ -1,0 +1,93 @@
+"""World-size-2 CPU (gloo) tests of the multi-GPU host logic: whole-lane sharding and the one
+per-step all-reduce (loss + shared-parameter gradients).  Per-shard results come from the
+fp64 oracle, so the test checks that sharded-then-reduced equals unsharded."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2412_16750_b200 import parallel, synth
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_shard_lanes_partition():
+    for n_lanes in (1, 2, 7, 100, 20000, 20001):
+        for world in (1, 2, 3, 4, 8):
+            for align in (1, 4, 64):
+                ranges = [parallel.shard_lanes(n_lanes, world, r, align) for r in range(world)]
+                assert ranges[0][0] == 0 and ranges[-1][1] == n_lanes
+                for (a0, a1), (b0, b1) in zip(ranges, ranges[1:]):
+                    assert a1 == b0
+                    assert a1 % align == 0 or a1 == n_lanes
+                sizes = [b - a for a, b in ranges]
+                assert max(sizes) - min(sizes) <= align
+
+
+def _worker(rank, world, port, shared, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as O
+        w = synth.make_workload("C2", lane_sizes=[12, 1, 7, 30, 5, 9, 16], K=40, seed=17)
+        obs = synth.kinematic_obs(w).astype(np.float64)
+        l0, l1 = parallel.shard_lanes(w.n_lanes, world, rank)
+        sub = synth.lane_subset(w, np.arange(l0, l1))
+        vi = sub.meta["vehicle_index"]
+        prm = np.array([8.0, 1.7, 3.0, 1.4, 33.0, 4.0]) if shared else \
+            synth.init_params(sub.n).astype(np.float64)
+        h = O.leader_from_lanes(sub.lane_offsets)
+        P, V = O.rollout(h, sub.length, sub.p0, sub.v0, prm, w.K)
+        L, gP = O.loss(P, obs[:, vi], "l1")
+        g = O.backward(h, sub.length, prm, P, V, gP)
+        loss = torch.tensor([L], dtype=torch.float64)
+        grads = torch.tensor(g["g_params"][:, 0]) if shared else None
+        parallel.reduce_step(loss, grads)
+        out_q.put((rank, float(loss.item()),
+                   None if grads is None else grads.numpy().copy(),
+                   None if shared else (vi, g["g_params"])))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("shared", [False, True])
+def test_two_rank_reduce_matches_unsharded(shared):
+    from oracle import oracle as O
+    O.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, shared, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # unsharded reference
+    w = synth.make_workload("C2", lane_sizes=[12, 1, 7, 30, 5, 9, 16], K=40, seed=17)
+    obs = synth.kinematic_obs(w).astype(np.float64)
+    prm = np.array([8.0, 1.7, 3.0, 1.4, 33.0, 4.0]) if shared else \
+        synth.init_params(w.n).astype(np.float64)
+    h = O.leader_from_lanes(w.lane_offsets)
+    P, V = O.rollout(h, w.length, w.p0, w.v0, prm, w.K)
+    L, gP = O.loss(P, obs, "l1")
+    g = O.backward(h, w.length, prm, P, V, gP)
+    for rank, loss, grads, per in res:
+        assert abs(loss - L) <= 1e-12 * abs(L)
+        if shared:
+            assert np.allclose(grads, g["g_params"][:, 0], rtol=1e-12, atol=1e-9)
+        else:
+            vi, gp = per
+            # lanes are independent: per-vehicle gradients are shard-invariant, bitwise
+            assert np.array_equal(gp, g["g_params"][:, vi])
