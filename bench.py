@@ -35,17 +35,32 @@ WORKLOAD = "C4"
 # Frozen algorithmic counts: thread-instructions (issue slots) per
 # vehicle-step that any implementation of the kernel's math must issue, and HBM bytes per
 # vehicle-step the method must move at k = 16, K = 300.
-ALG_INSTR = {"fwd": 36.0, "bwd": 114.0}
+ALG_INSTR = {"fwd": 36.0, "bwd": 114.0}  # SURVEY.md 8(d) frozen essential-op counts
 ISSUE_PER_CLK = 148 * 4 * 32  # SMs x schedulers x lanes (thread-instr / clk)
 
 
-def alg_bytes(K: int, k: int) -> dict:
+def alg_bytes(K: int, k: int, path: str) -> dict:
+    """Algorithmic HBM bytes per vehicle-step of each kernel."""
+    if path == "api":
+        return {
+            "fwd": 4.0 + 8.0 / k + (4 * 4 + 24 + 1) / K,        # P record + (s,v) ckpt + loads
+            "loss": 12.0,                                       # read P, obs; write dL/dP
+            "bwd": 4.0 + 8.0 / k + (24 + 24 + 8 + 1) / K,       # dL/dP + ckpt + params/grads
+            "adam": 6 * 28.0 / K,                               # x, g, m, v in; x, m, v out
+        }
     return {
-        "fwd": 4.0 + 8.0 / k + (4 * 4 + 24 + 1) / K,        # P record + (s,v) ckpt + loads
-        "loss": 12.0,                                       # read P, obs; write dL/dP
-        "bwd": 4.0 + 8.0 / k + (24 + 24 + 8 + 1) / K,       # dL/dP + ckpt + params/grads
-        "adam": 6 * 28.0 / K,                               # x, g, m, v in; x, m, v out
+        "fwd": 8.0 + 8.0 / k + (4 * 4 + 24 + 1) / K,            # obs in, dL/dP out, ckpt, loads
+        "bwd": 4.0 + 8.0 / k + (24 + 1 + 24 + 8 + 6 * 20) / K,  # dL/dP, ckpt, params, Adam
     }
+
+
+def load_traffic():
+    """ncu dram bytes per launch of the dominant kernel, from the committed capture summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
 
 
 def load_peaks():
@@ -176,19 +191,18 @@ def run_reference(args, rank, world):
 
 METRIC = "vehicle-steps/s, forward+loss+backward+Adam (C4: 2M vehicles, K=300)"
 WORKLOAD_DESC = ("C4: 20,000 lanes x 100 vehicles = 2M, K=300 steps, dt=0.1 s, Eq.4 L1 loss "
-                 "on dense noisy observations, per-vehicle IDM params, Adam, checkpoint k=16")
+                 "on dense noisy observations, per-vehicle IDM params, Adam")
 
 
 def run_ours(args, rank, world, local_rank):
     import torch
-    import torch.distributed as dist
 
     from paper_2412_16750_b200 import idm
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     w = make_rank_workload(rank, world, args.scaling)
-    K, k = w.K, args.ckpt
+    K, k = w.K, args.ckpt or idm.DEFAULT_CKPT
     # synthetic observations: truth rollout with theta_true (our forward) + N(0, 0.3^2)
     sim = idm.from_workload(w, w.theta_true, max_steps=K, ckpt_every=k, stage_obs=args.e2e > 0)
     sim.forward(K)
@@ -196,66 +210,60 @@ def run_ours(args, rank, world, local_rank):
     obs = sim.traj.clone()
     obs[1:].add_(torch.randn(obs[1:].shape, device=dev, generator=gen), alpha=0.3)
     init = torch.as_tensor(synth.init_params(w.n), device=dev)
-    sim.params.copy_(init)
     stream = sim.stream
-    torch.cuda.synchronize()
+    vsteps = float(w.n) * K * world
 
-    def step(it, ev=None):
-        if ev is not None:
-            ev[0].record(stream)
+    def reset():
+        sim.params.copy_(init)
+        sim.adam_m.zero_()
+        sim.adam_v.zero_()
+
+    def step_api(it):
         sim.forward(K)
-        if ev is not None:
-            ev[1].record(stream)
         sim.loss_grad(obs, kind="l1", sync=False)
         parallel.reduce_step(sim.loss_dev)  # total loss: one 8-byte NCCL all-reduce
-        if ev is not None:
-            ev[2].record(stream)
         sim.backward()
-        if ev is not None:
-            ev[3].record(stream)
         sim.adam_step(it % 500, 500, 0.1, 0.01)
-        if ev is not None:
-            ev[4].record(stream)
 
-    for i in range(args.warmup):
-        step(i)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    def step_fused(it):
+        sim.fit_step(obs, kind="l1", iteration=it % 500, total=500, lr0=0.1, lr1=0.01)
+        parallel.reduce_step(sim.loss_dev)
+
     clocks = ClockSampler(local_rank)
     clocks.wait_first()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n0 = sim.launch_count
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    tw0 = time.time()
-    start.record(stream)
-    for i in range(args.steps):
-        step(args.warmup + i, evs[i])
-    stop.record(stream)
-    torch.cuda.synchronize()
-    tw1 = time.time()
-    if world > 1:
-        dist.barrier()
-    launches = sim.launch_count - n0
+
+    def run_path(step_fn):
+        reset()
+        for i in range(args.warmup):
+            step_fn(i)
+        torch.cuda.synchronize()
+        parallel.barrier()
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n0 = sim.launch_count
+        tw0 = time.time()
+        start.record(stream)
+        for i in range(args.steps):
+            step_fn(args.warmup + i)
+        stop.record(stream)
+        torch.cuda.synchronize()
+        tw1 = time.time()
+        launches = sim.launch_count - n0
+        ms = parallel.max_over_ranks(start.elapsed_time(stop), dev) / args.steps
+        # per-kernel device time: the same steps again with per-launch events in the library
+        sim.timing(True)
+        sim.timing_read()
+        for i in range(args.steps):
+            step_fn(args.warmup + args.steps + i)
+        kt = sim.timing_read()
+        sim.timing(False)
+        kms = {kk: parallel.max_over_ranks(v[0], dev) / args.steps for kk, v in kt.items()
+               if v[1] > 0}
+        return {"ms_per_step": ms, "value": vsteps / (ms * 1e-3), "kernel_ms": kms,
+                "launches_per_step": launches / args.steps, "window": (tw0, tw1)}
+
+    api = run_path(step_api)
+    fused = run_path(step_fused)
     clocks.stop()
-    ms_total = start.elapsed_time(stop)
-    phase = {"fwd": 0.0, "loss": 0.0, "bwd": 0.0, "adam": 0.0}
-    for e in evs:
-        phase["fwd"] += e[0].elapsed_time(e[1])
-        phase["loss"] += e[1].elapsed_time(e[2])
-        phase["bwd"] += e[2].elapsed_time(e[3])
-        phase["adam"] += e[3].elapsed_time(e[4])
-    t = torch.tensor([ms_total] + [phase[p] for p in ("fwd", "loss", "bwd", "adam")],
-                     dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_total, ms_fwd, ms_loss, ms_bwd, ms_adam = (float(x) for x in t.tolist())
-    per_step = ms_total / args.steps
-    vsteps = float(w.n) * K * world
-    value = vsteps / (per_step * 1e-3)
 
     # ---- end to end through the C-ABI with HOST buffers (idm_step_host)
     e2e = None
@@ -265,42 +273,46 @@ def run_ours(args, rank, world, local_rank):
         v0_h = sim.vel0.cpu().pin_memory()
         sim.step_host(K, obs_h, p0_h, v0_h, iteration=0)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        parallel.barrier()
         t0 = time.perf_counter()
         for i in range(args.e2e):
             sim.step_host(K, obs_h, p0_h, v0_h, iteration=1 + i)
-        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": vsteps * args.e2e / float(te.item()), "unit": "vehicle-steps/s",
+        te = parallel.max_over_ranks(time.perf_counter() - t0, dev)
+        e2e = {"value": vsteps * args.e2e / te, "unit": "vehicle-steps/s",
                "h2d_bytes_per_step": int(obs_h.numel() * 4 + 8 * w.n),
                "d2h_bytes_per_step": 8, "steps": args.e2e,
-               "path": "idm_step_host: pinned host pos0/vel0/obs -> device, fwd, loss, bwd, "
-                       "adam, loss -> host (wall clock, max over ranks)"}
+               "path": "idm_step_host: pinned host pos0/vel0/obs -> device (obs upload "
+                       "overlapping the forward), fwd, loss, bwd, adam, loss -> host; wall "
+                       "clock, max over ranks"}
 
     if rank != 0:
         return
     hbm_gbs, sm_mhz_max, peak_src = load_peaks()
-    ab = alg_bytes(K, k)
     n_veh_steps = float(w.n) * K  # per rank per launch
-    ms = {"fwd": ms_fwd / args.steps, "loss": ms_loss / args.steps,
-          "bwd": ms_bwd / args.steps, "adam": ms_adam / args.steps}
-    dom = max(("fwd", "bwd"), key=lambda p: ms[p])
+    head = fused
+    kms = head["kernel_ms"]
+    dom = max(kms, key=kms.get)
     issue_peak = ISSUE_PER_CLK * sm_mhz_max * 1e6 / 1e12  # Tinstr/s
-    achieved = ALG_INSTR[dom] * n_veh_steps / (ms[dom] * 1e-3) / 1e12
-    roofline = {"bound": "alu", "kernel": f"{dom}_kernel", "achieved": achieved,
+    achieved = ALG_INSTR["bwd" if dom == "bwd" else "fwd"] * n_veh_steps / (kms[dom] * 1e-3) / 1e12
+    traffic = load_traffic().get(f"{dom}_kernel")
+    roofline = {"bound": "alu", "kernel": f"{dom}_kernel (fused path)", "achieved": achieved,
                 "peak": issue_peak, "unit": "Tinstr/s", "frac": achieved / issue_peak,
-                "traffic": args.traffic,
-                "basis": f"{ALG_INSTR[dom]:.0f} essential thread-instr per vehicle-step; peak ="
-                         f" 148 SM x 4 issue/clk x 32 lanes x {sm_mhz_max:.0f} MHz "
-                         f"(MEASURED_PEAKS sm_max, {peak_src})"}
-    bytes_step = sum(ab.values()) * n_veh_steps
-    hbm = {"bytes_per_vehicle_step": sum(ab.values()),
-           "achieved_GBps": bytes_step / (per_step * 1e-3) / 1e9, "peak_GBps": hbm_gbs,
-           "frac": bytes_step / (per_step * 1e-3) / 1e9 / hbm_gbs, "peak_source": peak_src,
-           "per_kernel_frac": {p: ab[p] * n_veh_steps / (ms[p] * 1e-3) / 1e9 / hbm_gbs
-                               for p in ab}}
+                "traffic": traffic,
+                "basis": f"{ALG_INSTR[dom]:.0f} essential thread-instr per vehicle-step x "
+                         f"{n_veh_steps:.3g} vehicle-steps per launch / CUDA-event launch time; "
+                         f"peak = 148 SM x 4 issue/clk x 32 lanes x {sm_mhz_max:.0f} MHz "
+                         f"(MEASURED_PEAKS sm_max, {peak_src}); traffic = ncu dram bytes/launch "
+                         f"(profiles/traffic.json)"}
+
+    def hbm_of(p, path):
+        ab = alg_bytes(K, k, path)
+        tot = sum(ab.values()) * n_veh_steps
+        return {"bytes_per_vehicle_step": round(sum(ab.values()), 3),
+                "achieved_GBps": tot / (p["ms_per_step"] * 1e-3) / 1e9, "peak_GBps": hbm_gbs,
+                "frac": tot / (p["ms_per_step"] * 1e-3) / 1e9 / hbm_gbs,
+                "per_kernel_frac": {kk: ab[kk] * n_veh_steps / (p["kernel_ms"][kk] * 1e-3) / 1e9
+                                    / hbm_gbs for kk in ab if kk in p["kernel_ms"]}}
+
     cpu = None
     if world == 1 and args.cpu_lanes > 0:
         vs_c, t_c = cpu_baseline(args.cpu_lanes, K)
@@ -309,23 +321,28 @@ def run_ours(args, rank, world, local_rank):
                          f"full step (fp64 rollout + Eq.4 L1 + adjoint + Adam), 1 thread, "
                          f"{t_c:.1f} s"}
     line = {
-        "metric": METRIC, "value": value, "unit": "vehicle-steps/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step,
+        "metric": METRIC, "value": head["value"], "unit": "vehicle-steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
         "higher_is_better": True, "scaling": args.scaling if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD_DESC, "vehicles_per_rank": w.n, "K": K,
-                   "ckpt_every": k, "parallelism": f"lane-sharded x{world}",
-                   "l2": "no flush: inputs larger than L2 (2.4 GB trajectory + obs + dL/dP per "
-                         "rank per step vs 126 MB L2)"},
-        "fwd": {"value": n_veh_steps * world / (ms["fwd"] * 1e-3), "unit": "vehicle-steps/s",
-                "ms": ms["fwd"]},
-        "phase_ms": ms,
+                   "ckpt_every": k, "path": "idm_fit_step (fused fwd+Eq.4 / bwd+Adam)",
+                   "parallelism": f"lane-sharded x{world}",
+                   "l2": "no flush: inputs larger than L2 (2.4 GB obs + 2.4 GB dL/dP per rank "
+                         "per step vs 126 MB L2)"},
+        "fwd": {"value": vsteps / (api["kernel_ms"]["fwd"] * 1e-3), "unit": "vehicle-steps/s",
+                "ms": api["kernel_ms"]["fwd"], "what": "idm_forward, trajectory record on"},
+        "fused_path": {kk: head[kk] for kk in ("ms_per_step", "value", "kernel_ms",
+                                               "launches_per_step")},
+        "api_path": {kk: api[kk] for kk in ("ms_per_step", "value", "kernel_ms",
+                                            "launches_per_step")},
         "roofline": roofline,
-        "hbm": hbm,
+        "hbm": {"fused": hbm_of(fused, "fused"), "api": hbm_of(api, "api"),
+                "peak_source": peak_src},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": launches,
-        "clocks": clocks.summary(tw0, tw1),
+        "gpu_launches": int(round(head["launches_per_step"] * args.steps)),
+        "clocks": clocks.summary(*head["window"]),
         "paper_context": "< 30 ms per timestep per pass at 2M vehicles on 16-thread Xeon "
                          "W-2255 or one RTX A5000 (PAPER.md:36, :253) = > 6.7e7 vehicle-steps/s "
                          "per pass",
@@ -340,7 +357,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
-    ap.add_argument("--ckpt", type=int, default=16)
+    ap.add_argument("--ckpt", type=int, default=None, help="checkpoint interval k")
     ap.add_argument("--e2e", type=int, default=3, help="end-to-end steps (0 = skip)")
     ap.add_argument("--cpu-lanes", type=int, default=2000,
                     help="C4 lanes in the oracle cpu_baseline sample (0 = skip)")

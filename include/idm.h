@@ -74,7 +74,9 @@ typedef struct {
     float* obs_stage;            /* [(max_steps+1)][N] device staging for idm_step_host (nullable) */
     uint8_t* mask_stage;         /* [(max_steps+1)][N] staging for the mask (nullable) */
     int32_t max_steps;           /* K_max >= 1 */
-    int32_t ckpt_every;          /* k: backward checkpoint interval, 1..64 (multiple of 1) */
+    int32_t ckpt_every;          /* k: backward checkpoint interval, 2, 4 (recommended) or 8 --
+                                    compile-time segment lengths of the kernels
+                                    (idm_workspace_bytes returns 0 otherwise) */
     float dt;                    /* Delta t > 0 (0.1 s) */
     float a_min;                 /* < 0, maximum deceleration (-10) */
     float eps_gap;               /* > 0, gap clamp (0.1 m, R#7) */
@@ -107,8 +109,8 @@ int idm_forward(idm_handle* h, int32_t steps);
 /* Eq. 4 over rows 0..steps of traj:
      L1: L = sum_{observed (t,i)} |obs - P|,  dL/dP = -sign(obs - P), sign(0) = 0 (R#11)
      L2: L = sum (obs - P)^2,                 dL/dP = -2 (obs - P)
-   obs: device [(steps+1)][N]; mask: device uint8 [(steps+1)][N], nonzero = observed, or NULL
-   (all observed).  Writes grad_traj; the loss (fixed-order fp64 reduction, deterministic) to
+   obs: device [(steps+1)][N]; mask: device uint8 [(steps+1)][N], nonzero = observed, or NULL.
+   (t,i) is observed iff the mask is set (or NULL) and obs is finite (NaN = missing).  Writes grad_traj; the loss (fixed-order fp64 reduction, deterministic) to
    *loss_dev (device double, nullable) and, if loss_host != NULL, to *loss_host (synchronizes;
    also reports a pending non-finite status as IDM_ENUMERIC). */
 int idm_loss_grad(idm_handle* h, const float* obs, const uint8_t* mask, int32_t kind,
@@ -126,6 +128,17 @@ int idm_backward(idm_handle* h);
    [5,10], [0.1,5], [1,10], [0.1,5], [20,60] (R#15).  iter is 0-based. */
 int idm_adam_step(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, float lr1);
 
+/* One whole optimizer iteration, fused: exactly forward(steps) -> loss_grad(obs, kind) ->
+   backward -> adam_step(iter, ...) (same arithmetic, same parameters bit for bit), in three
+   launches: the forward kernel evaluates Eq. 4 against each fresh position row and writes dL/dP
+   (traj is NOT written), a fixed-order reduction of the loss, and the backward kernel whose
+   epilogue applies Adam + box clamp per vehicle (shared mode: + reduce + Adam launches).
+   obs: device [(steps+1)][N]; missing observations are NaN (mask must be NULL).  Loss to
+   *loss_dev / *loss_host as in idm_loss_grad. */
+int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* mask,
+                 int32_t kind, int32_t iter, int32_t total_iters, float lr0, float lr1,
+                 double* loss_dev, double* loss_host);
+
 /* One whole optimizer iteration from HOST buffers (end-to-end path): async-copies pos0/vel0
    (nullable = keep), obs (required) and mask (nullable = all observed) from host memory
    (pinned for overlap) into desc->pos0/vel0/obs_stage/mask_stage, runs forward(steps) ->
@@ -134,6 +147,24 @@ int idm_adam_step(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, f
 int idm_step_host(idm_handle* h, int32_t steps, const float* pos0_host, const float* vel0_host,
                   const float* obs_host, const uint8_t* mask_host, int32_t kind, int32_t iter,
                   int32_t total_iters, float lr0, float lr1, double* loss_host);
+
+/* Kernel classes for idm_timing_read. */
+enum {
+    IDM_K_FWD = 0,      /* forward (fused with Eq. 4 in idm_fit_step) */
+    IDM_K_LOSS = 1,     /* Eq. 4 loss kernel (idm_loss_grad) */
+    IDM_K_REDUCE = 2,   /* fixed-order reductions (loss, shared gradients) */
+    IDM_K_BWD = 3,      /* backward (with the Adam epilogue in idm_fit_step) */
+    IDM_K_ADAM = 4,     /* Adam kernel */
+    IDM_K_OTHER = 5,    /* validation */
+    IDM_NKERNELS = 6
+};
+
+/* Launch timing for benchmarks: while enabled, every kernel launch of this handle is bracketed
+   by CUDA events recorded on desc->stream.  idm_timing_read synchronizes, writes the summed
+   device milliseconds and launch counts per class (arrays of IDM_NKERNELS, nullable) and resets
+   the accumulators. */
+int idm_timing_enable(idm_handle* h, int enable);
+int idm_timing_read(idm_handle* h, double* ms, int64_t* launches);
 
 /* Synchronize the stream and report a pending non-finite status (IDM_ENUMERIC) or CUDA error. */
 int idm_check(idm_handle* h);

@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -22,14 +23,20 @@ struct idm_handle {
     float *ckpt_s, *ckpt_v;
     double *loss_partials, *loss_scalar, *shared_partials;
     unsigned long long* status;
+    unsigned* flags;  // [0] = some delta != 4 (set by the validation kernel)
+    bool delta4;      // all delta == 4 and delta frozen => specialised kernels
     // host-side resources for idm_step_host / synchronous reads
     cudaStream_t copy_st;
     cudaEvent_t ev_obs, ev_loss_done;
-    double* pinned;  // [0] loss, [1] status (as bits)
+    double* pinned;  // [0] loss, [1] status (as bits), [2] flags
     int stage;       // 0 = initialised, 1 = forward done, 2 = loss done, 3 = backward done
     int32_t steps;
     int64_t launches;
     char err[512];
+    // launch timing (idm_timing_enable)
+    bool timing;
+    std::vector<cudaEvent_t>* ev_pool;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>>* ev_rec;
 };
 
 namespace {
@@ -58,7 +65,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
     size_t tile_start, lead, ckpt_s, ckpt_v, loss_partials, loss_scalar, shared_partials, status,
-        total;
+        flags, total;
 };
 
 int64_t max_tiles_for(const idm_desc* d) {
@@ -67,8 +74,8 @@ int64_t max_tiles_for(const idm_desc* d) {
 }
 
 bool layout_for(const idm_desc* d, Layout* L) {
-    if (!d || d->n_vehicles < 1 || d->n_lanes < 1 || d->max_steps < 1 || d->ckpt_every < 1 ||
-        d->ckpt_every > kMaxCkpt)
+    if (!d || d->n_vehicles < 1 || d->n_lanes < 1 || d->max_steps < 1 ||
+        !ckpt_supported(d->ckpt_every))
         return false;
     int64_t n = d->n_vehicles;
     int64_t mt = max_tiles_for(d);
@@ -78,10 +85,12 @@ bool layout_for(const idm_desc* d, Layout* L) {
     L->lead = off; off += align256((size_t)n);
     L->ckpt_s = off; off += align256(sizeof(float) * (size_t)(nck * n));
     L->ckpt_v = off; off += align256(sizeof(float) * (size_t)(nck * n));
-    L->loss_partials = off; off += align256(sizeof(double) * kLossBlocks);
+    L->loss_partials = off;
+    off += align256(sizeof(double) * (kLossBlocks > mt ? kLossBlocks : mt));
     L->loss_scalar = off; off += align256(sizeof(double));
     L->shared_partials = off; off += align256(sizeof(double) * 6 * (size_t)mt);
     L->status = off; off += align256(sizeof(unsigned long long));
+    L->flags = off; off += align256(sizeof(unsigned));
     L->total = off;
     return true;
 }
@@ -92,6 +101,9 @@ Consts consts_of(const idm_desc& d) {
     k.inv_dt = 1.0f / d.dt;
     k.a_min = d.a_min;
     k.eps = d.eps_gap;
+    k.dt_ln2 = (float)((double)d.dt * 0.6931471805599453);
+    k.a_min2 = (float)((double)d.a_min * 1.4426950408889634);
+    k.ninv_dt2 = (float)(-1.4426950408889634 / (double)d.dt);
     return k;
 }
 
@@ -102,6 +114,10 @@ int consume_status(idm_handle* h, unsigned long long st) {
     if (hi == kBadInput)
         return fail(h, IDM_EINVAL, "invalid initial state at vehicle %u (non-finite, v < 0 or "
                                    "length < 0)", lo);
+    if (hi == kBadDelta)
+        return fail(h, IDM_EINVAL, "delta of vehicle %u is not 4 but the handle was specialised for "
+                                   "delta = 4 at idm_init (delta frozen by opt_mask); re-create "
+                                   "the handle after changing delta", lo);
     if (hi == kBadParam)
         return fail(h, IDM_EINVAL, "invalid IDM parameter %u of vehicle %lld (must be finite "
                                    "and > 0)", (unsigned)(lo / (h->n_par)),
@@ -109,6 +125,36 @@ int consume_status(idm_handle* h, unsigned long long st) {
     return fail(h, IDM_ENUMERIC, "non-finite state detected at step %u (checkpoint), vehicle %u",
                 hi, lo);
 }
+
+// Launch timing: events around a launch on the handle's stream (no-op unless enabled).
+cudaEvent_t pool_event(idm_handle* h) {
+    if (!h->ev_pool->empty()) {
+        cudaEvent_t e = h->ev_pool->back();
+        h->ev_pool->pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+struct TimedLaunch {
+    idm_handle* h;
+    int kind;
+    cudaEvent_t a = nullptr, b = nullptr;
+    TimedLaunch(idm_handle* h_, int kind_) : h(h_), kind(kind_) {
+        if (h->timing) {
+            a = pool_event(h);
+            b = pool_event(h);
+            cudaEventRecord(a, h->st);
+        }
+    }
+    ~TimedLaunch() {
+        if (h->timing && a && b) {
+            cudaEventRecord(b, h->st);
+            h->ev_rec->push_back({kind, {a, b}});
+        }
+    }
+};
 
 int sync_status(idm_handle* h) {
     CK(h, cudaMemcpyAsync(&h->pinned[1], h->status, sizeof(unsigned long long),
@@ -141,6 +187,17 @@ int64_t idm_launch_count(const idm_handle* h) { return h ? h->launches : 0; }
 void idm_destroy(idm_handle* h) {
     if (!h) return;
     if (h->st) cudaStreamSynchronize(h->st);
+    if (h->ev_rec) {
+        for (auto& r : *h->ev_rec) {
+            cudaEventDestroy(r.second.first);
+            cudaEventDestroy(r.second.second);
+        }
+        delete h->ev_rec;
+    }
+    if (h->ev_pool) {
+        for (auto e : *h->ev_pool) cudaEventDestroy(e);
+        delete h->ev_pool;
+    }
     if (h->copy_st) cudaStreamDestroy(h->copy_st);
     if (h->ev_obs) cudaEventDestroy(h->ev_obs);
     if (h->ev_loss_done) cudaEventDestroy(h->ev_loss_done);
@@ -153,6 +210,8 @@ int idm_init(idm_handle** out, const idm_desc* d) {
     *out = nullptr;
     idm_handle* h = new idm_handle();
     std::memset(h, 0, sizeof(*h));
+    h->ev_pool = new std::vector<cudaEvent_t>();
+    h->ev_rec = new std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>>();
     int rc = IDM_OK;
     auto bail = [&](int code) { rc = code; };
     do {
@@ -161,7 +220,7 @@ int idm_init(idm_handle** out, const idm_desc* d) {
         h->d = *d;
         if (!layout_for(d, &L)) {
             bail(fail(h, IDM_EINVAL, "malformed descriptor (need N >= 1, L >= 1, max_steps >= 1, "
-                                     "1 <= ckpt_every <= %d)", kMaxCkpt));
+                                     "ckpt_every in {2, 4, 8})"));
             break;
         }
         if (!(d->dt > 0.f) || !(d->a_min < 0.f) || !(d->eps_gap > 0.f) || !std::isfinite(d->dt) ||
@@ -208,6 +267,8 @@ int idm_init(idm_handle** out, const idm_desc* d) {
         h->loss_scalar = (double*)(ws + L.loss_scalar);
         h->shared_partials = (double*)(ws + L.shared_partials);
         h->status = (unsigned long long*)(ws + L.status);
+        h->flags = (unsigned*)(ws + L.flags);
+
         h->nck = (int)((d->max_steps + d->ckpt_every - 1) / d->ckpt_every);
 
         // ---- lane plan on the host (cold path): whole lanes per tile, <= kCap vehicles
@@ -267,7 +328,8 @@ int idm_init(idm_handle** out, const idm_desc* d) {
         }
         if (ce == cudaSuccess) { what = "memset status"; ce = cudaMemsetAsync(h->status, 0xff, 8, h->st); }
         if (ce == cudaSuccess) { what = "memset loss"; ce = cudaMemsetAsync(h->loss_scalar, 0, 8, h->st); }
-        if (ce == cudaSuccess) { what = "bwd smem attribute"; ce = bwd_configure(d->ckpt_every); }
+        if (ce == cudaSuccess) { what = "memset flags"; ce = cudaMemsetAsync(h->flags, 0, 4, h->st); }
+        if (ce == cudaSuccess) { what = "smem attributes"; ce = kernels_configure(d->ckpt_every); }
         if (ce == cudaSuccess) {
             what = "copy stream";
             ce = cudaStreamCreateWithFlags(&h->copy_st, cudaStreamNonBlocking);
@@ -280,21 +342,32 @@ int idm_init(idm_handle** out, const idm_desc* d) {
             ce = cudaEventCreateWithFlags(&h->ev_loss_done, cudaEventDisableTiming);
         if (ce == cudaSuccess) {
             what = "pinned buffer";
-            ce = cudaMallocHost((void**)&h->pinned, 2 * sizeof(double));
+            ce = cudaMallocHost((void**)&h->pinned, 4 * sizeof(double));
         }
         if (ce != cudaSuccess) {
             bail(fail(h, IDM_ECUDA, "init (%s): %s", what, cudaGetErrorString(ce)));
             break;
         }
-        ValidateArgs va{d->pos0, d->vel0, d->length, d->params, h->n, h->n_par, h->status};
+        ValidateArgs va{d->pos0, d->vel0, d->length, d->params, h->n, h->n_par, h->status,
+                        h->flags};
         ce = launch_validate(va, h->st);
         h->launches++;
         if (ce != cudaSuccess) {
             bail(fail(h, IDM_ECUDA, "validate launch: %s", cudaGetErrorString(ce)));
             break;
         }
+        ce = cudaMemcpyAsync(&h->pinned[2], h->flags, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                             h->st);
+        if (ce != cudaSuccess) {
+            bail(fail(h, IDM_ECUDA, "init (flags): %s", cudaGetErrorString(ce)));
+            break;
+        }
         int s = sync_status(h);  // synchronizes (also keeps tiles/lead host vectors alive)
         if (s != IDM_OK) { bail(s); break; }
+        unsigned fl;
+        std::memcpy(&fl, &h->pinned[2], sizeof(fl));
+        h->delta4 = fl == 0 && !((d->opt_mask >> 5) & 1u);
+
     } while (0);
     if (rc != IDM_OK) {
         // keep the message reachable: the caller gets no handle, so print it
@@ -328,8 +401,19 @@ int idm_forward(idm_handle* h, int32_t steps) {
     a.ckpt_every = h->d.ckpt_every;
     a.k = consts_of(h->d);
     a.status = h->status;
-    bool kahan = steps > 2000;  // compensated displacement for long horizons (C3)
-    CK(h, launch_fwd(a, h->ntiles, kahan, h->st));
+    a.obs = nullptr;
+    a.grad_traj = nullptr;
+    a.kind = 0;
+    a.loss_partials = nullptr;
+    FwdVariant var;
+    var.delta4 = h->delta4;
+    var.kahan = steps > 2000;  // compensated displacement for long horizons (C3)
+    var.rec_v = h->d.vel_traj != nullptr;
+    var.loss = 0;
+    {
+        TimedLaunch tl(h, IDM_K_FWD);
+        CK(h, launch_fwd(a, h->ntiles, var, h->st));
+    }
     h->launches++;
     h->steps = steps;
     h->stage = 1;
@@ -351,8 +435,14 @@ int idm_loss_grad(idm_handle* h, const float* obs, const uint8_t* mask, int32_t 
     a.n_elem = (int64_t)(h->steps + 1) * h->n;
     a.kind = kind;
     a.partials = h->loss_partials;
-    CK(h, launch_loss(a, kLossBlocks, h->st));
-    CK(h, launch_reduce(h->loss_partials, kLossBlocks, 1, h->loss_scalar, nullptr, h->st));
+    {
+        TimedLaunch tl(h, IDM_K_LOSS);
+        CK(h, launch_loss(a, kLossBlocks, h->st));
+    }
+    {
+        TimedLaunch tl(h, IDM_K_REDUCE);
+        CK(h, launch_reduce(h->loss_partials, kLossBlocks, 1, h->loss_scalar, nullptr, h->st));
+    }
     h->launches += 2;
     if (loss_dev)
         CK(h, cudaMemcpyAsync(loss_dev, h->loss_scalar, sizeof(double), cudaMemcpyDeviceToDevice,
@@ -388,9 +478,14 @@ int idm_backward(idm_handle* h) {
     a.k = consts_of(h->d);
     a.status = h->status;
     bool shared = h->d.param_mode == IDM_PARAMS_SHARED;
-    CK(h, launch_bwd(a, h->ntiles, shared, h->st));
+    std::memset(&a.adam, 0, sizeof(a.adam));
+    {
+        TimedLaunch tl(h, IDM_K_BWD);
+        CK(h, launch_bwd(a, h->ntiles, h->delta4, shared, false, h->st));
+    }
     h->launches++;
     if (shared) {
+        TimedLaunch tl(h, IDM_K_REDUCE);
         CK(h, launch_reduce(h->shared_partials, h->ntiles, 6, nullptr, h->d.grad_params, h->st));
         h->launches++;
     }
@@ -398,11 +493,11 @@ int idm_backward(idm_handle* h) {
     return IDM_OK;
 }
 
-int idm_adam_step(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, float lr1) {
-    if (!h) return IDM_EINVAL;
-    if (h->stage < 3) return fail(h, IDM_ESTATE, "idm_adam_step before idm_backward");
-    if (iter < 0 || total_iters < 1 || iter >= total_iters)
-        return fail(h, IDM_EINVAL, "iter=%d outside [0, total_iters=%d)", iter, total_iters);
+}  // extern "C"
+
+namespace {
+// Adam + schedule arguments of iteration `iter` (R#14-R#16).
+AdamArgs make_adam(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, float lr1) {
     const double b1 = 0.9, b2 = 0.999;
     double lr = total_iters > 1 ? lr0 + (double)(lr1 - lr0) * iter / (double)(total_iters - 1)
                                 : lr0;
@@ -423,9 +518,152 @@ int idm_adam_step(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, f
     // boxes of PAPER.md:208 in parameter order (a_max, a_pref, s_min, T_pref, v_targ)
     const float lo[5] = {5.f, 0.1f, 1.f, 0.1f, 20.f}, hi[5] = {10.f, 5.f, 10.f, 5.f, 60.f};
     for (int q = 0; q < 5; ++q) { a.lo[q] = lo[q]; a.hi[q] = hi[q]; }
-    CK(h, launch_adam(a, h->st));
+    return a;
+}
+}  // namespace
+
+extern "C" {
+
+int idm_adam_step(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, float lr1) {
+    if (!h) return IDM_EINVAL;
+    if (h->stage < 3) return fail(h, IDM_ESTATE, "idm_adam_step before idm_backward");
+    if (iter < 0 || total_iters < 1 || iter >= total_iters)
+        return fail(h, IDM_EINVAL, "iter=%d outside [0, total_iters=%d)", iter, total_iters);
+    AdamArgs a = make_adam(h, iter, total_iters, lr0, lr1);
+    {
+        TimedLaunch tl(h, IDM_K_ADAM);
+        CK(h, launch_adam(a, h->st));
+    }
     h->launches++;
     h->stage = 0;  // parameters changed: a new forward is required
+    return IDM_OK;
+}
+
+int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* mask,
+                 int32_t kind, int32_t iter, int32_t total_iters, float lr0, float lr1,
+                 double* loss_dev, double* loss_host) {
+    if (!h) return IDM_EINVAL;
+    if (steps < 1 || steps > h->d.max_steps)
+        return fail(h, IDM_EINVAL, "steps=%d outside [1, max_steps=%d]", steps, h->d.max_steps);
+    if (!obs) return fail(h, IDM_EINVAL, "obs is NULL");
+    if (mask)
+        return fail(h, IDM_EINVAL, "idm_fit_step takes no mask: mark missing observations as NaN");
+    if (kind != IDM_LOSS_L1 && kind != IDM_LOSS_L2)
+        return fail(h, IDM_EINVAL, "bad loss kind %d", kind);
+    if (iter < 0 || total_iters < 1 || iter >= total_iters)
+        return fail(h, IDM_EINVAL, "iter=%d outside [0, total_iters=%d)", iter, total_iters);
+    // forward + Eq. 4 fused: dL/dP straight from the fresh positions, no P round trip
+    FwdArgs f;
+    f.tile_start = h->tile_start;
+    f.lead = h->lead;
+    f.pos0 = h->d.pos0;
+    f.vel0 = h->d.vel0;
+    f.length = h->d.length;
+    f.params = h->d.params;
+    f.n = h->n;
+    f.n_par = h->n_par;
+    f.traj = nullptr;
+    f.vel_traj = nullptr;
+    f.state_out = h->d.state_out;
+    f.ckpt_s = h->ckpt_s;
+    f.ckpt_v = h->ckpt_v;
+    f.steps = steps;
+    f.ckpt_every = h->d.ckpt_every;
+    f.k = consts_of(h->d);
+    f.status = h->status;
+    f.obs = obs;
+    f.grad_traj = h->d.grad_traj;
+    f.kind = kind;
+    f.loss_partials = h->loss_partials;
+    FwdVariant var;
+    var.delta4 = h->delta4;
+    var.kahan = steps > 2000;
+    var.rec_v = false;
+    var.loss = 1 + kind;
+    {
+        TimedLaunch tl(h, IDM_K_FWD);
+        CK(h, launch_fwd(f, h->ntiles, var, h->st));
+    }
+    {
+        TimedLaunch tl(h, IDM_K_REDUCE);
+        CK(h, launch_reduce(h->loss_partials, h->ntiles, 1, h->loss_scalar, nullptr, h->st));
+    }
+    h->launches += 2;
+    h->steps = steps;
+    // backward; per-vehicle parameters get Adam in the same kernel's epilogue
+    BwdArgs b;
+    b.tile_start = h->tile_start;
+    b.lead = h->lead;
+    b.params = h->d.params;
+    b.n = h->n;
+    b.n_par = h->n_par;
+    b.grad_traj = h->d.grad_traj;
+    b.ckpt_s = h->ckpt_s;
+    b.ckpt_v = h->ckpt_v;
+    b.grad_params = h->d.grad_params;
+    b.grad_state0 = h->d.grad_state0;
+    b.shared_partials = h->shared_partials;
+    b.steps = steps;
+    b.ckpt_every = h->d.ckpt_every;
+    b.k = consts_of(h->d);
+    b.status = h->status;
+    b.adam = make_adam(h, iter, total_iters, lr0, lr1);
+    const bool shared = h->d.param_mode == IDM_PARAMS_SHARED;
+    {
+        TimedLaunch tl(h, IDM_K_BWD);
+        CK(h, launch_bwd(b, h->ntiles, h->delta4, shared, !shared, h->st));
+    }
+    h->launches++;
+    if (shared) {
+        {
+            TimedLaunch tl(h, IDM_K_REDUCE);
+            CK(h, launch_reduce(h->shared_partials, h->ntiles, 6, nullptr, h->d.grad_params,
+                                h->st));
+        }
+        {
+            TimedLaunch tl(h, IDM_K_ADAM);
+            CK(h, launch_adam(b.adam, h->st));
+        }
+        h->launches += 2;
+    }
+    h->stage = 0;
+    if (loss_dev)
+        CK(h, cudaMemcpyAsync(loss_dev, h->loss_scalar, sizeof(double), cudaMemcpyDeviceToDevice,
+                              h->st));
+    if (loss_host) {
+        CK(h, cudaMemcpyAsync(&h->pinned[0], h->loss_scalar, sizeof(double),
+                              cudaMemcpyDeviceToHost, h->st));
+        int st2 = sync_status(h);
+        *loss_host = h->pinned[0];
+        if (st2 != IDM_OK) return st2;
+    }
+    return IDM_OK;
+}
+
+int idm_timing_enable(idm_handle* h, int enable) {
+    if (!h) return IDM_EINVAL;
+    h->timing = enable != 0;
+    return IDM_OK;
+}
+
+int idm_timing_read(idm_handle* h, double* ms, int64_t* launches) {
+    if (!h) return IDM_EINVAL;
+    double acc[IDM_NKERNELS] = {0};
+    int64_t cnt[IDM_NKERNELS] = {0};
+    for (auto& r : *h->ev_rec) {
+        CK(h, cudaEventSynchronize(r.second.second));
+        float t = 0.f;
+        CK(h, cudaEventElapsedTime(&t, r.second.first, r.second.second));
+        acc[r.first] += t;
+        cnt[r.first] += 1;
+        h->ev_pool->push_back(r.second.first);
+        h->ev_pool->push_back(r.second.second);
+    }
+    h->ev_rec->clear();
+    for (int i = 0; i < IDM_NKERNELS; ++i) {
+        if (ms) ms[i] = acc[i];
+        if (launches) launches[i] = cnt[i];
+    }
     return IDM_OK;
 }
 

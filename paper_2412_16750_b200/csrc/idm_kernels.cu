@@ -7,10 +7,12 @@
 //   NK4 reduce_kernel     fixed-order sum of per-block fp64 partials (loss / shared grads)
 //   NK5 adam_kernel       Adam + linear lr + box clamp
 //
-// A lane tile is a run of WHOLE lanes of at most kCap vehicles (lanes are independent, so no
-// tile ever needs another tile's data).  Local vehicle id = j * kThreads + threadIdx.x
-// (j < kVpt): every global access of a warp is 32 consecutive floats, and the leader of local
-// vehicle id is id + 1, exchanged through shared memory (one barrier per step).
+// A lane tile is a run of WHOLE lanes of at most kCap = 512 vehicles (lanes are independent, so
+// no tile ever needs another tile's data).  A CTA of kT = 256 threads owns one tile; local
+// vehicle id = j * kT + threadIdx.x (j < kVpt = 2), so every global access of a warp is 32
+// consecutive floats and the leader of local vehicle id is id + 1, exchanged through shared
+// memory (one barrier per step).  Checkpoint segments are KS steps (compile-time, unrolled);
+// step-major rows (observations, dL/dP) are prefetched a segment ahead into registers.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -33,6 +35,7 @@ __global__ void validate_kernel(ValidateArgs a) {
         float x = a.params[e];
         bool ok = isfinite(x) && x > 0.f;  // every IDM parameter is positive
         if (!ok) atomicMin(a.status, (unsigned long long)(kBadParam) << 32 | (uint64_t)e);
+        if (e >= 5 * a.n_par && x != 4.f) atomicOr(a.delta_not4, 1u);
     }
 }
 
@@ -41,280 +44,412 @@ __device__ __forceinline__ void report_nonfinite(unsigned long long* status, int
     atomicMin(status, (unsigned long long)(unsigned)step << 32 | (uint64_t)(uint32_t)veh);
 }
 
-__device__ __forceinline__ VehP load_params(const float* __restrict__ prm, int64_t n_par,
-                                            int64_t i) {
-    int64_t j = n_par == 1 ? 0 : i;
-    float a_max = prm[j], a_pref = prm[n_par + j];
-    VehP p;
-    p.a_max = a_max;
-    p.s_min = prm[2 * n_par + j];
-    p.T = prm[3 * n_par + j];
-    p.inv_vtarg = 1.f / prm[4 * n_par + j];
-    p.delta = prm[5 * n_par + j];
-    p.c = 0.5f / sqrtf(a_max * a_pref);
-    return p;
+struct RawP {
+    float a_max, a_pref, s_min, T, v_targ, delta;
+};
+
+__device__ __forceinline__ RawP load_raw(const float* __restrict__ prm, int64_t n_par,
+                                         int64_t i) {
+    const int64_t j = n_par == 1 ? 0 : i;
+    RawP r;
+    r.a_max = prm[j];
+    r.a_pref = prm[n_par + j];
+    r.s_min = prm[2 * n_par + j];
+    r.T = prm[3 * n_par + j];
+    r.v_targ = prm[4 * n_par + j];
+    r.delta = prm[5 * n_par + j];
+    return r;
 }
 
-__device__ __forceinline__ VehP dummy_params() {
-    VehP p;
-    p.a_max = 1.f; p.s_min = 1.f; p.T = 1.f; p.inv_vtarg = 1.f; p.delta = 4.f; p.c = 0.5f;
-    return p;
+__device__ __forceinline__ RawP dummy_raw() { return RawP{1.f, 1.f, 1.f, 1.f, 1.f, 4.f}; }
+
+constexpr int kVpt = 2;          // vehicles per thread
+constexpr int kT = kCap / kVpt;   // 256 threads per CTA
+
+// Eq. 4 term of one observation, branch-free: observed iff finite (NaN =
+// missing).  Returns dL/dP; adds the loss term to acc.
+template <int KIND>
+__device__ __forceinline__ float loss_term(float o, float P, bool valid, float& acc) {
+    const float r = o - P;
+    const bool ok = valid && fabsf(o) <= 3.4e38f;
+    if (KIND == 0) {  // L1: |r|, dL/dP = -sign(r), sign(0) = 0 (R#11)
+        acc += ok ? fabsf(r) : 0.f;
+        const float sg = r > 0.f ? -1.f : (r < 0.f ? 1.f : 0.f);
+        return ok ? sg : 0.f;
+    }
+    acc = ok ? fmaf(r, r, acc) : acc;  // L2: r^2, dL/dP = -2 r
+    return ok ? -2.f * r : 0.f;
+}
+
+// fixed-order CTA reduction of one double per thread -> out[blockIdx.x] (deterministic)
+__device__ __forceinline__ void block_sum_to(double x, double* out) {
+    __shared__ double red[kT / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double y = 0.0;
+        for (int w = 0; w < kT / 32; ++w) y += red[w];
+        out[blockIdx.x] = y;
+    }
 }
 
 // ------------------------------------------------------------------------------ NK1
-// One CTA = one lane tile.  All `steps` steps run in one launch; per step one __syncthreads
-// separates the speed publication from the leader read (double-buffered exchange).
-template <bool KAHAN>
-__global__ void __launch_bounds__(kThreads) fwd_kernel(FwdArgs a) {
+// One CTA = one lane tile.  All `steps` steps run in one launch, in checkpoint segments of KS
+// steps (compile-time, fully unrolled); per step one __syncthreads separates the speed
+// publication from the leader read (double-buffered exchange).
+// LOSS = 1 (L1) / 2 (L2): fused Eq. 4 for idm_fit_step -- the observation rows of the next
+// segment are prefetched into registers while the current one runs; each step evaluates Eq. 4
+// against the fresh positions and writes dL/dP instead of P.
+template <bool D4, bool KAHAN, bool RECV, int LOSS, int KS>
+__global__ void __launch_bounds__(kT, 4) fwd_kernel(FwdArgs a) {
     __shared__ float xv[2][kCap + 1];
     const int tid = threadIdx.x;
     const int64_t base = a.tile_start[blockIdx.x];
     const int n_loc = (int)(a.tile_start[blockIdx.x + 1] - base);
     const Consts k = a.k;
+    const int64_t N = a.n;
+    const int steps = a.steps;
+    const int nseg = (steps + KS - 1) / KS;
 
     float s[kVpt], v[kVpt], D[kVpt], cmp[kVpt], p0[kVpt];
     bool lead[kVpt], valid[kVpt];
     VehP P[kVpt];
 #pragma unroll
     for (int j = 0; j < kVpt; ++j) {
-        int id = j * kThreads + tid;
-        int64_t i = base + id;
+        const int id = j * kT + tid;
+        const int64_t i = base + id;
         valid[j] = id < n_loc;
         D[j] = 0.f;
         cmp[j] = 0.f;
+        RawP r = dummy_raw();
         if (valid[j]) {
             p0[j] = a.pos0[i];
             v[j] = a.vel0[i];
             lead[j] = a.lead[i] != 0;
             s[j] = lead[j] ? (a.pos0[i + 1] - p0[j]) - a.length[i + 1] : 0.f;
-            P[j] = load_params(a.params, a.n_par, i);
+            r = load_raw(a.params, a.n_par, i);
+            if (D4 && r.delta != 4.f)
+                atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
         } else {
             p0[j] = 0.f; v[j] = 0.f; s[j] = 0.f; lead[j] = false;
-            P[j] = dummy_params();
         }
+        P[j] = make_vehp(r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta);
     }
     if (tid == 0) { xv[0][kCap] = 0.f; xv[1][kCap] = 0.f; }
 
-    const int64_t N = a.n;
-    float* traj = a.traj;
-    float* vtraj = a.vel_traj;
-    // row 0 (P(0) = p(0)) and checkpoint 0
+    float* prow = a.traj ? a.traj + base + tid : nullptr;  // P row of the current step
+    float* grow = LOSS ? a.grad_traj + base + tid : nullptr;  // dL/dP row (LOSS)
+    float* vrow = RECV ? a.vel_traj + base + tid : nullptr;
+    float* cks = a.ckpt_s + base + tid;
+    float* ckv = a.ckpt_v + base + tid;
+    const float* obs = LOSS ? a.obs + base + tid : nullptr;
+    float onx[LOSS ? KS : 1][kVpt];  // observation rows of the next segment (registers)
+    float lseg = 0.f;                // loss of this thread's vehicles, this segment (fp32)
+    double lacc = 0.0;               // and across segments (fp64)
+    if (LOSS) {
+#pragma unroll
+        for (int tt = 0; tt < KS; ++tt)
+#pragma unroll
+            for (int j = 0; j < kVpt; ++j)
+                onx[tt][j] = (valid[j] && tt + 1 <= steps)
+                                 ? __ldcs(obs + (int64_t)(tt + 1) * N + j * kT) : 0.f;
+    }
 #pragma unroll
     for (int j = 0; j < kVpt; ++j) {
         if (!valid[j]) continue;
-        int64_t i = base + j * kThreads + tid;
-        if (traj) traj[i] = p0[j];
-        if (vtraj) vtraj[i] = v[j];
-        a.ckpt_s[i] = s[j];
-        a.ckpt_v[i] = v[j];
+        if (prow) __stcs(prow + j * kT, p0[j]);
+        if (LOSS) __stcs(grow + j * kT, loss_term<LOSS - 1>(obs[j * kT], p0[j], true, lseg));
+        if (RECV) vrow[j * kT] = v[j];
+        cks[j * kT] = s[j];
+        ckv[j * kT] = v[j];
     }
-    int next_ck = a.ckpt_every;
-    int ck = 1;
-    for (int t = 0; t < a.steps; ++t) {
-        const int par = t & 1;
+    int par = 0;
+    for (int seg = 0; seg < nseg; ++seg) {
+        const int t0 = seg * KS;
+        const int len = min(KS, steps - t0);
+        if (seg > 0) {  // checkpoint (gap, speed) at step t0 + finiteness check
+            cks += N;
+            ckv += N;
 #pragma unroll
-        for (int j = 0; j < kVpt; ++j) xv[par][j * kThreads + tid] = v[j];
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < kVpt; ++j) {
-            float vl = xv[par][j * kThreads + tid + 1];
-            vl = lead[j] ? vl : v[j];
-            if (KAHAN) {  // compensated displacement for long horizons (C3)
-                float y = __fmaf_rn(k.dt, v[j], -cmp[j]);
-                float tt = __fadd_rn(D[j], y);
-                cmp[j] = __fsub_rn(__fsub_rn(tt, D[j]), y);
-                D[j] = tt;
-            } else {
-                D[j] = __fmaf_rn(k.dt, v[j], D[j]);
+            for (int j = 0; j < kVpt; ++j) {
+                if (!valid[j]) continue;
+                cks[j * kT] = s[j];
+                ckv[j * kT] = v[j];
+                if (!(isfinite(s[j]) && isfinite(v[j]) && isfinite(D[j])))
+                    report_nonfinite(a.status, t0, base + j * kT + tid);
             }
-            fwd_step(s[j], v[j], vl, lead[j], P[j], k);
         }
-        const int t1 = t + 1;
-        if (traj) {
-            float* row = traj + (int64_t)t1 * N + base + tid;
+        float ocur[LOSS ? KS : 1][kVpt];
+        if (LOSS) {
 #pragma unroll
-            for (int j = 0; j < kVpt; ++j)
-                if (valid[j]) row[j * kThreads] = __fadd_rn(p0[j], D[j]);
-        }
-        if (vtraj) {
-            float* row = vtraj + (int64_t)t1 * N + base + tid;
+            for (int tt = 0; tt < KS; ++tt)
 #pragma unroll
-            for (int j = 0; j < kVpt; ++j)
-                if (valid[j]) row[j * kThreads] = v[j];
+                for (int j = 0; j < kVpt; ++j) ocur[tt][j] = onx[tt][j];
+            const float* on = obs + (int64_t)(t0 + KS + 1) * N;
+#pragma unroll
+            for (int tt = 0; tt < KS; ++tt)
+#pragma unroll
+                for (int j = 0; j < kVpt; ++j)
+                    onx[tt][j] = (valid[j] && t0 + KS + 1 + tt <= steps)
+                                     ? __ldcs(on + (int64_t)tt * N + j * kT) : 0.f;
         }
-        if (t1 == next_ck || t1 == a.steps) {
-            if (t1 == next_ck && t1 < a.steps) {
-                int64_t off = (int64_t)ck * N + base + tid;
+#pragma unroll
+        for (int tt = 0; tt < KS; ++tt) {
+            if (tt < len) {  // CTA-uniform
+#pragma unroll
+                for (int j = 0; j < kVpt; ++j) xv[par][j * kT + tid] = v[j];
+                __syncthreads();
+                float vl[kVpt];
+#pragma unroll
+                for (int j = 0; j < kVpt; ++j) vl[j] = xv[par][j * kT + tid + 1];
+                par ^= 1;
 #pragma unroll
                 for (int j = 0; j < kVpt; ++j) {
-                    if (!valid[j]) continue;
-                    a.ckpt_s[off + j * kThreads] = s[j];
-                    a.ckpt_v[off + j * kThreads] = v[j];
+                    const float vlj = lead[j] ? vl[j] : v[j];
+                    if (KAHAN) {  // compensated displacement for long horizons (C3)
+                        const float y = __fmaf_rn(k.dt, v[j], -cmp[j]);
+                        const float tt2 = __fadd_rn(D[j], y);
+                        cmp[j] = __fsub_rn(__fsub_rn(tt2, D[j]), y);
+                        D[j] = tt2;
+                    } else {
+                        D[j] = __fmaf_rn(k.dt, v[j], D[j]);
+                    }
+                    fwd_step<D4>(s[j], v[j], vlj, lead[j], P[j], k);
                 }
-                ++ck;
-                next_ck += a.ckpt_every;
-            }
+                if (prow) prow += N;
+                if (LOSS) grow += N;
+                if (RECV) vrow += N;
 #pragma unroll
-            for (int j = 0; j < kVpt; ++j)
-                if (valid[j] && !(isfinite(s[j]) && isfinite(v[j]) && isfinite(D[j])))
-                    report_nonfinite(a.status, t1, base + j * kThreads + tid);
+                for (int j = 0; j < kVpt; ++j) {
+                    const float Pv = __fadd_rn(p0[j], D[j]);
+                    if (LOSS) {
+                        const float g = loss_term<LOSS - 1>(ocur[tt][j], Pv, valid[j], lseg);
+                        if (valid[j]) __stcs(grow + j * kT, g);
+                    }
+                    if (valid[j]) {
+                        if (prow) __stcs(prow + j * kT, Pv);
+                        if (RECV) vrow[j * kT] = v[j];
+                    }
+                }
+            }
+        }
+        if (LOSS) {
+            lacc += (double)lseg;
+            lseg = 0.f;
         }
     }
-    if (a.state_out) {
 #pragma unroll
-        for (int j = 0; j < kVpt; ++j) {
-            if (!valid[j]) continue;
-            int64_t i = base + j * kThreads + tid;
+    for (int j = 0; j < kVpt; ++j) {
+        if (!valid[j]) continue;
+        const int64_t i = base + j * kT + tid;
+        if (!(isfinite(s[j]) && isfinite(v[j]) && isfinite(D[j])))
+            report_nonfinite(a.status, steps, i);
+        if (a.state_out) {
             a.state_out[i] = __fadd_rn(p0[j], D[j]);
             a.state_out[N + i] = v[j];
         }
     }
+    if (LOSS) block_sum_to(lacc + (double)lseg, a.loss_partials);
+}
+
+// Adam (Kingma & Ba, bias-corrected) + box clamp of one scalar;
+// shared by adam_kernel and the fused backward epilogue so both paths agree bitwise.
+__device__ __forceinline__ void adam_update(const AdamArgs& a, int q, int64_t e, float g) {
+    const float m1 = a.m[e] * a.beta1 + (1.f - a.beta1) * g;
+    const float m2 = a.v[e] * a.beta2 + (1.f - a.beta2) * g * g;
+    a.m[e] = m1;
+    a.v[e] = m2;
+    const float denom = sqrtf(m2) / a.sqrt_bc2 + a.eps;
+    float x = a.x[e] - a.step_size * (m1 / denom);
+    if (q < 5) x = fminf(fmaxf(x, a.lo[q]), a.hi[q]);
+    a.x[e] = x;
 }
 
 // ------------------------------------------------------------------------------ NK3
-// Per CTA (lane tile), segments of ckpt_every steps from last to first:
-//   recompute: reload the (gap, speed) checkpoint, re-run the segment's steps bit-identically,
-//              storing the state at every step in shared memory (hist);
-//   reverse:   sweep the segment backwards; the follower -> leader adjoint term F is passed
-//              through shared memory (local id -> id + 1, one barrier per step).
-// Per-vehicle gradient accumulators stay in registers for the whole rollout.
-template <bool SHARED>
-__global__ void __launch_bounds__(kThreads) bwd_kernel(BwdArgs a) {
-    extern __shared__ float2 hist[];  // [ckpt_every][kCap + 1]
+// Per CTA (lane tile), segments of KS steps (compile-time, unrolled) from last to first:
+//   recompute: reload the (gap, speed) checkpoint (prefetched one segment ahead) and re-run the
+//              segment bit-identically; per step store the speed (leader reads) and the 24-byte
+//              local-Jacobian record in shared memory; the segment's dL/dP rows are loaded into
+//              registers meanwhile;
+//   reverse:   sweep the segment backwards from the stored records; the follower -> leader
+//              adjoint term F passes through shared memory (local id -> id + 1).
+// Gradient accumulators stay in registers for the whole rollout; ADAM: per-vehicle Adam in the
+// epilogue (idm_fit_step).
+template <int KS>
+constexpr size_t bwd_smem_of() {
+    return (size_t)KS * (kCap * (sizeof(float4) + sizeof(float2)) + (kCap + 1) * sizeof(float));
+}
+
+template <bool D4, bool SHARED, bool ADAM, int KS>
+__global__ void __launch_bounds__(kT) bwd_kernel(BwdArgs a) {
+    constexpr int HS = kCap + 1;
+    extern __shared__ __align__(16) float4 smem4[];
+    float4* hR1 = smem4;                                                  // [KS][kCap]
+    float2* hR2 = reinterpret_cast<float2*>(hR1 + KS * kCap);             // [KS][kCap]
+    float* hv = reinterpret_cast<float*>(hR2 + KS * kCap);                // [KS][kCap + 1]
     __shared__ float fx[2][kCap + 1];
     const int tid = threadIdx.x;
     const int64_t base = a.tile_start[blockIdx.x];
     const int n_loc = (int)(a.tile_start[blockIdx.x + 1] - base);
     const Consts k = a.k;
     const int64_t N = a.n;
-    const int HS = kCap + 1;
+    const int steps = a.steps;
 
-    float ls[kVpt], lv[kVpt], lD[kVpt], s[kVpt], v[kVpt];
+    float ls[kVpt], lv[kVpt], lD[kVpt], s[kVpt], v[kVpt], cs[kVpt], cv[kVpt];
     bool lead[kVpt], valid[kVpt];
     VehP P[kVpt];
+    VehB B[kVpt];
     GradAcc G[kVpt];
+    const int nseg = (steps + KS - 1) / KS;
 #pragma unroll
     for (int j = 0; j < kVpt; ++j) {
-        int id = j * kThreads + tid;
-        int64_t i = base + id;
+        const int id = j * kT + tid;
+        const int64_t i = base + id;
         valid[j] = id < n_loc;
         ls[j] = 0.f;
         lv[j] = 0.f;
         G[j] = GradAcc{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        RawP r = dummy_raw();
+        lead[j] = false;
+        lD[j] = 0.f;
+        cs[j] = 0.f;
+        cv[j] = 0.f;
         if (valid[j]) {
             lead[j] = a.lead[i] != 0;
-            P[j] = load_params(a.params, a.n_par, i);
-            lD[j] = a.grad_traj[(int64_t)a.steps * N + i];  // lambda_D^K = dL/dP(K)
-        } else {
-            lead[j] = false;
-            P[j] = dummy_params();
-            lD[j] = 0.f;
+            r = load_raw(a.params, a.n_par, i);
+            if (D4 && r.delta != 4.f)
+                atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
+            lD[j] = a.grad_traj[(int64_t)steps * N + i];   // lambda_D^K = dL/dP(K)
+            cs[j] = a.ckpt_s[(int64_t)(nseg - 1) * N + i];  // checkpoint of the last segment
+            cv[j] = a.ckpt_v[(int64_t)(nseg - 1) * N + i];
         }
+        P[j] = make_vehp(r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta);
+        B[j] = make_vehb(r.a_max, r.a_pref, r.v_targ, r.delta);
     }
-    if (tid == 0) { fx[0][0] = 0.f; fx[1][0] = 0.f; }
-    // (fx[.][0] is never written again: slot id+1 >= 1.)
+    if (tid == 0) { fx[0][0] = 0.f; fx[1][0] = 0.f; }  // never written again (slots id+1 >= 1)
 
-    const int kseg = a.ckpt_every;
-    const int nseg = (a.steps + kseg - 1) / kseg;
     int par = 0;
     for (int seg = nseg - 1; seg >= 0; --seg) {
-        const int t0 = seg * kseg;
-        const int len = min(kseg, a.steps - t0);
-        // ---- recompute the segment from its checkpoint
+        const int t0 = seg * KS;
+        const int len = min(KS, steps - t0);
+        // ---- this segment's dL/dP rows into registers (consumed by the reverse sweep)
+        float gr_[KS][kVpt];
+        {
+            const float* g = a.grad_traj + (int64_t)t0 * N + base + tid;
+#pragma unroll
+            for (int tt = 0; tt < KS; ++tt)
+#pragma unroll
+                for (int j = 0; j < kVpt; ++j)
+                    gr_[tt][j] = (valid[j] && tt < len) ? __ldcs(g + (int64_t)tt * N + j * kT)
+                                                        : 0.f;
+        }
+        // ---- recompute the segment from its checkpoint; prefetch the next one
 #pragma unroll
         for (int j = 0; j < kVpt; ++j) {
-            int64_t off = (int64_t)seg * N + base + j * kThreads + tid;
-            s[j] = valid[j] ? a.ckpt_s[off] : 0.f;
-            v[j] = valid[j] ? a.ckpt_v[off] : 0.f;
+            s[j] = cs[j];
+            v[j] = cv[j];
+            if (seg > 0 && valid[j]) {
+                const int64_t off = (int64_t)(seg - 1) * N + base + j * kT + tid;
+                cs[j] = a.ckpt_s[off];
+                cv[j] = a.ckpt_v[off];
+            }
         }
-        for (int tt = 0; tt < len; ++tt) {
-            float2* h = hist + tt * HS;
 #pragma unroll
-            for (int j = 0; j < kVpt; ++j) h[j * kThreads + tid] = make_float2(s[j], v[j]);
-            __syncthreads();
-            if (tt + 1 < len) {
+        for (int tt = 0; tt < KS; ++tt) {
+            if (tt < len) {  // CTA-uniform
+                float* hvr = hv + tt * HS + tid;
+#pragma unroll
+                for (int j = 0; j < kVpt; ++j) hvr[j * kT] = v[j];
+                __syncthreads();
 #pragma unroll
                 for (int j = 0; j < kVpt; ++j) {
-                    float vl = h[j * kThreads + tid + 1].y;
-                    vl = lead[j] ? vl : v[j];
-                    fwd_step(s[j], v[j], vl, lead[j], P[j], k);
+                    const float vl = lead[j] ? hvr[j * kT + 1] : v[j];
+                    Core c;
+                    core<D4>(s[j], v[j], vl, lead[j], P[j], k, c);
+                    float4 R1;
+                    float2 R2;
+                    jac_record<D4>(c, s[j], v[j], lead[j], P[j], B[j], k, R1, R2);
+                    hR1[tt * kCap + j * kT + tid] = R1;
+                    hR2[tt * kCap + j * kT + tid] = R2;
+                    if (tt + 1 < len) advance(c, s[j], v[j], lead[j], k);
                 }
             }
         }
-        // ---- reverse sweep
-        for (int tt = len - 1; tt >= 0; --tt) {
-            const int t = t0 + tt;
-            const float2* h = hist + tt * HS;
-            float gt[kVpt];
+        // ---- reverse sweep, t = t0 + len - 1 ... t0 (reads only this thread's records and
+        //      the speed rows, all written before the last recompute barrier)
 #pragma unroll
-            for (int j = 0; j < kVpt; ++j)
-                gt[j] = valid[j] ? a.grad_traj[(int64_t)t * N + base + j * kThreads + tid] : 0.f;
-            float F[kVpt];
+        for (int tt = KS - 1; tt >= 0; --tt) {
+            if (tt < len) {  // CTA-uniform
+                const float* hvr = hv + tt * HS + tid;
+                float F[kVpt];
 #pragma unroll
-            for (int j = 0; j < kVpt; ++j) {
-                int id = j * kThreads + tid;
-                float2 sv = h[id];
-                float vl = lead[j] ? h[id + 1].y : sv.y;
-                F[j] = bwd_step(sv.x, sv.y, vl, lead[j], P[j], k, ls[j], lv[j], lD[j], G[j]);
+                for (int j = 0; j < kVpt; ++j) {
+                    const float vj = hvr[j * kT];
+                    const float vl = lead[j] ? hvr[j * kT + 1] : vj;
+                    F[j] = bwd_from_record<D4>(hR1[tt * kCap + j * kT + tid],
+                                               hR2[tt * kCap + j * kT + tid], vj, vl, P[j], B[j],
+                                               k, ls[j], lv[j], lD[j], G[j]);
+                }
+#pragma unroll
+                for (int j = 0; j < kVpt; ++j) fx[par][j * kT + tid + 1] = F[j];
+                __syncthreads();
+#pragma unroll
+                for (int j = 0; j < kVpt; ++j) {
+                    lv[j] += fx[par][j * kT + tid];  // F from the follower (id - 1)
+                    lD[j] += gr_[tt][j];             // lambda_D^t = g^t + lambda_D^{t+1}
+                }
+                par ^= 1;
             }
-#pragma unroll
-            for (int j = 0; j < kVpt; ++j) fx[par][j * kThreads + tid + 1] = F[j];
-            __syncthreads();
-#pragma unroll
-            for (int j = 0; j < kVpt; ++j) {
-                lv[j] += fx[par][j * kThreads + tid];  // F from the follower (id - 1)
-                lD[j] += gt[j];                        // lambda_D^t = g^t + lambda_D^{t+1}
-            }
-            par ^= 1;
         }
     }
     // dL/dp0_i = lambda_D - lambda_s_i + lambda_s_{follower}; dL/dv0 = lambda_v
 #pragma unroll
-    for (int j = 0; j < kVpt; ++j) fx[par][j * kThreads + tid + 1] = lead[j] ? ls[j] : 0.f;
+    for (int j = 0; j < kVpt; ++j) fx[par][j * kT + tid + 1] = lead[j] ? ls[j] : 0.f;
     __syncthreads();
     float gp0[kVpt];
 #pragma unroll
     for (int j = 0; j < kVpt; ++j)
-        gp0[j] = lD[j] - (lead[j] ? ls[j] : 0.f) + fx[par][j * kThreads + tid];
+        gp0[j] = lD[j] - (lead[j] ? ls[j] : 0.f) + fx[par][j * kT + tid];
 
     // parameter gradients from the factored accumulators
     float gr[kVpt][6];
 #pragma unroll
     for (int j = 0; j < kVpt; ++j) {
-        if (!valid[j]) {
 #pragma unroll
-            for (int q = 0; q < 6; ++q) gr[j][q] = 0.f;
-            continue;
-        }
-        int64_t i = base + j * kThreads + tid;
-        int64_t jj = a.n_par == 1 ? 0 : i;
-        float a_max = a.params[jj], a_pref = a.params[a.n_par + jj];
-        float c = P[j].c;
-        gr[j][0] = G[j].S1 - c * (0.5f / a_max) * G[j].S2;              // a_max
-        gr[j][1] = -c * (0.5f / a_pref) * G[j].S2;                       // a_pref
-        gr[j][2] = G[j].S3;                                              // s_min
-        gr[j][3] = G[j].S4;                                              // T_pref
-        gr[j][4] = a_max * P[j].delta * P[j].inv_vtarg * G[j].S5;       // v_targ
-        gr[j][5] = -a_max * G[j].S6;                                     // delta
+        for (int q = 0; q < 6; ++q) gr[j][q] = 0.f;
+        if (!valid[j]) continue;
+        const int64_t i = base + j * kT + tid;
+        const RawP r = load_raw(a.params, a.n_par, i);
+        const float c = 0.5f / sqrtf(r.a_max * r.a_pref);
+        gr[j][0] = G[j].S1 - c * (0.5f / r.a_max) * G[j].S2;             // a_max
+        gr[j][1] = -c * (0.5f / r.a_pref) * G[j].S2;                      // a_pref
+        gr[j][2] = G[j].S3;                                               // s_min
+        gr[j][3] = G[j].S4;                                               // T_pref
+        gr[j][4] = r.a_max * r.delta / r.v_targ * G[j].S5;               // v_targ
+        gr[j][5] = -r.a_max * kLn2 * G[j].S6;                             // delta
         if (a.grad_state0) {
             a.grad_state0[i] = gp0[j];
             a.grad_state0[N + i] = lv[j];
         }
+        if (!(isfinite(lv[j]) && isfinite(gp0[j]))) report_nonfinite(a.status, 0, i);
     }
     if (!SHARED) {
 #pragma unroll
         for (int j = 0; j < kVpt; ++j) {
             if (!valid[j]) continue;
-            int64_t i = base + j * kThreads + tid;
+            const int64_t i = base + j * kT + tid;
 #pragma unroll
-            for (int q = 0; q < 6; ++q) a.grad_params[q * N + i] = gr[j][q];
+            for (int q = 0; q < 6; ++q) {
+                a.grad_params[q * N + i] = gr[j][q];
+                // fused iteration: Adam on this vehicle's parameters right here (idm_fit_step)
+                if (ADAM && ((a.adam.opt_mask >> q) & 1u)) adam_update(a.adam, q, q * N + i, gr[j][q]);
+            }
         }
-        for (int j = 0; j < kVpt; ++j)
-            if (valid[j] && !(isfinite(lv[j]) && isfinite(gp0[j])))
-                report_nonfinite(a.status, 0, base + j * kThreads + tid);
     } else {
         // fixed-order block reduction in fp64 -> partial[tile][6]
-        __shared__ double red[kThreads / 32][6];
+        __shared__ double red[kT / 32][6];
         double acc[6];
 #pragma unroll
         for (int q = 0; q < 6; ++q) {
@@ -331,7 +466,7 @@ __global__ void __launch_bounds__(kThreads) bwd_kernel(BwdArgs a) {
         __syncthreads();
         if (tid < 6) {
             double x = 0.0;
-            for (int w = 0; w < kThreads / 32; ++w) x += red[w][tid];
+            for (int w = 0; w < kT / 32; ++w) x += red[w][tid];
             a.shared_partials[(int64_t)blockIdx.x * 6 + tid] = x;
         }
     }
@@ -355,30 +490,33 @@ __global__ void __launch_bounds__(256) loss_kernel(LossArgs a) {
         for (int64_t e = t0; e < n4; e += stride) {
             float4 p = __ldcs(P4 + e), o = __ldcs(O4 + e);
             uchar4 m = a.mask ? __ldcs(M4 + e) : make_uchar4(1, 1, 1, 1);
+            // an observation is used iff its mask is set and it is finite (NaN = missing)
+            m.x = m.x && fabsf(o.x) <= 3.4e38f;
+            m.y = m.y && fabsf(o.y) <= 3.4e38f;
+            m.z = m.z && fabsf(o.z) <= 3.4e38f;
+            m.w = m.w && fabsf(o.w) <= 3.4e38f;
             float r0 = o.x - p.x, r1 = o.y - p.y, r2 = o.z - p.z, r3 = o.w - p.w;
             float4 g;
-            float part;
             if (l1) {
                 g.x = m.x ? -copysignf(r0 != 0.f, r0) : 0.f;
                 g.y = m.y ? -copysignf(r1 != 0.f, r1) : 0.f;
                 g.z = m.z ? -copysignf(r2 != 0.f, r2) : 0.f;
                 g.w = m.w ? -copysignf(r3 != 0.f, r3) : 0.f;
-                part = (m.x ? fabsf(r0) : 0.f) + (m.y ? fabsf(r1) : 0.f) +
-                       (m.z ? fabsf(r2) : 0.f) + (m.w ? fabsf(r3) : 0.f);
+                acc += (m.x ? (double)fabsf(r0) : 0.0) + (m.y ? (double)fabsf(r1) : 0.0) +
+                       (m.z ? (double)fabsf(r2) : 0.0) + (m.w ? (double)fabsf(r3) : 0.0);
             } else {
                 g.x = m.x ? -2.f * r0 : 0.f;
                 g.y = m.y ? -2.f * r1 : 0.f;
                 g.z = m.z ? -2.f * r2 : 0.f;
                 g.w = m.w ? -2.f * r3 : 0.f;
-                part = (m.x ? r0 * r0 : 0.f) + (m.y ? r1 * r1 : 0.f) +
-                       (m.z ? r2 * r2 : 0.f) + (m.w ? r3 * r3 : 0.f);
+                acc += (m.x ? (double)r0 * r0 : 0.0) + (m.y ? (double)r1 * r1 : 0.0) +
+                       (m.z ? (double)r2 * r2 : 0.0) + (m.w ? (double)r3 * r3 : 0.0);
             }
             __stcs(G4 + e, g);
-            acc += (double)part;
         }
         // tail (n_elem % 4) handled by the first threads
         for (int64_t e = (n4 << 2) + t0; e < a.n_elem; e += stride) {
-            bool m = a.mask ? a.mask[e] != 0 : true;
+            bool m = (a.mask ? a.mask[e] != 0 : true) && fabsf(a.obs[e]) <= 3.4e38f;
             float r = a.obs[e] - a.traj[e];
             float g = l1 ? -copysignf(r != 0.f, r) : -2.f * r;
             a.grad[e] = m ? g : 0.f;
@@ -386,7 +524,7 @@ __global__ void __launch_bounds__(256) loss_kernel(LossArgs a) {
         }
     } else {
         for (int64_t e = t0; e < a.n_elem; e += stride) {
-            bool m = a.mask ? a.mask[e] != 0 : true;
+            bool m = (a.mask ? a.mask[e] != 0 : true) && fabsf(a.obs[e]) <= 3.4e38f;
             float r = a.obs[e] - a.traj[e];
             float g = l1 ? -copysignf(r != 0.f, r) : -2.f * r;
             a.grad[e] = m ? g : 0.f;
@@ -433,17 +571,8 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
     const int64_t m = 6 * a.n_par;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
          e += (int64_t)gridDim.x * blockDim.x) {
-        int q = (int)(e / a.n_par);
-        if (!((a.opt_mask >> q) & 1u)) continue;
-        float g = a.grad[e];
-        float m1 = a.m[e] * a.beta1 + (1.f - a.beta1) * g;
-        float m2 = a.v[e] * a.beta2 + (1.f - a.beta2) * g * g;
-        a.m[e] = m1;
-        a.v[e] = m2;
-        float denom = sqrtf(m2) / a.sqrt_bc2 + a.eps;
-        float x = a.x[e] - a.step_size * (m1 / denom);
-        if (q < 5) x = fminf(fmaxf(x, a.lo[q]), a.hi[q]);
-        a.x[e] = x;
+        const int q = (int)(e / a.n_par);
+        if ((a.opt_mask >> q) & 1u) adam_update(a, q, e, a.grad[e]);
     }
 }
 
@@ -453,31 +582,90 @@ cudaError_t launch_validate(const ValidateArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_fwd(const FwdArgs& a, int ntiles, bool kahan, cudaStream_t st) {
-    if (kahan)
-        fwd_kernel<true><<<ntiles, kThreads, 0, st>>>(a);
-    else
-        fwd_kernel<false><<<ntiles, kThreads, 0, st>>>(a);
+bool ckpt_supported(int k) { return k == 2 || k == 4 || k == 8; }
+
+size_t bwd_smem_bytes(int ckpt_every) {
+    return ckpt_every == 2 ? bwd_smem_of<2>() : ckpt_every == 8 ? bwd_smem_of<8>()
+                                                                : bwd_smem_of<4>();
+}
+
+template <bool D4, bool KH, int KS>
+static void launch_fwd_k(const FwdArgs& a, int ntiles, const FwdVariant& var, cudaStream_t st) {
+    dim3 g(ntiles), b(kT);
+    if (var.loss == 1) fwd_kernel<D4, KH, false, 1, KS><<<g, b, 0, st>>>(a);
+    else if (var.loss == 2) fwd_kernel<D4, KH, false, 2, KS><<<g, b, 0, st>>>(a);
+    else if (var.rec_v) fwd_kernel<D4, KH, true, 0, KS><<<g, b, 0, st>>>(a);
+    else fwd_kernel<D4, KH, false, 0, KS><<<g, b, 0, st>>>(a);
+}
+
+template <bool D4, bool KH>
+static void launch_fwd_dk(const FwdArgs& a, int ntiles, const FwdVariant& var, cudaStream_t st) {
+    switch (a.ckpt_every) {
+        case 2: launch_fwd_k<D4, KH, 2>(a, ntiles, var, st); break;
+        case 8: launch_fwd_k<D4, KH, 8>(a, ntiles, var, st); break;
+        default: launch_fwd_k<D4, KH, 4>(a, ntiles, var, st); break;
+    }
+}
+
+cudaError_t launch_fwd(const FwdArgs& a, int ntiles, const FwdVariant& var, cudaStream_t st) {
+    if (!ckpt_supported(a.ckpt_every)) return cudaErrorInvalidValue;
+    if (var.delta4) {
+        if (var.kahan) launch_fwd_dk<true, true>(a, ntiles, var, st);
+        else launch_fwd_dk<true, false>(a, ntiles, var, st);
+    } else {
+        if (var.kahan) launch_fwd_dk<false, true>(a, ntiles, var, st);
+        else launch_fwd_dk<false, false>(a, ntiles, var, st);
+    }
     return cudaGetLastError();
 }
 
-size_t bwd_smem_bytes(int ckpt_every) { return (size_t)ckpt_every * (kCap + 1) * sizeof(float2); }
-
-cudaError_t bwd_configure(int ckpt_every) {
-    size_t mx = bwd_smem_bytes(ckpt_every);
-    cudaError_t e = cudaFuncSetAttribute(bwd_kernel<false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)mx);
+template <int KS>
+static cudaError_t configure_k() {
+    cudaError_t e = cudaSuccess;
+    const int mb = (int)bwd_smem_of<KS>();
+#define IDM_CFG(D4, SH, AD)                                                                 \
+    if (e == cudaSuccess)                                                                  \
+        e = cudaFuncSetAttribute(bwd_kernel<D4, SH, AD, KS>,                               \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, mb);
+    IDM_CFG(true, true, false) IDM_CFG(true, false, false) IDM_CFG(false, true, false)
+    IDM_CFG(false, false, false) IDM_CFG(true, false, true) IDM_CFG(false, false, true)
+#undef IDM_CFG
+    return e;
 }
 
-cudaError_t launch_bwd(const BwdArgs& a, int ntiles, bool shared, cudaStream_t st) {
-    size_t smem = bwd_smem_bytes(a.ckpt_every);
-    if (shared)
-        bwd_kernel<true><<<ntiles, kThreads, smem, st>>>(a);
-    else
-        bwd_kernel<false><<<ntiles, kThreads, smem, st>>>(a);
+cudaError_t kernels_configure(int ckpt_every) {
+    switch (ckpt_every) {
+        case 2: return configure_k<2>();
+        case 4: return configure_k<4>();
+        case 8: return configure_k<8>();
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int KS>
+static void launch_bwd_k(const BwdArgs& a, int ntiles, bool delta4, bool shared, bool adam,
+                         cudaStream_t st) {
+    const size_t smem = bwd_smem_of<KS>();
+    dim3 g(ntiles), b(kT);
+    if (delta4) {
+        if (shared) bwd_kernel<true, true, false, KS><<<g, b, smem, st>>>(a);
+        else if (adam) bwd_kernel<true, false, true, KS><<<g, b, smem, st>>>(a);
+        else bwd_kernel<true, false, false, KS><<<g, b, smem, st>>>(a);
+    } else {
+        if (shared) bwd_kernel<false, true, false, KS><<<g, b, smem, st>>>(a);
+        else if (adam) bwd_kernel<false, false, true, KS><<<g, b, smem, st>>>(a);
+        else bwd_kernel<false, false, false, KS><<<g, b, smem, st>>>(a);
+    }
+}
+
+cudaError_t launch_bwd(const BwdArgs& a, int ntiles, bool delta4, bool shared, bool adam,
+                       cudaStream_t st) {
+    switch (a.ckpt_every) {
+        case 2: launch_bwd_k<2>(a, ntiles, delta4, shared, adam, st); break;
+        case 4: launch_bwd_k<4>(a, ntiles, delta4, shared, adam, st); break;
+        case 8: launch_bwd_k<8>(a, ntiles, delta4, shared, adam, st); break;
+        default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 

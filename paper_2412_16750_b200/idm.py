@@ -26,6 +26,7 @@ STATUS_NAMES = {0: "IDM_OK", 1: "IDM_EINVAL", 2: "IDM_ENUMERIC", 3: "IDM_ECUDA",
 PARAMS_PER_VEHICLE, PARAMS_SHARED = 0, 1
 LOSS_KINDS = {"l1": 0, "l2": 1}
 PAPER_OPT_MASK = 0x1F  # the paper optimizes five parameters; delta frozen
+DEFAULT_CKPT = 4  # backward checkpoint interval k (tuned on B200)
 
 
 class IdmDesc(C.Structure):
@@ -99,9 +100,16 @@ def load_library(path: str | None = None):
     L.idm_backward.argtypes = [vp]
     L.idm_adam_step.restype = C.c_int
     L.idm_adam_step.argtypes = [vp, i32, i32, C.c_float, C.c_float]
+    L.idm_fit_step.restype = C.c_int
+    L.idm_fit_step.argtypes = [vp, i32, vp, vp, i32, i32, i32, C.c_float, C.c_float, vp,
+                               C.POINTER(C.c_double)]
     L.idm_step_host.restype = C.c_int
     L.idm_step_host.argtypes = [vp, i32, vp, vp, vp, vp, i32, i32, i32, C.c_float, C.c_float,
                                 C.POINTER(C.c_double)]
+    L.idm_timing_enable.restype = C.c_int
+    L.idm_timing_enable.argtypes = [vp, C.c_int]
+    L.idm_timing_read.restype = C.c_int
+    L.idm_timing_read.argtypes = [vp, vp, vp]
     L.idm_check.restype = C.c_int
     L.idm_check.argtypes = [vp]
     L.idm_launch_count.restype = i64
@@ -134,7 +142,7 @@ class IdmSim:
     params [6, N] (per-vehicle) or [6] (shared)."""
 
     def __init__(self, lane_offsets, pos0, vel0, length, params=None, *, max_steps: int,
-                 ckpt_every: int = 16, dt: float = 0.1, a_min: float = -10.0,
+                 ckpt_every: int = DEFAULT_CKPT, dt: float = 0.1, a_min: float = -10.0,
                  eps_gap: float = 0.1, shared_params: bool = False,
                  opt_mask: int = PAPER_OPT_MASK, record_velocity: bool = False,
                  stage_obs: bool = False, stage_mask: bool = False, state_out: bool = True,
@@ -241,6 +249,22 @@ class IdmSim:
     def adam_step(self, iteration: int, total: int = 500, lr0: float = 0.1, lr1: float = 0.01):
         self._check(self._lib.idm_adam_step(self.handle, iteration, total, lr0, lr1))
 
+    def fit_step(self, obs: torch.Tensor, kind: str = "l1", iteration: int = 0,
+                 total: int = 500, lr0: float = 0.1, lr1: float = 0.01, steps: int | None = None,
+                 sync: bool = False):
+        """One fused iteration (idm_fit_step): forward + Eq. 4 + backward + Adam in three
+        launches.  Missing observations are NaN.  Returns the loss if sync, else None (the
+        loss is in self.loss_dev)."""
+        steps = self.max_steps if steps is None else int(steps)
+        assert obs.dtype == torch.float32 and obs.is_contiguous() and obs.device == self.device
+        assert obs.numel() >= (steps + 1) * self.n
+        out = C.c_double(0.0)
+        self._check(self._lib.idm_fit_step(self.handle, steps, _ptr(obs), None, LOSS_KINDS[kind],
+                                           iteration, total, lr0, lr1, _ptr(self.loss_dev),
+                                           C.byref(out) if sync else None))
+        self.steps = steps
+        return out.value if sync else None
+
     def step_host(self, steps, obs_host: torch.Tensor, pos0_host=None, vel0_host=None,
                   mask_host=None, kind="l1", iteration=0, total=500, lr0=0.1, lr1=0.01):
         """One full iteration from HOST tensors (pinned for overlap); returns the loss."""
@@ -252,6 +276,18 @@ class IdmSim:
             _ptr(mask_host), LOSS_KINDS[kind], iteration, total, lr0, lr1, C.byref(out)))
         self.steps = int(steps)
         return out.value
+
+    def timing(self, enable: bool = True):
+        """Bracket every launch with CUDA events on the handle's stream (benchmarks)."""
+        self._check(self._lib.idm_timing_enable(self.handle, int(enable)))
+
+    def timing_read(self) -> dict:
+        """Summed device ms and launch counts per kernel class since the last read."""
+        ms = (C.c_double * 6)()
+        n = (C.c_int64 * 6)()
+        self._check(self._lib.idm_timing_read(self.handle, ms, n))
+        names = ("fwd", "loss", "reduce", "bwd", "adam", "other")
+        return {k: (ms[i], n[i]) for i, k in enumerate(names)}
 
     def check(self):
         self._check(self._lib.idm_check(self.handle))
@@ -291,6 +327,11 @@ def idm_backward(sim: IdmSim):
 
 def idm_adam_step(sim: IdmSim, iteration: int, total: int = 500, lr0=0.1, lr1=0.01):
     sim.adam_step(iteration, total, lr0, lr1)
+
+
+def idm_fit_step(sim: IdmSim, obs, kind="l1", iteration=0, total=500, lr0=0.1, lr1=0.01,
+                 sync=False):
+    return sim.fit_step(obs, kind, iteration, total, lr0, lr1, sync=sync)
 
 
 def from_workload(w, params=None, **kw) -> IdmSim:

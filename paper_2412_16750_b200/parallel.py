@@ -46,3 +46,9 @@ def max_over_ranks(x: float, device, group=None) -> float:
     t = torch.tensor([x], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+def barrier(group=None):
+    """dist.barrier() when distributed, else nothing."""
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier(group=group)

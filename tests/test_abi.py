@@ -46,14 +46,15 @@ def test_workspace_bytes_and_descriptor_checks(lib):
     d.n_vehicles = 1000
     d.n_lanes = 10
     d.max_steps = 300
-    d.ckpt_every = 16
+    d.ckpt_every = 4
     ws = lib.idm_workspace_bytes(C.byref(d))
-    # checkpoints (gap, speed) fp32 for ceil(300/16) = 19 segments dominate
-    assert ws >= 19 * 2 * 4 * 1000
+    # checkpoints (gap, speed) fp32 for ceil(300/4) = 75 segments dominate
+    assert ws >= 75 * 2 * 4 * 1000
     assert ws % 256 == 0
-    d.ckpt_every = 0
-    assert lib.idm_workspace_bytes(C.byref(d)) == 0
-    d.ckpt_every = 16
+    for bad in (0, 1, 3, 5, 16):
+        d.ckpt_every = bad
+        assert lib.idm_workspace_bytes(C.byref(d)) == 0
+    d.ckpt_every = 4
     d.n_vehicles = 0
     assert lib.idm_workspace_bytes(C.byref(d)) == 0
     assert lib.idm_max_lane_vehicles() >= 333  # NGSIM-shaped lanes (C3) fit one tile

@@ -2,7 +2,7 @@
 
 Sizes: C1 (every state, every step), C2 (all 10^5 vehicles, every step to 100 and step 300),
 ragged multi-tile layouts with edge cases, and the full C4 configuration bench.py times
-(2M vehicles, K = 300, k = 16) on 256 random lanes (lanes are independent units, so the
+(2M vehicles, K = 300, k = DEFAULT_CKPT) on 256 random lanes (lanes are independent units, so the
 oracle on the subset is exactly the oracle on the whole).
 """
 import numpy as np
@@ -10,6 +10,7 @@ import pytest
 import torch
 
 from paper_2412_16750_b200 import synth
+from paper_2412_16750_b200.idm import DEFAULT_CKPT
 from tests.parity_helpers import grad_check, oracle_truth_obs, state_violation
 
 pytestmark = pytest.mark.gpu
@@ -25,7 +26,7 @@ def idm():
     return I
 
 
-def run_gpu(idm, w, params, K, obs=None, kind="l1", ckpt_every=16, shared=False, backward=True):
+def run_gpu(idm, w, params, K, obs=None, kind="l1", ckpt_every=DEFAULT_CKPT, shared=False, backward=True):
     sim = idm.from_workload(w, params, max_steps=K, ckpt_every=ckpt_every, record_velocity=True,
                             shared_params=shared)
     sim.forward(K)
@@ -80,7 +81,7 @@ def test_forward_c2_all_vehicles(idm, oracle):
     assert state_violation(r["V"], V) <= 1.0
 
 
-@pytest.mark.parametrize("ckpt_every", [1, 7, 16, 48])
+@pytest.mark.parametrize("ckpt_every", [2, 4, 8])
 def test_forward_ragged_tiles_and_edge_lanes(idm, oracle, ckpt_every):
     """Ragged lanes across several tiles: single-vehicle lanes, a lane of exactly the tile
     capacity, near-capacity lanes, and a ragged tail; steps not a multiple of k."""
@@ -95,11 +96,11 @@ def test_forward_ragged_tiles_and_edge_lanes(idm, oracle, ckpt_every):
 
 
 def test_forward_c4_full_size_subset(idm, oracle):
-    """C4 in bench.py's launch configuration (2M vehicles in 20k lanes, K = 300, k = 16),
+    """C4 in bench.py's launch configuration (2M vehicles in 20k lanes, K = 300, default k),
     256 random lanes against the oracle on those lanes."""
     w = synth.make_workload("C4")
     prm = synth.init_params(w.n)
-    sim = idm.from_workload(w, prm, max_steps=w.K, ckpt_every=16)
+    sim = idm.from_workload(w, prm, max_steps=w.K, ckpt_every=DEFAULT_CKPT)
     sim.forward(w.K)
     torch.cuda.synchronize()
     lanes = np.sort(np.random.default_rng(0).choice(w.n_lanes, 256, replace=False))
@@ -132,7 +133,7 @@ def test_long_horizon_c3_kahan(idm, oracle):
     """C3-shaped (6 lanes x 333 vehicles, dt 0.1, 27,000 steps = 45 min): compensated
     displacement keeps positions within tolerance at 100 ... 27,000 steps."""
     w = synth.make_workload("C3")
-    r = run_gpu(idm, w, w.theta_true, w.K, ckpt_every=32)
+    r = run_gpu(idm, w, w.theta_true, w.K, ckpt_every=8)
     P, V = oracle.rollout(oracle.leader_from_lanes(w.lane_offsets), w.length, w.p0, w.v0,
                           w.theta_true, w.K, w.dt)
     for t in (100, 1000, 3000, 10000, 27000):
@@ -216,12 +217,12 @@ def test_gradients_shared_params(idm, oracle):
 
 
 def test_gradients_c4_subset(idm, oracle):
-    """Full C4 in bench configuration (K = 300, k = 16, L1, paper init); 64 random lanes vs
+    """Full C4 in bench configuration (K = 300, default k, L1, paper init); 64 random lanes vs
     the oracle with the sign protocol."""
     w = synth.make_workload("C4")
     obs = synth.kinematic_obs(w)
     prm = synth.init_params(w.n)
-    sim = idm.from_workload(w, prm, max_steps=w.K, ckpt_every=16)
+    sim = idm.from_workload(w, prm, max_steps=w.K, ckpt_every=DEFAULT_CKPT)
     sim.forward(w.K)
     sim.loss_grad(torch.as_tensor(obs, device="cuda"), kind="l1")
     sim.backward()
@@ -311,6 +312,68 @@ def test_step_host_matches_device_path(idm, oracle):
     assert torch.equal(a.params, b.params)
 
 
+# ------------------------------------------------------------------- fused iteration
+@pytest.mark.parametrize("kind", ["l1", "l2"])
+def test_fit_step_equals_separate_calls(idm, kind):
+    """idm_fit_step (fused fwd+Eq.4, bwd+Adam) computes exactly the separate-call sequence:
+    same dL/dP, gradients and parameters bit for bit, loss equal to rounding of the fp64 sum
+    order; ragged multi-tile lanes, missing (NaN) observations."""
+    cap = idm.load_library().idm_max_lane_vehicles()
+    w = synth.make_workload("C2", lane_sizes=[100] * 30 + [1, 7, cap, 3], K=90, seed=21)
+    obs = synth.kinematic_obs(w)
+    rng = np.random.default_rng(3)
+    obs[rng.random(obs.shape) < 0.2] = np.nan  # sparse: 20% missing
+    o = torch.as_tensor(obs, device="cuda")
+    a = idm.from_workload(w, None, max_steps=w.K)
+    b = idm.from_workload(w, None, max_steps=w.K)
+    for it in range(4):
+        a.forward(w.K)
+        La = a.loss_grad(o, kind=kind)
+        a.backward()
+        ga = a.grad_params.clone()
+        gta = a.grad_traj.clone()
+        a.adam_step(it)
+        Lb = b.fit_step(o, kind=kind, iteration=it, sync=True)
+        torch.cuda.synchronize()
+        assert abs(La - Lb) <= 1e-6 * abs(La)  # fused sums fp32 per segment, then fp64
+        assert torch.equal(gta, b.grad_traj)
+        assert torch.equal(ga, b.grad_params)
+        assert torch.equal(a.params, b.params)
+        assert torch.equal(a.adam_m, b.adam_m) and torch.equal(a.adam_v, b.adam_v)
+
+
+def test_fit_step_shared_params(idm):
+    w = synth.make_workload("C2", lane_sizes=[100] * 12 + [5], K=60, seed=5)
+    o = torch.as_tensor(synth.kinematic_obs(w), device="cuda")
+    prm = np.array([8.0, 1.7, 3.0, 1.4, 33.0, 4.0], np.float32)
+    a = idm.from_workload(w, prm, max_steps=w.K, shared_params=True)
+    b = idm.from_workload(w, prm, max_steps=w.K, shared_params=True)
+    for it in range(3):
+        a.forward(w.K)
+        La = a.loss_grad(o)
+        a.backward()
+        a.adam_step(it)
+        Lb = b.fit_step(o, iteration=it, sync=True)
+        assert abs(La - Lb) <= 1e-6 * abs(La)  # fused sums fp32 per segment, then fp64
+        assert torch.equal(a.params, b.params)
+
+
+def test_missing_observations_nan_equals_mask(idm):
+    """NaN observations are 'not observed' (R#12 sparse data): same loss and dL/dP as the mask."""
+    w = synth.make_workload("C2", lane_sizes=[100] * 10, K=50, seed=6)
+    obs = synth.kinematic_obs(w)
+    miss = np.random.default_rng(0).random(obs.shape) < 0.5
+    sim = idm.from_workload(w, None, max_steps=w.K)
+    sim.forward(w.K)
+    L1 = sim.loss_grad(torch.as_tensor(obs, device="cuda"),
+                       torch.as_tensor((~miss).astype(np.uint8), device="cuda"))
+    g1 = sim.grad_traj.clone()
+    obs2 = obs.copy()
+    obs2[miss] = np.nan
+    L2 = sim.loss_grad(torch.as_tensor(obs2, device="cuda"))
+    assert L1 == L2 and torch.equal(g1, sim.grad_traj)
+
+
 # ------------------------------------------------------------------- error paths
 def test_error_paths(idm):
     w = synth.make_workload("C1")
@@ -348,3 +411,6 @@ def test_launch_count(idm):
     sim.backward()
     sim.adam_step(0)
     assert sim.launch_count - n0 == 5  # fwd, loss, loss-reduce, bwd, adam
+    n1 = sim.launch_count
+    sim.fit_step(torch.zeros(w.K + 1, w.n, device="cuda"))
+    assert sim.launch_count - n1 == 3  # fwd+loss, loss-reduce, bwd+adam
