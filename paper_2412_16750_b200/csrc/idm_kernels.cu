@@ -14,6 +14,7 @@
 // memory (one barrier per step).  Checkpoint segments are KS steps (compile-time, unrolled);
 // step-major rows (observations, dL/dP) are prefetched a segment ahead into registers.
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "idm_device.cuh"
@@ -97,13 +98,17 @@ __device__ __forceinline__ void block_sum_to(double x, double* out) {
 
 // ------------------------------------------------------------------------------ NK1
 // One CTA = one lane tile.  All `steps` steps run in one launch, in checkpoint segments of KS
-// steps (compile-time, fully unrolled); per step one __syncthreads separates the speed
-// publication from the leader read (double-buffered exchange).
-// LOSS = 1 (L1) / 2 (L2): fused Eq. 4 for idm_fit_step -- the observation rows of the next
-// segment are prefetched into registers while the current one runs; each step evaluates Eq. 4
-// against the fresh positions and writes dL/dP instead of P.
-template <bool D4, bool KAHAN, bool RECV, int LOSS, int KS>
-__global__ void __launch_bounds__(kT, 4) fwd_kernel(FwdArgs a) {
+// steps (compile-time, fully unrolled; the K mod KS tail runs as one predicated segment); per
+// step one __syncthreads separates the speed publication from the leader read
+// (double-buffered exchange).  LOSS = 0: record P (idm_forward).  LOSS = 1 (L1) / 2 (L2):
+// fused Eq. 4 for idm_fit_step -- the observation rows of the next segment are prefetched into
+// registers while the current one runs; each step evaluates Eq. 4 against the fresh positions
+// and writes dL/dP instead of P.
+// CK = checkpoint interval (the backward's segment length); the forward's own prefetch
+// segment is KS = max(4, CK) steps, so CK | KS and checkpoints fall at static positions.
+template <bool D4, bool KAHAN, bool RECV, int LOSS, int CK>
+__global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? 3 : 4))) fwd_kernel(FwdArgs a) {
+    constexpr int KS = CK > 4 ? CK : 4;
     __shared__ float xv[2][kCap + 1];
     const int tid = threadIdx.x;
     const int64_t base = a.tile_start[blockIdx.x];
@@ -111,7 +116,7 @@ __global__ void __launch_bounds__(kT, 4) fwd_kernel(FwdArgs a) {
     const Consts k = a.k;
     const int64_t N = a.n;
     const int steps = a.steps;
-    const int nseg = (steps + KS - 1) / KS;
+    const int nfull = steps / KS, tail = steps - nfull * KS;
 
     float s[kVpt], v[kVpt], D[kVpt], cmp[kVpt], p0[kVpt];
     bool lead[kVpt], valid[kVpt];
@@ -139,105 +144,108 @@ __global__ void __launch_bounds__(kT, 4) fwd_kernel(FwdArgs a) {
     }
     if (tid == 0) { xv[0][kCap] = 0.f; xv[1][kCap] = 0.f; }
 
-    float* prow = a.traj ? a.traj + base + tid : nullptr;  // P row of the current step
-    float* grow = LOSS ? a.grad_traj + base + tid : nullptr;  // dL/dP row (LOSS)
+    // out: P row (LOSS = 0) or dL/dP row (LOSS) of the current step
+    float* orow = (LOSS ? a.grad_traj : a.traj) + base + tid;
     float* vrow = RECV ? a.vel_traj + base + tid : nullptr;
     float* cks = a.ckpt_s + base + tid;
     float* ckv = a.ckpt_v + base + tid;
     const float* obs = LOSS ? a.obs + base + tid : nullptr;
-    float onx[LOSS ? KS : 1][kVpt];  // observation rows of the next segment (registers)
-    float lseg = 0.f;                // loss of this thread's vehicles, this segment (fp32)
-    double lacc = 0.0;               // and across segments (fp64)
-    if (LOSS) {
+    float onx[KS][kVpt];  // LOSS: observation rows of the next segment (registers)
+    float lseg = 0.f;     // loss of this thread's vehicles in this segment (fp32)
+    double lacc = 0.0;    // and across segments (fp64)
+    // prefetch the observation rows 1 .. KS (predicated for a short rollout)
+    auto prefetch = [&](int row0, int nrows) {
+        const float* o = obs + (int64_t)row0 * N;
 #pragma unroll
-        for (int tt = 0; tt < KS; ++tt)
+        for (int tt = 0; tt < KS; ++tt, o += N)
 #pragma unroll
             for (int j = 0; j < kVpt; ++j)
-                onx[tt][j] = (valid[j] && tt + 1 <= steps)
-                                 ? __ldcs(obs + (int64_t)(tt + 1) * N + j * kT) : 0.f;
-    }
+                onx[tt][j] = (valid[j] && tt < nrows) ? __ldcs(o + j * kT) : 0.f;
+    };
+    if (LOSS) prefetch(1, min(KS, steps));
 #pragma unroll
     for (int j = 0; j < kVpt; ++j) {
         if (!valid[j]) continue;
-        if (prow) __stcs(prow + j * kT, p0[j]);
-        if (LOSS) __stcs(grow + j * kT, loss_term<LOSS - 1>(obs[j * kT], p0[j], true, lseg));
+        __stcs(orow + j * kT, LOSS ? loss_term<LOSS - 1>(obs[j * kT], p0[j], true, lseg) : p0[j]);
         if (RECV) vrow[j * kT] = v[j];
         cks[j * kT] = s[j];
         ckv[j * kT] = v[j];
     }
     int par = 0;
-    for (int seg = 0; seg < nseg; ++seg) {
-        const int t0 = seg * KS;
-        const int len = min(KS, steps - t0);
-        if (seg > 0) {  // checkpoint (gap, speed) at step t0 + finiteness check
-            cks += N;
-            ckv += N;
+    // one synchronous step of the whole tile; o = this step's observations (LOSS)
+    auto step = [&](const float (&o)[kVpt]) {
 #pragma unroll
-            for (int j = 0; j < kVpt; ++j) {
-                if (!valid[j]) continue;
-                cks[j * kT] = s[j];
-                ckv[j * kT] = v[j];
-                if (!(isfinite(s[j]) && isfinite(v[j]) && isfinite(D[j])))
-                    report_nonfinite(a.status, t0, base + j * kT + tid);
+        for (int j = 0; j < kVpt; ++j) xv[par][j * kT + tid] = v[j];
+        __syncthreads();
+        float vl[kVpt];
+#pragma unroll
+        for (int j = 0; j < kVpt; ++j) vl[j] = xv[par][j * kT + tid + 1];
+        par ^= 1;
+#pragma unroll
+        for (int j = 0; j < kVpt; ++j) {
+            const float vlj = lead[j] ? vl[j] : v[j];
+            if (KAHAN) {  // compensated displacement for long horizons (C3)
+                const float y = __fmaf_rn(k.dt, v[j], -cmp[j]);
+                const float tt2 = __fadd_rn(D[j], y);
+                cmp[j] = __fsub_rn(__fsub_rn(tt2, D[j]), y);
+                D[j] = tt2;
+            } else {
+                D[j] = __fmaf_rn(k.dt, v[j], D[j]);
+            }
+            fwd_step<D4>(s[j], v[j], vlj, lead[j], P[j], k);
+        }
+        orow += N;
+        if (RECV) vrow += N;
+#pragma unroll
+        for (int j = 0; j < kVpt; ++j) {
+            const float Pv = __fadd_rn(p0[j], D[j]);
+            const float out = LOSS ? loss_term<LOSS - 1>(o[j], Pv, valid[j], lseg) : Pv;
+            if (valid[j]) {
+                __stcs(orow + j * kT, out);
+                if (RECV) vrow[j * kT] = v[j];
             }
         }
-        float ocur[LOSS ? KS : 1][kVpt];
+    };
+    auto checkpoint = [&](int t0) {  // (gap, speed) at step t0 > 0 + finiteness check
+        cks += N;
+        ckv += N;
+#pragma unroll
+        for (int j = 0; j < kVpt; ++j) {
+            if (!valid[j]) continue;
+            cks[j * kT] = s[j];
+            ckv[j * kT] = v[j];
+            if (!(isfinite(s[j]) && isfinite(v[j]) && isfinite(D[j])))
+                report_nonfinite(a.status, t0, base + j * kT + tid);
+        }
+    };
+    for (int seg = 0; seg < nfull; ++seg) {
+        const int t0 = seg * KS;
+        float ocur[KS][kVpt];
         if (LOSS) {
 #pragma unroll
             for (int tt = 0; tt < KS; ++tt)
 #pragma unroll
                 for (int j = 0; j < kVpt; ++j) ocur[tt][j] = onx[tt][j];
-            const float* on = obs + (int64_t)(t0 + KS + 1) * N;
-#pragma unroll
-            for (int tt = 0; tt < KS; ++tt)
-#pragma unroll
-                for (int j = 0; j < kVpt; ++j)
-                    onx[tt][j] = (valid[j] && t0 + KS + 1 + tt <= steps)
-                                     ? __ldcs(on + (int64_t)tt * N + j * kT) : 0.f;
+            const int nxt = (seg + 1) * KS;  // the next segment observes rows nxt+1 ..
+            if (nxt < steps) prefetch(nxt + 1, min(KS, steps - nxt));
         }
 #pragma unroll
         for (int tt = 0; tt < KS; ++tt) {
-            if (tt < len) {  // CTA-uniform
-#pragma unroll
-                for (int j = 0; j < kVpt; ++j) xv[par][j * kT + tid] = v[j];
-                __syncthreads();
-                float vl[kVpt];
-#pragma unroll
-                for (int j = 0; j < kVpt; ++j) vl[j] = xv[par][j * kT + tid + 1];
-                par ^= 1;
-#pragma unroll
-                for (int j = 0; j < kVpt; ++j) {
-                    const float vlj = lead[j] ? vl[j] : v[j];
-                    if (KAHAN) {  // compensated displacement for long horizons (C3)
-                        const float y = __fmaf_rn(k.dt, v[j], -cmp[j]);
-                        const float tt2 = __fadd_rn(D[j], y);
-                        cmp[j] = __fsub_rn(__fsub_rn(tt2, D[j]), y);
-                        D[j] = tt2;
-                    } else {
-                        D[j] = __fmaf_rn(k.dt, v[j], D[j]);
-                    }
-                    fwd_step<D4>(s[j], v[j], vlj, lead[j], P[j], k);
-                }
-                if (prow) prow += N;
-                if (LOSS) grow += N;
-                if (RECV) vrow += N;
-#pragma unroll
-                for (int j = 0; j < kVpt; ++j) {
-                    const float Pv = __fadd_rn(p0[j], D[j]);
-                    if (LOSS) {
-                        const float g = loss_term<LOSS - 1>(ocur[tt][j], Pv, valid[j], lseg);
-                        if (valid[j]) __stcs(grow + j * kT, g);
-                    }
-                    if (valid[j]) {
-                        if (prow) __stcs(prow + j * kT, Pv);
-                        if (RECV) vrow[j * kT] = v[j];
-                    }
-                }
-            }
+            if (tt % CK == 0 && (tt > 0 || seg > 0)) checkpoint(t0 + tt);
+            step(ocur[tt]);
         }
         if (LOSS) {
             lacc += (double)lseg;
             lseg = 0.f;
+        }
+    }
+    if (tail > 0) {
+#pragma unroll
+        for (int tt = 0; tt < KS; ++tt) {
+            if (tt < tail) {  // CTA-uniform predicate
+                if (tt % CK == 0 && (tt > 0 || nfull > 0)) checkpoint(nfull * KS + tt);
+                step(onx[tt]);
+            }
         }
     }
 #pragma unroll
@@ -283,7 +291,7 @@ constexpr size_t bwd_smem_of() {
 }
 
 template <bool D4, bool SHARED, bool ADAM, int KS>
-__global__ void __launch_bounds__(kT) bwd_kernel(BwdArgs a) {
+__global__ void __launch_bounds__(kT, (KS <= 4 ? 3 : 1)) bwd_kernel(BwdArgs a) {
     constexpr int HS = kCap + 1;
     extern __shared__ __align__(16) float4 smem4[];
     float4* hR1 = smem4;                                                  // [KS][kCap]
@@ -331,34 +339,39 @@ __global__ void __launch_bounds__(kT) bwd_kernel(BwdArgs a) {
     if (tid == 0) { fx[0][0] = 0.f; fx[1][0] = 0.f; }  // never written again (slots id+1 >= 1)
 
     int par = 0;
-    for (int seg = nseg - 1; seg >= 0; --seg) {
+    // one checkpoint segment [t0, t0 + len); FULL (len == KS) drops every step predicate
+    auto run_segment = [&](const int seg, const int len, auto FULL) {
+        constexpr bool kFull = decltype(FULL)::value;
         const int t0 = seg * KS;
-        const int len = min(KS, steps - t0);
         // ---- this segment's dL/dP rows into registers (consumed by the reverse sweep)
         float gr_[KS][kVpt];
         {
             const float* g = a.grad_traj + (int64_t)t0 * N + base + tid;
 #pragma unroll
-            for (int tt = 0; tt < KS; ++tt)
+            for (int tt = 0; tt < KS; ++tt, g += N)
 #pragma unroll
                 for (int j = 0; j < kVpt; ++j)
-                    gr_[tt][j] = (valid[j] && tt < len) ? __ldcs(g + (int64_t)tt * N + j * kT)
-                                                        : 0.f;
+                    gr_[tt][j] = (valid[j] && (kFull || tt < len)) ? __ldcs(g + j * kT) : 0.f;
         }
         // ---- recompute the segment from its checkpoint; prefetch the next one
 #pragma unroll
         for (int j = 0; j < kVpt; ++j) {
             s[j] = cs[j];
             v[j] = cv[j];
-            if (seg > 0 && valid[j]) {
-                const int64_t off = (int64_t)(seg - 1) * N + base + j * kT + tid;
-                cs[j] = a.ckpt_s[off];
-                cv[j] = a.ckpt_v[off];
+        }
+        if (seg > 0) {
+            const int64_t off = (int64_t)(seg - 1) * N + base + tid;
+#pragma unroll
+            for (int j = 0; j < kVpt; ++j) {
+                if (valid[j]) {
+                    cs[j] = a.ckpt_s[off + j * kT];
+                    cv[j] = a.ckpt_v[off + j * kT];
+                }
             }
         }
 #pragma unroll
         for (int tt = 0; tt < KS; ++tt) {
-            if (tt < len) {  // CTA-uniform
+            if (kFull || tt < len) {  // CTA-uniform
                 float* hvr = hv + tt * HS + tid;
 #pragma unroll
                 for (int j = 0; j < kVpt; ++j) hvr[j * kT] = v[j];
@@ -373,7 +386,7 @@ __global__ void __launch_bounds__(kT) bwd_kernel(BwdArgs a) {
                     jac_record<D4>(c, s[j], v[j], lead[j], P[j], B[j], k, R1, R2);
                     hR1[tt * kCap + j * kT + tid] = R1;
                     hR2[tt * kCap + j * kT + tid] = R2;
-                    if (tt + 1 < len) advance(c, s[j], v[j], lead[j], k);
+                    if (tt + 1 < (kFull ? KS : len)) advance(c, s[j], v[j], lead[j], k);
                 }
             }
         }
@@ -381,7 +394,7 @@ __global__ void __launch_bounds__(kT) bwd_kernel(BwdArgs a) {
         //      the speed rows, all written before the last recompute barrier)
 #pragma unroll
         for (int tt = KS - 1; tt >= 0; --tt) {
-            if (tt < len) {  // CTA-uniform
+            if (kFull || tt < len) {  // CTA-uniform
                 const float* hvr = hv + tt * HS + tid;
                 float F[kVpt];
 #pragma unroll
@@ -403,7 +416,11 @@ __global__ void __launch_bounds__(kT) bwd_kernel(BwdArgs a) {
                 par ^= 1;
             }
         }
-    }
+    };
+    const int tail = steps - (nseg - 1) * KS;  // length of the last segment (1..KS)
+    int seg = nseg - 1;
+    if (tail < KS) run_segment(seg--, tail, std::false_type{});
+    for (; seg >= 0; --seg) run_segment(seg, KS, std::true_type{});
     // dL/dp0_i = lambda_D - lambda_s_i + lambda_s_{follower}; dL/dv0 = lambda_v
 #pragma unroll
     for (int j = 0; j < kVpt; ++j) fx[par][j * kT + tid + 1] = lead[j] ? ls[j] : 0.f;
