@@ -31,7 +31,7 @@ sys.path.insert(0, ROOT)
 from paper_2412_16750_b200 import parallel, synth  # noqa: E402
 
 LANE_VEH = 100
-WORKLOAD = "C4"
+WORKLOAD = "C4"  # the headline configuration (BASELINE.json configs[3]); --config selects others
 # Frozen algorithmic counts: thread-instructions (issue slots) per
 # vehicle-step that any implementation of the kernel's math must issue, and HBM bytes per
 # vehicle-step the method must move at k = 16, K = 300.
@@ -143,9 +143,11 @@ def make_rank_workload(rank: int, world: int, scaling: str):
 
 def cpu_baseline(lanes: int, K: int, seed: int = 99):
     """The fp64 oracle as it stands, single-threaded, one full step (rollout, Eq. 4 L1 loss,
-    adjoint, Adam) on `lanes` lanes of the C4 workload."""
+    adjoint, Adam) on the first `lanes` lanes of the configured workload."""
     from oracle import oracle as O
-    w = synth.make_workload(WORKLOAD, lane_sizes=[LANE_VEH] * lanes, K=K, seed=seed)
+    full = synth.make_workload(WORKLOAD, seed=seed)
+    w = synth.lane_subset(full, np.arange(min(lanes, full.n_lanes)))
+    w.K = K
     obs = synth.kinematic_obs(w).astype(np.float64)
     st = dict(leader=O.leader_from_lanes(w.lane_offsets), length=w.length, p0=w.p0, v0=w.v0,
               params=synth.init_params(w.n).astype(np.float64), m1=np.zeros((6, w.n)),
@@ -162,7 +164,7 @@ def run_reference(args, rank, world):
         return
     K = synth.CONFIGS[WORKLOAD]["K"]
     vs, t = cpu_baseline(4, K)
-    per_lane = t / 4
+    per_lane = t / min(4, synth.make_workload(WORKLOAD).n_lanes)
     budget = 150.0  # seconds for the whole --warmup + --steps run
     lanes = int(max(1, min(20000, budget / max(1, args.steps + args.warmup) / per_lane)))
     for _ in range(args.warmup):
@@ -173,7 +175,7 @@ def run_reference(args, rank, world):
         tot_vs += vs
         tot_t += t
     value = tot_vs / tot_t
-    sample = (f"{lanes} lanes x {LANE_VEH} vehicles x {K} steps of {WORKLOAD} per step "
+    sample = (f"first {lanes} lanes x {K} steps of {WORKLOAD} per step "
               f"(rollout + Eq.4 L1 + adjoint + Adam, fp64, single thread)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "vehicle-steps/s",
@@ -192,6 +194,23 @@ def run_reference(args, rank, world):
 METRIC = "vehicle-steps/s, forward+loss+backward+Adam (C4: 2M vehicles, K=300)"
 WORKLOAD_DESC = ("C4: 20,000 lanes x 100 vehicles = 2M, K=300 steps, dt=0.1 s, Eq.4 L1 loss "
                  "on dense noisy observations, per-vehicle IDM params, Adam")
+CONFIG_DESC = {
+    "C1": "C1: 1 lane x 10 vehicles, K=100, dt=0.1 s (latency-bound: one CTA)",
+    "C2": "C2: 1,000 lanes x 100 vehicles = 1e5, K=300, dt=0.1 s, filtering",
+    "C3": "C3: NGSIM-shaped, 6 lanes x 333 vehicles, K=27,000 (45 min at 0.1 s; latency-bound: "
+          "6 CTAs)",
+    "C4": WORKLOAD_DESC,
+    "C5": "C5: Waymo-shaped, 100k scenes x 4-12 lanes x 1+Bin(7,0.2) vehicles (~1.9M), K=10 "
+          "history fit",
+}
+
+
+def set_config(name: str):
+    global WORKLOAD, METRIC, WORKLOAD_DESC
+    WORKLOAD = name
+    WORKLOAD_DESC = CONFIG_DESC[name]
+    if name != "C4":
+        METRIC = "vehicle-steps/s, forward+loss+backward+Adam (" + name + ")"
 
 
 def run_ours(args, rank, world, local_rank):
@@ -317,7 +336,7 @@ def run_ours(args, rank, world, local_rank):
     if world == 1 and args.cpu_lanes > 0:
         vs_c, t_c = cpu_baseline(args.cpu_lanes, K)
         cpu = {"value": vs_c / t_c, "unit": "vehicle-steps/s", "cores": 1, "kind": "oracle",
-               "sample": f"{args.cpu_lanes} lanes x {LANE_VEH} vehicles x {K} steps of C4, one "
+               "sample": f"first {args.cpu_lanes} lanes x {K} steps of {WORKLOAD}, one "
                          f"full step (fp64 rollout + Eq.4 L1 + adjoint + Adam), 1 thread, "
                          f"{t_c:.1f} s"}
     line = {
@@ -356,6 +375,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=["C1", "C2", "C3", "C4", "C5"], default="C4",
+                    help="BASELINE.json configuration (C4 = the headline)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--ckpt", type=int, default=None, help="checkpoint interval k")
     ap.add_argument("--e2e", type=int, default=3, help="end-to-end steps (0 = skip)")
@@ -364,6 +385,7 @@ def main():
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the dominant kernel (from profiles/)")
     args = ap.parse_args()
+    set_config(args.config)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

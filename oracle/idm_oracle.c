@@ -447,3 +447,118 @@ void ora_project(int64_t n_par, double* params)
             if (*x > BOX_HI[k]) *x = BOX_HI[k];
         }
 }
+
+/* ----------------------------------------------------- virtual-leader mode */
+/* PAPER.md:208 ("We also optimize the lists of Delta p_k and Delta v_k for each simulation step
+   k, initializing them to 10 and 0"; SPEC rollout_virtual_leader): each
+   trajectory is fitted alone and its leader terms at step k are free variables dp[k][i],
+   dv[k][i] (step-major [K][n]) instead of the gather of Sec. III-A.  dp < eps_gap is clamped
+   with zero gradient (R#7). */
+int ora_rollout_vl(int64_t n, const double* p0, const double* v0, const double* params,
+                   int64_t n_par, int32_t K, double dt, double a_min, double eps_gap,
+                   const double* dp, const double* dv, double* P, double* V)
+{
+    memcpy(P, p0, sizeof(double) * (size_t)n);
+    memcpy(V, v0, sizeof(double) * (size_t)n);
+    for (int32_t t = 0; t < K; ++t) {
+        int bad = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            double th[NPAR];
+            load_theta(params, n_par, i, th);
+            double gap = dp[(int64_t)t * n + i];
+            double dpu = gap < eps_gap ? eps_gap : gap;
+            double p = P[(int64_t)t * n + i], v = V[(int64_t)t * n + i];
+            double a = ora_accel(th, v, dpu, dv[(int64_t)t * n + i], 1, dt, a_min);
+            P[(int64_t)(t + 1) * n + i] = p + dt * v;
+            V[(int64_t)(t + 1) * n + i] = v + dt * a;
+            if (!isfinite(P[(int64_t)(t + 1) * n + i]) || !isfinite(V[(int64_t)(t + 1) * n + i]))
+                bad = 1;
+        }
+        if (bad) return 1 + t;
+    }
+    return 0;
+}
+
+/* Reverse mode of ora_rollout_vl: lp^t = gP^t + lp^{t+1}; lv^t = lv^{t+1} + dt lp^{t+1} +
+   q da/dv (dv is a free variable here, so v enters only directly); g_dp[t] = q da/d(dp),
+   g_dv[t] = q da/d(dv), g_theta += q da/dtheta, q = dt lv^{t+1}.  Outputs as ora_backward plus
+   g_dp, g_dv [K][n]. */
+int ora_backward_vl(int64_t n, const double* params, int64_t n_par, int32_t K, double dt,
+                    double a_min, double eps_gap, const double* dp, const double* dv,
+                    const double* P, const double* V, const double* gP, double* g_params,
+                    double* g_abs, double* g_dp, double* g_dv, double* g_p0, double* g_v0)
+{
+    (void)P;
+    memset(g_params, 0, sizeof(double) * NPAR * (size_t)n_par);
+    if (g_abs) memset(g_abs, 0, sizeof(double) * NPAR * (size_t)n_par);
+    int rc = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        double lp = gP[(int64_t)K * n + i], lv = 0.0;
+        double th[NPAR];
+        load_theta(params, n_par, i, th);
+        int64_t j = (n_par == 1) ? 0 : i;
+        for (int32_t t = K - 1; t >= 0; --t) {
+            double gap = dp[(int64_t)t * n + i];
+            int clamped = gap < eps_gap;
+            double d[10];
+            ora_accel_partials(th, V[(int64_t)t * n + i], clamped ? eps_gap : gap,
+                               dv[(int64_t)t * n + i], 1, clamped, dt, a_min, d);
+            double q = dt * lv;
+            double lp_new = gP[(int64_t)t * n + i] + lp;
+            double lv_new = lv + dt * lp + q * d[1];
+            g_dp[(int64_t)t * n + i] = q * d[2];
+            g_dv[(int64_t)t * n + i] = q * d[3];
+            for (int k = 0; k < NPAR; ++k) {
+                double c = q * d[4 + k];
+                g_params[k * n_par + j] += c;
+                if (g_abs) g_abs[k * n_par + j] += fabs(c);
+            }
+            lp = lp_new;
+            lv = lv_new;
+        }
+        if (!isfinite(lp) || !isfinite(lv)) rc = 1;
+        if (g_p0) g_p0[i] = lp;
+        if (g_v0) g_v0[i] = lv;
+    }
+    return rc;
+}
+
+/* Forward mode (dual numbers) of ora_rollout_vl, independent of the hand adjoint: seeds for
+   p0, v0 [n], params [6][n_par], dp, dv [K][n] (each nullable).  Outputs P, dP [(K+1)][n]. */
+int ora_rollout_vl_tangent(int64_t n, const double* p0, const double* v0, const double* params,
+                           int64_t n_par, int32_t K, double dt, double a_min, double eps_gap,
+                           const double* dp, const double* dv, const double* tp0,
+                           const double* tv0, const double* tparams, const double* tdp,
+                           const double* tdv, double* P, double* dP)
+{
+    int rc = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        dual th[NPAR];
+        int64_t j = (n_par == 1) ? 0 : i;
+        for (int k = 0; k < NPAR; ++k) {
+            th[k].x = params[k * n_par + j];
+            th[k].d = tparams ? tparams[k * n_par + j] : 0.0;
+        }
+        dual p = {p0[i], tp0 ? tp0[i] : 0.0}, v = {v0[i], tv0 ? tv0[i] : 0.0};
+        P[i] = p.x;
+        dP[i] = p.d;
+        for (int32_t t = 0; t < K; ++t) {
+            int64_t e = (int64_t)t * n + i;
+            dual gap = {dp[e], tdp ? tdp[e] : 0.0};
+            if (gap.x < eps_gap) gap = dc(eps_gap); /* R#7: clamp, zero gradient */
+            dual ddv = {dv[e], tdv ? tdv[e] : 0.0};
+            dual a = dual_accel(th, v, gap, ddv, 1, dt, a_min);
+            dual pn = dadd(p, dmul(dc(dt), v));
+            dual vn = dadd(v, dmul(dc(dt), a));
+            p = pn;
+            v = vn;
+            P[(int64_t)(t + 1) * n + i] = p.x;
+            dP[(int64_t)(t + 1) * n + i] = p.d;
+            if (!isfinite(p.x) || !isfinite(v.x)) rc = 1 + t;
+        }
+    }
+    return rc;
+}
+
+/* Adam over unconstrained variables (the virtual-leader lists, PAPER.md:208 gives them no
+   box): ora_adam_step without projection -- provided for symmetry of the fit loop. */

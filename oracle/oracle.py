@@ -65,6 +65,14 @@ def lib():
         L.ora_rollout_tangent.restype = C.c_int
         L.ora_rollout_tangent.argtypes = [i64, _ip, _dp, _dp, _dp, _dp, i64, i32, d, d, d,
                                           vp, vp, vp, _dp, _dp]
+        L.ora_rollout_vl.restype = C.c_int
+        L.ora_rollout_vl.argtypes = [i64, _dp, _dp, _dp, i64, i32, d, d, d, _dp, _dp, _dp, _dp]
+        L.ora_backward_vl.restype = C.c_int
+        L.ora_backward_vl.argtypes = [i64, _dp, i64, i32, d, d, d, _dp, _dp, _dp, _dp, _dp, _dp,
+                                      vp, _dp, _dp, vp, vp]
+        L.ora_rollout_vl_tangent.restype = C.c_int
+        L.ora_rollout_vl_tangent.argtypes = [i64, _dp, _dp, _dp, i64, i32, d, d, d, _dp, _dp,
+                                             vp, vp, vp, vp, vp, _dp, _dp]
         L.ora_lr.restype = d
         L.ora_lr.argtypes = [i32, i32, d, d]
         L.ora_adam_step.restype = None
@@ -195,6 +203,59 @@ def rollout_tangent(leader, length, p0, v0, params, K, tp0=None, tv0=None, tpara
                                    _ptr(tpr), P, dP)
     if rc:
         raise OracleError(f"non-finite tangent at step {rc - 1}")
+    return P, dP
+
+
+# ---------------------------------------------------------- virtual-leader mode
+def rollout_vl(p0, v0, params, dp, dv, dt=0.1, a_min=-10.0, eps_gap=0.1):
+    """Virtual-leader rollout: dp, dv [K, n] free leader terms.  Returns P, V."""
+    dp = _f64(dp)
+    K, n = dp.shape
+    prm = _params2d(params, n)
+    P = np.empty((K + 1, n))
+    V = np.empty((K + 1, n))
+    rc = lib().ora_rollout_vl(n, _f64(p0), _f64(v0), prm, prm.shape[1], K, dt, a_min, eps_gap,
+                              dp, _f64(dv), P, V)
+    if rc:
+        raise OracleError(f"non-finite state at step {rc - 1}")
+    return P, V
+
+
+def backward_vl(params, dp, dv, P, V, gP, dt=0.1, a_min=-10.0, eps_gap=0.1):
+    """Adjoint of rollout_vl.  Returns dict(g_params, g_abs, g_dp, g_dv, g_p0, g_v0)."""
+    dp = _f64(dp)
+    K, n = dp.shape
+    prm = _params2d(params, n)
+    g = np.empty_like(prm)
+    ga = np.empty_like(prm)
+    gdp = np.empty((K, n))
+    gdv = np.empty((K, n))
+    gp0 = np.empty(n)
+    gv0 = np.empty(n)
+    rc = lib().ora_backward_vl(n, prm, prm.shape[1], K, dt, a_min, eps_gap, dp, _f64(dv),
+                               _f64(P), _f64(V), _f64(gP), g, _ptr(ga), gdp, gdv, _ptr(gp0),
+                               _ptr(gv0))
+    if rc:
+        raise OracleError("non-finite adjoint")
+    return {"g_params": g, "g_abs": ga, "g_dp": gdp, "g_dv": gdv, "g_p0": gp0, "g_v0": gv0}
+
+
+def rollout_vl_tangent(p0, v0, params, dp, dv, tp0=None, tv0=None, tparams=None, tdp=None,
+                       tdv=None, dt=0.1, a_min=-10.0, eps_gap=0.1):
+    dp = _f64(dp)
+    K, n = dp.shape
+    prm = _params2d(params, n)
+    arr = [None if x is None else _f64(x) for x in (tp0, tv0)]
+    tpr = None if tparams is None else np.ascontiguousarray(_f64(tparams).reshape(prm.shape))
+    tdp_ = None if tdp is None else _f64(tdp)
+    tdv_ = None if tdv is None else _f64(tdv)
+    P = np.empty((K + 1, n))
+    dP = np.empty((K + 1, n))
+    rc = lib().ora_rollout_vl_tangent(n, _f64(p0), _f64(v0), prm, prm.shape[1], K, dt, a_min,
+                                      eps_gap, dp, _f64(dv), _ptr(arr[0]), _ptr(arr[1]),
+                                      _ptr(tpr), _ptr(tdp_), _ptr(tdv_), P, dP)
+    if rc:
+        raise OracleError("non-finite tangent")
     return P, dP
 
 

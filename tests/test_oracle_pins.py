@@ -488,3 +488,66 @@ def test_fit_reduces_loss_c1(oracle):
     for k, (lo, hi) in enumerate([(5, 10), (0.1, 5), (1, 10), (0.1, 5), (20, 60)]):
         assert p[k].min() >= lo and p[k].max() <= hi
     assert np.all(p[5] == 4.0)
+
+
+# ------------------------------------------------------------ virtual-leader mode
+def test_virtual_leader_reproduces_lane_rollout(oracle):
+    """fed the (dp, dv) a real leader produced, the virtual-leader rollout of the
+    follower is the lane rollout's follower trajectory exactly (same arithmetic)."""
+    w = synth.make_workload("C1", lane_sizes=[2], K=120, seed=4)
+    h = oracle.leader_from_lanes(w.lane_offsets)
+    th = w.theta_true.astype(np.float64)
+    P, V = oracle.rollout(h, w.length, w.p0, w.v0, th, w.K)
+    dp = (P[:-1, 1] - P[:-1, 0] - w.length[1].astype(np.float64))[:, None]
+    dv = (V[:-1, 0] - V[:-1, 1])[:, None]
+    Pv, Vv = oracle.rollout_vl(w.p0[:1], w.v0[:1], th[:, :1], dp, dv)
+    assert np.array_equal(Pv[:, 0], P[:, 0]) and np.array_equal(Vv[:, 0], V[:, 0])
+
+
+def test_virtual_leader_far_gap_is_free_road(oracle):
+    """A virtual leader 1e9 m ahead at the same speed is the free road to rounding: the lone
+    vehicle at its closed-form equilibrium speed v_f stays there."""
+    th = np.array([7.0, 1.5, 2.0, 1.2, 30.0, 4.0])
+    vf = free_road_equilibrium_speed(th)
+    K = 200
+    P, V = oracle.rollout_vl([0.0], [vf], th, np.full((K, 1), 1e9), np.zeros((K, 1)))
+    assert np.max(np.abs(V - vf)) < 1e-9
+
+
+def test_virtual_leader_paper_init_accelerates_from_rest(oracle):
+    """dp = 10, dv = 0 (the paper's init) with default parameters and
+    v0 = 0: speeds never go negative and rise toward the equilibrium of the 10 m gap."""
+    K = 300
+    P, V = oracle.rollout_vl([0.0], [0.0], DEFAULT, np.full((K, 1), 10.0), np.zeros((K, 1)))
+    v = V[:, 0]
+    assert v.min() >= 0.0
+    i_peak = int(np.argmax(v))
+    assert np.all(np.diff(v[:i_peak + 1]) >= -1e-12) and v[i_peak] > 1.0
+
+
+@pytest.mark.parametrize("kind", ["l2", "l1"])
+def test_virtual_leader_adjoint_matches_dual_numbers(oracle, kind):
+    """Hand adjoint of the virtual-leader rollout vs forward-mode dual numbers, in the
+    directions of p0, v0, all parameters and every dp_k, dv_k (clamped steps included)."""
+    rng = np.random.default_rng(7)
+    n, K = 5, 60
+    th = np.stack([rng.uniform(5, 10, n), rng.uniform(0.5, 3, n), rng.uniform(1.5, 4, n),
+                   rng.uniform(0.8, 2, n), rng.uniform(25, 40, n), rng.uniform(3, 5, n)])
+    p0 = rng.uniform(0, 50, n)
+    v0 = rng.uniform(5, 20, n)
+    dp = rng.uniform(5, 40, (K, n))
+    dp[3, 1] = 0.05  # a clamped gap (R#7)
+    dv = rng.uniform(-3, 3, (K, n))
+    P, V = oracle.rollout_vl(p0, v0, th, dp, dv)
+    obs = P + rng.normal(0, 0.3, P.shape)
+    L, gP = oracle.loss(P, obs, kind)
+    g = oracle.backward_vl(th, dp, dv, P, V, gP)
+    assert g["g_dp"][3, 1] == 0.0
+    for _ in range(5):
+        d = [rng.standard_normal(x.shape) for x in (p0, v0, th, dp, dv)]
+        _, dP = oracle.rollout_vl_tangent(p0, v0, th, dp, dv, *d)
+        fwd = float(np.sum(gP * dP))
+        rev = float(np.sum(g["g_p0"] * d[0]) + np.sum(g["g_v0"] * d[1]) +
+                    np.sum(g["g_params"] * d[2]) + np.sum(g["g_dp"] * d[3]) +
+                    np.sum(g["g_dv"] * d[4]))
+        assert abs(fwd - rev) <= 1e-10 * max(1.0, abs(fwd)), (fwd, rev)
