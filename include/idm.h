@@ -53,6 +53,10 @@ typedef enum {
 
 typedef enum { IDM_PARAMS_PER_VEHICLE = 0, IDM_PARAMS_SHARED = 1 } idm_param_mode;
 typedef enum { IDM_LOSS_L1 = 0 /* Eq. 4 */, IDM_LOSS_L2 = 1 /* smooth variant */ } idm_loss_kind;
+typedef enum {
+    IDM_LEADER_LANE = 0,    /* leader = next vehicle ahead in the lane */
+    IDM_LEADER_VIRTUAL = 1  /* free per-step leader terms (Delta p_k, Delta v_k) */
+} idm_leader_mode;
 
 typedef struct {
     int64_t n_vehicles;          /* N >= 1 */
@@ -86,6 +90,18 @@ typedef struct {
     void* stream;                /* cudaStream_t (NULL = legacy default stream) */
     void* workspace;             /* device, >= idm_workspace_bytes(desc), 256-B aligned */
     size_t workspace_bytes;
+    /* Virtual-leader mode ("We also optimize the lists of Delta p_k and Delta v_k
+       for each simulation step k, initializing them to 10 and 0"): each vehicle is fitted alone
+       and its leader terms at step k are the free variables below (lanes are ignored; gaps
+       below eps_gap are clamped with zero gradient, R#7).  idm_backward writes their
+       gradients, idm_adam_step / idm_fit_step update them with the same Adam schedule (no
+       box).  Requires ckpt_every == 4. */
+    int32_t leader_mode;         /* idm_leader_mode (0 = lane leader) */
+    float* vl_dp;                /* [max_steps][N] Delta p_k */
+    float* vl_dv;                /* [max_steps][N] Delta v_k */
+    float* vl_grad;              /* [2][max_steps][N] dL/dDelta p_k, dL/dDelta v_k */
+    float* vl_adam_m;            /* [2][max_steps][N] Adam moments of the leaves (zeroed) */
+    float* vl_adam_v;            /* [2][max_steps][N] */
 } idm_desc;
 
 /* Bytes of device workspace idm_init needs for this descriptor (checkpoints of (gap, speed)

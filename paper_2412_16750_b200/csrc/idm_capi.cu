@@ -86,7 +86,9 @@ bool layout_for(const idm_desc* d, Layout* L) {
     L->ckpt_s = off; off += align256(sizeof(float) * (size_t)(nck * n));
     L->ckpt_v = off; off += align256(sizeof(float) * (size_t)(nck * n));
     L->loss_partials = off;
-    off += align256(sizeof(double) * (kLossBlocks > mt ? kLossBlocks : mt));
+    int64_t np_ = kLossBlocks > mt ? kLossBlocks : mt;
+    if (vl_blocks(n) > np_) np_ = vl_blocks(n);
+    off += align256(sizeof(double) * np_);
     L->loss_scalar = off; off += align256(sizeof(double));
     L->shared_partials = off; off += align256(sizeof(double) * 6 * (size_t)mt);
     L->status = off; off += align256(sizeof(unsigned long long));
@@ -169,6 +171,34 @@ int sync_status(idm_handle* h) {
     return IDM_OK;
 }
 
+VlArgs vl_args(idm_handle* h, int32_t steps) {
+    VlArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.pos0 = h->d.pos0;
+    a.vel0 = h->d.vel0;
+    a.params = h->d.params;
+    a.n = h->n;
+    a.n_par = h->n_par;
+    a.steps = steps;
+    a.max_steps = h->d.max_steps;
+    a.ckpt_every = h->d.ckpt_every;
+    a.k = consts_of(h->d);
+    a.vl_dp = h->d.vl_dp;
+    a.vl_dv = h->d.vl_dv;
+    a.vl_grad = h->d.vl_grad;
+    a.traj = h->d.traj;
+    a.grad_traj = h->d.grad_traj;
+    a.state_out = h->d.state_out;
+    a.ckpt_v = h->ckpt_v;
+    a.grad_params = h->d.grad_params;
+    a.grad_state0 = h->d.grad_state0;
+    a.loss_partials = h->loss_partials;
+    a.status = h->status;
+    return a;
+}
+
+bool is_vl(const idm_handle* h) { return h->d.leader_mode == IDM_LEADER_VIRTUAL; }
+
 }  // namespace
 
 extern "C" {
@@ -230,6 +260,17 @@ int idm_init(idm_handle** out, const idm_desc* d) {
         }
         if (d->param_mode != IDM_PARAMS_PER_VEHICLE && d->param_mode != IDM_PARAMS_SHARED) {
             bail(fail(h, IDM_EINVAL, "bad param_mode %d", d->param_mode));
+            break;
+        }
+        if (d->leader_mode != IDM_LEADER_LANE && d->leader_mode != IDM_LEADER_VIRTUAL) {
+            bail(fail(h, IDM_EINVAL, "bad leader_mode %d", d->leader_mode));
+            break;
+        }
+        if (d->leader_mode == IDM_LEADER_VIRTUAL &&
+            (!d->vl_dp || !d->vl_dv || !d->vl_grad || !d->vl_adam_m || !d->vl_adam_v ||
+             d->ckpt_every != 4 || d->param_mode != IDM_PARAMS_PER_VEHICLE)) {
+            bail(fail(h, IDM_EINVAL, "virtual-leader mode needs vl_dp, vl_dv, vl_grad, vl_adam_m, "
+                                     "vl_adam_v, ckpt_every == 4 and per-vehicle parameters"));
             break;
         }
         if (!d->lane_offsets || !d->pos0 || !d->vel0 || !d->length || !d->params ||
@@ -383,6 +424,17 @@ int idm_forward(idm_handle* h, int32_t steps) {
     if (!h) return IDM_EINVAL;
     if (steps < 1 || steps > h->d.max_steps)
         return fail(h, IDM_EINVAL, "steps=%d outside [1, max_steps=%d]", steps, h->d.max_steps);
+    if (is_vl(h)) {
+        VlArgs va = vl_args(h, steps);
+        {
+            TimedLaunch tl(h, IDM_K_FWD);
+            CK(h, launch_vl_fwd(va, h->delta4, 0, h->st));
+        }
+        h->launches++;
+        h->steps = steps;
+        h->stage = 1;
+        return IDM_OK;
+    }
     FwdArgs a;
     a.tile_start = h->tile_start;
     a.lead = h->lead;
@@ -461,6 +513,16 @@ int idm_loss_grad(idm_handle* h, const float* obs, const uint8_t* mask, int32_t 
 int idm_backward(idm_handle* h) {
     if (!h) return IDM_EINVAL;
     if (h->stage < 2) return fail(h, IDM_ESTATE, "idm_backward before idm_loss_grad");
+    if (is_vl(h)) {
+        VlArgs va = vl_args(h, h->steps);
+        {
+            TimedLaunch tl(h, IDM_K_BWD);
+            CK(h, launch_vl_bwd(va, h->delta4, false, h->st));
+        }
+        h->launches++;
+        h->stage = 3;
+        return IDM_OK;
+    }
     BwdArgs a;
     a.tile_start = h->tile_start;
     a.lead = h->lead;
@@ -524,6 +586,23 @@ AdamArgs make_adam(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, 
 
 extern "C" {
 
+}  // extern "C"
+
+namespace {
+// Adam over the virtual-leader leaves of the last `steps` rows (dp plane, dv plane).
+int adam_leaves(idm_handle* h, const AdamArgs& a) {
+    const int64_t kn = (int64_t)h->d.max_steps * h->n, n = (int64_t)h->steps * h->n;
+    TimedLaunch tl(h, IDM_K_ADAM);
+    CK(h, launch_adam_free(h->d.vl_dp, h->d.vl_grad, h->d.vl_adam_m, h->d.vl_adam_v, n, a, h->st));
+    CK(h, launch_adam_free(h->d.vl_dv, h->d.vl_grad + kn, h->d.vl_adam_m + kn,
+                           h->d.vl_adam_v + kn, n, a, h->st));
+    h->launches += 2;
+    return IDM_OK;
+}
+}  // namespace
+
+extern "C" {
+
 int idm_adam_step(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, float lr1) {
     if (!h) return IDM_EINVAL;
     if (h->stage < 3) return fail(h, IDM_ESTATE, "idm_adam_step before idm_backward");
@@ -535,6 +614,10 @@ int idm_adam_step(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, f
         CK(h, launch_adam(a, h->st));
     }
     h->launches++;
+    if (is_vl(h)) {
+        int s = adam_leaves(h, a);
+        if (s != IDM_OK) return s;
+    }
     h->stage = 0;  // parameters changed: a new forward is required
     return IDM_OK;
 }
@@ -552,6 +635,40 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
         return fail(h, IDM_EINVAL, "bad loss kind %d", kind);
     if (iter < 0 || total_iters < 1 || iter >= total_iters)
         return fail(h, IDM_EINVAL, "iter=%d outside [0, total_iters=%d)", iter, total_iters);
+    if (is_vl(h)) {
+        VlArgs va = vl_args(h, steps);
+        va.obs = obs;
+        va.adam = make_adam(h, iter, total_iters, lr0, lr1);
+        {
+            TimedLaunch tl(h, IDM_K_FWD);
+            CK(h, launch_vl_fwd(va, h->delta4, 1 + kind, h->st));
+        }
+        {
+            TimedLaunch tl(h, IDM_K_REDUCE);
+            CK(h, launch_reduce(h->loss_partials, vl_blocks(h->n), 1, h->loss_scalar, nullptr,
+                                h->st));
+        }
+        {
+            TimedLaunch tl(h, IDM_K_BWD);
+            CK(h, launch_vl_bwd(va, h->delta4, true, h->st));
+        }
+        h->launches += 3;
+        h->steps = steps;
+        int s = adam_leaves(h, va.adam);
+        if (s != IDM_OK) return s;
+        h->stage = 0;
+        if (loss_dev)
+            CK(h, cudaMemcpyAsync(loss_dev, h->loss_scalar, sizeof(double),
+                                  cudaMemcpyDeviceToDevice, h->st));
+        if (loss_host) {
+            CK(h, cudaMemcpyAsync(&h->pinned[0], h->loss_scalar, sizeof(double),
+                                  cudaMemcpyDeviceToHost, h->st));
+            int st2 = sync_status(h);
+            *loss_host = h->pinned[0];
+            if (st2 != IDM_OK) return st2;
+        }
+        return IDM_OK;
+    }
     // forward + Eq. 4 fused: dL/dP straight from the fresh positions, no P round trip
     FwdArgs f;
     f.tile_start = h->tile_start;

@@ -76,8 +76,20 @@ struct Core {
 // without a leader (R#8), gap clamped at eps (R#7).  Explicit _rn intrinsics: the forward
 // kernel and the backward recompute produce bitwise identical states.
 template <bool D4>
+__device__ __forceinline__ void core_dv(float s, float v, float dv, bool lead, const VehP& p,
+                                        const Consts& k, Core& c);
+
+template <bool D4>
 __device__ __forceinline__ void core(float s, float v, float vl, bool lead, const VehP& p,
                                      const Consts& k, Core& c) {
+    core_dv<D4>(s, v, __fsub_rn(v, vl), lead, p, k, c);  // Delta v = v_i - v_h
+}
+
+// The step core given the approach rate dv directly (virtual-leader mode, where
+// (Delta p_k, Delta v_k) are free variables; the lane path passes dv = v - v_h).
+template <bool D4>
+__device__ __forceinline__ void core_dv(float s, float v, float dv, bool lead, const VehP& p,
+                                        const Consts& k, Core& c) {
     c.x = __fmul_rn(v, p.ivt);
     c.x2 = __fmul_rn(c.x, c.x);
     if (D4) {
@@ -87,7 +99,7 @@ __device__ __forceinline__ void core(float s, float v, float vl, bool lead, cons
         c.lx = c.x > 0.f ? lg2(c.x) : 0.f;
         c.w = c.x > 0.f ? ex2(__fmul_rn(p.delta, c.lx)) : 0.f;
     }
-    c.dv = __fsub_rn(v, vl);                                   // Delta v = v_i - v_h
+    c.dv = dv;
     c.c12 = __fmaf_rn(c.dv, p.c2, p.T2);
     c.s_opt2 = __fmaf_rn(v, c.c12, p.sm2);                     // s_opt log2 e
     c.es = ex2(-fabsf(c.s_opt2));
@@ -209,6 +221,45 @@ __device__ __forceinline__ float bwd_from_record(float4 R1, float2 R2, float v, 
     g.S5 = fmaf(qa, w, g.S5);
     g.S6 = fmaf(qa, R2.y, g.S6);
     return F_out;
+}
+
+// Virtual-leader reverse step: at state v with free leader terms (dp, dv) the
+// local Jacobian is d a*/d v |_{dv} (dv is a leaf, so v enters only directly), d a*/d dp and
+// d a*/d dv = beta v c.  Consumes lambda^{t+1} = (lv, lD); writes q d a*/d dp and q d a*/d dv
+// (the leaf gradients of step t) and updates lv and the parameter accumulators.
+template <bool D4>
+__device__ __forceinline__ void bwd_vl(const Core& c, float dp, float v, const VehP& p,
+                                       const VehB& b, const Consts& k, float& lv, float lD,
+                                       GradAcc& g, float& gdp, float& gdv) {
+    const float rs = rcp(c.ones);
+    const float sig_s = c.s_opt2 >= 0.f ? rs : c.es * rs;
+    const float ra = rcp(c.onea);
+    const float eara = c.ea * ra;
+    const bool zpos = c.z2 >= 0.f;
+    const float sig_a = zpos ? ra : eara;
+    const float omsa = zpos ? eara : ra;
+    const float As = b.nam2ln2 * c.qr * c.idp;                  // d a_raw/d s*
+    const float beta = sig_a * As * sig_s;                      // d a*/d s_opt
+    const float xm1 = D4 ? c.x2 * c.x : (c.x > 0.f ? c.w * rcp(c.x) : 0.f);
+    // d a*/d v at fixed dv: free term + s_opt term (T + dv c) + a_lb branch (R#5)
+    float Jv = fmaf(beta * kLn2, c.c12, sig_a * b.ndamivt * xm1);
+    if (c.lb_act) Jv = fmaf(-omsa, k.inv_dt, Jv);
+    const float Js = dp >= k.eps ? -sig_a * As * c.qr * kLn2 : 0.f;  // R#7
+    const float q = k.dt * lv;
+    const float qa = q * sig_a;
+    const float qb = q * beta;
+    gdp = q * Js;
+    gdv = -qb * v * b.nc;                                       // d s_opt/d dv = v c
+    lv = fmaf(k.dt, lD, fmaf(q, Jv, lv));
+    const float lx = D4 ? (c.x > 0.f ? lg2(c.x) : 0.f) : c.lx;
+    g.S1 = fmaf(qa, fmaf(-kLn2Sq, c.inter2, c.t1), g.S1);
+    const float qbv = qb * v;
+    g.S2 = fmaf(qbv, c.dv, g.S2);
+    g.S3 += qb;
+    g.S4 += qbv;
+    const float qaw = qa * c.w;
+    g.S5 += qaw;
+    g.S6 = fmaf(qaw, lx, g.S6);
 }
 
 }  // namespace idm

@@ -67,6 +67,21 @@ struct BwdArgs {
     AdamArgs adam;  // fused Adam epilogue (ADAM variant)
 };
 
+// virtual-leader mode (idm_vl.cu)
+struct VlArgs {
+    const float *pos0, *vel0, *params;
+    int64_t n, n_par;
+    int steps, max_steps, ckpt_every;
+    Consts k;
+    const float *vl_dp, *vl_dv;
+    float *vl_grad;  // [2][max_steps][N]
+    float *traj, *grad_traj, *state_out, *ckpt_v, *grad_params, *grad_state0;
+    const float* obs;
+    double* loss_partials;
+    unsigned long long* status;
+    AdamArgs adam;
+};
+
 struct LossArgs {
     const float *traj, *obs;
     const uint8_t* mask;
@@ -87,6 +102,28 @@ cudaError_t launch_loss(const LossArgs& a, int nblocks, cudaStream_t st);
 cudaError_t launch_reduce(const double* partials, int64_t n, int width, double* out, float* out_f,
                           cudaStream_t st);
 cudaError_t launch_adam(const AdamArgs& a, cudaStream_t st);
+cudaError_t launch_vl_fwd(const VlArgs& a, bool delta4, int loss, cudaStream_t st);
+cudaError_t launch_vl_bwd(const VlArgs& a, bool delta4, bool adam, cudaStream_t st);
+cudaError_t launch_adam_free(float* x, const float* g, float* m, float* v, int64_t n,
+                             const AdamArgs& hp, cudaStream_t st);
+int64_t vl_blocks(int64_t n);
+
+// Adam (Kingma & Ba, bias-corrected) + box clamp of one scalar;
+// shared by adam_kernel and the fused backward epilogue so both paths agree bitwise.
+#ifdef __CUDACC__
+__device__ __forceinline__ void adam_update(const AdamArgs& a, int q, int64_t e, float g) {
+    const float m1 = a.m[e] * a.beta1 + (1.f - a.beta1) * g;
+    const float m2 = a.v[e] * a.beta2 + (1.f - a.beta2) * g * g;
+    a.m[e] = m1;
+    a.v[e] = m2;
+    const float denom = sqrtf(m2) / a.sqrt_bc2 + a.eps;
+    float x = a.x[e] - a.step_size * (m1 / denom);
+    if (q < 5) x = fminf(fmaxf(x, a.lo[q]), a.hi[q]);
+    a.x[e] = x;
+}
+
+#endif
+
 
 constexpr int kLossBlocks = 148 * 8;  // fixed => deterministic loss reduction
 

@@ -262,19 +262,6 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? 3 : 4))) fwd_kernel(
     if (LOSS) block_sum_to(lacc + (double)lseg, a.loss_partials);
 }
 
-// Adam (Kingma & Ba, bias-corrected) + box clamp of one scalar;
-// shared by adam_kernel and the fused backward epilogue so both paths agree bitwise.
-__device__ __forceinline__ void adam_update(const AdamArgs& a, int q, int64_t e, float g) {
-    const float m1 = a.m[e] * a.beta1 + (1.f - a.beta1) * g;
-    const float m2 = a.v[e] * a.beta2 + (1.f - a.beta2) * g * g;
-    a.m[e] = m1;
-    a.v[e] = m2;
-    const float denom = sqrtf(m2) / a.sqrt_bc2 + a.eps;
-    float x = a.x[e] - a.step_size * (m1 / denom);
-    if (q < 5) x = fminf(fmaxf(x, a.lo[q]), a.hi[q]);
-    a.x[e] = x;
-}
-
 // ------------------------------------------------------------------------------ NK3
 // Per CTA (lane tile), segments of KS steps (compile-time, unrolled) from last to first:
 //   recompute: reload the (gap, speed) checkpoint (prefetched one segment ahead) and re-run the

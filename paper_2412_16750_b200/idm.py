@@ -24,6 +24,8 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "idm.h")
 IDM_OK, IDM_EINVAL, IDM_ENUMERIC, IDM_ECUDA, IDM_ESTATE = range(5)
 STATUS_NAMES = {0: "IDM_OK", 1: "IDM_EINVAL", 2: "IDM_ENUMERIC", 3: "IDM_ECUDA", 4: "IDM_ESTATE"}
 PARAMS_PER_VEHICLE, PARAMS_SHARED = 0, 1
+LEADER_LANE, LEADER_VIRTUAL = 0, 1
+VL_INIT = (10.0, 0.0)  # initial (Delta p_k, Delta v_k)
 LOSS_KINDS = {"l1": 0, "l2": 1}
 PAPER_OPT_MASK = 0x1F  # the paper optimizes five parameters; delta frozen
 DEFAULT_CKPT = 4  # backward checkpoint interval k (tuned on B200)
@@ -59,6 +61,12 @@ class IdmDesc(C.Structure):
         ("stream", C.c_void_p),
         ("workspace", C.c_void_p),
         ("workspace_bytes", C.c_size_t),
+        ("leader_mode", C.c_int32),
+        ("vl_dp", C.c_void_p),
+        ("vl_dv", C.c_void_p),
+        ("vl_grad", C.c_void_p),
+        ("vl_adam_m", C.c_void_p),
+        ("vl_adam_v", C.c_void_p),
     ]
 
 
@@ -146,6 +154,7 @@ class IdmSim:
                  eps_gap: float = 0.1, shared_params: bool = False,
                  opt_mask: int = PAPER_OPT_MASK, record_velocity: bool = False,
                  stage_obs: bool = False, stage_mask: bool = False, state_out: bool = True,
+                 virtual_leader: bool = False, vl_dp=None, vl_dv=None,
                  device=None, stream: torch.cuda.Stream | None = None):
         L = load_library()
         if not torch.cuda.is_available():
@@ -181,6 +190,18 @@ class IdmSim:
             if stage_mask else None
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=dev)
         self.max_steps = max_steps
+        self.virtual_leader = virtual_leader
+        if virtual_leader:
+            # free per-step leader terms, paper init (10, 0) unless given
+            self.vl_dp = _dev(vl_dp, f32, dev).reshape(max_steps, n).contiguous() \
+                if vl_dp is not None else torch.full((max_steps, n), VL_INIT[0], dtype=f32,
+                                                     device=dev)
+            self.vl_dv = _dev(vl_dv, f32, dev).reshape(max_steps, n).contiguous() \
+                if vl_dv is not None else torch.full((max_steps, n), VL_INIT[1], dtype=f32,
+                                                     device=dev)
+            self.vl_grad = torch.zeros(2, max_steps, n, dtype=f32, device=dev)
+            self.vl_adam_m = torch.zeros(2, max_steps, n, dtype=f32, device=dev)
+            self.vl_adam_v = torch.zeros(2, max_steps, n, dtype=f32, device=dev)
         d = IdmDesc()
         d.n_vehicles = n
         d.n_lanes = self.n_lanes
@@ -207,6 +228,13 @@ class IdmSim:
         d.param_mode = PARAMS_SHARED if shared_params else PARAMS_PER_VEHICLE
         d.opt_mask = opt_mask
         d.stream = self.stream.cuda_stream
+        if virtual_leader:
+            d.leader_mode = LEADER_VIRTUAL
+            d.vl_dp = self.vl_dp.data_ptr()
+            d.vl_dv = self.vl_dv.data_ptr()
+            d.vl_grad = self.vl_grad.data_ptr()
+            d.vl_adam_m = self.vl_adam_m.data_ptr()
+            d.vl_adam_v = self.vl_adam_v.data_ptr()
         nbytes = L.idm_workspace_bytes(C.byref(d))
         if nbytes == 0:
             raise IdmError(IDM_EINVAL, "malformed descriptor")

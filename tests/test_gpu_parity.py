@@ -414,3 +414,68 @@ def test_launch_count(idm):
     n1 = sim.launch_count
     sim.fit_step(torch.zeros(w.K + 1, w.n, device="cuda"))
     assert sim.launch_count - n1 == 3  # fwd+loss, loss-reduce, bwd+adam
+
+
+# ------------------------------------------------------------- virtual-leader mode
+def _vl_case(n_lanes=40, K=90, seed=13):
+    """Independent trajectories (PAPER.md:208 fits each alone) with random leaf values."""
+    w = synth.make_workload("C2", lane_sizes=[1] * n_lanes, K=K, seed=seed)
+    rng = np.random.default_rng(seed)
+    dp = rng.uniform(6.0, 60.0, (K, w.n)).astype(np.float32)
+    dp[5, 3] = 0.05  # a clamped gap (R#7)
+    dv = rng.uniform(-3.0, 3.0, (K, w.n)).astype(np.float32)
+    return w, dp, dv
+
+
+def test_virtual_leader_forward_and_gradients(idm, oracle):
+    w, dp, dv = _vl_case()
+    prm = synth.init_params(w.n)
+    sim = idm.from_workload(w, prm, max_steps=w.K, ckpt_every=4, virtual_leader=True,
+                            vl_dp=dp, vl_dv=dv)
+    sim.forward(w.K)
+    P_o, V_o = oracle.rollout_vl(w.p0, w.v0, prm.astype(np.float64), dp, dv)
+    obs = (P_o + np.random.default_rng(1).normal(0, 0.3, P_o.shape)).astype(np.float32)
+    sim.loss_grad(torch.as_tensor(obs, device="cuda"), kind="l2")
+    sim.backward()
+    torch.cuda.synchronize()
+    assert state_violation(sim.traj.cpu().numpy(), P_o) <= 1.0
+    # the backward is linear in dL/dP: give the oracle the GPU's upstream gradient so the
+    # check isolates the adjoint (an L2 residual of 0.3 m makes dL/dP sensitive to the 1e-4
+    # relative position tolerance)
+    gP = sim.grad_traj.cpu().numpy().astype(np.float64)
+    g = oracle.backward_vl(prm.astype(np.float64), dp, dv, P_o, V_o, gP)
+    worst, _ = grad_check(sim.grad_params.cpu().numpy(), g["g_params"], g["g_abs"])
+    assert worst <= 1.0
+    vg = sim.vl_grad.cpu().numpy().astype(np.float64)
+    for got, ref in ((vg[0], g["g_dp"]), (vg[1], g["g_dv"])):
+        scale = np.abs(ref).max(axis=0, keepdims=True)  # per trajectory
+        assert np.all(np.abs(got - ref) <= 1e-3 * np.abs(ref) + 1e-3 * scale)
+    assert vg[0][5, 3] == 0.0  # clamped gap: zero gradient
+
+
+def test_virtual_leader_fit_step_equals_api_and_adam(idm, oracle):
+    """Fused and separate calls agree bitwise in virtual-leader mode; the leaves get the
+    paper's Adam schedule without a box (oracle Adam as reference)."""
+    w, dp, dv = _vl_case(n_lanes=700, K=60, seed=3)
+    obs = synth.kinematic_obs(w)
+    o = torch.as_tensor(obs, device="cuda")
+    a = idm.from_workload(w, None, max_steps=w.K, ckpt_every=4, virtual_leader=True)
+    b = idm.from_workload(w, None, max_steps=w.K, ckpt_every=4, virtual_leader=True)
+    x = a.vl_dp.cpu().numpy().astype(np.float64)
+    m1 = np.zeros_like(x)
+    m2 = np.zeros_like(x)
+    for it in range(3):
+        a.forward(w.K)
+        La = a.loss_grad(o, kind="l1")
+        a.backward()
+        torch.cuda.synchronize()
+        gdp = a.vl_grad[0].cpu().numpy().astype(np.float64)
+        a.adam_step(it)
+        Lb = b.fit_step(o, kind="l1", iteration=it, sync=True)
+        torch.cuda.synchronize()
+        assert abs(La - Lb) <= 1e-6 * abs(La)
+        assert torch.equal(a.params, b.params)
+        assert torch.equal(a.vl_dp, b.vl_dp) and torch.equal(a.vl_dv, b.vl_dv)
+        oracle.adam_step(x, gdp, m1, m2, it + 1, oracle.lr(it, 500, 0.1, 0.01))
+        assert np.allclose(a.vl_dp.cpu().numpy(), x, rtol=2e-6, atol=2e-6)
+        x = a.vl_dp.cpu().numpy().astype(np.float64)
