@@ -41,6 +41,19 @@ ISSUE_PER_CLK = 148 * 4 * 32  # SMs x schedulers x lanes (thread-instr / clk)
 
 def alg_bytes(K: int, k: int, path: str) -> dict:
     """Algorithmic HBM bytes per vehicle-step of each kernel."""
+    if path == "vl":  # virtual leader, fused: leaves dp, dv in fwd and bwd; leaf Adam in bwd
+        return {
+            "fwd": 8.0 + 4.0 + 4.0 + 4.0 / k + (4 * 2 + 24) / K,  # dp, dv, obs in; dL/dP out
+            # dp, dv, dL/dP, 2x(m, v) in; 2x(x, m, v) out; ckpt; params + Adam per vehicle
+            "bwd": 8.0 + 4.0 + 16.0 + 24.0 + 4.0 / k + (24 + 24 + 8 + 120) / K,
+        }
+    if path == "vl_api":
+        return {
+            "fwd": 8.0 + 4.0 + 4.0 / k + (4 * 2 + 24) / K,
+            "loss": 12.0,
+            "bwd": 8.0 + 4.0 + 8.0 + 4.0 / k + (24 + 24 + 8) / K,
+            "adam": 2 * 28.0 + 6 * 28.0 / K,
+        }
     if path == "api":
         return {
             "fwd": 4.0 + 8.0 / k + (4 * 4 + 24 + 1) / K,        # P record + (s,v) ckpt + loads
@@ -221,13 +234,20 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     w = make_rank_workload(rank, world, args.scaling)
-    K, k = w.K, args.ckpt or idm.DEFAULT_CKPT
+    vl = args.leader == "virtual"
+    K, k = w.K, (4 if vl else (args.ckpt or idm.DEFAULT_CKPT))
     # synthetic observations: truth rollout with theta_true (our forward) + N(0, 0.3^2)
     sim = idm.from_workload(w, w.theta_true, max_steps=K, ckpt_every=k, stage_obs=args.e2e > 0)
     sim.forward(K)
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     obs = sim.traj.clone()
     obs[1:].add_(torch.randn(obs[1:].shape, device=dev, generator=gen), alpha=0.3)
+    if vl:  # the paper's per-trajectory fit: free leader terms
+        sim.close()
+        del sim
+        torch.cuda.empty_cache()
+        sim = idm.from_workload(w, None, max_steps=K, ckpt_every=k, stage_obs=args.e2e > 0,
+                                virtual_leader=True)
     init = torch.as_tensor(synth.init_params(w.n), device=dev)
     stream = sim.stream
     vsteps = float(w.n) * K * world
@@ -236,6 +256,11 @@ def run_ours(args, rank, world, local_rank):
         sim.params.copy_(init)
         sim.adam_m.zero_()
         sim.adam_v.zero_()
+        if vl:
+            sim.vl_dp.fill_(idm.VL_INIT[0])
+            sim.vl_dv.fill_(idm.VL_INIT[1])
+            sim.vl_adam_m.zero_()
+            sim.vl_adam_v.zero_()
 
     def step_api(it):
         sim.forward(K)
@@ -311,17 +336,29 @@ def run_ours(args, rank, world, local_rank):
     head = fused
     kms = head["kernel_ms"]
     dom = max(kms, key=kms.get)
-    issue_peak = ISSUE_PER_CLK * sm_mhz_max * 1e6 / 1e12  # Tinstr/s
-    achieved = ALG_INSTR["bwd" if dom == "bwd" else "fwd"] * n_veh_steps / (kms[dom] * 1e-3) / 1e12
-    traffic = load_traffic().get(f"{dom}_kernel")
-    roofline = {"bound": "alu", "kernel": f"{dom}_kernel (fused path)", "achieved": achieved,
-                "peak": issue_peak, "unit": "Tinstr/s", "frac": achieved / issue_peak,
-                "traffic": traffic,
-                "basis": f"{ALG_INSTR[dom]:.0f} essential thread-instr per vehicle-step x "
-                         f"{n_veh_steps:.3g} vehicle-steps per launch / CUDA-event launch time; "
-                         f"peak = 148 SM x 4 issue/clk x 32 lanes x {sm_mhz_max:.0f} MHz "
-                         f"(MEASURED_PEAKS sm_max, {peak_src}); traffic = ncu dram bytes/launch "
-                         f"(profiles/traffic.json)"}
+    if vl:  # HBM-bound mode: roofline against the measured copy bandwidth
+        ab = alg_bytes(K, k, "vl")
+        achieved = ab[dom] * n_veh_steps / (kms[dom] * 1e-3) / 1e9
+        traffic = load_traffic().get(f"vl_{dom}_kernel")
+        roofline = {"bound": "hbm", "kernel": f"vl_{dom}_kernel (fused path)",
+                    "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s",
+                    "frac": achieved / hbm_gbs, "traffic": traffic,
+                    "basis": f"{ab[dom]:.2f} algorithmic bytes per vehicle-step x "
+                             f"{n_veh_steps:.3g} per launch / CUDA-event launch time; peak = "
+                             f"MEASURED_PEAKS hbm_gbs ({peak_src})"}
+    else:
+        issue_peak = ISSUE_PER_CLK * sm_mhz_max * 1e6 / 1e12  # Tinstr/s
+        achieved = ALG_INSTR["bwd" if dom == "bwd" else "fwd"] * n_veh_steps / \
+            (kms[dom] * 1e-3) / 1e12
+        traffic = load_traffic().get(f"{dom}_kernel")
+        roofline = {"bound": "alu", "kernel": f"{dom}_kernel (fused path)", "achieved": achieved,
+                    "peak": issue_peak, "unit": "Tinstr/s", "frac": achieved / issue_peak,
+                    "traffic": traffic,
+                    "basis": f"{ALG_INSTR[dom]:.0f} essential thread-instr per vehicle-step x "
+                             f"{n_veh_steps:.3g} vehicle-steps per launch / CUDA-event launch "
+                             f"time; peak = 148 SM x 4 issue/clk x 32 lanes x {sm_mhz_max:.0f} "
+                             f"MHz (MEASURED_PEAKS sm_max, {peak_src}); traffic = ncu dram "
+                             f"bytes/launch (profiles/traffic.json)"}
 
     def hbm_of(p, path):
         ab = alg_bytes(K, k, path)
@@ -344,7 +381,10 @@ def run_ours(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
         "higher_is_better": True, "scaling": args.scaling if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD_DESC, "vehicles_per_rank": w.n, "K": K,
+        "config": {"workload": WORKLOAD_DESC + ("; virtual-leader mode (PAPER.md:208): every "
+                                                "vehicle fitted alone with free per-step "
+                                                "(dp, dv) leaves" if vl else ""),
+                   "vehicles_per_rank": w.n, "K": K,
                    "ckpt_every": k, "path": "idm_fit_step (fused fwd+Eq.4 / bwd+Adam)",
                    "parallelism": f"lane-sharded x{world}",
                    "l2": "no flush: inputs larger than L2 (2.4 GB obs + 2.4 GB dL/dP per rank "
@@ -356,8 +396,8 @@ def run_ours(args, rank, world, local_rank):
         "api_path": {kk: api[kk] for kk in ("ms_per_step", "value", "kernel_ms",
                                             "launches_per_step")},
         "roofline": roofline,
-        "hbm": {"fused": hbm_of(fused, "fused"), "api": hbm_of(api, "api"),
-                "peak_source": peak_src},
+        "hbm": {"fused": hbm_of(fused, "vl" if vl else "fused"),
+                "api": hbm_of(api, "vl_api" if vl else "api"), "peak_source": peak_src},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(round(head["launches_per_step"] * args.steps)),
@@ -375,6 +415,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--leader", choices=["lane", "virtual"], default="lane",
+                    help="lane leader (default) or the paper's virtual-leader fit (PAPER.md:208)")
     ap.add_argument("--config", choices=["C1", "C2", "C3", "C4", "C5"], default="C4",
                     help="BASELINE.json configuration (C4 = the headline)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
@@ -386,6 +428,9 @@ def main():
                     help="ncu dram bytes per launch of the dominant kernel (from profiles/)")
     args = ap.parse_args()
     set_config(args.config)
+    if args.leader == "virtual":
+        global METRIC
+        METRIC = METRIC.replace("forward+loss+backward+Adam", "virtual-leader fit step")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

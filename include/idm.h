@@ -95,7 +95,8 @@ typedef struct {
        and its leader terms at step k are the free variables below (lanes are ignored; gaps
        below eps_gap are clamped with zero gradient, R#7).  idm_backward writes their
        gradients, idm_adam_step / idm_fit_step update them with the same Adam schedule (no
-       box).  Requires ckpt_every == 4. */
+       box; idm_fit_step applies it inside the backward sweep and does not write vl_grad).
+       Requires ckpt_every == 4. */
     int32_t leader_mode;         /* idm_leader_mode (0 = lane leader) */
     float* vl_dp;                /* [max_steps][N] Delta p_k */
     float* vl_dv;                /* [max_steps][N] Delta v_k */

@@ -186,6 +186,8 @@ VlArgs vl_args(idm_handle* h, int32_t steps) {
     a.vl_dp = h->d.vl_dp;
     a.vl_dv = h->d.vl_dv;
     a.vl_grad = h->d.vl_grad;
+    a.vl_adam_m = h->d.vl_adam_m;
+    a.vl_adam_v = h->d.vl_adam_v;
     a.traj = h->d.traj;
     a.grad_traj = h->d.grad_traj;
     a.state_out = h->d.state_out;
@@ -652,10 +654,8 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
             TimedLaunch tl(h, IDM_K_BWD);
             CK(h, launch_vl_bwd(va, h->delta4, true, h->st));
         }
-        h->launches += 3;
+        h->launches += 3;  // the leaves' Adam runs in the backward's reverse sweep
         h->steps = steps;
-        int s = adam_leaves(h, va.adam);
-        if (s != IDM_OK) return s;
         h->stage = 0;
         if (loss_dev)
             CK(h, cudaMemcpyAsync(loss_dev, h->loss_scalar, sizeof(double),

@@ -75,6 +75,7 @@ struct VlArgs {
     Consts k;
     const float *vl_dp, *vl_dv;
     float *vl_grad;  // [2][max_steps][N]
+    float *vl_adam_m, *vl_adam_v;  // [2][max_steps][N] (fused leaf Adam)
     float *traj, *grad_traj, *state_out, *ckpt_v, *grad_params, *grad_state0;
     const float* obs;
     double* loss_partials;

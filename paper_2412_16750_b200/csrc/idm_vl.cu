@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(kVT) vl_bwd_kernel(VlArgs a) {
     const int steps = a.steps;
     const int64_t base = (int64_t)blockIdx.x * kVB + tid;
     const Consts k = a.k;
+    const int64_t KN = (int64_t)a.max_steps * N;  // leaf plane stride
     float lv[kVV], lD[kVV];
     bool valid[kVV];
     VehP P[kVV];
@@ -191,12 +192,13 @@ __global__ void __launch_bounds__(kVT) vl_bwd_kernel(VlArgs a) {
         B[j] = make_vehb(r[0], r[1], r[4], r[5]);
         G[j] = GradAcc{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     }
-    const int64_t KN = (int64_t)a.max_steps * N;  // leaf-gradient plane stride
     const int nseg = (steps + KS - 1) / KS;
     for (int seg = nseg - 1; seg >= 0; --seg) {
         const int t0 = seg * KS;
         const int len = min(KS, steps - t0);
         float dp[KS][kVV], dv[KS][kVV], gr[KS][kVV], vt[KS][kVV];
+        // ADAM (fused iteration): the leaves' Adam moments of this segment, updated in place
+        float am[ADAM ? KS : 1][kVV][2], av[ADAM ? KS : 1][kVV][2];
 #pragma unroll
         for (int tt = 0; tt < KS; ++tt)
 #pragma unroll
@@ -206,6 +208,13 @@ __global__ void __launch_bounds__(kVT) vl_bwd_kernel(VlArgs a) {
                 dp[tt][j] = ok ? __ldcs(a.vl_dp + off) : 10.f;
                 dv[tt][j] = ok ? __ldcs(a.vl_dv + off) : 0.f;
                 gr[tt][j] = ok ? __ldcs(a.grad_traj + off) : 0.f;
+                if (ADAM) {
+#pragma unroll
+                    for (int pl = 0; pl < 2; ++pl) {
+                        am[tt][j][pl] = ok ? __ldcs(a.vl_adam_m + pl * KN + off) : 0.f;
+                        av[tt][j][pl] = ok ? __ldcs(a.vl_adam_v + pl * KN + off) : 0.f;
+                    }
+                }
             }
         // recompute the segment's speeds from its checkpoint (bit-identical to the forward)
 #pragma unroll
@@ -238,8 +247,27 @@ __global__ void __launch_bounds__(kVT) vl_bwd_kernel(VlArgs a) {
                                gdv);
                     lD[j] += gr[tt][j];  // lambda_P^t = g^t + lambda_P^{t+1}
                     if (valid[j]) {
-                        __stcs(a.vl_grad + off + j * kVT, gdp);
-                        __stcs(a.vl_grad + KN + off + j * kVT, gdv);
+                        if (ADAM) {  // Adam on the two leaves of step t, in place (no box)
+                            const float gg[2] = {gdp, gdv};
+                            float* xs[2] = {const_cast<float*>(a.vl_dp), const_cast<float*>(a.vl_dv)};
+                            const float x0[2] = {dp[tt][j], dv[tt][j]};
+#pragma unroll
+                            for (int pl = 0; pl < 2; ++pl) {
+                                const float m1 = am[tt][j][pl] * a.adam.beta1 +
+                                                 (1.f - a.adam.beta1) * gg[pl];
+                                const float m2 = av[tt][j][pl] * a.adam.beta2 +
+                                                 (1.f - a.adam.beta2) * gg[pl] * gg[pl];
+                                __stcs(a.vl_adam_m + pl * KN + off + j * kVT, m1);
+                                __stcs(a.vl_adam_v + pl * KN + off + j * kVT, m2);
+                                __stcs(xs[pl] + off + j * kVT,
+                                       x0[pl] - a.adam.step_size *
+                                                    (m1 / (sqrtf(m2) / a.adam.sqrt_bc2 +
+                                                           a.adam.eps)));
+                            }
+                        } else {
+                            __stcs(a.vl_grad + off + j * kVT, gdp);
+                            __stcs(a.vl_grad + KN + off + j * kVT, gdv);
+                        }
                     }
                 }
             }
