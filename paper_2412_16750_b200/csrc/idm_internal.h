@@ -123,6 +123,18 @@ __device__ __forceinline__ void adam_update(const AdamArgs& a, int q, int64_t e,
     a.x[e] = x;
 }
 
+
+// Adam on one unconstrained leaf (virtual-leader lists), explicit roundings so the separate
+// kernel and the fused backward produce the same bits.
+__device__ __forceinline__ float leaf_adam(float x, float g, float& m, float& v, float step_size,
+                                           float sqrt_bc2, float b1, float b2, float eps) {
+    const float m1 = __fmaf_rn(__fsub_rn(1.f, b1), g, __fmul_rn(m, b1));
+    const float m2 = __fmaf_rn(__fmul_rn(__fsub_rn(1.f, b2), g), g, __fmul_rn(v, b2));
+    m = m1;
+    v = m2;
+    const float denom = __fadd_rn(__fdiv_rn(__fsqrt_rn(m2), sqrt_bc2), eps);
+    return __fmaf_rn(-step_size, __fdiv_rn(m1, denom), x);
+}
 #endif
 
 

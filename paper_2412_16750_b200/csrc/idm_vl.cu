@@ -253,16 +253,13 @@ __global__ void __launch_bounds__(kVT) vl_bwd_kernel(VlArgs a) {
                             const float x0[2] = {dp[tt][j], dv[tt][j]};
 #pragma unroll
                             for (int pl = 0; pl < 2; ++pl) {
-                                const float m1 = am[tt][j][pl] * a.adam.beta1 +
-                                                 (1.f - a.adam.beta1) * gg[pl];
-                                const float m2 = av[tt][j][pl] * a.adam.beta2 +
-                                                 (1.f - a.adam.beta2) * gg[pl] * gg[pl];
-                                __stcs(a.vl_adam_m + pl * KN + off + j * kVT, m1);
-                                __stcs(a.vl_adam_v + pl * KN + off + j * kVT, m2);
-                                __stcs(xs[pl] + off + j * kVT,
-                                       x0[pl] - a.adam.step_size *
-                                                    (m1 / (sqrtf(m2) / a.adam.sqrt_bc2 +
-                                                           a.adam.eps)));
+                                float mm = am[tt][j][pl], vv = av[tt][j][pl];
+                                const float xn = leaf_adam(x0[pl], gg[pl], mm, vv,
+                                                           a.adam.step_size, a.adam.sqrt_bc2,
+                                                           a.adam.beta1, a.adam.beta2, a.adam.eps);
+                                __stcs(a.vl_adam_m + pl * KN + off + j * kVT, mm);
+                                __stcs(a.vl_adam_v + pl * KN + off + j * kVT, vv);
+                                __stcs(xs[pl] + off + j * kVT, xn);
                             }
                         } else {
                             __stcs(a.vl_grad + off + j * kVT, gdp);
@@ -308,12 +305,10 @@ __global__ void __launch_bounds__(256) adam_free_kernel(float* x, const float* g
                                                          float eps) {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
          e += (int64_t)gridDim.x * blockDim.x) {
-        const float gg = g[e];
-        const float m1 = m[e] * b1 + (1.f - b1) * gg;
-        const float m2 = v[e] * b2 + (1.f - b2) * gg * gg;
-        m[e] = m1;
-        v[e] = m2;
-        x[e] -= step_size * (m1 / (sqrtf(m2) / sqrt_bc2 + eps));
+        float mm = m[e], vv = v[e];
+        x[e] = leaf_adam(x[e], g[e], mm, vv, step_size, sqrt_bc2, b1, b2, eps);
+        m[e] = mm;
+        v[e] = vv;
     }
 }
 
