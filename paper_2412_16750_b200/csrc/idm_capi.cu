@@ -189,6 +189,7 @@ VlArgs vl_args(idm_handle* h, int32_t steps) {
     a.vl_adam_m = h->d.vl_adam_m;
     a.vl_adam_v = h->d.vl_adam_v;
     a.traj = h->d.traj;
+    a.vel_traj = h->d.vel_traj;
     a.grad_traj = h->d.grad_traj;
     a.state_out = h->d.state_out;
     a.ckpt_v = h->ckpt_v;

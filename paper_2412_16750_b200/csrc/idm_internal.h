@@ -77,6 +77,7 @@ struct VlArgs {
     float *vl_grad;  // [2][max_steps][N]
     float *vl_adam_m, *vl_adam_v;  // [2][max_steps][N] (fused leaf Adam)
     float *traj, *grad_traj, *state_out, *ckpt_v, *grad_params, *grad_state0;
+    float* vel_traj;  // nullable: record speeds
     const float* obs;
     double* loss_partials;
     unsigned long long* status;

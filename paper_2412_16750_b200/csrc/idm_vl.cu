@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(kVT) vl_fwd_kernel(VlArgs a) {
     }
     const Consts k = a.k;
     float* orow = (LOSS ? a.grad_traj : a.traj) + base;
+    float* vrow = (!LOSS && a.vel_traj) ? a.vel_traj + base : nullptr;
     float* ckv = a.ckpt_v + base;
     const float* dpr = a.vl_dp + base;
     const float* dvr = a.vl_dv + base;
@@ -97,6 +98,7 @@ __global__ void __launch_bounds__(kVT) vl_fwd_kernel(VlArgs a) {
         if (!valid[j]) continue;
         __stcs(orow + j * kVT,
                LOSS ? vl_loss_term(LOSS - 1, obs[j * kVT], p0[j], true, lseg) : p0[j]);
+        if (vrow) vrow[j * kVT] = v[j];
         ckv[j * kVT] = v[j];
     }
     const int nseg = (steps + KS - 1) / KS;
@@ -130,6 +132,7 @@ __global__ void __launch_bounds__(kVT) vl_fwd_kernel(VlArgs a) {
         for (int tt = 0; tt < KS; ++tt) {
             if (tt < len) {
                 orow += N;
+                if (vrow) vrow += N;
 #pragma unroll
                 for (int j = 0; j < kVV; ++j) {
                     D[j] = __fmaf_rn(k.dt, v[j], D[j]);
@@ -140,7 +143,10 @@ __global__ void __launch_bounds__(kVT) vl_fwd_kernel(VlArgs a) {
                     const float Pv = __fadd_rn(p0[j], D[j]);
                     const float out =
                         LOSS ? vl_loss_term(LOSS - 1, ob[tt][j], Pv, valid[j], lseg) : Pv;
-                    if (valid[j]) __stcs(orow + j * kVT, out);
+                    if (valid[j]) {
+                        __stcs(orow + j * kVT, out);
+                        if (vrow) vrow[j * kVT] = v[j];
+                    }
                 }
             }
         }

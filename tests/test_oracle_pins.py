@@ -551,3 +551,39 @@ def test_virtual_leader_adjoint_matches_dual_numbers(oracle, kind):
                     np.sum(g["g_params"] * d[2]) + np.sum(g["g_dp"] * d[3]) +
                     np.sum(g["g_dv"] * d[4]))
         assert abs(fwd - rev) <= 1e-10 * max(1.0, abs(fwd)), (fwd, rev)
+
+
+# ------------------------------------------------------- reconstruction bookkeeping
+def test_nearest_step_and_table1_worked_values():
+    """SPEC.md:300-302 (alignment), :421-441 (metrics) worked values."""
+    from oracle import tasks_oracle as T
+    assert T.nearest_step(0.34, 0.1) == 3
+    assert T.nearest_step(0.35, 0.1) == 4  # half-up tie
+    assert T.nearest_step(0.0, 0.7) == 0
+    assert T.nearest_step(2.5, 1.0) == 3 and T.nearest_step(2.49, 1.0) == 2
+    # exact fit -> 0 %; one data point off by 1 m on a 1000 m trajectory, 10 points -> 0.01 %
+    P = [[0.0], [100.0], [200.0], [300.0], [400.0], [500.0], [600.0], [700.0], [800.0],
+         [900.0], [1000.0]]
+    pts = {0: [(0.1 * k, P[k][0]) for k in range(1, 11)]}
+    assert T.positional_error_rate(P, pts, 0.1) == 0.0
+    pts[0][3] = (0.4, P[4][0] + 1.0)
+    assert abs(T.positional_error_rate(P, pts, 0.1) - 0.01) < 1e-12
+    assert T.acceleration_stats([0.0, 0.0]) == (0.0, 0.0)
+    assert T.acceleration_stats([1.0, -1.0]) == (1.0, 0.0)
+    assert T.acceleration_stats([0.0, 2.0]) == (1.0, 1.0)
+    assert T.implausible([66.0]) and not T.implausible([10.0]) and not T.implausible([3, -3])
+    L, g = T.loss_sparse([[0.0], [8.0]], [(0, 0.1, 10.0, 0.1)])
+    assert L == 2.0 and g == {(1, 0): -1.0}
+
+
+def test_product_alignment_agrees_with_oracle_alignment():
+    """The host-side alignment of the product (tasks.nearest_steps) against the decimal
+    half-up oracle on random and tie timestamps."""
+    from oracle import tasks_oracle as T
+    from paper_2412_16750_b200 import tasks
+    rng = np.random.default_rng(0)
+    for dt in (0.1, 1.0, 0.25):
+        Ts = list(np.round(rng.uniform(0, 300, 500), 3)) + [dt * (k + 0.5) for k in range(50)]
+        got = tasks.nearest_steps(Ts, dt)
+        exp = [T.nearest_step(float(t), dt) for t in Ts]
+        assert list(got) == exp
