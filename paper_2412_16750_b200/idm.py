@@ -167,9 +167,13 @@ class IdmSim:
         self.lane_offsets = _dev(lane_offsets, torch.int32, dev)
         self.n = n = int(self.lane_offsets[-1].item())
         self.n_lanes = int(self.lane_offsets.numel() - 1)
-        self.pos0 = _dev(pos0, f32, dev)
-        self.vel0 = _dev(vel0, f32, dev)
-        self.length = _dev(length, f32, dev)
+        self.pos0 = _dev(pos0, f32, dev).reshape(-1)
+        self.vel0 = _dev(vel0, f32, dev).reshape(-1)
+        self.length = _dev(length, f32, dev).reshape(-1)
+        for name, t in (("pos0", self.pos0), ("vel0", self.vel0), ("length", self.length)):
+            if t.numel() != n:
+                raise IdmError(IDM_EINVAL, f"{name} has {t.numel()} entries; lane_offsets "
+                                           f"describe {n} vehicles")
         n_par = 1 if shared_params else n
         if params is None:
             from .synth import init_params

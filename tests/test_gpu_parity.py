@@ -586,3 +586,92 @@ def test_reconstruction_dt1_virtual_leader_and_table1(idm, oracle):
     assert abs(m["pos_pct"] - pos) <= 1e-9 * max(pos, 1e-12)
     assert abs(m["acc_mean"] - am) <= 1e-9 * am and abs(m["acc_std"] - asd) <= 1e-9 * asd
     assert not TO.implausible(acc[np.abs(acc) > 10.0 + tasks.IMP_ATOL])
+
+
+# ------------------------------------------------------------------- more edge cases
+@pytest.mark.parametrize("fused", [False, True])
+def test_general_delta_and_delta_optimised(idm, oracle, fused):
+    """delta != 4 (the general x^delta = 2^(delta log2 x) kernels) and delta optimised by
+    Adam (opt_mask bit 5): gradients against the oracle, then one Adam step."""
+    w = synth.make_workload("C2", lane_sizes=[40] * 8 + [3, 1], K=70, seed=17)
+    obs = oracle_truth_obs(oracle, w)
+    prm = synth.init_params(w.n)
+    prm[5] = np.random.default_rng(0).uniform(2.5, 6.0, w.n).astype(np.float32)
+    sim = idm.from_workload(w, prm, max_steps=w.K, opt_mask=0x3F, record_velocity=True)
+    o = torch.as_tensor(obs, device="cuda")
+    if fused:
+        sim.fit_step(o, kind="l2", iteration=0)
+    else:
+        sim.forward(w.K)
+        sim.loss_grad(o, kind="l2")
+        sim.backward()
+    torch.cuda.synchronize()
+    h = oracle.leader_from_lanes(w.lane_offsets)
+    P, V = oracle.rollout(h, w.length, w.p0, w.v0, prm.astype(np.float64), w.K)
+    if not fused:
+        assert state_violation(sim.traj.cpu().numpy(), P) <= 1.0
+    g = oracle.backward(h, w.length, prm.astype(np.float64), P, V,
+                        sim.grad_traj[:w.K + 1].cpu().numpy().astype(np.float64))
+    worst, _ = grad_check(sim.grad_params.cpu().numpy(), g["g_params"], g["g_abs"])
+    assert worst <= 1.0
+    if not fused:
+        before = sim.params.clone()
+        sim.adam_step(0)
+        torch.cuda.synchronize()
+        assert not torch.equal(before[5], sim.params[5])  # delta moved
+
+
+def test_degenerate_starts(idm, oracle):
+    """Vehicles at rest, a queue behind a stopped leader with gaps below eps_gap (clamped,
+    R#7), and free-road heads: states, no backward motion, gradients."""
+    n = 8
+    off = np.array([0, 5, 6, 8], np.int32)
+    p0 = np.array([0.0, 4.6, 9.25, 13.9, 18.5, 0.0, 0.0, 30.0], np.float32)  # gaps ~0.05-0.1
+    v0 = np.array([12.0, 0.0, 0.0, 3.0, 0.0, 0.0, 25.0, 0.0], np.float32)
+    length = np.full(n, 4.5, np.float32)
+    K = 120
+    prm = synth.init_params(n)
+    sim = idm.IdmSim(off, p0, v0, length, prm, max_steps=K, record_velocity=True)
+    sim.forward(K)
+    h = oracle.leader_from_lanes(off)
+    P, V = oracle.rollout(h, length, p0, v0, prm.astype(np.float64), K)
+    obs = (P + 0.5).astype(np.float32)
+    sim.loss_grad(torch.as_tensor(obs, device="cuda"), kind="l2")
+    sim.backward()
+    torch.cuda.synchronize()
+    assert state_violation(sim.traj.cpu().numpy(), P) <= 1.0
+    assert state_violation(sim.vel_traj.cpu().numpy(), V) <= 1.0
+    assert sim.vel_traj.cpu().numpy().min() >= 0.0
+    g = oracle.backward(h, length, prm.astype(np.float64), P, V,
+                        sim.grad_traj.cpu().numpy().astype(np.float64))
+    worst, _ = grad_check(sim.grad_params.cpu().numpy(), g["g_params"], g["g_abs"])
+    assert worst <= 1.0
+
+
+def test_fused_long_horizon_kahan(idm, oracle):
+    """idm_fit_step beyond 2,000 steps (compensated displacement in the fused forward) equals
+    the separate calls bit for bit."""
+    w = synth.make_workload("C3", lane_sizes=[60, 60], K=2500, seed=3)
+    obs = torch.as_tensor(synth.kinematic_obs(w), device="cuda")
+    a = idm.from_workload(w, w.theta_true, max_steps=w.K)
+    b = idm.from_workload(w, w.theta_true, max_steps=w.K)
+    a.forward(w.K)
+    La = a.loss_grad(obs)
+    a.backward()
+    a.adam_step(0)
+    Lb = b.fit_step(obs, iteration=0, sync=True)
+    torch.cuda.synchronize()
+    assert abs(La - Lb) <= 1e-6 * La
+    assert torch.equal(a.params, b.params)
+
+
+def test_empty_and_malformed_inputs(idm):
+    with pytest.raises(idm.IdmError):  # N = 0
+        idm.IdmSim(np.array([0], np.int32), np.zeros(0), np.zeros(0), np.zeros(0),
+                   max_steps=10)
+    with pytest.raises(idm.IdmError):  # offsets not ending at N
+        idm.IdmSim(np.array([0, 3], np.int32), np.zeros(4), np.ones(4), np.full(4, 4.0),
+                   max_steps=10)
+    with pytest.raises(idm.IdmError):  # negative speed
+        idm.IdmSim(np.array([0, 2], np.int32), np.array([0.0, 30.0]), np.array([-1.0, 5.0]),
+                   np.full(2, 4.0), max_steps=10)
