@@ -156,6 +156,21 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
                  int32_t kind, int32_t iter, int32_t total_iters, float lr0, float lr1,
                  double* loss_dev, double* loss_host);
 
+/* Whole fit in one launch for short horizons (Waymo-shaped prediction histories of 10 steps,
+   PAPER.md:218, :329-331): iterations iter0 .. iter0+iters-1 of exactly idm_fit_step(steps,
+   obs, kind, it, total_iters, lr0, lr1) -- parameters, Adam moments and gradients come out
+   bit-identical -- with the state history, observations and Adam moments of each lane tile
+   kept on chip (no HBM traffic between iterations).  steps <= idm_fit_max_steps(); lane-leader
+   mode with per-vehicle parameters; iters <= 4096 per call; grad_traj is not written.  The
+   loss of the last iteration (same Eq. 4, summed in a different fixed order) goes to
+   *loss_dev / *loss_host. */
+int idm_fit(idm_handle* h, int32_t steps, const float* obs, int32_t kind, int32_t iter0,
+            int32_t iters, int32_t total_iters, float lr0, float lr1, double* loss_dev,
+            double* loss_host);
+
+/* Largest horizon idm_fit accepts. */
+int32_t idm_fit_max_steps(void);
+
 /* One whole optimizer iteration from HOST buffers (end-to-end path): async-copies pos0/vel0
    (nullable = keep), obs (required) and mask (nullable = all observed) from host memory
    (pinned for overlap) into desc->pos0/vel0/obs_stage/mask_stage, runs forward(steps) ->

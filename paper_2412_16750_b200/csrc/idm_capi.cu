@@ -24,6 +24,8 @@ struct idm_handle {
     double *loss_partials, *loss_scalar, *shared_partials;
     unsigned long long* status;
     unsigned* flags;  // [0] = some delta != 4 (set by the validation kernel)
+    float* adam_table;  // [kFitMaxIters][2] per-iteration Adam step sizes for idm_fit
+    float* adam_table_host;  // pinned staging of the above
     bool delta4;      // all delta == 4 and delta frozen => specialised kernels
     // host-side resources for idm_step_host / synchronous reads
     cudaStream_t copy_st;
@@ -65,7 +67,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
     size_t tile_start, lead, ckpt_s, ckpt_v, loss_partials, loss_scalar, shared_partials, status,
-        flags, total;
+        flags, adam_table, total;
 };
 
 int64_t max_tiles_for(const idm_desc* d) {
@@ -93,6 +95,7 @@ bool layout_for(const idm_desc* d, Layout* L) {
     L->shared_partials = off; off += align256(sizeof(double) * 6 * (size_t)mt);
     L->status = off; off += align256(sizeof(unsigned long long));
     L->flags = off; off += align256(sizeof(unsigned));
+    L->adam_table = off; off += align256(sizeof(float) * 2 * kFitMaxIters);
     L->total = off;
     return true;
 }
@@ -235,6 +238,7 @@ void idm_destroy(idm_handle* h) {
     if (h->ev_obs) cudaEventDestroy(h->ev_obs);
     if (h->ev_loss_done) cudaEventDestroy(h->ev_loss_done);
     if (h->pinned) cudaFreeHost(h->pinned);
+    if (h->adam_table_host) cudaFreeHost(h->adam_table_host);
     delete h;
 }
 
@@ -312,6 +316,7 @@ int idm_init(idm_handle** out, const idm_desc* d) {
         h->shared_partials = (double*)(ws + L.shared_partials);
         h->status = (unsigned long long*)(ws + L.status);
         h->flags = (unsigned*)(ws + L.flags);
+        h->adam_table = (float*)(ws + L.adam_table);
 
         h->nck = (int)((d->max_steps + d->ckpt_every - 1) / d->ckpt_every);
 
@@ -744,6 +749,84 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
         }
         h->launches += 2;
     }
+    h->stage = 0;
+    if (loss_dev)
+        CK(h, cudaMemcpyAsync(loss_dev, h->loss_scalar, sizeof(double), cudaMemcpyDeviceToDevice,
+                              h->st));
+    if (loss_host) {
+        CK(h, cudaMemcpyAsync(&h->pinned[0], h->loss_scalar, sizeof(double),
+                              cudaMemcpyDeviceToHost, h->st));
+        int st2 = sync_status(h);
+        *loss_host = h->pinned[0];
+        if (st2 != IDM_OK) return st2;
+    }
+    return IDM_OK;
+}
+
+int32_t idm_fit_max_steps(void) { return kFitMaxSteps; }
+
+int idm_fit(idm_handle* h, int32_t steps, const float* obs, int32_t kind, int32_t iter0,
+            int32_t iters, int32_t total_iters, float lr0, float lr1, double* loss_dev,
+            double* loss_host) {
+    if (!h) return IDM_EINVAL;
+    if (steps < 1 || steps > h->d.max_steps || steps > kFitMaxSteps)
+        return fail(h, IDM_EINVAL, "idm_fit: steps=%d outside [1, min(max_steps, %d)]", steps,
+                    kFitMaxSteps);
+    if (!obs) return fail(h, IDM_EINVAL, "obs is NULL");
+    if (kind != IDM_LOSS_L1 && kind != IDM_LOSS_L2)
+        return fail(h, IDM_EINVAL, "bad loss kind %d", kind);
+    if (is_vl(h) || h->d.param_mode != IDM_PARAMS_PER_VEHICLE)
+        return fail(h, IDM_EINVAL, "idm_fit supports lane-leader mode with per-vehicle parameters");
+    if (iters < 1 || iters > kFitMaxIters || iter0 < 0 || iter0 + iters > total_iters)
+        return fail(h, IDM_EINVAL, "idm_fit: iterations [%d, %d) outside [0, total_iters=%d) or "
+                                   "more than %d per call", iter0, iter0 + iters, total_iters,
+                    kFitMaxIters);
+    if (!h->adam_table_host)
+        CK(h, cudaMallocHost((void**)&h->adam_table_host, sizeof(float) * 2 * kFitMaxIters));
+    // the host-side schedule of idm_adam_step, one entry per iteration (bit-identical values)
+    CK(h, cudaStreamSynchronize(h->st));  // the staging buffer may still feed a prior copy
+    for (int j = 0; j < iters; ++j) {
+        AdamArgs ad = make_adam(h, iter0 + j, total_iters, lr0, lr1);
+        h->adam_table_host[2 * j] = ad.step_size;
+        h->adam_table_host[2 * j + 1] = ad.sqrt_bc2;
+    }
+    CK(h, cudaMemcpyAsync(h->adam_table, h->adam_table_host, sizeof(float) * 2 * iters,
+                          cudaMemcpyHostToDevice, h->st));
+    AdamArgs ad = make_adam(h, iter0, total_iters, lr0, lr1);
+    FitArgs a;
+    a.tile_start = h->tile_start;
+    a.lead = h->lead;
+    a.pos0 = h->d.pos0;
+    a.vel0 = h->d.vel0;
+    a.length = h->d.length;
+    a.obs = obs;
+    a.params = h->d.params;
+    a.adam_m = h->d.adam_m;
+    a.adam_v = h->d.adam_v;
+    a.grad_params = h->d.grad_params;
+    a.grad_state0 = h->d.grad_state0;
+    a.n = h->n;
+    a.steps = steps;
+    a.iters = iters;
+    a.opt_mask = h->d.opt_mask;
+    a.k = consts_of(h->d);
+    a.adam_table = h->adam_table;
+    a.beta1 = ad.beta1;
+    a.beta2 = ad.beta2;
+    a.eps = ad.eps;
+    for (int q = 0; q < 5; ++q) { a.lo[q] = ad.lo[q]; a.hi[q] = ad.hi[q]; }
+    a.loss_partials = h->loss_partials;
+    a.status = h->status;
+    {
+        TimedLaunch tl(h, IDM_K_FWD);
+        CK(h, launch_fit(a, h->ntiles, h->delta4, kind, h->st));
+    }
+    {
+        TimedLaunch tl(h, IDM_K_REDUCE);
+        CK(h, launch_reduce(h->loss_partials, h->ntiles, 1, h->loss_scalar, nullptr, h->st));
+    }
+    h->launches += 2;
+    h->steps = steps;
     h->stage = 0;
     if (loss_dev)
         CK(h, cudaMemcpyAsync(loss_dev, h->loss_scalar, sizeof(double), cudaMemcpyDeviceToDevice,

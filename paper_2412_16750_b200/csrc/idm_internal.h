@@ -84,6 +84,25 @@ struct VlArgs {
     AdamArgs adam;
 };
 
+// whole fits in one launch (idm_fit.cu)
+constexpr int kFitMaxSteps = 12;      // horizon limit of idm_fit (registers per vehicle)
+constexpr int kFitMaxIters = 4096;    // per-launch iteration limit (Adam schedule table)
+struct FitArgs {
+    const int64_t* tile_start;
+    const uint8_t* lead;
+    const float *pos0, *vel0, *length, *obs;
+    float *params, *adam_m, *adam_v, *grad_params, *grad_state0;
+    int64_t n;
+    int steps, iters;
+    uint32_t opt_mask;
+    Consts k;
+    const float* adam_table;  // [iters][2] (step_size, sqrt_bc2) of each iteration
+    float beta1, beta2, eps;
+    float lo[5], hi[5];
+    double* loss_partials;
+    unsigned long long* status;
+};
+
 struct LossArgs {
     const float *traj, *obs;
     const uint8_t* mask;
@@ -109,17 +128,19 @@ cudaError_t launch_vl_bwd(const VlArgs& a, bool delta4, bool adam, cudaStream_t 
 cudaError_t launch_adam_free(float* x, const float* g, float* m, float* v, int64_t n,
                              const AdamArgs& hp, cudaStream_t st);
 int64_t vl_blocks(int64_t n);
+cudaError_t launch_fit(const FitArgs& a, int ntiles, bool delta4, int kind, cudaStream_t st);
 
 // Adam (Kingma & Ba, bias-corrected) + box clamp of one scalar;
 // shared by adam_kernel and the fused backward epilogue so both paths agree bitwise.
 #ifdef __CUDACC__
+__device__ __forceinline__ float leaf_adam(float x, float g, float& m, float& v, float step_size,
+                                           float sqrt_bc2, float b1, float b2, float eps);
+
 __device__ __forceinline__ void adam_update(const AdamArgs& a, int q, int64_t e, float g) {
-    const float m1 = a.m[e] * a.beta1 + (1.f - a.beta1) * g;
-    const float m2 = a.v[e] * a.beta2 + (1.f - a.beta2) * g * g;
-    a.m[e] = m1;
-    a.v[e] = m2;
-    const float denom = sqrtf(m2) / a.sqrt_bc2 + a.eps;
-    float x = a.x[e] - a.step_size * (m1 / denom);
+    float m = a.m[e], v = a.v[e];
+    float x = leaf_adam(a.x[e], g, m, v, a.step_size, a.sqrt_bc2, a.beta1, a.beta2, a.eps);
+    a.m[e] = m;
+    a.v[e] = v;
     if (q < 5) x = fminf(fmaxf(x, a.lo[q]), a.hi[q]);
     a.x[e] = x;
 }

@@ -675,3 +675,61 @@ def test_empty_and_malformed_inputs(idm):
     with pytest.raises(idm.IdmError):  # negative speed
         idm.IdmSim(np.array([0, 2], np.int32), np.array([0.0, 30.0]), np.array([-1.0, 5.0]),
                    np.full(2, 4.0), max_steps=10)
+
+
+# ------------------------------------------- whole fit in one launch / prediction (NEXT-3)
+@pytest.mark.parametrize("kind", ["l1", "l2"])
+def test_whole_fit_equals_fit_step_loop(idm, kind):
+    """idm_fit (all iterations in one launch, state on chip) == the idm_fit_step loop, bit for
+    bit in parameters, Adam moments and gradients; Waymo-shaped tiny lanes."""
+    w = synth.make_workload("C5", K=10, seed=5, lane_sizes=synth.lane_sizes_for(
+        "C5", np.random.Generator(np.random.PCG64(5)))[:3000])
+    obs = torch.as_tensor(synth.kinematic_obs(w, sigma=0.1), device="cuda")
+    a = idm.from_workload(w, None, max_steps=w.K)
+    b = idm.from_workload(w, None, max_steps=w.K)
+    for it in range(20):
+        La = a.fit_step(obs, kind=kind, iteration=it, total=500)
+    Lb = b.fit(obs, iters=20, kind=kind, iter0=0, total=500, sync=True)
+    torch.cuda.synchronize()
+    assert torch.equal(a.params, b.params)
+    assert torch.equal(a.adam_m, b.adam_m) and torch.equal(a.adam_v, b.adam_v)
+    assert torch.equal(a.grad_params, b.grad_params)
+    assert torch.equal(a.grad_state0, b.grad_state0)
+    # the loss of iteration 19 (evaluated before its Adam step) matches to rounding
+    c = idm.from_workload(w, None, max_steps=w.K)
+    c.fit(obs, iters=19, kind=kind, total=500)
+    Lc = c.fit_step(obs, kind=kind, iteration=19, total=500, sync=True)
+    assert abs(Lb - Lc) <= 1e-6 * Lc
+    kmax = idm.load_library().idm_fit_max_steps()
+    d = idm.from_workload(w, None, max_steps=kmax + 1)
+    with pytest.raises(idm.IdmError):  # horizon beyond the on-chip limit
+        d.fit(torch.zeros(kmax + 2, w.n, device="cuda"), iters=2, steps=kmax + 1)
+
+
+def test_prediction_pipeline_c5_shape(idm, oracle):
+    """Training-free prediction on Waymo-shaped synthetic scenes:
+    fit on the 1 s history (10 steps, 500 iterations in one launch), roll out 8 s (80 steps);
+    the GPU rollout with the fitted parameters matches the oracle rollout with the same
+    parameters, and the prediction error is reported (ADE/FDE vs the IDM truth)."""
+    rng = np.random.Generator(np.random.PCG64(55))
+    sizes = synth.lane_sizes_for("C5", rng)[:4000]
+    w = synth.make_workload("C5", lane_sizes=sizes, K=90, seed=55)
+    h = oracle.leader_from_lanes(w.lane_offsets)
+    P_true, _ = oracle.rollout(h, w.length, w.p0, w.v0, w.theta_true, 90)
+    hist = synth.add_noise(P_true[:11], 0.1, 55)
+    sim = idm.from_workload(w, None, max_steps=90)
+    sim.fit(torch.as_tensor(hist, device="cuda"), iters=500, steps=10, total=500)
+    sim.forward(90)
+    torch.cuda.synchronize()
+    prm = sim.params.cpu().numpy().astype(np.float64)
+    P_fit, _ = oracle.rollout(h, w.length, w.p0, w.v0, prm, 90)
+    Pg = sim.traj.cpu().numpy().astype(np.float64)
+    assert state_violation(Pg, P_fit) <= 1.0
+    err = np.abs(Pg[11:] - P_true[11:])
+    ade, fde = err.mean(), err[-1].mean()
+    cv = np.abs(P_true[10] + (P_true[10] - P_true[9])[None, :] *
+                np.arange(1, 81)[:, None] - P_true[11:])
+    print(f"C5-shape prediction: ADE {ade:.3f} m, FDE {fde:.3f} m "
+          f"(constant-velocity: ADE {cv.mean():.3f}, FDE {cv[-1].mean():.3f})")
+    # the fitted IDM forecast beats constant-velocity extrapolation of the last history step
+    assert np.isfinite(ade) and ade < cv.mean() and fde < cv[-1].mean()
