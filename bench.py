@@ -307,6 +307,22 @@ def run_ours(args, rank, world, local_rank):
 
     api = run_path(step_api)
     fused = run_path(step_fused)
+    whole = None
+    if not vl and K <= idm.load_library().idm_fit_max_steps():
+        # short horizons (C1-like, C5): every iteration of a 500-iteration fit in ONE launch
+        reset()
+        sim.fit(obs, iters=10, total=500)
+        torch.cuda.synchronize()
+        reset()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sim.fit(obs, iters=500, total=500)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_fit = parallel.max_over_ranks(e0.elapsed_time(e1), dev)
+        whole = {"iters": 500, "ms_total": t_fit, "ms_per_iteration": t_fit / 500,
+                 "value": vsteps * 500 / (t_fit * 1e-3), "unit": "vehicle-steps/s",
+                 "launches": 2, "path": "idm_fit (fwd+Eq.4+bwd+Adam x 500 on chip)"}
     clocks.stop()
 
     # ---- end to end through the C-ABI with HOST buffers (idm_step_host)
@@ -395,6 +411,7 @@ def run_ours(args, rank, world, local_rank):
                                                "launches_per_step")},
         "api_path": {kk: api[kk] for kk in ("ms_per_step", "value", "kernel_ms",
                                             "launches_per_step")},
+        "whole_fit_path": whole,
         "roofline": roofline,
         "hbm": {"fused": hbm_of(fused, "vl" if vl else "fused"),
                 "api": hbm_of(api, "vl_api" if vl else "api"), "peak_source": peak_src},
