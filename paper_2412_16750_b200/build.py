@@ -39,12 +39,16 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Build libidm.so (or a variant at `out` with extra -D defines, for tuning sweeps)."""
+    lib = out or LIB
+    if out is None and not force and not _stale():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, "-shared", "-Xlinker", "--exclude-libs,ALL",
-           "-I", os.path.join(ROOT, "include"), *sources(), "-o", tmp, "-lcudart_static"]
+    tmp = lib + f".tmp{os.getpid()}"
+    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-shared", "-Xlinker",
+           "--exclude-libs,ALL", "-I", os.path.join(ROOT, "include"), *sources(), "-o", tmp,
+           "-lcudart_static"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:
@@ -54,8 +58,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

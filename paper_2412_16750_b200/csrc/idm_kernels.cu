@@ -278,7 +278,10 @@ constexpr size_t bwd_smem_of() {
 }
 
 template <bool D4, bool SHARED, bool ADAM, int KS>
-__global__ void __launch_bounds__(kT, (KS <= 4 ? 3 : 1)) bwd_kernel(BwdArgs a) {
+#ifndef IDM_BWD_MINB
+#define IDM_BWD_MINB 3  // CTAs per SM the backward is register-budgeted for (80 registers)
+#endif
+__global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(BwdArgs a) {
     constexpr int HS = kCap + 1;
     extern __shared__ __align__(16) float4 smem4[];
     float4* hR1 = smem4;                                                  // [KS][kCap]

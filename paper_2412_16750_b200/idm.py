@@ -90,7 +90,7 @@ def load_library(path: str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    path = path or LIB_PATH
+    path = path or os.environ.get("IDM_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise ImportError(f"{path} not found: build it with `python -m paper_2412_16750_b200.build`"
                           " (there is no CPU fallback)")
