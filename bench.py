@@ -178,7 +178,7 @@ def run_reference(args, rank, world):
     K = synth.CONFIGS[WORKLOAD]["K"]
     vs, t = cpu_baseline(4, K)
     per_lane = t / min(4, synth.make_workload(WORKLOAD).n_lanes)
-    budget = 150.0  # seconds for the whole --warmup + --steps run
+    budget = args.ref_budget  # seconds for the whole --warmup + --steps run
     lanes = int(max(1, min(20000, budget / max(1, args.steps + args.warmup) / per_lane)))
     for _ in range(args.warmup):
         cpu_baseline(lanes, K)
@@ -231,7 +231,7 @@ def run_ours(args, rank, world, local_rank):
 
     from paper_2412_16750_b200 import idm
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", local_rank % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     w = make_rank_workload(rank, world, args.scaling)
     vl = args.leader == "virtual"
@@ -432,6 +432,11 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="collective backend for N > 1 (gloo only to exercise the multi-rank "
+                         "host path on fewer GPUs than ranks)")
+    ap.add_argument("--ref-budget", type=float, default=150.0,
+                    help="seconds of oracle work for --impl reference")
     ap.add_argument("--leader", choices=["lane", "virtual"], default="lane",
                     help="lane leader (default) or the paper's virtual-leader fit (PAPER.md:208)")
     ap.add_argument("--config", choices=["C1", "C2", "C3", "C4", "C5"], default="C4",
@@ -459,8 +464,12 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dev = torch.device("cuda", local_rank % torch.cuda.device_count())
+        torch.cuda.set_device(dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # host-logic check of the multi-rank path on fewer GPUs than ranks
+            dist.init_process_group("gloo")
     try:
         run_ours(args, rank, world, local_rank)
     finally:
