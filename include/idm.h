@@ -105,8 +105,10 @@ typedef struct {
     float* vl_adam_v;            /* [2][max_steps][N] */
 } idm_desc;
 
-/* Bytes of device workspace idm_init needs for this descriptor (checkpoints of (gap, speed)
-   every ckpt_every steps, the lane-tile plan, leader flags, reduction partials, status word).
+/* Bytes of device workspace idm_init needs for this descriptor: the lane-mode state history
+   (every vehicle's speed at every step and (gap, displacement) every ckpt_every steps, in a
+   tile-local layout sized for the worst-case tile count, about 2 (max_steps + 1) N floats),
+   the lane-tile plan, leader flags, reduction partials, status word.
    Returns 0 if the descriptor is malformed. */
 size_t idm_workspace_bytes(const idm_desc* d);
 
@@ -133,7 +135,7 @@ int idm_forward(idm_handle* h, int32_t steps);
 int idm_loss_grad(idm_handle* h, const float* obs, const uint8_t* mask, int32_t kind,
                   double* loss_dev, double* loss_host);
 
-/* Reverse-mode adjoint of the last idm_forward through grad_traj: recomputes each checkpoint
+/* Reverse-mode adjoint of the last idm_forward through grad_traj: rebuilds each checkpoint
    segment on chip and sweeps it backwards.  Writes grad_params (per vehicle, or in shared
    mode the sum over this process's vehicles -- the caller all-reduces across ranks) and
    grad_state0.  No atomics: fixed-order reductions, bitwise deterministic. */
@@ -146,10 +148,13 @@ int idm_backward(idm_handle* h);
 int idm_adam_step(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, float lr1);
 
 /* One whole optimizer iteration, fused: exactly forward(steps) -> loss_grad(obs, kind) ->
-   backward -> adam_step(iter, ...) (same arithmetic, same parameters bit for bit), in three
-   launches: the forward kernel evaluates Eq. 4 against each fresh position row and writes dL/dP
-   (traj is NOT written), a fixed-order reduction of the loss, and the backward kernel whose
-   epilogue applies Adam + box clamp per vehicle (shared mode: + reduce + Adam launches).
+   backward -> adam_step(iter, ...) (same arithmetic; grad_params, grad_state0, Adam moments and
+   parameters bit for bit), in three launches when ckpt_every == 4: the forward kernel sums
+   Eq. 4 against each fresh position row (writing only the internal state history), a
+   fixed-order reduction of the loss, and the backward kernel, which re-derives dL/dP from obs
+   and the rebuilt positions and whose epilogue applies Adam + box clamp per vehicle (shared
+   mode: + reduce + Adam launches).  traj and grad_traj are NOT written on this path; with any
+   other ckpt_every the defining sequence runs as is (and writes them).
    obs: device [(steps+1)][N]; missing observations are NaN (mask must be NULL).  Loss to
    *loss_dev / *loss_host as in idm_loss_grad. */
 int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* mask,

@@ -20,7 +20,8 @@ struct idm_handle {
     // workspace carve-outs
     int64_t* tile_start;
     uint8_t* lead;
-    float *ckpt_s, *ckpt_v;
+    float *vt, *ckt, *ckpt_v;     // lane-mode state history (tile-local), VL speed checkpoints
+    int64_t vt_stride, ck_stride;
     double *loss_partials, *loss_scalar, *shared_partials;
     unsigned long long* status;
     unsigned* flags;  // [0] = some delta != 4 (set by the validation kernel)
@@ -66,8 +67,9 @@ int fail(idm_handle* h, int code, const char* fmt, ...) {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-    size_t tile_start, lead, ckpt_s, ckpt_v, loss_partials, loss_scalar, shared_partials, status,
+    size_t tile_start, lead, vt, ckt, ckpt_v, loss_partials, loss_scalar, shared_partials, status,
         flags, adam_table, total;
+    int64_t vt_stride, ck_stride;  // floats per tile
 };
 
 int64_t max_tiles_for(const idm_desc* d) {
@@ -85,7 +87,14 @@ bool layout_for(const idm_desc* d, Layout* L) {
     size_t off = 0;
     L->tile_start = off; off += align256(sizeof(int64_t) * (mt + 1));
     L->lead = off; off += align256((size_t)n);
-    L->ckpt_s = off; off += align256(sizeof(float) * (size_t)(nck * n));
+    // lane mode: tile-local state history (idm_internal.h); sized for the worst-case tile
+    // count (the plan is built at idm_init), +64 floats so the leader read of a tile's last
+    // slot stays in bounds
+    L->vt_stride = (int64_t)(d->max_steps + 1) * kCap;
+    L->ck_stride = nck * kCkRows * kCap;
+    L->vt = off; off += align256(sizeof(float) * ((size_t)(mt * L->vt_stride) + 64));
+    L->ckt = off; off += align256(sizeof(float) * (size_t)(mt * L->ck_stride));
+    // virtual-leader mode: speed checkpoints every 4 steps
     L->ckpt_v = off; off += align256(sizeof(float) * (size_t)(nck * n));
     L->loss_partials = off;
     int64_t np_ = kLossBlocks > mt ? kLossBlocks : mt;
@@ -109,6 +118,7 @@ Consts consts_of(const idm_desc& d) {
     k.dt_ln2 = (float)((double)d.dt * 0.6931471805599453);
     k.a_min2 = (float)((double)d.a_min * 1.4426950408889634);
     k.ninv_dt2 = (float)(-1.4426950408889634 / (double)d.dt);
+    k.dt_amin = d.dt * d.a_min;  // fp32 product, as the device would round it
     return k;
 }
 
@@ -309,7 +319,10 @@ int idm_init(idm_handle** out, const idm_desc* d) {
         char* ws = (char*)d->workspace;
         h->tile_start = (int64_t*)(ws + L.tile_start);
         h->lead = (uint8_t*)(ws + L.lead);
-        h->ckpt_s = (float*)(ws + L.ckpt_s);
+        h->vt = (float*)(ws + L.vt);
+        h->ckt = (float*)(ws + L.ckt);
+        h->vt_stride = L.vt_stride;
+        h->ck_stride = L.ck_stride;
         h->ckpt_v = (float*)(ws + L.ckpt_v);
         h->loss_partials = (double*)(ws + L.loss_partials);
         h->loss_scalar = (double*)(ws + L.loss_scalar);
@@ -428,6 +441,53 @@ int idm_init(idm_handle** out, const idm_desc* d) {
     return IDM_OK;
 }
 
+namespace {
+FwdArgs fwd_args(idm_handle* h, int32_t steps) {
+    FwdArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.tile_start = h->tile_start;
+    a.lead = h->lead;
+    a.pos0 = h->d.pos0;
+    a.vel0 = h->d.vel0;
+    a.length = h->d.length;
+    a.params = h->d.params;
+    a.n = h->n;
+    a.n_par = h->n_par;
+    a.state_out = h->d.state_out;
+    a.vt = h->vt;
+    a.ckt = h->ckt;
+    a.vt_stride = h->vt_stride;
+    a.ck_stride = h->ck_stride;
+    a.steps = steps;
+    a.ckpt_every = h->d.ckpt_every;
+    a.k = consts_of(h->d);
+    a.status = h->status;
+    return a;
+}
+
+BwdArgs bwd_args(idm_handle* h, int32_t steps) {
+    BwdArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.tile_start = h->tile_start;
+    a.lead = h->lead;
+    a.params = h->d.params;
+    a.n = h->n;
+    a.n_par = h->n_par;
+    a.vt = h->vt;
+    a.ckt = h->ckt;
+    a.vt_stride = h->vt_stride;
+    a.ck_stride = h->ck_stride;
+    a.grad_params = h->d.grad_params;
+    a.grad_state0 = h->d.grad_state0;
+    a.shared_partials = h->shared_partials;
+    a.steps = steps;
+    a.ckpt_every = h->d.ckpt_every;
+    a.k = consts_of(h->d);
+    a.status = h->status;
+    return a;
+}
+}  // namespace
+
 int idm_forward(idm_handle* h, int32_t steps) {
     if (!h) return IDM_EINVAL;
     if (steps < 1 || steps > h->d.max_steps)
@@ -443,28 +503,9 @@ int idm_forward(idm_handle* h, int32_t steps) {
         h->stage = 1;
         return IDM_OK;
     }
-    FwdArgs a;
-    a.tile_start = h->tile_start;
-    a.lead = h->lead;
-    a.pos0 = h->d.pos0;
-    a.vel0 = h->d.vel0;
-    a.length = h->d.length;
-    a.params = h->d.params;
-    a.n = h->n;
-    a.n_par = h->n_par;
+    FwdArgs a = fwd_args(h, steps);
     a.traj = h->d.traj;
     a.vel_traj = h->d.vel_traj;
-    a.state_out = h->d.state_out;
-    a.ckpt_s = h->ckpt_s;
-    a.ckpt_v = h->ckpt_v;
-    a.steps = steps;
-    a.ckpt_every = h->d.ckpt_every;
-    a.k = consts_of(h->d);
-    a.status = h->status;
-    a.obs = nullptr;
-    a.grad_traj = nullptr;
-    a.kind = 0;
-    a.loss_partials = nullptr;
     FwdVariant var;
     var.delta4 = h->delta4;
     var.kahan = steps > 2000;  // compensated displacement for long horizons (C3)
@@ -531,27 +572,13 @@ int idm_backward(idm_handle* h) {
         h->stage = 3;
         return IDM_OK;
     }
-    BwdArgs a;
-    a.tile_start = h->tile_start;
-    a.lead = h->lead;
-    a.params = h->d.params;
-    a.n = h->n;
-    a.n_par = h->n_par;
+    BwdArgs a = bwd_args(h, h->steps);
     a.grad_traj = h->d.grad_traj;
-    a.ckpt_s = h->ckpt_s;
-    a.ckpt_v = h->ckpt_v;
-    a.grad_params = h->d.grad_params;
-    a.grad_state0 = h->d.grad_state0;
-    a.shared_partials = h->shared_partials;
-    a.steps = h->steps;
-    a.ckpt_every = h->d.ckpt_every;
-    a.k = consts_of(h->d);
-    a.status = h->status;
     bool shared = h->d.param_mode == IDM_PARAMS_SHARED;
     std::memset(&a.adam, 0, sizeof(a.adam));
     {
         TimedLaunch tl(h, IDM_K_BWD);
-        CK(h, launch_bwd(a, h->ntiles, h->delta4, shared, false, h->st));
+        CK(h, launch_bwd(a, h->ntiles, h->delta4, shared, false, 0, false, h->st));
     }
     h->launches++;
     if (shared) {
@@ -675,27 +702,27 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
         }
         return IDM_OK;
     }
-    // forward + Eq. 4 fused: dL/dP straight from the fresh positions, no P round trip
-    FwdArgs f;
-    f.tile_start = h->tile_start;
-    f.lead = h->lead;
-    f.pos0 = h->d.pos0;
-    f.vel0 = h->d.vel0;
-    f.length = h->d.length;
-    f.params = h->d.params;
-    f.n = h->n;
-    f.n_par = h->n_par;
-    f.traj = nullptr;
-    f.vel_traj = nullptr;
-    f.state_out = h->d.state_out;
-    f.ckpt_s = h->ckpt_s;
-    f.ckpt_v = h->ckpt_v;
-    f.steps = steps;
-    f.ckpt_every = h->d.ckpt_every;
-    f.k = consts_of(h->d);
-    f.status = h->status;
+    if (h->d.ckpt_every != 4) {
+        // the fused kernels are specialised to 4-step segments; any other interval runs the
+        // defining sequence itself (same arithmetic, same bits)
+        int s = idm_forward(h, steps);
+        if (s == IDM_OK) s = idm_loss_grad(h, obs, nullptr, kind, loss_dev, nullptr);
+        if (s == IDM_OK) s = idm_backward(h);
+        if (s == IDM_OK) s = idm_adam_step(h, iter, total_iters, lr0, lr1);
+        if (s != IDM_OK) return s;
+        if (loss_host) {
+            CK(h, cudaMemcpyAsync(&h->pinned[0], h->loss_scalar, sizeof(double),
+                                  cudaMemcpyDeviceToHost, h->st));
+            int st2 = sync_status(h);
+            *loss_host = h->pinned[0];
+            if (st2 != IDM_OK) return st2;
+        }
+        return IDM_OK;
+    }
+    // forward + Eq. 4 value fused (the state history goes to the tile-local rows; no P or
+    // dL/dP round trip through HBM)
+    FwdArgs f = fwd_args(h, steps);
     f.obs = obs;
-    f.grad_traj = h->d.grad_traj;
     f.kind = kind;
     f.loss_partials = h->loss_partials;
     FwdVariant var;
@@ -713,28 +740,16 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
     }
     h->launches += 2;
     h->steps = steps;
-    // backward; per-vehicle parameters get Adam in the same kernel's epilogue
-    BwdArgs b;
-    b.tile_start = h->tile_start;
-    b.lead = h->lead;
-    b.params = h->d.params;
-    b.n = h->n;
-    b.n_par = h->n_par;
-    b.grad_traj = h->d.grad_traj;
-    b.ckpt_s = h->ckpt_s;
-    b.ckpt_v = h->ckpt_v;
-    b.grad_params = h->d.grad_params;
-    b.grad_state0 = h->d.grad_state0;
-    b.shared_partials = h->shared_partials;
-    b.steps = steps;
-    b.ckpt_every = h->d.ckpt_every;
-    b.k = consts_of(h->d);
-    b.status = h->status;
+    // backward: dL/dP re-derived from obs and the rebuilt positions; per-vehicle parameters
+    // get Adam in the same kernel's epilogue
+    BwdArgs b = bwd_args(h, steps);
+    b.obs = obs;
+    b.pos0 = h->d.pos0;
     b.adam = make_adam(h, iter, total_iters, lr0, lr1);
     const bool shared = h->d.param_mode == IDM_PARAMS_SHARED;
     {
         TimedLaunch tl(h, IDM_K_BWD);
-        CK(h, launch_bwd(b, h->ntiles, h->delta4, shared, !shared, h->st));
+        CK(h, launch_bwd(b, h->ntiles, h->delta4, shared, !shared, 1 + kind, var.kahan, h->st));
     }
     h->launches++;
     if (shared) {

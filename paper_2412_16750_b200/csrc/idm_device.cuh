@@ -9,6 +9,12 @@
 //
 // The softplus arguments are carried in base-2 units (x2 = x log2 e) with the log2(e) / ln 2
 // factors folded into per-vehicle constants, so each softplus is ex2 + lg2 + 3 FP ops.
+//
+// Every function is a template over the lane type T: T = float is one vehicle, T = float2 is
+// TWO vehicles whose FP32 arithmetic issues as packed f32x2 instructions (FFMA2 / FMUL2 /
+// FADD2, sm_100): one issue slot for two vehicles' multiply-adds.  The same template with the
+// same operation order serves both widths and every rounding is explicit (_rn), so a vehicle
+// gets bit-identical results whichever width computes it (FFMA2 = two FFMA.RN).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -26,13 +32,12 @@ struct Consts {
     float dt_ln2;     // dt ln 2
     float a_min2;     // a_min log2 e
     float ninv_dt2;   // -log2(e) / dt
+    float dt_amin;    // dt a_min (fp32 product)
 };
 
-// Forward constants of one vehicle (hoisted out of the time loop), base-2 scaled:
-//   s_opt log2e = sm2 + v (T2 + dv c2)          (Eq. 1)
-//   a_raw log2e = am2 (1 - w) - amln2 qr^2      (Eq. 2, qr = s*_opt log2e / dp)
-struct VehP {
-    float sm2, T2, c2, ivt, am2, amln2, delta;
+// ------------------------------------------------------------------ lane arithmetic
+struct bool2 {
+    bool x, y;
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -50,6 +55,74 @@ __device__ __forceinline__ float rcp(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+__device__ __forceinline__ float2 ex2(float2 x) { return make_float2(ex2(x.x), ex2(x.y)); }
+__device__ __forceinline__ float2 lg2(float2 x) { return make_float2(lg2(x.x), lg2(x.y)); }
+__device__ __forceinline__ float2 rcp(float2 x) { return make_float2(rcp(x.x), rcp(x.y)); }
+
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+__device__ __forceinline__ float vadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float2 vadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 vadd(float2 a, float b) { return __fadd2_rn(a, f2(b)); }
+__device__ __forceinline__ float vsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float2 vsub(float2 a, float2 b) {
+    return __fadd2_rn(a, make_float2(-b.x, -b.y));
+}
+__device__ __forceinline__ float2 vsub(float a, float2 b) {
+    return __fadd2_rn(make_float2(-b.x, -b.y), f2(a));
+}
+__device__ __forceinline__ float vmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float2 vmul(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 vmul(float2 a, float b) { return __fmul2_rn(a, f2(b)); }
+__device__ __forceinline__ float vfma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ float2 vfma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 vfma(float2 a, float b, float2 c) {
+    return __ffma2_rn(a, f2(b), c);
+}
+__device__ __forceinline__ float vneg(float a) { return -a; }
+__device__ __forceinline__ float2 vneg(float2 a) { return make_float2(-a.x, -a.y); }
+__device__ __forceinline__ float vnabs(float a) { return -fabsf(a); }
+__device__ __forceinline__ float2 vnabs(float2 a) { return make_float2(-fabsf(a.x), -fabsf(a.y)); }
+__device__ __forceinline__ float vabs(float a) { return fabsf(a); }
+__device__ __forceinline__ float2 vabs(float2 a) { return make_float2(fabsf(a.x), fabsf(a.y)); }
+// -sign(a) with sign(0) = 0: one LOP3 builds -+1 from the sign bit, one select zeroes a == 0
+__device__ __forceinline__ float vnsign(float a) {
+    const float m1 = __int_as_float((__float_as_int(a) & 0x80000000) ^ 0xBF800000);
+    return a != 0.f ? m1 : 0.f;
+}
+__device__ __forceinline__ float2 vnsign(float2 a) { return make_float2(vnsign(a.x), vnsign(a.y)); }
+__device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ float2 vmax(float2 a, float b) {
+    return make_float2(fmaxf(a.x, b), fmaxf(a.y, b));
+}
+__device__ __forceinline__ float2 vmax(float2 a, float2 b) {
+    return make_float2(fmaxf(a.x, b.x), fmaxf(a.y, b.y));
+}
+__device__ __forceinline__ bool vge(float a, float b) { return a >= b; }
+__device__ __forceinline__ bool2 vge(float2 a, float b) { return bool2{a.x >= b, a.y >= b}; }
+__device__ __forceinline__ bool vgt(float a, float b) { return a > b; }
+__device__ __forceinline__ bool2 vgt(float2 a, float b) { return bool2{a.x > b, a.y > b}; }
+__device__ __forceinline__ float vsel(bool m, float a, float b) { return m ? a : b; }
+__device__ __forceinline__ float2 vsel(bool2 m, float2 a, float2 b) {
+    return make_float2(m.x ? a.x : b.x, m.y ? a.y : b.y);
+}
+template <class T> __device__ __forceinline__ T splat(float a);
+template <> __device__ __forceinline__ float splat<float>(float a) { return a; }
+template <> __device__ __forceinline__ float2 splat<float2>(float a) { return f2(a); }
+
+template <class T> struct MaskOf { using type = bool; };
+template <> struct MaskOf<float2> { using type = bool2; };
+template <class T> using Mask = typename MaskOf<T>::type;
+
+// ------------------------------------------------------------------ per-vehicle constants
+// Forward constants of one vehicle (hoisted out of the time loop), base-2 scaled:
+//   s_opt log2e = sm2 + v (T2 + dv c2)          (Eq. 1)
+//   a_raw log2e = am2 (1 - w) - amln2 qr^2      (Eq. 2, qr = s*_opt log2e / dp)
+template <class T>
+struct VehPT {
+    T sm2, T2, c2, ivt, am2, amln2, delta;
+};
+using VehP = VehPT<float>;
 
 __device__ __forceinline__ VehP make_vehp(float a_max, float a_pref, float s_min, float T,
                                           float v_targ, float delta) {
@@ -65,84 +138,109 @@ __device__ __forceinline__ VehP make_vehp(float a_max, float a_pref, float s_min
     return p;
 }
 
-// Everything one step computes from (s, v, v_leader) before the state update; shared by the
-// forward update and the adjoint so both see the same values.
-struct Core {
-    float x, x2, w, dv, c12, s_opt2, es, ones, ss2, idp, qr, inter2, t1, vda, z2, ea, onea, lx;
-    bool lb_act;
-};
-
-// Eqs. 1-2 with the Sec. III-C bounds (PAPER.md:114-115, :142, :148-149), exact free road
-// without a leader (R#8), gap clamped at eps (R#7).  Explicit _rn intrinsics: the forward
-// kernel and the backward recompute produce bitwise identical states.
-template <bool D4>
-__device__ __forceinline__ void core_dv(float s, float v, float dv, bool lead, const VehP& p,
-                                        const Consts& k, Core& c);
-
-template <bool D4>
-__device__ __forceinline__ void core(float s, float v, float vl, bool lead, const VehP& p,
-                                     const Consts& k, Core& c) {
-    core_dv<D4>(s, v, __fsub_rn(v, vl), lead, p, k, c);  // Delta v = v_i - v_h
+__device__ __forceinline__ VehPT<float2> pack(const VehP& a, const VehP& b) {
+    return VehPT<float2>{make_float2(a.sm2, b.sm2),     make_float2(a.T2, b.T2),
+                         make_float2(a.c2, b.c2),       make_float2(a.ivt, b.ivt),
+                         make_float2(a.am2, b.am2),     make_float2(a.amln2, b.amln2),
+                         make_float2(a.delta, b.delta)};
 }
 
-// The step core given the approach rate dv directly (virtual-leader mode, where
-// (Delta p_k, Delta v_k) are free variables; the lane path passes dv = v - v_h).
-template <bool D4>
-__device__ __forceinline__ void core_dv(float s, float v, float dv, bool lead, const VehP& p,
-                                        const Consts& k, Core& c) {
-    c.x = __fmul_rn(v, p.ivt);
-    c.x2 = __fmul_rn(c.x, c.x);
+// Everything one step computes from (s, v, v_leader) before the state update; shared by the
+// forward update and the adjoint so both see the same values.
+template <class T>
+struct CoreT {
+    T x, x2, w, dv, c12, s_opt2, es, ones, ss2, idp, qr, inter2, t1, vda, z2, ea, onea, lx,
+        vlb2;
+};
+using Core = CoreT<float>;
+
+// Eqs. 1-2 with the Sec. III-C bounds (PAPER.md:114-115, :142, :148-149), exact free road
+// without a leader (R#8), gap clamped at eps (R#7), given the approach rate dv = v_i - v_h
+// directly (the virtual-leader mode, passes its free variable).
+//   leadf: 1 with a leader, 0 without (folded into 1/Delta p: the interaction term and every
+//   derivative through it vanish exactly for a lane head).
+// Explicit _rn intrinsics: the forward kernel and the backward recompute produce bitwise
+// identical states.
+template <bool D4, class T, class LF>
+__device__ __forceinline__ void core_dv(T s, T v, T dv, LF leadf, const VehPT<T>& p,
+                                        const Consts& k, CoreT<T>& c) {
+    c.x = vmul(v, p.ivt);
+    c.x2 = vmul(c.x, c.x);
     if (D4) {
-        c.w = __fmul_rn(c.x2, c.x2);  // (v / v_targ)^4
-        c.lx = 0.f;
+        c.w = vmul(c.x2, c.x2);  // (v / v_targ)^4
+        c.lx = splat<T>(0.f);
     } else {
-        c.lx = c.x > 0.f ? lg2(c.x) : 0.f;
-        c.w = c.x > 0.f ? ex2(__fmul_rn(p.delta, c.lx)) : 0.f;
+        const Mask<T> xp = vgt(c.x, 0.f);
+        c.lx = vsel(xp, lg2(c.x), splat<T>(0.f));
+        c.w = vsel(xp, ex2(vmul(p.delta, c.lx)), splat<T>(0.f));
     }
     c.dv = dv;
-    c.c12 = __fmaf_rn(c.dv, p.c2, p.T2);
-    c.s_opt2 = __fmaf_rn(v, c.c12, p.sm2);                     // s_opt log2 e
-    c.es = ex2(-fabsf(c.s_opt2));
-    c.ones = __fadd_rn(1.f, c.es);
-    c.ss2 = __fadd_rn(fmaxf(c.s_opt2, 0.f), lg2(c.ones));      // softplus(s_opt) log2 e
-    c.idp = rcp(fmaxf(s, k.eps));                              // 1 / Delta p
-    c.qr = __fmul_rn(c.ss2, c.idp);                            // (s*/Delta p) log2 e
-    c.inter2 = lead ? __fmul_rn(c.qr, c.qr) : 0.f;
-    c.t1 = __fsub_rn(1.f, c.w);
-    const float a_raw2 = __fmaf_rn(-p.amln2, c.inter2, __fmul_rn(p.am2, c.t1));
-    c.vda = __fmaf_rn(k.dt, k.a_min, v);                       // v + dt a_min
-    c.lb_act = c.vda < 0.f;                                    // a_lb = -v/dt branch
-    const float a_lb2 = c.lb_act ? __fmul_rn(v, k.ninv_dt2) : k.a_min2;
-    c.z2 = __fsub_rn(a_raw2, a_lb2);                           // (a - a_lb) log2 e
-    c.ea = ex2(-fabsf(c.z2));
-    c.onea = __fadd_rn(1.f, c.ea);
+    c.c12 = vfma(c.dv, p.c2, p.T2);
+    c.s_opt2 = vfma(v, c.c12, p.sm2);                          // s_opt log2 e
+    c.es = ex2(vnabs(c.s_opt2));
+    c.ones = vadd(c.es, 1.f);
+    c.ss2 = vadd(vmax(c.s_opt2, 0.f), lg2(c.ones));            // softplus(s_opt) log2 e
+    c.idp = vmul(rcp(vmax(s, k.eps)), leadf);                  // lead / Delta p
+    c.qr = vmul(c.ss2, c.idp);                                 // (s*/Delta p) log2 e
+    c.inter2 = vmul(c.qr, c.qr);
+    c.t1 = vsub(1.f, c.w);
+    const T a_raw2 = vfma(vneg(p.amln2), c.inter2, vmul(p.am2, c.t1));
+    c.vda = vadd(v, k.dt_amin);                                // v + dt a_min
+    c.vlb2 = vmul(v, k.ninv_dt2);                              // (-v / dt) log2 e
+    const T a_lb2 = vmax(c.vlb2, k.a_min2);                    // a_lb = max(-v/dt, a_min)
+    c.z2 = vsub(a_raw2, a_lb2);                                // (a - a_lb) log2 e
+    c.ea = ex2(vnabs(c.z2));
+    c.onea = vadd(c.ea, 1.f);
+}
+
+template <bool D4, class T, class LF>
+__device__ __forceinline__ void core(T s, T v, T vl, LF leadf, const VehPT<T>& p,
+                                     const Consts& k, CoreT<T>& c) {
+    core_dv<D4>(s, v, vsub(v, vl), leadf, p, k, c);  // Delta v = v_i - v_h
 }
 
 // State update of one vehicle from its step core (Eq. 3).  v' = v + dt a* computed as
 // max(0, v + dt a_min) + dt softplus(a - a_lb): exact identity, >= 0 in floats.
-__device__ __forceinline__ void advance(const Core& c, float& s, float& v, bool lead,
-                                        const Consts& k) {
-    const float sp2 = __fadd_rn(fmaxf(c.z2, 0.f), lg2(c.onea));  // softplus(a - a_lb) log2 e
-    const float vn = __fmaf_rn(k.dt_ln2, sp2, fmaxf(c.vda, 0.f));
-    if (lead) s = __fmaf_rn(-k.dt, c.dv, s);                       // s + dt (v_h - v)
+// The gap moves by dt (v_h - v); a lane head's gap is never read (leadf = 0).
+template <class T>
+__device__ __forceinline__ void advance(const CoreT<T>& c, T& s, T& v, const Consts& k) {
+    const T sp2 = vadd(vmax(c.z2, 0.f), lg2(c.onea));          // softplus(a - a_lb) log2 e
+    const T vn = vfma(sp2, k.dt_ln2, vmax(c.vda, 0.f));
+    s = vfma(c.dv, -k.dt, s);                                  // s + dt (v_h - v)
     v = vn;
 }
 
-// One synchronous IDM + Euler step of one vehicle (Eqs. 1-3, Sec. III-C).
-template <bool D4>
-__device__ __forceinline__ void fwd_step(float& s, float& v, float vl, bool lead, const VehP& p,
+// One synchronous IDM + Euler step (Eqs. 1-3, Sec. III-C).
+template <bool D4, class T, class LF>
+__device__ __forceinline__ void fwd_step(T& s, T& v, T vl, LF leadf, const VehPT<T>& p,
                                          const Consts& k) {
-    Core c;
-    core<D4>(s, v, vl, lead, p, k, c);
-    advance(c, s, v, lead, k);
+    CoreT<T> c;
+    core<D4>(s, v, vl, leadf, p, k, c);
+    advance(c, s, v, k);
+}
+
+// Eq. 4 terms of a vehicle (pair), branch-free: observed iff finite (NaN =
+// missing; absent vehicles are fed NaN).  Returns dL/dP; adds the loss terms to acc.
+template <int KIND, class T>
+__device__ __forceinline__ T loss_term(T o, T P, T& acc) {
+    const T r = vsub(o, P);
+    const T rm = vsel(vge(vnabs(o), -3.4e38f), r, splat<T>(0.f));  // 0 where unobserved
+    if (KIND == 0) {  // L1: |r|, dL/dP = -sign(r), sign(0) = 0 (R#11)
+        acc = vadd(acc, vabs(rm));
+        return vnsign(rm);
+    }
+    acc = vfma(rm, rm, acc);  // L2: r^2, dL/dP = -2 r
+    return vmul(rm, -2.f);
 }
 
 // Backward-only per-vehicle constants.
-struct VehB {
-    float nam2ln2;  // -2 a_max ln2          (d a_raw / d s* = nam2ln2 qr idp)
-    float ndamivt;  // -delta a_max / v_targ (d a_raw / d v, free term, times x^(delta-1))
-    float nc;       // -c                    (d s_opt / d v_h)
+template <class T>
+struct VehBT {
+    T nam2ln2;  // -2 a_max ln2          (d a_raw / d s* = nam2ln2 qr idp)
+    T ndamivt;  // -delta a_max / v_targ (d a_raw / d v, free term, times x^(delta-1))
+    T nc;       // -c                    (d s_opt / d v_h)
 };
+using VehB = VehBT<float>;
 
 __device__ __forceinline__ VehB make_vehb(float a_max, float a_pref, float v_targ, float delta) {
     VehB b;
@@ -152,74 +250,90 @@ __device__ __forceinline__ VehB make_vehb(float a_max, float a_pref, float v_tar
     return b;
 }
 
+__device__ __forceinline__ VehBT<float2> pack(const VehB& a, const VehB& b) {
+    return VehBT<float2>{make_float2(a.nam2ln2, b.nam2ln2), make_float2(a.ndamivt, b.ndamivt),
+                         make_float2(a.nc, b.nc)};
+}
+
 // Accumulators of q * d a*/d theta, factored so per-vehicle constants are applied once at the
 // end (q = dt lambda_v^{t+1}, qa = q sigma_a, qB = q d a*/d s_opt):
 //   S1 = sum qa (1 - w - r^2)   S2 = sum qB v dv   S3 = sum qB   S4 = sum qB v
 //   S5 = sum qa w               S6 = sum qa w log2 x
-struct GradAcc {
-    float S1, S2, S3, S4, S5, S6;
+template <class T>
+struct GradAccT {
+    T S1, S2, S3, S4, S5, S6;
+};
+using GradAcc = GradAccT<float>;
+
+// Local Jacobian of one vehicle-step (derivation: DESIGN.md "Adjoint (gap form)"), 24 bytes per
+// vehicle: (sigma_a, beta = d a*/d s_opt, J_v = d a*/d v |_{v_h}, J_s = d a*/d s,
+// r1 = 1 - w - r^2, r2 = w log2 x) with w = (v/v_targ)^delta, r = s*/dp.
+// sigma_a = d a*/d a_raw (PAPER.md:149), d s*/d s_opt = sigmoid(s_opt) (:148); beta = 0 without
+// a leader (idp = 0, R#8) and J_s = 0 while the gap is clamped (R#7).
+template <class T>
+struct RecT {
+    T sig_a, beta, Jv, Js, r1, r2;
 };
 
-// Per vehicle-step record the backward recompute stores in shared memory (24 B), the local
-// Jacobian of one step (derivation: DESIGN.md "Adjoint (gap form)"):
-//   R1 = (sigma_a, beta = d a*/d s_opt, J_v = d a*/d v |_{v_h}, J_s = d a*/d s)
-//   R2 = (1 - w - r^2, w log2 x)          with w = (v/v_targ)^delta, r = s*/dp
-// sigma_a = d a*/d a_raw (PAPER.md:149), d s*/d s_opt = sigmoid(s_opt) (:148); beta = 0 without
-// a leader (R#8) and J_s = 0 while the gap is clamped (R#7).
-template <bool D4>
-__device__ __forceinline__ void jac_record(const Core& c, float s, float v, bool lead,
-                                           const VehP& p, const VehB& b, const Consts& k,
-                                           float4& R1, float2& R2) {
-    const float rs = rcp(c.ones);
-    const float sig_s = c.s_opt2 >= 0.f ? rs : c.es * rs;       // d s*/d s_opt
-    const float ra = rcp(c.onea);
-    const float eara = c.ea * ra;
-    const bool zpos = c.z2 >= 0.f;
-    const float sig_a = zpos ? ra : eara;                        // d a*/d a_raw
-    const float omsa = zpos ? eara : ra;                         // d a*/d a_lb
-    const float As = b.nam2ln2 * c.qr * c.idp;                  // d a_raw/d s*
-    const float beta = lead ? sig_a * As * sig_s : 0.f;          // d a*/d s_opt
-    const float xm1 = D4 ? c.x2 * c.x : (c.x > 0.f ? c.w * rcp(c.x) : 0.f);  // x^(delta-1)
+template <bool D4, class T>
+__device__ __forceinline__ RecT<T> jac_record(const CoreT<T>& c, T s, T v, const VehPT<T>& p,
+                                              const VehBT<T>& b, const Consts& k) {
+    const T rs = rcp(c.ones);
+    const T sig_s = vsel(vge(c.s_opt2, 0.f), rs, vmul(c.es, rs));   // d s*/d s_opt
+    const T ra = rcp(c.onea);
+    const T eara = vmul(c.ea, ra);
+    const Mask<T> zpos = vge(c.z2, 0.f);
+    const T sig_a = vsel(zpos, ra, eara);                            // d a*/d a_raw
+    const T omsa = vsel(zpos, eara, ra);                             // d a*/d a_lb
+    const T As = vmul(vmul(b.nam2ln2, c.qr), c.idp);                // d a_raw/d s*
+    const T sAs = vmul(sig_a, As);
+    RecT<T> R;
+    R.sig_a = sig_a;
+    R.beta = vmul(sAs, sig_s);                                       // d a*/d s_opt
+    T xm1;                                                           // x^(delta-1)
+    if (D4) xm1 = vmul(c.x2, c.x);
+    else xm1 = vsel(vgt(c.x, 0.f), vmul(c.w, rcp(c.x)), splat<T>(0.f));
     // d a*/d v at fixed leader speed: free term + s_opt term (T + (dv + v) c) + a_lb branch (R#5)
-    float Jv = fmaf(beta * kLn2, fmaf(v, p.c2, c.c12), sig_a * b.ndamivt * xm1);
-    if (c.lb_act) Jv = fmaf(-omsa, k.inv_dt, Jv);
-    const float Js = (lead && s >= k.eps) ? -sig_a * As * c.qr * kLn2 : 0.f;
-    const float lx = D4 ? (c.x > 0.f ? lg2(c.x) : 0.f) : c.lx;
-    R1 = make_float4(sig_a, beta, Jv, Js);
-    R2 = make_float2(fmaf(-kLn2Sq, c.inter2, c.t1), c.w * lx);
+    const T Jv = vfma(vmul(R.beta, kLn2), vfma(v, p.c2, c.c12), vmul(vmul(sig_a, b.ndamivt), xm1));
+    const Mask<T> lb_act = vgt(c.vlb2, k.a_min2);                    // a_lb = -v/dt branch
+    R.Jv = vsel(lb_act, vfma(omsa, -k.inv_dt, Jv), Jv);
+    R.Js = vsel(vge(s, k.eps), vmul(vmul(sAs, c.qr), -kLn2), splat<T>(0.f));
+    const T lx = D4 ? vsel(vgt(c.x, 0.f), lg2(c.x), splat<T>(0.f)) : c.lx;
+    R.r1 = vfma(c.inter2, -kLn2Sq, c.t1);
+    R.r2 = vmul(c.w, lx);
+    return R;
 }
 
 // Reverse step from the stored record: consumes lambda^{t+1} = (ls, lv, lD), returns F_out
 // (this vehicle's term for its LEADER's lambda_v), updates ls, lv (the follower's F_in is added
 // by the caller) and the gradient accumulators.  ls = 0 and beta = 0 for a lane head, so no
-// leader predicates are needed.
-template <bool D4>
-__device__ __forceinline__ float bwd_from_record(float4 R1, float2 R2, float v, float vl,
-                                                 const VehP& p, const VehB& b, const Consts& k,
-                                                 float& ls, float& lv, float lD, GradAcc& g) {
-    const float q = k.dt * lv;
-    const float qa = q * R1.x;
-    const float qb = q * R1.y;
-    const float dtls = k.dt * ls;
-    const float qbv = qb * v;
-    const float F_out = fmaf(qbv, b.nc, dtls);                   // q d a*/d v_h + dt lambda_s
-    lv = fmaf(k.dt, lD, fmaf(q, R1.z, lv)) - dtls;
-    ls = fmaf(q, R1.w, ls);
-    float w;
+// leader predicates are needed (vl only has to be finite there).
+template <bool D4, class T>
+__device__ __forceinline__ T bwd_from_record(const RecT<T>& R, T v, T vl, const VehPT<T>& p,
+                                             const VehBT<T>& b, const Consts& k, T& ls, T& lv,
+                                             T lD, GradAccT<T>& g) {
+    const T q = vmul(lv, k.dt);
+    const T qa = vmul(q, R.sig_a);
+    const T qb = vmul(q, R.beta);
+    const T dtls = vmul(ls, k.dt);
+    const T qbv = vmul(qb, v);
+    const T F_out = vfma(qbv, b.nc, dtls);                       // q d a*/d v_h + dt lambda_s
+    lv = vsub(vfma(lD, k.dt, vfma(q, R.Jv, lv)), dtls);
+    ls = vfma(q, R.Js, ls);
+    T w;
+    const T x = vmul(v, p.ivt);
     if (D4) {
-        const float x = v * p.ivt;
-        const float x2 = x * x;
-        w = x2 * x2;
+        const T x2 = vmul(x, x);
+        w = vmul(x2, x2);
     } else {
-        const float x = v * p.ivt;
-        w = x > 0.f ? ex2(p.delta * lg2(x)) : 0.f;
+        w = vsel(vgt(x, 0.f), ex2(vmul(p.delta, lg2(x))), splat<T>(0.f));
     }
-    g.S1 = fmaf(qa, R2.x, g.S1);
-    g.S2 = fmaf(qbv, v - vl, g.S2);
-    g.S3 += qb;
-    g.S4 += qbv;
-    g.S5 = fmaf(qa, w, g.S5);
-    g.S6 = fmaf(qa, R2.y, g.S6);
+    g.S1 = vfma(qa, R.r1, g.S1);
+    g.S2 = vfma(qbv, vsub(v, vl), g.S2);
+    g.S3 = vadd(g.S3, qb);
+    g.S4 = vadd(g.S4, qbv);
+    g.S5 = vfma(qa, w, g.S5);
+    g.S6 = vfma(qa, R.r2, g.S6);
     return F_out;
 }
 
@@ -227,39 +341,42 @@ __device__ __forceinline__ float bwd_from_record(float4 R1, float2 R2, float v, 
 // local Jacobian is d a*/d v |_{dv} (dv is a leaf, so v enters only directly), d a*/d dp and
 // d a*/d dv = beta v c.  Consumes lambda^{t+1} = (lv, lD); writes q d a*/d dp and q d a*/d dv
 // (the leaf gradients of step t) and updates lv and the parameter accumulators.
-template <bool D4>
-__device__ __forceinline__ void bwd_vl(const Core& c, float dp, float v, const VehP& p,
-                                       const VehB& b, const Consts& k, float& lv, float lD,
-                                       GradAcc& g, float& gdp, float& gdv) {
-    const float rs = rcp(c.ones);
-    const float sig_s = c.s_opt2 >= 0.f ? rs : c.es * rs;
-    const float ra = rcp(c.onea);
-    const float eara = c.ea * ra;
-    const bool zpos = c.z2 >= 0.f;
-    const float sig_a = zpos ? ra : eara;
-    const float omsa = zpos ? eara : ra;
-    const float As = b.nam2ln2 * c.qr * c.idp;                  // d a_raw/d s*
-    const float beta = sig_a * As * sig_s;                      // d a*/d s_opt
-    const float xm1 = D4 ? c.x2 * c.x : (c.x > 0.f ? c.w * rcp(c.x) : 0.f);
+template <bool D4, class T>
+__device__ __forceinline__ void bwd_vl(const CoreT<T>& c, T dp, T v, const VehPT<T>& p,
+                                       const VehBT<T>& b, const Consts& k, T& lv, T lD,
+                                       GradAccT<T>& g, T& gdp, T& gdv) {
+    const T rs = rcp(c.ones);
+    const T sig_s = vsel(vge(c.s_opt2, 0.f), rs, vmul(c.es, rs));
+    const T ra = rcp(c.onea);
+    const T eara = vmul(c.ea, ra);
+    const Mask<T> zpos = vge(c.z2, 0.f);
+    const T sig_a = vsel(zpos, ra, eara);
+    const T omsa = vsel(zpos, eara, ra);
+    const T As = vmul(vmul(b.nam2ln2, c.qr), c.idp);            // d a_raw/d s*
+    const T sAs = vmul(sig_a, As);
+    const T beta = vmul(sAs, sig_s);                            // d a*/d s_opt
+    T xm1;
+    if (D4) xm1 = vmul(c.x2, c.x);
+    else xm1 = vsel(vgt(c.x, 0.f), vmul(c.w, rcp(c.x)), splat<T>(0.f));
     // d a*/d v at fixed dv: free term + s_opt term (T + dv c) + a_lb branch (R#5)
-    float Jv = fmaf(beta * kLn2, c.c12, sig_a * b.ndamivt * xm1);
-    if (c.lb_act) Jv = fmaf(-omsa, k.inv_dt, Jv);
-    const float Js = dp >= k.eps ? -sig_a * As * c.qr * kLn2 : 0.f;  // R#7
-    const float q = k.dt * lv;
-    const float qa = q * sig_a;
-    const float qb = q * beta;
-    gdp = q * Js;
-    gdv = -qb * v * b.nc;                                       // d s_opt/d dv = v c
-    lv = fmaf(k.dt, lD, fmaf(q, Jv, lv));
-    const float lx = D4 ? (c.x > 0.f ? lg2(c.x) : 0.f) : c.lx;
-    g.S1 = fmaf(qa, fmaf(-kLn2Sq, c.inter2, c.t1), g.S1);
-    const float qbv = qb * v;
-    g.S2 = fmaf(qbv, c.dv, g.S2);
-    g.S3 += qb;
-    g.S4 += qbv;
-    const float qaw = qa * c.w;
-    g.S5 += qaw;
-    g.S6 = fmaf(qaw, lx, g.S6);
+    const T Jv0 = vfma(vmul(beta, kLn2), c.c12, vmul(vmul(sig_a, b.ndamivt), xm1));
+    const T Jv = vsel(vgt(c.vlb2, k.a_min2), vfma(omsa, -k.inv_dt, Jv0), Jv0);
+    const T Js = vsel(vge(dp, k.eps), vmul(vmul(sAs, c.qr), -kLn2), splat<T>(0.f));  // R#7
+    const T q = vmul(lv, k.dt);
+    const T qa = vmul(q, sig_a);
+    const T qb = vmul(q, beta);
+    gdp = vmul(q, Js);
+    const T qbv = vmul(qb, v);
+    gdv = vmul(vneg(qbv), b.nc);                                // d s_opt/d dv = v c
+    lv = vfma(lD, k.dt, vfma(q, Jv, lv));
+    const T lx = D4 ? vsel(vgt(c.x, 0.f), lg2(c.x), splat<T>(0.f)) : c.lx;
+    g.S1 = vfma(qa, vfma(c.inter2, -kLn2Sq, c.t1), g.S1);
+    g.S2 = vfma(qbv, c.dv, g.S2);
+    g.S3 = vadd(g.S3, qb);
+    g.S4 = vadd(g.S4, qbv);
+    const T qaw = vmul(qa, c.w);
+    g.S5 = vadd(g.S5, qaw);
+    g.S6 = vfma(qaw, lx, g.S6);
 }
 
 }  // namespace idm

@@ -15,22 +15,7 @@
 
 namespace idm {
 
-namespace {
 constexpr int kFT = kCap;  // one vehicle per thread, 512 threads per CTA
-
-template <int KIND>
-__device__ __forceinline__ float fit_loss_term(float o, float P, bool valid, float& acc) {
-    const float r = o - P;
-    const bool ok = valid && fabsf(o) <= 3.4e38f;
-    if (KIND == 0) {
-        acc += ok ? fabsf(r) : 0.f;
-        const float sg = r > 0.f ? -1.f : (r < 0.f ? 1.f : 0.f);
-        return ok ? sg : 0.f;
-    }
-    acc = ok ? fmaf(r, r, acc) : acc;
-    return ok ? -2.f * r : 0.f;
-}
-}  // namespace
 
 template <int KM, bool D4, int KIND>
 __global__ void __launch_bounds__(kFT, 1) fit_kernel(FitArgs a) {
@@ -46,14 +31,14 @@ __global__ void __launch_bounds__(kFT, 1) fit_kernel(FitArgs a) {
     const bool valid = tid < n_loc;
     const int64_t i = base + tid;
 
-    float p0 = 0.f, v0 = 0.f, s0 = 0.f;
-    bool lead = false;
+    float p0 = 0.f, v0 = 0.f, s0 = 0.f, leadf = 0.f;
     float x[6] = {1.f, 1.f, 1.f, 1.f, 1.f, 4.f}, m1[6], m2[6];
     float ob[KM + 1];
     if (valid) {
         p0 = a.pos0[i];
         v0 = a.vel0[i];
-        lead = a.lead[i] != 0;
+        const bool lead = a.lead[i] != 0;
+        leadf = lead ? 1.f : 0.f;
         s0 = lead ? (a.pos0[i + 1] - p0) - a.length[i + 1] : 0.f;
 #pragma unroll
         for (int q = 0; q < 6; ++q) {
@@ -66,11 +51,13 @@ __global__ void __launch_bounds__(kFT, 1) fit_kernel(FitArgs a) {
         for (int q = 0; q < 6; ++q) { m1[q] = 0.f; m2[q] = 0.f; }
     }
 #pragma unroll
-    for (int t = 0; t <= KM; ++t) ob[t] = (valid && t <= K) ? a.obs[(int64_t)t * N + i] : 0.f;
+    for (int t = 0; t <= KM; ++t)  // absent vehicles observe NaN (= missing)
+        ob[t] = (valid && t <= K) ? a.obs[(int64_t)t * N + i] : __int_as_float(0x7fc00000);
     if (tid == 0) {
         fx[0][0] = 0.f;
         fx[1][0] = 0.f;
     }
+    if (tid < KM) hv[tid][kCap] = 0.f;  // leader-read sentinel of the last thread
     if (D4 && valid && x[5] != 4.f)
         atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
 
@@ -83,7 +70,7 @@ __global__ void __launch_bounds__(kFT, 1) fit_kernel(FitArgs a) {
         // ---- forward + Eq. 4 (as fwd_kernel<LOSS>)
         float s = s0, v = v0, D = 0.f;
         lsum = 0.f;
-        g[0] = fit_loss_term<KIND>(ob[0], p0, valid, lsum);
+        g[0] = loss_term<KIND>(ob[0], p0, lsum);
 #pragma unroll
         for (int t = 0; t < KM; ++t) {
             if (t < K) {
@@ -91,10 +78,10 @@ __global__ void __launch_bounds__(kFT, 1) fit_kernel(FitArgs a) {
                 vt[t] = v;
                 hv[t][tid] = v;
                 __syncthreads();
-                const float vl = lead ? hv[t][tid + 1] : v;
-                D = __fmaf_rn(k.dt, v, D);
-                fwd_step<D4>(s, v, vl, lead, P, k);
-                g[t + 1] = fit_loss_term<KIND>(ob[t + 1], __fadd_rn(p0, D), valid, lsum);
+                const float vl = hv[t][tid + 1];
+                D = vfma(v, k.dt, D);
+                fwd_step<D4>(s, v, vl, leadf, P, k);
+                g[t + 1] = loss_term<KIND>(ob[t + 1], vadd(p0, D), lsum);
             }
         }
         // ---- reverse sweep (as bwd_kernel: local Jacobian of each step, then the update)
@@ -106,17 +93,15 @@ __global__ void __launch_bounds__(kFT, 1) fit_kernel(FitArgs a) {
 #pragma unroll
         for (int t = KM - 1; t >= 0; --t) {
             if (t < K) {
-                const float vl = lead ? hv[t][tid + 1] : vt[t];
+                const float vl = hv[t][tid + 1];
                 Core c;
-                core<D4>(st[t], vt[t], vl, lead, P, k, c);
-                float4 R1;
-                float2 R2;
-                jac_record<D4>(c, st[t], vt[t], lead, P, B, k, R1, R2);
-                const float F = bwd_from_record<D4>(R1, R2, vt[t], vl, P, B, k, ls, lv, lD, G);
+                core<D4>(st[t], vt[t], vl, leadf, P, k, c);
+                const RecT<float> R = jac_record<D4>(c, st[t], vt[t], P, B, k);
+                const float F = bwd_from_record<D4>(R, vt[t], vl, P, B, k, ls, lv, lD, G);
                 fx[par][tid + 1] = F;
                 __syncthreads();
-                lv += fx[par][tid];
-                lD += g[t];
+                lv = vadd(lv, fx[par][tid]);
+                lD = vadd(lD, g[t]);
                 par ^= 1;
             }
         }
@@ -141,14 +126,12 @@ __global__ void __launch_bounds__(kFT, 1) fit_kernel(FitArgs a) {
         if (it + 1 == a.iters && valid) {
 #pragma unroll
             for (int q = 0; q < 6; ++q) a.grad_params[q * N + i] = gr[q];
-            if (a.grad_state0) {
-                fx[par][tid + 1] = lead ? ls : 0.f;
-            }
+            if (a.grad_state0) fx[par][tid + 1] = vmul(ls, leadf);
         }
         if (it + 1 == a.iters) {
             __syncthreads();
             if (a.grad_state0 && valid) {
-                a.grad_state0[i] = lD - (lead ? ls : 0.f) + fx[par][tid];
+                a.grad_state0[i] = vadd(vsub(lD, vmul(ls, leadf)), fx[par][tid]);
                 a.grad_state0[N + i] = lv;
             }
         }

@@ -26,19 +26,28 @@ struct FwdVariant {
     int loss;     // 0, or fused Eq. 4 (1 = L1, 2 = L2): read obs, write dL/dP (idm_fit_step)
 };
 
+// Lane-mode state history in HBM, TILE-LOCAL layout (internal workspace):
+//   vt  [tile][max_steps + 1][kCap]     speed of every vehicle slot at every step
+//   ckt [tile][nck][3][kCap]            (gap, displacement, Kahan compensation) at every
+//                                       ckpt_every-th step
+// A tile's rows are kCap floats apart (compile-time), so a thread's vehicle pair is one
+// aligned 8-byte access at an immediate offset, and slots past the tile's vehicles are
+// private padding (stores need no predicate).
+constexpr int kCkRows = 3;
+
 struct FwdArgs {
     const int64_t* tile_start;
     const uint8_t* lead;
     const float *pos0, *vel0, *length, *params;
     int64_t n, n_par;
     float *traj, *vel_traj, *state_out;
-    float *ckpt_s, *ckpt_v;
+    float *vt, *ckt;
+    int64_t vt_stride, ck_stride;  // floats per tile
     int steps, ckpt_every;
     Consts k;
     unsigned long long* status;
-    // fused loss (LOSS variant)
+    // fused loss (LOSS variant): Eq. 4 value only (the backward re-derives dL/dP)
     const float* obs;
-    float* grad_traj;
     int kind;
     double* loss_partials;  // [ntiles]
 };
@@ -57,8 +66,10 @@ struct BwdArgs {
     const uint8_t* lead;
     const float* params;
     int64_t n, n_par;
-    const float* grad_traj;
-    const float *ckpt_s, *ckpt_v;
+    const float* grad_traj;        // dL/dP rows (API path)
+    const float *obs, *pos0;       // fused path: dL/dP re-derived from obs and positions
+    const float *vt, *ckt;
+    int64_t vt_stride, ck_stride;
     float *grad_params, *grad_state0;
     double* shared_partials;  // [ntiles][6] (shared mode)
     int steps, ckpt_every;
@@ -116,8 +127,9 @@ cudaError_t launch_validate(const ValidateArgs& a, cudaStream_t st);
 cudaError_t launch_fwd(const FwdArgs& a, int ntiles, const FwdVariant& var, cudaStream_t st);
 cudaError_t kernels_configure(int ckpt_every);
 size_t bwd_smem_bytes(int ckpt_every);
+// gobs = 0: dL/dP from grad_traj; 1 + kind: re-derived from obs (fused, ckpt_every == 4)
 cudaError_t launch_bwd(const BwdArgs& a, int ntiles, bool delta4, bool shared, bool adam,
-                       cudaStream_t st);
+                       int gobs, bool kahan, cudaStream_t st);
 bool ckpt_supported(int k);
 cudaError_t launch_loss(const LossArgs& a, int nblocks, cudaStream_t st);
 cudaError_t launch_reduce(const double* partials, int64_t n, int width, double* out, float* out_f,

@@ -64,23 +64,8 @@ __device__ __forceinline__ RawP load_raw(const float* __restrict__ prm, int64_t 
 
 __device__ __forceinline__ RawP dummy_raw() { return RawP{1.f, 1.f, 1.f, 1.f, 1.f, 4.f}; }
 
-constexpr int kVpt = 2;          // vehicles per thread
+constexpr int kVpt = 2;          // vehicles per thread (one float2 lane pair)
 constexpr int kT = kCap / kVpt;   // 256 threads per CTA
-
-// Eq. 4 term of one observation, branch-free: observed iff finite (NaN =
-// missing).  Returns dL/dP; adds the loss term to acc.
-template <int KIND>
-__device__ __forceinline__ float loss_term(float o, float P, bool valid, float& acc) {
-    const float r = o - P;
-    const bool ok = valid && fabsf(o) <= 3.4e38f;
-    if (KIND == 0) {  // L1: |r|, dL/dP = -sign(r), sign(0) = 0 (R#11)
-        acc += ok ? fabsf(r) : 0.f;
-        const float sg = r > 0.f ? -1.f : (r < 0.f ? 1.f : 0.f);
-        return ok ? sg : 0.f;
-    }
-    acc = ok ? fmaf(r, r, acc) : acc;  // L2: r^2, dL/dP = -2 r
-    return ok ? -2.f * r : 0.f;
-}
 
 // fixed-order CTA reduction of one double per thread -> out[blockIdx.x] (deterministic)
 __device__ __forceinline__ void block_sum_to(double x, double* out) {
@@ -97,19 +82,22 @@ __device__ __forceinline__ void block_sum_to(double x, double* out) {
 }
 
 // ------------------------------------------------------------------------------ NK1
-// One CTA = one lane tile.  All `steps` steps run in one launch, in checkpoint segments of KS
-// steps (compile-time, fully unrolled; the K mod KS tail runs as one predicated segment); per
-// step one __syncthreads separates the speed publication from the leader read
-// (double-buffered exchange).  LOSS = 0: record P (idm_forward).  LOSS = 1 (L1) / 2 (L2):
-// fused Eq. 4 for idm_fit_step -- the observation rows of the next segment are prefetched into
-// registers while the current one runs; each step evaluates Eq. 4 against the fresh positions
-// and writes dL/dP instead of P.
+// One CTA = one lane tile; thread t owns the adjacent local vehicles 2t, 2t + 1 as one float2
+// lane pair (packed f32x2 arithmetic).  Vehicle 2t's leader is 2t + 1 (same thread); vehicle
+// 2t + 1's leader is 2t + 2, thread t + 1's first vehicle, so one speed per thread crosses shared
+// memory per step (one __syncthreads, double-buffered).  A lane head has leadf = 0, which zeroes
+// its interaction term whatever "leader" speed it reads.
+// All `steps` steps run in one launch, in segments of KS steps (compile-time, fully unrolled;
+// the K mod KS tail runs as one predicated segment).  LOSS = 0: record P (idm_forward).
+// LOSS = 1 (L1) / 2 (L2): fused Eq. 4 for idm_fit_step -- the observation rows of the next
+// segment are prefetched into registers while the current one runs; each step evaluates Eq. 4
+// against the fresh positions and writes dL/dP instead of P.
 // CK = checkpoint interval (the backward's segment length); the forward's own prefetch
 // segment is KS = max(4, CK) steps, so CK | KS and checkpoints fall at static positions.
 template <bool D4, bool KAHAN, bool RECV, int LOSS, int CK>
 __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? 3 : 4))) fwd_kernel(FwdArgs a) {
     constexpr int KS = CK > 4 ? CK : 4;
-    __shared__ float xv[2][kCap + 1];
+    __shared__ float xv[2][kT + 1];  // speed of each thread's first vehicle; [kT] = 0 sentinel
     const int tid = threadIdx.x;
     const int64_t base = a.tile_start[blockIdx.x];
     const int n_loc = (int)(a.tile_start[blockIdx.x + 1] - base);
@@ -117,115 +105,112 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? 3 : 4))) fwd_kernel(
     const int64_t N = a.n;
     const int steps = a.steps;
     const int nfull = steps / KS, tail = steps - nfull * KS;
+    const int id0 = 2 * tid;
+    const int64_t i0 = base + id0;
+    const bool val[2] = {id0 < n_loc, id0 + 1 < n_loc};
 
-    float s[kVpt], v[kVpt], D[kVpt], cmp[kVpt], p0[kVpt];
-    bool lead[kVpt], valid[kVpt];
-    VehP P[kVpt];
+    float sj[2], vj[2], pj[2], lf[2];
+    VehP Pj[2];
 #pragma unroll
-    for (int j = 0; j < kVpt; ++j) {
-        const int id = j * kT + tid;
-        const int64_t i = base + id;
-        valid[j] = id < n_loc;
-        D[j] = 0.f;
-        cmp[j] = 0.f;
+    for (int j = 0; j < 2; ++j) {
+        const int64_t i = i0 + j;
         RawP r = dummy_raw();
-        if (valid[j]) {
-            p0[j] = a.pos0[i];
-            v[j] = a.vel0[i];
-            lead[j] = a.lead[i] != 0;
-            s[j] = lead[j] ? (a.pos0[i + 1] - p0[j]) - a.length[i + 1] : 0.f;
+        sj[j] = 0.f; vj[j] = 0.f; pj[j] = 0.f; lf[j] = 0.f;
+        if (val[j]) {
+            pj[j] = a.pos0[i];
+            vj[j] = a.vel0[i];
+            const bool lead = a.lead[i] != 0;
+            lf[j] = lead ? 1.f : 0.f;
+            sj[j] = lead ? (a.pos0[i + 1] - pj[j]) - a.length[i + 1] : 0.f;
             r = load_raw(a.params, a.n_par, i);
             if (D4 && r.delta != 4.f)
                 atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
-        } else {
-            p0[j] = 0.f; v[j] = 0.f; s[j] = 0.f; lead[j] = false;
         }
-        P[j] = make_vehp(r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta);
+        Pj[j] = make_vehp(r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta);
     }
-    if (tid == 0) { xv[0][kCap] = 0.f; xv[1][kCap] = 0.f; }
+    float2 s = make_float2(sj[0], sj[1]), v = make_float2(vj[0], vj[1]);
+    const float2 p0 = make_float2(pj[0], pj[1]), leadf = make_float2(lf[0], lf[1]);
+    const VehPT<float2> P = pack(Pj[0], Pj[1]);
+    float2 D = f2(0.f), cmp = f2(0.f);
+    if (tid == 0) { xv[0][kT] = 0.f; xv[1][kT] = 0.f; }
 
-    // out: P row (LOSS = 0) or dL/dP row (LOSS) of the current step
-    float* orow = (LOSS ? a.grad_traj : a.traj) + base + tid;
-    float* vrow = RECV ? a.vel_traj + base + tid : nullptr;
-    float* cks = a.ckpt_s + base + tid;
-    float* ckv = a.ckpt_v + base + tid;
-    const float* obs = LOSS ? a.obs + base + tid : nullptr;
-    float onx[KS][kVpt];  // LOSS: observation rows of the next segment (registers)
-    float lseg = 0.f;     // loss of this thread's vehicles in this segment (fp32)
-    double lacc = 0.0;    // and across segments (fp64)
-    // prefetch the observation rows 1 .. KS (predicated for a short rollout)
+    auto put = [&](float* row, float2 x) {  // row points at local vehicle 2 tid
+        if (val[0]) __stcs(row, x.x);
+        if (val[1]) __stcs(row + 1, x.y);
+    };
+    // out: P row of the current step (LOSS = 0; the fused variant only sums Eq. 4)
+    float* orow = LOSS ? nullptr : a.traj + i0;
+    float* vrow = RECV ? a.vel_traj + i0 : nullptr;
+    // tile-local state history: speed row of every step, (gap, D, compensation) every CK steps
+    float2* vtp = reinterpret_cast<float2*>(a.vt + blockIdx.x * a.vt_stride) + tid;
+    float2* ckp = reinterpret_cast<float2*>(a.ckt + blockIdx.x * a.ck_stride) + tid;
+    constexpr int kR2 = kCap / 2;  // one row in float2 units
+    const float* obs = LOSS ? a.obs + i0 : nullptr;
+    const float qnan = __int_as_float(0x7fc00000);
+    float2 onx[KS];      // LOSS: observation rows of the next segment (registers)
+    float2 lseg = f2(0.f);  // loss of this thread's vehicles in this segment (fp32)
+    double lacc = 0.0;   // and across segments (fp64)
+    auto ld_obs = [&](const float* o) {  // absent vehicles observe NaN (= missing)
+        return make_float2(val[0] ? __ldcs(o) : qnan, val[1] ? __ldcs(o + 1) : qnan);
+    };
+    // prefetch the observation rows row0 .. row0 + nrows - 1
     auto prefetch = [&](int row0, int nrows) {
         const float* o = obs + (int64_t)row0 * N;
 #pragma unroll
-        for (int tt = 0; tt < KS; ++tt, o += N)
-#pragma unroll
-            for (int j = 0; j < kVpt; ++j)
-                onx[tt][j] = (valid[j] && tt < nrows) ? __ldcs(o + j * kT) : 0.f;
+        for (int tt = 0; tt < KS; ++tt, o += N) onx[tt] = tt < nrows ? ld_obs(o) : f2(qnan);
     };
     if (LOSS) prefetch(1, min(KS, steps));
-#pragma unroll
-    for (int j = 0; j < kVpt; ++j) {
-        if (!valid[j]) continue;
-        __stcs(orow + j * kT, LOSS ? loss_term<LOSS - 1>(obs[j * kT], p0[j], true, lseg) : p0[j]);
-        if (RECV) vrow[j * kT] = v[j];
-        cks[j * kT] = s[j];
-        ckv[j * kT] = v[j];
-    }
+    if (LOSS) (void)loss_term<LOSS - 1>(ld_obs(obs), p0, lseg);
+    else put(orow, p0);
+    if (RECV) put(vrow, v);
+    __stcs(vtp, v);
+    __stcs(ckp, s);
+    __stcs(ckp + kR2, D);
+    __stcs(ckp + 2 * kR2, cmp);
     int par = 0;
     // one synchronous step of the whole tile; o = this step's observations (LOSS)
-    auto step = [&](const float (&o)[kVpt]) {
-#pragma unroll
-        for (int j = 0; j < kVpt; ++j) xv[par][j * kT + tid] = v[j];
+    auto step = [&](float2 o) {
+        xv[par][tid] = v.x;
         __syncthreads();
-        float vl[kVpt];
-#pragma unroll
-        for (int j = 0; j < kVpt; ++j) vl[j] = xv[par][j * kT + tid + 1];
+        const float2 vl = make_float2(v.y, xv[par][tid + 1]);
         par ^= 1;
-#pragma unroll
-        for (int j = 0; j < kVpt; ++j) {
-            const float vlj = lead[j] ? vl[j] : v[j];
-            if (KAHAN) {  // compensated displacement for long horizons (C3)
-                const float y = __fmaf_rn(k.dt, v[j], -cmp[j]);
-                const float tt2 = __fadd_rn(D[j], y);
-                cmp[j] = __fsub_rn(__fsub_rn(tt2, D[j]), y);
-                D[j] = tt2;
-            } else {
-                D[j] = __fmaf_rn(k.dt, v[j], D[j]);
-            }
-            fwd_step<D4>(s[j], v[j], vlj, lead[j], P[j], k);
+        if (KAHAN) {  // compensated displacement for long horizons (C3)
+            const float2 y = vfma(v, k.dt, vneg(cmp));
+            const float2 t2 = vadd(D, y);
+            cmp = vsub(vsub(t2, D), y);
+            D = t2;
+        } else {
+            D = vfma(v, k.dt, D);
         }
-        orow += N;
+        fwd_step<D4>(s, v, vl, leadf, P, k);
+        if (!LOSS) orow += N;
         if (RECV) vrow += N;
-#pragma unroll
-        for (int j = 0; j < kVpt; ++j) {
-            const float Pv = __fadd_rn(p0[j], D[j]);
-            const float out = LOSS ? loss_term<LOSS - 1>(o[j], Pv, valid[j], lseg) : Pv;
-            if (valid[j]) {
-                __stcs(orow + j * kT, out);
-                if (RECV) vrow[j * kT] = v[j];
-            }
-        }
+        vtp += kR2;
+        const float2 Pv = vadd(p0, D);
+        if (LOSS) (void)loss_term<LOSS - 1>(o, Pv, lseg);
+        else put(orow, Pv);
+        __stcs(vtp, v);
+        if (RECV) put(vrow, v);
     };
-    auto checkpoint = [&](int t0) {  // (gap, speed) at step t0 > 0 + finiteness check
-        cks += N;
-        ckv += N;
-#pragma unroll
-        for (int j = 0; j < kVpt; ++j) {
-            if (!valid[j]) continue;
-            cks[j * kT] = s[j];
-            ckv[j * kT] = v[j];
-            if (!(isfinite(s[j]) && isfinite(v[j]) && isfinite(D[j])))
-                report_nonfinite(a.status, t0, base + j * kT + tid);
-        }
+    auto finite2 = [&](int t0) {
+        const bool ok0 = isfinite(s.x) && isfinite(v.x) && isfinite(D.x);
+        const bool ok1 = isfinite(s.y) && isfinite(v.y) && isfinite(D.y);
+        if (val[0] && !ok0) report_nonfinite(a.status, t0, i0);
+        if (val[1] && !ok1) report_nonfinite(a.status, t0, i0 + 1);
+    };
+    auto checkpoint = [&](int t0) {  // (gap, D, compensation) at step t0 > 0 + finiteness check
+        ckp += kCkRows * kR2;
+        __stcs(ckp, s);
+        __stcs(ckp + kR2, D);
+        __stcs(ckp + 2 * kR2, cmp);
+        finite2(t0);
     };
     for (int seg = 0; seg < nfull; ++seg) {
         const int t0 = seg * KS;
-        float ocur[KS][kVpt];
+        float2 ocur[KS];
         if (LOSS) {
 #pragma unroll
-            for (int tt = 0; tt < KS; ++tt)
-#pragma unroll
-                for (int j = 0; j < kVpt; ++j) ocur[tt][j] = onx[tt][j];
+            for (int tt = 0; tt < KS; ++tt) ocur[tt] = onx[tt];
             const int nxt = (seg + 1) * KS;  // the next segment observes rows nxt+1 ..
             if (nxt < steps) prefetch(nxt + 1, min(KS, steps - nxt));
         }
@@ -235,8 +220,8 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? 3 : 4))) fwd_kernel(
             step(ocur[tt]);
         }
         if (LOSS) {
-            lacc += (double)lseg;
-            lseg = 0.f;
+            lacc += (double)lseg.x + (double)lseg.y;
+            lseg = f2(0.f);
         }
     }
     if (tail > 0) {
@@ -248,205 +233,297 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? 3 : 4))) fwd_kernel(
             }
         }
     }
-#pragma unroll
-    for (int j = 0; j < kVpt; ++j) {
-        if (!valid[j]) continue;
-        const int64_t i = base + j * kT + tid;
-        if (!(isfinite(s[j]) && isfinite(v[j]) && isfinite(D[j])))
-            report_nonfinite(a.status, steps, i);
-        if (a.state_out) {
-            a.state_out[i] = __fadd_rn(p0[j], D[j]);
-            a.state_out[N + i] = v[j];
-        }
+    finite2(steps);
+    if (a.state_out) {
+        put(a.state_out + i0, vadd(p0, D));
+        put(a.state_out + N + i0, v);
     }
-    if (LOSS) block_sum_to(lacc + (double)lseg, a.loss_partials);
+    if (LOSS) block_sum_to(lacc + (double)lseg.x + (double)lseg.y, a.loss_partials);
 }
+
+// ------------------------------------------------------------------------------ async copies
+// 1-D bulk copies (global -> shared, completion counted on an mbarrier in bytes): the
+// tile-local rows are 16-byte aligned and contiguous, so one elected thread moves a whole
+// 2 KB row per instruction and no register holds data in flight.
+namespace {
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "IDM_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra IDM_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// per-thread 4-byte async copy global -> shared (src_size 0: zero-fill, nothing read)
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool on) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(on ? 4 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+}  // namespace
 
 // ------------------------------------------------------------------------------ NK3
-// Per CTA (lane tile), segments of KS steps (compile-time, unrolled) from last to first:
-//   recompute: reload the (gap, speed) checkpoint (prefetched one segment ahead) and re-run the
-//              segment bit-identically; per step store the speed (leader reads) and the 24-byte
-//              local-Jacobian record in shared memory; the segment's dL/dP rows are loaded into
-//              registers meanwhile;
-//   reverse:   sweep the segment backwards from the stored records; the follower -> leader
-//              adjoint term F passes through shared memory (local id -> id + 1).
+// Per CTA (lane tile, thread t = vehicles 2t, 2t + 1 as in NK1), segments of KS steps from last
+// to first.  The forward stored every vehicle's speed at every step and (gap, displacement,
+// compensation) at every KS-th step in the tile-local rows, so nothing here is a long serial
+// chain: inside a segment the gaps and displacements follow from the checkpoint by the
+// forward's own one-FMA recurrences (bit-identical), every step's local Jacobian (core +
+// jac_record) depends only on stored state, and the one sequential dependency left is the
+// adjoint itself -- lambda^{t+1} -> lambda^t plus the follower -> leader term F of vehicle
+// 2t + 1, passed to thread t + 1 through shared memory (one barrier per step).  The next
+// segment's rows are prefetched into registers while the current one is swept.
+//   GOBS = 0:      dL/dP rows from grad_traj (idm_backward after idm_loss_grad);
+//   GOBS = 1 + k:  fused idm_fit_step -- dL/dP re-derived from obs and the rebuilt positions
+//                  P = p0 + D with the forward's loss term (same bits as idm_loss_grad).
 // Gradient accumulators stay in registers for the whole rollout; ADAM: per-vehicle Adam in the
 // epilogue (idm_fit_step).
-template <int KS>
-constexpr size_t bwd_smem_of() {
-    return (size_t)KS * (kCap * (sizeof(float4) + sizeof(float2)) + (kCap + 1) * sizeof(float));
-}
-
-template <bool D4, bool SHARED, bool ADAM, int KS>
+template <bool D4, bool SHARED, bool ADAM, int KS, int GOBS, bool KAHAN>
 #ifndef IDM_BWD_MINB
-#define IDM_BWD_MINB 3  // CTAs per SM the backward is register-budgeted for (80 registers)
+#define IDM_BWD_MINB 2  // CTAs per SM the backward is register-budgeted for (128 registers)
 #endif
 __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(BwdArgs a) {
-    constexpr int HS = kCap + 1;
-    extern __shared__ __align__(16) float4 smem4[];
-    float4* hR1 = smem4;                                                  // [KS][kCap]
-    float2* hR2 = reinterpret_cast<float2*>(hR1 + KS * kCap);             // [KS][kCap]
-    float* hv = reinterpret_cast<float*>(hR2 + KS * kCap);                // [KS][kCap + 1]
-    __shared__ float fx[2][kCap + 1];
+    __shared__ float fx[2][kT + 1];
     const int tid = threadIdx.x;
     const int64_t base = a.tile_start[blockIdx.x];
     const int n_loc = (int)(a.tile_start[blockIdx.x + 1] - base);
     const Consts k = a.k;
     const int64_t N = a.n;
     const int steps = a.steps;
-
-    float ls[kVpt], lv[kVpt], lD[kVpt], s[kVpt], v[kVpt], cs[kVpt], cv[kVpt];
-    bool lead[kVpt], valid[kVpt];
-    VehP P[kVpt];
-    VehB B[kVpt];
-    GradAcc G[kVpt];
+    const int id0 = 2 * tid;
+    const int64_t i0 = base + id0;
+    const bool val[2] = {id0 < n_loc, id0 + 1 < n_loc};
     const int nseg = (steps + KS - 1) / KS;
+    const int tail = steps - (nseg - 1) * KS;  // length of the last segment (1..KS)
+
+    float lf[2], ldj[2], pj[2];
+    VehP Pj[2];
+    VehB Bj[2];
 #pragma unroll
-    for (int j = 0; j < kVpt; ++j) {
-        const int id = j * kT + tid;
-        const int64_t i = base + id;
-        valid[j] = id < n_loc;
-        ls[j] = 0.f;
-        lv[j] = 0.f;
-        G[j] = GradAcc{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < 2; ++j) {
+        const int64_t i = i0 + j;
         RawP r = dummy_raw();
-        lead[j] = false;
-        lD[j] = 0.f;
-        cs[j] = 0.f;
-        cv[j] = 0.f;
-        if (valid[j]) {
-            lead[j] = a.lead[i] != 0;
+        lf[j] = 0.f;
+        ldj[j] = 0.f;
+        pj[j] = 0.f;
+        if (val[j]) {
+            lf[j] = a.lead[i] != 0 ? 1.f : 0.f;
             r = load_raw(a.params, a.n_par, i);
             if (D4 && r.delta != 4.f)
                 atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
-            lD[j] = a.grad_traj[(int64_t)steps * N + i];   // lambda_D^K = dL/dP(K)
-            cs[j] = a.ckpt_s[(int64_t)(nseg - 1) * N + i];  // checkpoint of the last segment
-            cv[j] = a.ckpt_v[(int64_t)(nseg - 1) * N + i];
+            if (!GOBS) ldj[j] = a.grad_traj[(int64_t)steps * N + i];  // lambda_D^K = dL/dP(K)
+            else pj[j] = a.pos0[i];
         }
-        P[j] = make_vehp(r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta);
-        B[j] = make_vehb(r.a_max, r.a_pref, r.v_targ, r.delta);
+        Pj[j] = make_vehp(r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta);
+        Bj[j] = make_vehb(r.a_max, r.a_pref, r.v_targ, r.delta);
     }
-    if (tid == 0) { fx[0][0] = 0.f; fx[1][0] = 0.f; }  // never written again (slots id+1 >= 1)
+    const float2 leadf = make_float2(lf[0], lf[1]);
+    const float2 p0 = make_float2(pj[0], pj[1]);
+    const VehPT<float2> P = pack(Pj[0], Pj[1]);
+    const VehBT<float2> B = pack(Bj[0], Bj[1]);
+    float2 lD = make_float2(ldj[0], ldj[1]);
+    float2 ls = f2(0.f), lv = f2(0.f);
+    GradAccT<float2> G = {f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
+    if (tid == 0) { fx[0][0] = 0.f; fx[1][0] = 0.f; }  // never written again (slots t+1 >= 1)
 
+    // Segment rows are staged in shared memory, two segments ahead, in a ring of 3 buffers:
+    // speeds and the checkpoint by bulk copy (one thread, mbarrier-counted), dL/dP rows (or the
+    // observation rows, plus one for the rollout's last step) by per-thread cp.async.  No
+    // register holds data in flight.
+    extern __shared__ __align__(16) float smem_b[];
+    constexpr int NB = 3;
+    constexpr int VP = kCap + 4;  // speed row pitch: [kCap] = 0 is the leader read of slot 511
+    constexpr int KO = GOBS ? KS + 1 : KS;
+    float* vrow = smem_b;                              // [NB][KS][VP]
+    float* ckrow = vrow + NB * KS * VP;                // [NB][3][kCap]
+    float* orow = ckrow + NB * kCkRows * kCap;         // [NB][KO][kCap]
+    __shared__ __align__(8) uint64_t mbar[NB];
+    constexpr int nckr = GOBS ? (KAHAN ? 3 : 2) : 1;   // checkpoint rows used
+    if (tid == 0) {
+#pragma unroll
+        for (int q = 0; q < NB; ++q) mbar_init(&mbar[q], 1);
+        mbar_fence_init();
+    }
+    if (tid < NB * KS) vrow[tid * VP + kCap] = 0.f;
+    __syncthreads();
+    uint32_t phase = 0;  // bit q: parity of buffer q's next completion
+    auto fetch = [&](int seg, int len) {
+        const int b = seg % NB;
+        const int64_t t0 = (int64_t)seg * KS;
+        if (tid == 0) {
+            // buffer b was last read (generic proxy) before the barriers of an earlier
+            // segment; order those reads before the async-proxy writes
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const uint32_t bytes = (uint32_t)(len + nckr) * kCap * sizeof(float);
+            mbar_expect_tx(&mbar[b], bytes);
+            const float* src = a.vt + blockIdx.x * a.vt_stride + t0 * kCap;
+            for (int tt = 0; tt < len; ++tt)
+                bulk_g2s(vrow + (b * KS + tt) * VP, src + tt * kCap, kCap * sizeof(float), &mbar[b]);
+            bulk_g2s(ckrow + b * kCkRows * kCap,
+                     a.ckt + blockIdx.x * a.ck_stride + (int64_t)seg * kCkRows * kCap,
+                     nckr * kCap * sizeof(float), &mbar[b]);
+        }
+        const float* src = (GOBS ? a.obs : a.grad_traj) + t0 * N + i0;
+        float* dst = orow + b * KO * kCap + 2 * tid;
+#pragma unroll
+        for (int tt = 0; tt < KO; ++tt, src += N) {
+            const bool on = tt < len || (GOBS && tt == len && seg == nseg - 1);
+            cp_async4(dst + tt * kCap, src, val[0] && on);
+            cp_async4(dst + tt * kCap + 1, src + 1, val[1] && on);
+        }
+        cp_async_commit();
+    };
     int par = 0;
-    // one checkpoint segment [t0, t0 + len); FULL (len == KS) drops every step predicate
-    auto run_segment = [&](const int seg, const int len, auto FULL) {
+    fetch(nseg - 1, tail);
+    if (nseg > 1) fetch(nseg - 2, KS);
+    auto segment = [&](const int seg, const int len, auto FULL) {
         constexpr bool kFull = decltype(FULL)::value;
-        const int t0 = seg * KS;
-        // ---- this segment's dL/dP rows into registers (consumed by the reverse sweep)
-        float gr_[KS][kVpt];
-        {
-            const float* g = a.grad_traj + (int64_t)t0 * N + base + tid;
-#pragma unroll
-            for (int tt = 0; tt < KS; ++tt, g += N)
-#pragma unroll
-                for (int j = 0; j < kVpt; ++j)
-                    gr_[tt][j] = (valid[j] && (kFull || tt < len)) ? __ldcs(g + j * kT) : 0.f;
-        }
-        // ---- recompute the segment from its checkpoint; prefetch the next one
-#pragma unroll
-        for (int j = 0; j < kVpt; ++j) {
-            s[j] = cs[j];
-            v[j] = cv[j];
-        }
-        if (seg > 0) {
-            const int64_t off = (int64_t)(seg - 1) * N + base + tid;
-#pragma unroll
-            for (int j = 0; j < kVpt; ++j) {
-                if (valid[j]) {
-                    cs[j] = a.ckpt_s[off + j * kT];
-                    cv[j] = a.ckpt_v[off + j * kT];
-                }
-            }
-        }
+        const int b = seg % NB;
+        mbar_wait(&mbar[b], (phase >> b) & 1u);
+        phase ^= 1u << b;
+        if (seg > 0) cp_async_wait<1>();  // this segment's rows; seg - 1's may stay in flight
+        else cp_async_wait<0>();
+        const float* orr = orow + b * KO * kCap + 2 * tid;
+        float2 v[KS], g[KO], vl[KS], sg[KS];
+        const float* vr = vrow + b * KS * VP + 2 * tid;
 #pragma unroll
         for (int tt = 0; tt < KS; ++tt) {
-            if (kFull || tt < len) {  // CTA-uniform
-                float* hvr = hv + tt * HS + tid;
+            if (kFull || tt < len) {
+                v[tt] = *reinterpret_cast<const float2*>(vr + tt * VP);
+                vl[tt] = make_float2(v[tt].y, vr[tt * VP + 2]);
+            } else {
+                v[tt] = f2(0.f);
+                vl[tt] = f2(0.f);
+            }
+        }
 #pragma unroll
-                for (int j = 0; j < kVpt; ++j) hvr[j * kT] = v[j];
-                __syncthreads();
+        for (int tt = 0; tt < KO; ++tt)
+            g[tt] = (kFull || tt <= len) ? *reinterpret_cast<const float2*>(orr + tt * kCap) : f2(0.f);
+        // gaps (and positions) inside the segment: the forward's recurrences from the
+        // checkpoint, bitwise
+        const float* cr = ckrow + b * kCkRows * kCap + 2 * tid;
+        float2 s = *reinterpret_cast<const float2*>(cr);
+        float2 D = f2(0.f), cmp = f2(0.f);
+        if (GOBS) D = *reinterpret_cast<const float2*>(cr + kCap);
+        if (GOBS && KAHAN) cmp = *reinterpret_cast<const float2*>(cr + 2 * kCap);
 #pragma unroll
-                for (int j = 0; j < kVpt; ++j) {
-                    const float vl = lead[j] ? hvr[j * kT + 1] : v[j];
-                    Core c;
-                    core<D4>(s[j], v[j], vl, lead[j], P[j], k, c);
-                    float4 R1;
-                    float2 R2;
-                    jac_record<D4>(c, s[j], v[j], lead[j], P[j], B[j], k, R1, R2);
-                    hR1[tt * kCap + j * kT + tid] = R1;
-                    hR2[tt * kCap + j * kT + tid] = R2;
-                    if (tt + 1 < (kFull ? KS : len)) advance(c, s[j], v[j], lead[j], k);
+        for (int tt = 0; tt < KO; ++tt) {
+            if (GOBS) {
+                // dL/dP at step t0 + tt (the forward's loss term on the same P bits); the
+                // rollout's last step K adds its term to lambda_D^K below
+                float2 dummy = f2(0.f);
+                if (kFull || tt <= len) g[tt] = loss_term<GOBS - 1>(g[tt], vadd(p0, D), dummy);
+            }
+            if (tt < KS) {
+                sg[tt] = s;
+                if (kFull || tt < len) {
+                    s = vfma(vsub(v[tt], vl[tt]), -k.dt, s);
+                    if (GOBS) {
+                        if (KAHAN) {
+                            const float2 y = vfma(v[tt], k.dt, vneg(cmp));
+                            const float2 t2 = vadd(D, y);
+                            cmp = vsub(vsub(t2, D), y);
+                            D = t2;
+                        } else {
+                            D = vfma(v[tt], k.dt, D);
+                        }
+                    }
                 }
             }
         }
-        // ---- reverse sweep, t = t0 + len - 1 ... t0 (reads only this thread's records and
-        //      the speed rows, all written before the last recompute barrier)
+        if (GOBS && seg == nseg - 1) {  // lambda_D^K = dL/dP(K) (static selects, no indexing)
+#pragma unroll
+            for (int tt = 0; tt < KO; ++tt)
+                if (tt == len) lD = g[tt];
+        }
+        if (seg > 1) fetch(seg - 2, KS);
+        // reverse sweep t = t0 + len - 1 ... t0; the local Jacobian of the next step down is
+        // independent of the adjoint chain, so the scheduler overlaps it with this one
 #pragma unroll
         for (int tt = KS - 1; tt >= 0; --tt) {
             if (kFull || tt < len) {  // CTA-uniform
-                const float* hvr = hv + tt * HS + tid;
-                float F[kVpt];
-#pragma unroll
-                for (int j = 0; j < kVpt; ++j) {
-                    const float vj = hvr[j * kT];
-                    const float vl = lead[j] ? hvr[j * kT + 1] : vj;
-                    F[j] = bwd_from_record<D4>(hR1[tt * kCap + j * kT + tid],
-                                               hR2[tt * kCap + j * kT + tid], vj, vl, P[j], B[j],
-                                               k, ls[j], lv[j], lD[j], G[j]);
-                }
-#pragma unroll
-                for (int j = 0; j < kVpt; ++j) fx[par][j * kT + tid + 1] = F[j];
+                CoreT<float2> c;
+                core<D4>(sg[tt], v[tt], vl[tt], leadf, P, k, c);
+                const RecT<float2> R = jac_record<D4>(c, sg[tt], v[tt], P, B, k);
+                const float2 F = bwd_from_record<D4>(R, v[tt], vl[tt], P, B, k, ls, lv, lD, G);
+                fx[par][tid + 1] = F.y;  // vehicle 2t + 1 -> its leader 2t + 2 (thread t + 1)
                 __syncthreads();
-#pragma unroll
-                for (int j = 0; j < kVpt; ++j) {
-                    lv[j] += fx[par][j * kT + tid];  // F from the follower (id - 1)
-                    lD[j] += gr_[tt][j];             // lambda_D^t = g^t + lambda_D^{t+1}
-                }
+                // F from the follower: 2t - 1 (thread t - 1) for 2t, 2t (this thread) for 2t + 1
+                lv = vadd(lv, make_float2(fx[par][tid], F.x));
+                lD = vadd(lD, g[tt]);  // lambda_D^t = g^t + lambda_D^{t+1}
                 par ^= 1;
             }
         }
     };
-    const int tail = steps - (nseg - 1) * KS;  // length of the last segment (1..KS)
     int seg = nseg - 1;
-    if (tail < KS) run_segment(seg--, tail, std::false_type{});
-    for (; seg >= 0; --seg) run_segment(seg, KS, std::true_type{});
+    if (tail < KS) segment(seg--, tail, std::false_type{});
+    for (; seg >= 0; --seg) segment(seg, KS, std::true_type{});
     // dL/dp0_i = lambda_D - lambda_s_i + lambda_s_{follower}; dL/dv0 = lambda_v
-#pragma unroll
-    for (int j = 0; j < kVpt; ++j) fx[par][j * kT + tid + 1] = lead[j] ? ls[j] : 0.f;
+    const float2 lsl = vmul(ls, leadf);
+    fx[par][tid + 1] = lsl.y;
     __syncthreads();
-    float gp0[kVpt];
-#pragma unroll
-    for (int j = 0; j < kVpt; ++j)
-        gp0[j] = lD[j] - (lead[j] ? ls[j] : 0.f) + fx[par][j * kT + tid];
+    const float2 gp0 = vadd(vsub(lD, lsl), make_float2(fx[par][tid], lsl.x));
 
     // parameter gradients from the factored accumulators
+    const float Sj[6][2] = {{G.S1.x, G.S1.y}, {G.S2.x, G.S2.y}, {G.S3.x, G.S3.y},
+                            {G.S4.x, G.S4.y}, {G.S5.x, G.S5.y}, {G.S6.x, G.S6.y}};
+    const float lvj[2] = {lv.x, lv.y}, gpj[2] = {gp0.x, gp0.y};
     float gr[kVpt][6];
 #pragma unroll
     for (int j = 0; j < kVpt; ++j) {
 #pragma unroll
         for (int q = 0; q < 6; ++q) gr[j][q] = 0.f;
-        if (!valid[j]) continue;
-        const int64_t i = base + j * kT + tid;
+        if (!val[j]) continue;
+        const int64_t i = i0 + j;
         const RawP r = load_raw(a.params, a.n_par, i);
         const float c = 0.5f / sqrtf(r.a_max * r.a_pref);
-        gr[j][0] = G[j].S1 - c * (0.5f / r.a_max) * G[j].S2;             // a_max
-        gr[j][1] = -c * (0.5f / r.a_pref) * G[j].S2;                      // a_pref
-        gr[j][2] = G[j].S3;                                               // s_min
-        gr[j][3] = G[j].S4;                                               // T_pref
-        gr[j][4] = r.a_max * r.delta / r.v_targ * G[j].S5;               // v_targ
-        gr[j][5] = -r.a_max * kLn2 * G[j].S6;                             // delta
+        gr[j][0] = Sj[0][j] - c * (0.5f / r.a_max) * Sj[1][j];           // a_max
+        gr[j][1] = -c * (0.5f / r.a_pref) * Sj[1][j];                     // a_pref
+        gr[j][2] = Sj[2][j];                                              // s_min
+        gr[j][3] = Sj[3][j];                                              // T_pref
+        gr[j][4] = r.a_max * r.delta / r.v_targ * Sj[4][j];               // v_targ
+        gr[j][5] = -r.a_max * kLn2 * Sj[5][j];                            // delta
         if (a.grad_state0) {
-            a.grad_state0[i] = gp0[j];
-            a.grad_state0[N + i] = lv[j];
+            a.grad_state0[i] = gpj[j];
+            a.grad_state0[N + i] = lvj[j];
         }
-        if (!(isfinite(lv[j]) && isfinite(gp0[j]))) report_nonfinite(a.status, 0, i);
+        if (!(isfinite(lvj[j]) && isfinite(gpj[j]))) report_nonfinite(a.status, 0, i);
     }
     if (!SHARED) {
 #pragma unroll
         for (int j = 0; j < kVpt; ++j) {
-            if (!valid[j]) continue;
-            const int64_t i = base + j * kT + tid;
+            if (!val[j]) continue;
+            const int64_t i = i0 + j;
 #pragma unroll
             for (int q = 0; q < 6; ++q) {
                 a.grad_params[q * N + i] = gr[j][q];
@@ -591,17 +668,16 @@ cudaError_t launch_validate(const ValidateArgs& a, cudaStream_t st) {
 
 bool ckpt_supported(int k) { return k == 2 || k == 4 || k == 8; }
 
-size_t bwd_smem_bytes(int ckpt_every) {
-    return ckpt_every == 2 ? bwd_smem_of<2>() : ckpt_every == 8 ? bwd_smem_of<8>()
-                                                                : bwd_smem_of<4>();
-}
+size_t bwd_smem_bytes(int) { return 0; }  // the backward uses static shared memory only
 
 template <bool D4, bool KH, int KS>
 static void launch_fwd_k(const FwdArgs& a, int ntiles, const FwdVariant& var, cudaStream_t st) {
     dim3 g(ntiles), b(kT);
-    if (var.loss == 1) fwd_kernel<D4, KH, false, 1, KS><<<g, b, 0, st>>>(a);
-    else if (var.loss == 2) fwd_kernel<D4, KH, false, 2, KS><<<g, b, 0, st>>>(a);
-    else if (var.rec_v) fwd_kernel<D4, KH, true, 0, KS><<<g, b, 0, st>>>(a);
+    if constexpr (KS == 4) {  // the fused idm_fit_step forward exists for 4-step segments
+        if (var.loss == 1) { fwd_kernel<D4, KH, false, 1, KS><<<g, b, 0, st>>>(a); return; }
+        if (var.loss == 2) { fwd_kernel<D4, KH, false, 2, KS><<<g, b, 0, st>>>(a); return; }
+    }
+    if (var.rec_v) fwd_kernel<D4, KH, true, 0, KS><<<g, b, 0, st>>>(a);
     else fwd_kernel<D4, KH, false, 0, KS><<<g, b, 0, st>>>(a);
 }
 
@@ -626,53 +702,70 @@ cudaError_t launch_fwd(const FwdArgs& a, int ntiles, const FwdVariant& var, cuda
     return cudaGetLastError();
 }
 
-template <int KS>
-static cudaError_t configure_k() {
-    cudaError_t e = cudaSuccess;
-    const int mb = (int)bwd_smem_of<KS>();
-#define IDM_CFG(D4, SH, AD)                                                                 \
-    if (e == cudaSuccess)                                                                  \
-        e = cudaFuncSetAttribute(bwd_kernel<D4, SH, AD, KS>,                               \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, mb);
-    IDM_CFG(true, true, false) IDM_CFG(true, false, false) IDM_CFG(false, true, false)
-    IDM_CFG(false, false, false) IDM_CFG(true, false, true) IDM_CFG(false, false, true)
-#undef IDM_CFG
-    return e;
+cudaError_t kernels_configure(int ckpt_every) {
+    return ckpt_supported(ckpt_every) ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-cudaError_t kernels_configure(int ckpt_every) {
-    switch (ckpt_every) {
-        case 2: return configure_k<2>();
-        case 4: return configure_k<4>();
-        case 8: return configure_k<8>();
+template <int KS, int GOBS>
+constexpr size_t bwd_smem_of() {  // ring of 3: speed rows + checkpoint rows + dL/dP/obs rows
+    return (size_t)3 * (KS * (kCap + 4) + kCkRows * kCap + (GOBS ? KS + 1 : KS) * kCap) *
+           sizeof(float);
+}
+
+template <bool D4, bool SH, bool AD, int KS, int GO, bool KH>
+static void launch_bwd_v(const BwdArgs& a, int ntiles, cudaStream_t st) {
+    constexpr size_t smem = bwd_smem_of<KS, GO>();
+    static bool configured = false;  // one opt-in per instantiation (one device per process)
+    if (!configured) {
+        cudaFuncSetAttribute(bwd_kernel<D4, SH, AD, KS, GO, KH>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    bwd_kernel<D4, SH, AD, KS, GO, KH><<<ntiles, kT, smem, st>>>(a);
+}
+
+template <bool D4, int KS>
+static void launch_bwd_k(const BwdArgs& a, int ntiles, bool shared, bool adam, cudaStream_t st) {
+    if (shared) launch_bwd_v<D4, true, false, KS, 0, false>(a, ntiles, st);
+    else if (adam) launch_bwd_v<D4, false, true, KS, 0, false>(a, ntiles, st);
+    else launch_bwd_v<D4, false, false, KS, 0, false>(a, ntiles, st);
+}
+
+// fused idm_fit_step backward (ckpt_every == 4): dL/dP from obs
+template <bool D4, int GO, bool KH>
+static void launch_bwd_obs(const BwdArgs& a, int ntiles, bool shared, cudaStream_t st) {
+    if (shared) launch_bwd_v<D4, true, false, 4, GO, KH>(a, ntiles, st);
+    else launch_bwd_v<D4, false, true, 4, GO, KH>(a, ntiles, st);
+}
+
+template <bool D4>
+static cudaError_t launch_bwd_d(const BwdArgs& a, int ntiles, bool shared, bool adam, int gobs,
+                                bool kahan, cudaStream_t st) {
+    if (gobs) {
+        if (a.ckpt_every != 4) return cudaErrorInvalidValue;
+        if (gobs == 1) {
+            if (kahan) launch_bwd_obs<D4, 1, true>(a, ntiles, shared, st);
+            else launch_bwd_obs<D4, 1, false>(a, ntiles, shared, st);
+        } else {
+            if (kahan) launch_bwd_obs<D4, 2, true>(a, ntiles, shared, st);
+            else launch_bwd_obs<D4, 2, false>(a, ntiles, shared, st);
+        }
+        return cudaSuccess;
+    }
+    switch (a.ckpt_every) {
+        case 2: launch_bwd_k<D4, 2>(a, ntiles, shared, adam, st); break;
+        case 4: launch_bwd_k<D4, 4>(a, ntiles, shared, adam, st); break;
+        case 8: launch_bwd_k<D4, 8>(a, ntiles, shared, adam, st); break;
         default: return cudaErrorInvalidValue;
     }
-}
-
-template <int KS>
-static void launch_bwd_k(const BwdArgs& a, int ntiles, bool delta4, bool shared, bool adam,
-                         cudaStream_t st) {
-    const size_t smem = bwd_smem_of<KS>();
-    dim3 g(ntiles), b(kT);
-    if (delta4) {
-        if (shared) bwd_kernel<true, true, false, KS><<<g, b, smem, st>>>(a);
-        else if (adam) bwd_kernel<true, false, true, KS><<<g, b, smem, st>>>(a);
-        else bwd_kernel<true, false, false, KS><<<g, b, smem, st>>>(a);
-    } else {
-        if (shared) bwd_kernel<false, true, false, KS><<<g, b, smem, st>>>(a);
-        else if (adam) bwd_kernel<false, false, true, KS><<<g, b, smem, st>>>(a);
-        else bwd_kernel<false, false, false, KS><<<g, b, smem, st>>>(a);
-    }
+    return cudaSuccess;
 }
 
 cudaError_t launch_bwd(const BwdArgs& a, int ntiles, bool delta4, bool shared, bool adam,
-                       cudaStream_t st) {
-    switch (a.ckpt_every) {
-        case 2: launch_bwd_k<2>(a, ntiles, delta4, shared, adam, st); break;
-        case 4: launch_bwd_k<4>(a, ntiles, delta4, shared, adam, st); break;
-        case 8: launch_bwd_k<8>(a, ntiles, delta4, shared, adam, st); break;
-        default: return cudaErrorInvalidValue;
-    }
+                       int gobs, bool kahan, cudaStream_t st) {
+    cudaError_t e = delta4 ? launch_bwd_d<true>(a, ntiles, shared, adam, gobs, kahan, st)
+                           : launch_bwd_d<false>(a, ntiles, shared, adam, gobs, kahan, st);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

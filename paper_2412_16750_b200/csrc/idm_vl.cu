@@ -137,9 +137,9 @@ __global__ void __launch_bounds__(kVT) vl_fwd_kernel(VlArgs a) {
                 for (int j = 0; j < kVV; ++j) {
                     D[j] = __fmaf_rn(k.dt, v[j], D[j]);
                     Core c;
-                    core_dv<D4>(dp[tt][j], v[j], dv[tt][j], true, P[j], k, c);
+                    core_dv<D4>(dp[tt][j], v[j], dv[tt][j], 1.f, P[j], k, c);
                     float sdummy = 0.f;
-                    advance(c, sdummy, v[j], false, k);
+                    advance(c, sdummy, v[j], k);
                     const float Pv = __fadd_rn(p0[j], D[j]);
                     const float out =
                         LOSS ? vl_loss_term(LOSS - 1, ob[tt][j], Pv, valid[j], lseg) : Pv;
@@ -232,9 +232,9 @@ __global__ void __launch_bounds__(kVT) vl_bwd_kernel(VlArgs a) {
 #pragma unroll
                 for (int j = 0; j < kVV; ++j) {
                     Core c;
-                    core_dv<D4>(dp[tt][j], vt[tt][j], dv[tt][j], true, P[j], k, c);
+                    core_dv<D4>(dp[tt][j], vt[tt][j], dv[tt][j], 1.f, P[j], k, c);
                     float sdummy = 0.f, vn = vt[tt][j];
-                    advance(c, sdummy, vn, false, k);
+                    advance(c, sdummy, vn, k);
                     vt[tt + 1][j] = vn;
                 }
             }
@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kVT) vl_bwd_kernel(VlArgs a) {
 #pragma unroll
                 for (int j = 0; j < kVV; ++j) {
                     Core c;
-                    core_dv<D4>(dp[tt][j], vt[tt][j], dv[tt][j], true, P[j], k, c);
+                    core_dv<D4>(dp[tt][j], vt[tt][j], dv[tt][j], 1.f, P[j], k, c);
                     float gdp, gdv;
                     bwd_vl<D4>(c, dp[tt][j], vt[tt][j], P[j], B[j], k, lv[j], lD[j], G[j], gdp,
                                gdv);

@@ -313,31 +313,34 @@ def test_step_host_matches_device_path(idm, oracle):
 
 
 # ------------------------------------------------------------------- fused iteration
-@pytest.mark.parametrize("kind", ["l1", "l2"])
-def test_fit_step_equals_separate_calls(idm, kind):
-    """idm_fit_step (fused fwd+Eq.4, bwd+Adam) computes exactly the separate-call sequence:
-    same dL/dP, gradients and parameters bit for bit, loss equal to rounding of the fp64 sum
-    order; ragged multi-tile lanes, missing (NaN) observations."""
+@pytest.mark.parametrize("kind,ckpt,K", [("l1", 4, 90), ("l2", 4, 90), ("l1", 4, 92),
+                                          ("l1", 8, 90), ("l2", 2, 91)])
+def test_fit_step_equals_separate_calls(idm, kind, ckpt, K):
+    """idm_fit_step computes exactly the separate-call sequence: gradients, grad_state0, Adam
+    moments and parameters bit for bit, loss equal to rounding of the fp64 sum order; ragged
+    multi-tile lanes, missing (NaN) observations, full and partial last segments.  ckpt 4 is the
+    fused path (the backward re-derives dL/dP from obs and the rebuilt positions); other
+    intervals run the defining sequence."""
     cap = idm.load_library().idm_max_lane_vehicles()
-    w = synth.make_workload("C2", lane_sizes=[100] * 30 + [1, 7, cap, 3], K=90, seed=21)
+    w = synth.make_workload("C2", lane_sizes=[100] * 30 + [1, 7, cap, 3], K=K, seed=21)
     obs = synth.kinematic_obs(w)
     rng = np.random.default_rng(3)
     obs[rng.random(obs.shape) < 0.2] = np.nan  # sparse: 20% missing
     o = torch.as_tensor(obs, device="cuda")
-    a = idm.from_workload(w, None, max_steps=w.K)
-    b = idm.from_workload(w, None, max_steps=w.K)
+    a = idm.from_workload(w, None, max_steps=w.K, ckpt_every=ckpt)
+    b = idm.from_workload(w, None, max_steps=w.K, ckpt_every=ckpt)
     for it in range(4):
         a.forward(w.K)
         La = a.loss_grad(o, kind=kind)
         a.backward()
         ga = a.grad_params.clone()
-        gta = a.grad_traj.clone()
+        gsa = a.grad_state0.clone()
         a.adam_step(it)
         Lb = b.fit_step(o, kind=kind, iteration=it, sync=True)
         torch.cuda.synchronize()
         assert abs(La - Lb) <= 1e-6 * abs(La)  # fused sums fp32 per segment, then fp64
-        assert torch.equal(gta, b.grad_traj)
         assert torch.equal(ga, b.grad_params)
+        assert torch.equal(gsa, b.grad_state0)
         assert torch.equal(a.params, b.params)
         assert torch.equal(a.adam_m, b.adam_m) and torch.equal(a.adam_v, b.adam_v)
 
