@@ -110,6 +110,14 @@ template <class T> __device__ __forceinline__ T splat(float a);
 template <> __device__ __forceinline__ float splat<float>(float a) { return a; }
 template <> __device__ __forceinline__ float2 splat<float2>(float a) { return f2(a); }
 
+// 0.5 + sign(z) |h| (z >= 0 keeps h's value bit for bit; one LOP3 per lane): with h = r - 0.5
+// and r = 1 / (1 + 2^-|z|) in [0.5, 1] (Sterbenz: exact), this is sigmoid(z) and 0.5 - ... is
+// 1 - sigmoid(z), branch-free.
+__device__ __forceinline__ float vcopysign(float h, float z) { return copysignf(h, z); }
+__device__ __forceinline__ float2 vcopysign(float2 h, float2 z) {
+    return make_float2(copysignf(h.x, z.x), copysignf(h.y, z.y));
+}
+
 template <class T> struct MaskOf { using type = bool; };
 template <> struct MaskOf<float2> { using type = bool2; };
 template <class T> using Mask = typename MaskOf<T>::type;
@@ -273,21 +281,22 @@ using GradAcc = GradAccT<float>;
 template <class T>
 struct RecT {
     T sig_a, beta, Jv, Js, r1, r2;
+    T w, dv;  // (v/v_targ)^delta and v - v_h, reused by the reverse step
 };
 
 template <bool D4, class T>
 __device__ __forceinline__ RecT<T> jac_record(const CoreT<T>& c, T s, T v, const VehPT<T>& p,
                                               const VehBT<T>& b, const Consts& k) {
-    const T rs = rcp(c.ones);
-    const T sig_s = vsel(vge(c.s_opt2, 0.f), rs, vmul(c.es, rs));   // d s*/d s_opt
-    const T ra = rcp(c.onea);
-    const T eara = vmul(c.ea, ra);
-    const Mask<T> zpos = vge(c.z2, 0.f);
-    const T sig_a = vsel(zpos, ra, eara);                            // d a*/d a_raw
-    const T omsa = vsel(zpos, eara, ra);                             // d a*/d a_lb
+    const T hs = vcopysign(vadd(rcp(c.ones), -0.5f), c.s_opt2);
+    const T sig_s = vadd(hs, 0.5f);                                  // d s*/d s_opt
+    const T ha = vcopysign(vadd(rcp(c.onea), -0.5f), c.z2);
+    const T sig_a = vadd(ha, 0.5f);                                  // d a*/d a_raw
+    const T omsa = vsub(0.5f, ha);                                   // d a*/d a_lb
     const T As = vmul(vmul(b.nam2ln2, c.qr), c.idp);                // d a_raw/d s*
     const T sAs = vmul(sig_a, As);
     RecT<T> R;
+    R.w = c.w;
+    R.dv = c.dv;
     R.sig_a = sig_a;
     R.beta = vmul(sAs, sig_s);                                       // d a*/d s_opt
     T xm1;                                                           // x^(delta-1)
@@ -298,7 +307,8 @@ __device__ __forceinline__ RecT<T> jac_record(const CoreT<T>& c, T s, T v, const
     const Mask<T> lb_act = vgt(c.vlb2, k.a_min2);                    // a_lb = -v/dt branch
     R.Jv = vsel(lb_act, vfma(omsa, -k.inv_dt, Jv), Jv);
     R.Js = vsel(vge(s, k.eps), vmul(vmul(sAs, c.qr), -kLn2), splat<T>(0.f));
-    const T lx = D4 ? vsel(vgt(c.x, 0.f), lg2(c.x), splat<T>(0.f)) : c.lx;
+    // log2 x (x = 0: w = 0 makes w log2 x = 0 with log2 of the smallest normal)
+    const T lx = D4 ? lg2(vmax(c.x, 1.17549435e-38f)) : c.lx;
     R.r1 = vfma(c.inter2, -kLn2Sq, c.t1);
     R.r2 = vmul(c.w, lx);
     return R;
@@ -320,19 +330,11 @@ __device__ __forceinline__ T bwd_from_record(const RecT<T>& R, T v, T vl, const 
     const T F_out = vfma(qbv, b.nc, dtls);                       // q d a*/d v_h + dt lambda_s
     lv = vsub(vfma(lD, k.dt, vfma(q, R.Jv, lv)), dtls);
     ls = vfma(q, R.Js, ls);
-    T w;
-    const T x = vmul(v, p.ivt);
-    if (D4) {
-        const T x2 = vmul(x, x);
-        w = vmul(x2, x2);
-    } else {
-        w = vsel(vgt(x, 0.f), ex2(vmul(p.delta, lg2(x))), splat<T>(0.f));
-    }
     g.S1 = vfma(qa, R.r1, g.S1);
-    g.S2 = vfma(qbv, vsub(v, vl), g.S2);
+    g.S2 = vfma(qbv, R.dv, g.S2);
     g.S3 = vadd(g.S3, qb);
     g.S4 = vadd(g.S4, qbv);
-    g.S5 = vfma(qa, w, g.S5);
+    g.S5 = vfma(qa, R.w, g.S5);
     g.S6 = vfma(qa, R.r2, g.S6);
     return F_out;
 }
@@ -345,13 +347,11 @@ template <bool D4, class T>
 __device__ __forceinline__ void bwd_vl(const CoreT<T>& c, T dp, T v, const VehPT<T>& p,
                                        const VehBT<T>& b, const Consts& k, T& lv, T lD,
                                        GradAccT<T>& g, T& gdp, T& gdv) {
-    const T rs = rcp(c.ones);
-    const T sig_s = vsel(vge(c.s_opt2, 0.f), rs, vmul(c.es, rs));
-    const T ra = rcp(c.onea);
-    const T eara = vmul(c.ea, ra);
-    const Mask<T> zpos = vge(c.z2, 0.f);
-    const T sig_a = vsel(zpos, ra, eara);
-    const T omsa = vsel(zpos, eara, ra);
+    const T hs = vcopysign(vadd(rcp(c.ones), -0.5f), c.s_opt2);
+    const T sig_s = vadd(hs, 0.5f);
+    const T ha = vcopysign(vadd(rcp(c.onea), -0.5f), c.z2);
+    const T sig_a = vadd(ha, 0.5f);
+    const T omsa = vsub(0.5f, ha);
     const T As = vmul(vmul(b.nam2ln2, c.qr), c.idp);            // d a_raw/d s*
     const T sAs = vmul(sig_a, As);
     const T beta = vmul(sAs, sig_s);                            // d a*/d s_opt
@@ -369,7 +369,7 @@ __device__ __forceinline__ void bwd_vl(const CoreT<T>& c, T dp, T v, const VehPT
     const T qbv = vmul(qb, v);
     gdv = vmul(vneg(qbv), b.nc);                                // d s_opt/d dv = v c
     lv = vfma(lD, k.dt, vfma(q, Jv, lv));
-    const T lx = D4 ? vsel(vgt(c.x, 0.f), lg2(c.x), splat<T>(0.f)) : c.lx;
+    const T lx = D4 ? lg2(vmax(c.x, 1.17549435e-38f)) : c.lx;
     g.S1 = vfma(qa, vfma(c.inter2, -kLn2Sq, c.t1), g.S1);
     g.S2 = vfma(qbv, c.dv, g.S2);
     g.S3 = vadd(g.S3, qb);

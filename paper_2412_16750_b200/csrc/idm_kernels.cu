@@ -163,10 +163,15 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? 3 : 4))) fwd_kernel(
     if (LOSS) (void)loss_term<LOSS - 1>(ld_obs(obs), p0, lseg);
     else put(orow, p0);
     if (RECV) put(vrow, v);
+    // checkpoint rows the consumer reads: the gap (idm_backward); + displacement (fused
+    // backward rebuilds positions); + compensation (and that with Kahan)
+    auto put_ck = [&] {
+        __stcs(ckp, s);
+        if (LOSS) __stcs(ckp + kR2, D);
+        if (LOSS && KAHAN) __stcs(ckp + 2 * kR2, cmp);
+    };
     __stcs(vtp, v);
-    __stcs(ckp, s);
-    __stcs(ckp + kR2, D);
-    __stcs(ckp + 2 * kR2, cmp);
+    put_ck();
     int par = 0;
     // one synchronous step of the whole tile; o = this step's observations (LOSS)
     auto step = [&](float2 o) {
@@ -200,9 +205,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? 3 : 4))) fwd_kernel(
     };
     auto checkpoint = [&](int t0) {  // (gap, D, compensation) at step t0 > 0 + finiteness check
         ckp += kCkRows * kR2;
-        __stcs(ckp, s);
-        __stcs(ckp + kR2, D);
-        __stcs(ckp + 2 * kR2, cmp);
+        put_ck();
         finite2(t0);
     };
     for (int seg = 0; seg < nfull; ++seg) {
