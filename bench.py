@@ -36,6 +36,10 @@ WORKLOAD = "C4"  # the headline configuration (BASELINE.json configs[3]); --conf
 # vehicle-step that any implementation of the kernel's math must issue, and HBM bytes per
 # vehicle-step the method must move at k = 16, K = 300.
 ALG_INSTR = {"fwd": 36.0, "bwd": 114.0}  # SURVEY.md 8(d) frozen essential-op counts
+# The same essential math counted in issue slots of THIS implementation, where two vehicles'
+# FP32 multiply-adds issue as one f32x2 instruction: the frozen scalar
+# counts over-credit a packed kernel, so both fractions are reported.
+PACKED_INSTR = {"fwd": 21.0, "bwd": 45.5}
 ISSUE_PER_CLK = 148 * 4 * 32  # SMs x schedulers x lanes (thread-instr / clk)
 
 
@@ -54,16 +58,19 @@ def alg_bytes(K: int, k: int, path: str) -> dict:
             "bwd": 8.0 + 4.0 + 8.0 + 4.0 / k + (24 + 24 + 8) / K,
             "adam": 2 * 28.0 + 6 * 28.0 / K,
         }
+    # lane mode: the forward stores the speed history (4 B) and the gap checkpoint (4 B / k;
+    # + displacement on the fused path); the backward reads them back instead of recomputing
     if path == "api":
         return {
-            "fwd": 4.0 + 8.0 / k + (4 * 4 + 24 + 1) / K,        # P record + (s,v) ckpt + loads
+            "fwd": 8.0 + 4.0 / k + (4 * 4 + 24 + 1) / K,        # P + speed rows, gap ckpt, loads
             "loss": 12.0,                                       # read P, obs; write dL/dP
-            "bwd": 4.0 + 8.0 / k + (24 + 24 + 8 + 1) / K,       # dL/dP + ckpt + params/grads
+            "bwd": 8.0 + 4.0 / k + (24 + 24 + 8 + 1) / K,       # speed + dL/dP rows, ckpt, params
             "adam": 6 * 28.0 / K,                               # x, g, m, v in; x, m, v out
         }
     return {
-        "fwd": 8.0 + 8.0 / k + (4 * 4 + 24 + 1) / K,            # obs in, dL/dP out, ckpt, loads
-        "bwd": 4.0 + 8.0 / k + (24 + 1 + 24 + 8 + 6 * 20) / K,  # dL/dP, ckpt, params, Adam
+        "fwd": 8.0 + 8.0 / k + (4 * 4 + 24 + 1) / K,            # obs in, speed rows out, ckpt
+        # speed + obs rows, ckpt, params + p0, Adam (x, m, v in and out, grads out)
+        "bwd": 8.0 + 8.0 / k + (24 + 4 + 1 + 24 + 8 + 6 * 20) / K,
     }
 
 
@@ -367,9 +374,12 @@ def run_ours(args, rank, world, local_rank):
         achieved = ALG_INSTR["bwd" if dom == "bwd" else "fwd"] * n_veh_steps / \
             (kms[dom] * 1e-3) / 1e12
         traffic = load_traffic().get(f"{dom}_kernel")
+        packed = PACKED_INSTR["bwd" if dom == "bwd" else "fwd"] * n_veh_steps / \
+            (kms[dom] * 1e-3) / 1e12
         roofline = {"bound": "alu", "kernel": f"{dom}_kernel (fused path)", "achieved": achieved,
                     "peak": issue_peak, "unit": "Tinstr/s", "frac": achieved / issue_peak,
                     "traffic": traffic,
+                    "frac_packed_slots": packed / issue_peak,
                     "basis": f"{ALG_INSTR[dom]:.0f} essential thread-instr per vehicle-step x "
                              f"{n_veh_steps:.3g} vehicle-steps per launch / CUDA-event launch "
                              f"time; peak = 148 SM x 4 issue/clk x 32 lanes x {sm_mhz_max:.0f} "
@@ -403,8 +413,8 @@ def run_ours(args, rank, world, local_rank):
                    "vehicles_per_rank": w.n, "K": K,
                    "ckpt_every": k, "path": "idm_fit_step (fused fwd+Eq.4 / bwd+Adam)",
                    "parallelism": f"lane-sharded x{world}",
-                   "l2": "no flush: inputs larger than L2 (2.4 GB obs + 2.4 GB dL/dP per rank "
-                         "per step vs 126 MB L2)"},
+                   "l2": "no flush: inputs larger than L2 (2.4 GB obs read by both kernels + "
+                         "2.4 GB speed history per rank per step vs 126 MB L2)"},
         "fwd": {"value": vsteps / (api["kernel_ms"]["fwd"] * 1e-3), "unit": "vehicle-steps/s",
                 "ms": api["kernel_ms"]["fwd"], "what": "idm_forward, trajectory record on"},
         "fused_path": {kk: head[kk] for kk in ("ms_per_step", "value", "kernel_ms",

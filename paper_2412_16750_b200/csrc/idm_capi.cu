@@ -21,7 +21,8 @@ struct idm_handle {
     int64_t* tile_start;
     uint8_t* lead;
     float *vt, *ckt, *ckpt_v;     // lane-mode state history (tile-local), VL speed checkpoints
-    int64_t vt_stride, ck_stride;
+    uint32_t* sgn;                // fused L1 sign words (tile-local)
+    int64_t vt_stride, ck_stride, sg_stride;
     double *loss_partials, *loss_scalar, *shared_partials;
     unsigned long long* status;
     unsigned* flags;  // [0] = some delta != 4 (set by the validation kernel)
@@ -67,9 +68,9 @@ int fail(idm_handle* h, int code, const char* fmt, ...) {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-    size_t tile_start, lead, vt, ckt, ckpt_v, loss_partials, loss_scalar, shared_partials, status,
-        flags, adam_table, total;
-    int64_t vt_stride, ck_stride;  // floats per tile
+    size_t tile_start, lead, vt, ckt, sgn, ckpt_v, loss_partials, loss_scalar, shared_partials,
+        status, flags, adam_table, total;
+    int64_t vt_stride, ck_stride, sg_stride;  // elements per tile
 };
 
 int64_t max_tiles_for(const idm_desc* d) {
@@ -94,6 +95,8 @@ bool layout_for(const idm_desc* d, Layout* L) {
     L->ck_stride = nck * kCkRows * kCap;
     L->vt = off; off += align256(sizeof(float) * ((size_t)(mt * L->vt_stride) + 64));
     L->ckt = off; off += align256(sizeof(float) * (size_t)(mt * L->ck_stride));
+    L->sg_stride = (int64_t)(d->max_steps + 1) * kSgnWords;
+    L->sgn = off; off += align256(sizeof(uint32_t) * (size_t)(mt * L->sg_stride));
     // virtual-leader mode: speed checkpoints every 4 steps
     L->ckpt_v = off; off += align256(sizeof(float) * (size_t)(nck * n));
     L->loss_partials = off;
@@ -323,6 +326,8 @@ int idm_init(idm_handle** out, const idm_desc* d) {
         h->ckt = (float*)(ws + L.ckt);
         h->vt_stride = L.vt_stride;
         h->ck_stride = L.ck_stride;
+        h->sgn = (uint32_t*)(ws + L.sgn);
+        h->sg_stride = L.sg_stride;
         h->ckpt_v = (float*)(ws + L.ckpt_v);
         h->loss_partials = (double*)(ws + L.loss_partials);
         h->loss_scalar = (double*)(ws + L.loss_scalar);
@@ -458,6 +463,8 @@ FwdArgs fwd_args(idm_handle* h, int32_t steps) {
     a.ckt = h->ckt;
     a.vt_stride = h->vt_stride;
     a.ck_stride = h->ck_stride;
+    a.sgn = h->sgn;
+    a.sg_stride = h->sg_stride;
     a.steps = steps;
     a.ckpt_every = h->d.ckpt_every;
     a.k = consts_of(h->d);
@@ -477,6 +484,8 @@ BwdArgs bwd_args(idm_handle* h, int32_t steps) {
     a.ckt = h->ckt;
     a.vt_stride = h->vt_stride;
     a.ck_stride = h->ck_stride;
+    a.sgn = h->sgn;
+    a.sg_stride = h->sg_stride;
     a.grad_params = h->d.grad_params;
     a.grad_state0 = h->d.grad_state0;
     a.shared_partials = h->shared_partials;

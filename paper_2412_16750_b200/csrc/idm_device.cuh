@@ -85,11 +85,8 @@ __device__ __forceinline__ float vnabs(float a) { return -fabsf(a); }
 __device__ __forceinline__ float2 vnabs(float2 a) { return make_float2(-fabsf(a.x), -fabsf(a.y)); }
 __device__ __forceinline__ float vabs(float a) { return fabsf(a); }
 __device__ __forceinline__ float2 vabs(float2 a) { return make_float2(fabsf(a.x), fabsf(a.y)); }
-// -sign(a) with sign(0) = 0: one LOP3 builds -+1 from the sign bit, one select zeroes a == 0
-__device__ __forceinline__ float vnsign(float a) {
-    const float m1 = __int_as_float((__float_as_int(a) & 0x80000000) ^ 0xBF800000);
-    return a != 0.f ? m1 : 0.f;
-}
+// -sign(a) with sign(0) = 0: one LOP3 copies the flipped sign bit onto 1, one select zeroes 0
+__device__ __forceinline__ float vnsign(float a) { return a != 0.f ? copysignf(1.f, -a) : 0.f; }
 __device__ __forceinline__ float2 vnsign(float2 a) { return make_float2(vnsign(a.x), vnsign(a.y)); }
 __device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
 __device__ __forceinline__ float2 vmax(float2 a, float b) {

@@ -34,6 +34,9 @@ struct FwdVariant {
 // aligned 8-byte access at an immediate offset, and slots past the tile's vehicles are
 // private padding (stores need no predicate).
 constexpr int kCkRows = 3;
+//   sgn [tile][max_steps + 1][kSgnWords] fused L1 only: dL/dP = -sign(obs - P) as two ballot
+//                                       bits per vehicle (observed-and-nonzero, negative)
+constexpr int kSgnWords = 32;  // per step per tile: 8 warps x (nz, neg) x 2 vehicles per thread
 
 struct FwdArgs {
     const int64_t* tile_start;
@@ -43,6 +46,8 @@ struct FwdArgs {
     float *traj, *vel_traj, *state_out;
     float *vt, *ckt;
     int64_t vt_stride, ck_stride;  // floats per tile
+    uint32_t* sgn;                 // fused L1: sign words
+    int64_t sg_stride;             // words per tile
     int steps, ckpt_every;
     Consts k;
     unsigned long long* status;
@@ -70,6 +75,8 @@ struct BwdArgs {
     const float *obs, *pos0;       // fused path: dL/dP re-derived from obs and positions
     const float *vt, *ckt;
     int64_t vt_stride, ck_stride;
+    const uint32_t* sgn;
+    int64_t sg_stride;
     float *grad_params, *grad_state0;
     double* shared_partials;  // [ntiles][6] (shared mode)
     int steps, ckpt_every;
@@ -127,7 +134,8 @@ cudaError_t launch_validate(const ValidateArgs& a, cudaStream_t st);
 cudaError_t launch_fwd(const FwdArgs& a, int ntiles, const FwdVariant& var, cudaStream_t st);
 cudaError_t kernels_configure(int ckpt_every);
 size_t bwd_smem_bytes(int ckpt_every);
-// gobs = 0: dL/dP from grad_traj; 1 + kind: re-derived from obs (fused, ckpt_every == 4)
+// gobs = 0: dL/dP from grad_traj; 1: L1 from the forward's sign words; 2: L2 re-derived from obs
+// and the rebuilt positions (gobs != 0: fused idm_fit_step, ckpt_every == 4)
 cudaError_t launch_bwd(const BwdArgs& a, int ntiles, bool delta4, bool shared, bool adam,
                        int gobs, bool kahan, cudaStream_t st);
 bool ckpt_supported(int k);

@@ -160,16 +160,38 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? 3 : 4))) fwd_kernel(
         for (int tt = 0; tt < KS; ++tt, o += N) onx[tt] = tt < nrows ? ld_obs(o) : f2(qnan);
     };
     if (LOSS) prefetch(1, min(KS, steps));
-    if (LOSS) (void)loss_term<LOSS - 1>(ld_obs(obs), p0, lseg);
-    else put(orow, p0);
-    if (RECV) put(vrow, v);
     // checkpoint rows the consumer reads: the gap (idm_backward); + displacement (fused
     // backward rebuilds positions); + compensation (and that with Kahan)
     auto put_ck = [&] {
         __stcs(ckp, s);
-        if (LOSS) __stcs(ckp + kR2, D);
-        if (LOSS && KAHAN) __stcs(ckp + 2 * kR2, cmp);
+        if (LOSS == 2) __stcs(ckp + kR2, D);
+        if (LOSS == 2 && KAHAN) __stcs(ckp + 2 * kR2, cmp);
     };
+    // fused L1: dL/dP = -sign(obs - P) of each vehicle as two ballot bits (nonzero, +1); lane 0
+    // of each warp stores the warp's four words of the step (16 B)
+    uint4* sgp = LOSS == 1 ? reinterpret_cast<uint4*>(a.sgn + blockIdx.x * a.sg_stride) +
+                                 (tid >> 5)
+                           : nullptr;
+    // Eq. 4 term of the fused forward: L2 sums r^2; L1 sums |r| and records -sign(r) as the
+    // bits (r != 0, r < 0) of the masked residual r (0 where unobserved), i.e. exactly
+    // loss_term<0>'s dL/dP
+    auto loss_step = [&](float2 o, float2 Pv) {
+        if (LOSS == 2) {
+            (void)loss_term<1>(o, Pv, lseg);
+            return;
+        }
+        const float2 rm = vsel(vge(vnabs(o), -3.4e38f), vsub(o, Pv), f2(0.f));
+        lseg = vadd(lseg, vabs(rm));
+        const unsigned nz0 = __ballot_sync(0xffffffffu, rm.x != 0.f);
+        const unsigned ps0 = __ballot_sync(0xffffffffu, rm.x < 0.f);
+        const unsigned nz1 = __ballot_sync(0xffffffffu, rm.y != 0.f);
+        const unsigned ps1 = __ballot_sync(0xffffffffu, rm.y < 0.f);
+        if ((tid & 31) == 0) __stcs(sgp, make_uint4(nz0, ps0, nz1, ps1));
+        sgp += kSgnWords / 4;
+    };
+    if (LOSS) loss_step(ld_obs(obs), p0);
+    else put(orow, p0);
+    if (RECV) put(vrow, v);
     __stcs(vtp, v);
     put_ck();
     int par = 0;
@@ -192,7 +214,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? 3 : 4))) fwd_kernel(
         if (RECV) vrow += N;
         vtp += kR2;
         const float2 Pv = vadd(p0, D);
-        if (LOSS) (void)loss_term<LOSS - 1>(o, Pv, lseg);
+        if (LOSS) loss_step(o, Pv);
         else put(orow, Pv);
         __stcs(vtp, v);
         if (RECV) put(vrow, v);
@@ -307,7 +329,9 @@ __device__ __forceinline__ void cp_async_wait() {
 // 2t + 1, passed to thread t + 1 through shared memory (one barrier per step).  The next
 // segment's rows are prefetched into registers while the current one is swept.
 //   GOBS = 0:      dL/dP rows from grad_traj (idm_backward after idm_loss_grad);
-//   GOBS = 1 + k:  fused idm_fit_step -- dL/dP re-derived from obs and the rebuilt positions
+//   GOBS = 1:      fused idm_fit_step, L1 -- dL/dP = -sign(obs - P) from the forward's ballot
+//                  words (2 bits per vehicle-step);
+//   GOBS = 2:      fused idm_fit_step, L2 -- dL/dP re-derived from obs and the rebuilt positions
 //                  P = p0 + D with the forward's loss term (same bits as idm_loss_grad).
 // Gradient accumulators stay in registers for the whole rollout; ADAM: per-vehicle Adam in the
 // epilogue (idm_fit_step).
@@ -345,7 +369,7 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
             if (D4 && r.delta != 4.f)
                 atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
             if (!GOBS) ldj[j] = a.grad_traj[(int64_t)steps * N + i];  // lambda_D^K = dL/dP(K)
-            else pj[j] = a.pos0[i];
+            if (GOBS == 2) pj[j] = a.pos0[i];
         }
         Pj[j] = make_vehp(r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta);
         Bj[j] = make_vehb(r.a_max, r.a_pref, r.v_targ, r.delta);
@@ -366,12 +390,15 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
     extern __shared__ __align__(16) float smem_b[];
     constexpr int NB = 3;
     constexpr int VP = kCap + 4;  // speed row pitch: [kCap] = 0 is the leader read of slot 511
-    constexpr int KO = GOBS ? KS + 1 : KS;
+    constexpr bool SGN = GOBS == 1, OBS = GOBS == 2;
+    constexpr int KO = GOBS ? KS + 1 : KS;             // + the rollout's last step (fused)
     float* vrow = smem_b;                              // [NB][KS][VP]
     float* ckrow = vrow + NB * KS * VP;                // [NB][3][kCap]
-    float* orow = ckrow + NB * kCkRows * kCap;         // [NB][KO][kCap]
+    float* orow = ckrow + NB * kCkRows * kCap;         // [NB][KO][kCap] (dL/dP or obs rows)
+    uint4* sbuf = reinterpret_cast<uint4*>(orow);      // [NB][KO][8 warps] (SGN: sign words)
     __shared__ __align__(8) uint64_t mbar[NB];
-    constexpr int nckr = GOBS ? (KAHAN ? 3 : 2) : 1;   // checkpoint rows used
+    constexpr int nckr = OBS ? (KAHAN ? 3 : 2) : 1;    // checkpoint rows used
+    const unsigned lmask = 1u << (tid & 31);
     if (tid == 0) {
 #pragma unroll
         for (int q = 0; q < NB; ++q) mbar_init(&mbar[q], 1);
@@ -387,8 +414,14 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
             // buffer b was last read (generic proxy) before the barriers of an earlier
             // segment; order those reads before the async-proxy writes
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            const uint32_t bytes = (uint32_t)(len + nckr) * kCap * sizeof(float);
+            const int srows = len + (seg == nseg - 1 ? 1 : 0);  // SGN: + row K
+            const uint32_t bytes = (uint32_t)(len + nckr) * kCap * sizeof(float) +
+                                   (SGN ? (uint32_t)srows * kSgnWords * sizeof(uint32_t) : 0u);
             mbar_expect_tx(&mbar[b], bytes);
+            if (SGN)
+                bulk_g2s(sbuf + b * KO * (kSgnWords / 4),
+                         a.sgn + blockIdx.x * a.sg_stride + t0 * kSgnWords,
+                         srows * kSgnWords * sizeof(uint32_t), &mbar[b]);
             const float* src = a.vt + blockIdx.x * a.vt_stride + t0 * kCap;
             for (int tt = 0; tt < len; ++tt)
                 bulk_g2s(vrow + (b * KS + tt) * VP, src + tt * kCap, kCap * sizeof(float), &mbar[b]);
@@ -396,15 +429,17 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
                      a.ckt + blockIdx.x * a.ck_stride + (int64_t)seg * kCkRows * kCap,
                      nckr * kCap * sizeof(float), &mbar[b]);
         }
-        const float* src = (GOBS ? a.obs : a.grad_traj) + t0 * N + i0;
-        float* dst = orow + b * KO * kCap + 2 * tid;
+        if (!SGN) {
+            const float* src = (OBS ? a.obs : a.grad_traj) + t0 * N + i0;
+            float* dst = orow + b * KO * kCap + 2 * tid;
 #pragma unroll
-        for (int tt = 0; tt < KO; ++tt, src += N) {
-            const bool on = tt < len || (GOBS && tt == len && seg == nseg - 1);
-            cp_async4(dst + tt * kCap, src, val[0] && on);
-            cp_async4(dst + tt * kCap + 1, src + 1, val[1] && on);
+            for (int tt = 0; tt < KO; ++tt, src += N) {
+                const bool on = tt < len || (OBS && tt == len && seg == nseg - 1);
+                cp_async4(dst + tt * kCap, src, val[0] && on);
+                cp_async4(dst + tt * kCap + 1, src + 1, val[1] && on);
+            }
+            cp_async_commit();
         }
-        cp_async_commit();
     };
     int par = 0;
     fetch(nseg - 1, tail);
@@ -414,8 +449,10 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
         const int b = seg % NB;
         mbar_wait(&mbar[b], (phase >> b) & 1u);
         phase ^= 1u << b;
-        if (seg > 0) cp_async_wait<1>();  // this segment's rows; seg - 1's may stay in flight
-        else cp_async_wait<0>();
+        if (!SGN) {
+            if (seg > 0) cp_async_wait<1>();  // this segment's rows; seg - 1's may stay in flight
+            else cp_async_wait<0>();
+        }
         const float* orr = orow + b * KO * kCap + 2 * tid;
         float2 v[KS], g[KO], vl[KS], sg[KS];
         const float* vr = vrow + b * KS * VP + 2 * tid;
@@ -430,28 +467,38 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
             }
         }
 #pragma unroll
-        for (int tt = 0; tt < KO; ++tt)
-            g[tt] = (kFull || tt <= len) ? *reinterpret_cast<const float2*>(orr + tt * kCap) : f2(0.f);
+        for (int tt = 0; tt < KO; ++tt) {
+            if (SGN) {  // -sign(obs - P): (nonzero, +1) bits of this thread's two vehicles
+                const uint4 w = sbuf[(b * KO + tt) * (kSgnWords / 4) + (tid >> 5)];
+                auto gv = [&](unsigned nz, unsigned ps) {
+                    return (nz & lmask) ? ((ps & lmask) ? 1.f : -1.f) : 0.f;
+                };
+                g[tt] = (kFull || tt <= len) ? make_float2(gv(w.x, w.y), gv(w.z, w.w)) : f2(0.f);
+            } else {
+                g[tt] = (kFull || tt <= len) ? *reinterpret_cast<const float2*>(orr + tt * kCap)
+                                             : f2(0.f);
+            }
+        }
         // gaps (and positions) inside the segment: the forward's recurrences from the
         // checkpoint, bitwise
         const float* cr = ckrow + b * kCkRows * kCap + 2 * tid;
         float2 s = *reinterpret_cast<const float2*>(cr);
         float2 D = f2(0.f), cmp = f2(0.f);
-        if (GOBS) D = *reinterpret_cast<const float2*>(cr + kCap);
-        if (GOBS && KAHAN) cmp = *reinterpret_cast<const float2*>(cr + 2 * kCap);
+        if (OBS) D = *reinterpret_cast<const float2*>(cr + kCap);
+        if (OBS && KAHAN) cmp = *reinterpret_cast<const float2*>(cr + 2 * kCap);
 #pragma unroll
         for (int tt = 0; tt < KO; ++tt) {
-            if (GOBS) {
+            if (OBS) {
                 // dL/dP at step t0 + tt (the forward's loss term on the same P bits); the
                 // rollout's last step K adds its term to lambda_D^K below
                 float2 dummy = f2(0.f);
-                if (kFull || tt <= len) g[tt] = loss_term<GOBS - 1>(g[tt], vadd(p0, D), dummy);
+                if (kFull || tt <= len) g[tt] = loss_term<1>(g[tt], vadd(p0, D), dummy);
             }
             if (tt < KS) {
                 sg[tt] = s;
                 if (kFull || tt < len) {
                     s = vfma(vsub(v[tt], vl[tt]), -k.dt, s);
-                    if (GOBS) {
+                    if (OBS) {
                         if (KAHAN) {
                             const float2 y = vfma(v[tt], k.dt, vneg(cmp));
                             const float2 t2 = vadd(D, y);
@@ -710,8 +757,10 @@ cudaError_t kernels_configure(int ckpt_every) {
 }
 
 template <int KS, int GOBS>
-constexpr size_t bwd_smem_of() {  // ring of 3: speed rows + checkpoint rows + dL/dP/obs rows
-    return (size_t)3 * (KS * (kCap + 4) + kCkRows * kCap + (GOBS ? KS + 1 : KS) * kCap) *
+constexpr size_t bwd_smem_of() {  // ring of 3: speed + checkpoint + dL/dP/obs (or sign) rows
+    return (size_t)3 *
+           (KS * (kCap + 4) + kCkRows * kCap +
+            (GOBS == 1 ? (KS + 1) * kSgnWords : (GOBS ? KS + 1 : KS) * kCap)) *
            sizeof(float);
 }
 
@@ -746,9 +795,8 @@ static cudaError_t launch_bwd_d(const BwdArgs& a, int ntiles, bool shared, bool 
                                 bool kahan, cudaStream_t st) {
     if (gobs) {
         if (a.ckpt_every != 4) return cudaErrorInvalidValue;
-        if (gobs == 1) {
-            if (kahan) launch_bwd_obs<D4, 1, true>(a, ntiles, shared, st);
-            else launch_bwd_obs<D4, 1, false>(a, ntiles, shared, st);
+        if (gobs == 1) {  // sign words: no positions needed, compensation irrelevant
+            launch_bwd_obs<D4, 1, false>(a, ntiles, shared, st);
         } else {
             if (kahan) launch_bwd_obs<D4, 2, true>(a, ntiles, shared, st);
             else launch_bwd_obs<D4, 2, false>(a, ntiles, shared, st);
