@@ -45,6 +45,21 @@ __device__ __forceinline__ void report_nonfinite(unsigned long long* status, int
     atomicMin(status, (unsigned long long)(unsigned)step << 32 | (uint64_t)(uint32_t)veh);
 }
 
+// Predicated streaming load / store (one instruction each, no branch: the compiler otherwise
+// branches around guarded accesses and rebuilds every 64-bit row address from scratch).
+__device__ __forceinline__ float ld_cs_if(const float* p, bool on, float dflt) {
+    float r = dflt;
+    asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.global.cs.f32 %0, [%1];\n}"
+        : "+f"(r)
+        : "l"(p), "r"((int)on));
+    return r;
+}
+__device__ __forceinline__ void st_cs_if(float* p, bool on, float x) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.cs.f32 [%0], %1;\n}"
+                 ::"l"(p), "f"(x), "r"((int)on)
+                 : "memory");
+}
+
 struct RawP {
     float a_max, a_pref, s_min, T, v_targ, delta;
 };
@@ -135,8 +150,8 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? 3 : 4))) fwd_kernel(
     if (tid == 0) { xv[0][kT] = 0.f; xv[1][kT] = 0.f; }
 
     auto put = [&](float* row, float2 x) {  // row points at local vehicle 2 tid
-        if (val[0]) __stcs(row, x.x);
-        if (val[1]) __stcs(row + 1, x.y);
+        st_cs_if(row, val[0], x.x);
+        st_cs_if(row + 1, val[1], x.y);
     };
     // out: P row of the current step (LOSS = 0; the fused variant only sums Eq. 4)
     float* orow = LOSS ? nullptr : a.traj + i0;
@@ -150,14 +165,14 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? 3 : 4))) fwd_kernel(
     float2 onx[KS];      // LOSS: observation rows of the next segment (registers)
     float2 lseg = f2(0.f);  // loss of this thread's vehicles in this segment (fp32)
     double lacc = 0.0;   // and across segments (fp64)
-    auto ld_obs = [&](const float* o) {  // absent vehicles observe NaN (= missing)
-        return make_float2(val[0] ? __ldcs(o) : qnan, val[1] ? __ldcs(o + 1) : qnan);
+    auto ld_obs = [&](const float* o, bool on) {  // absent vehicles observe NaN (= missing)
+        return make_float2(ld_cs_if(o, on && val[0], qnan), ld_cs_if(o + 1, on && val[1], qnan));
     };
     // prefetch the observation rows row0 .. row0 + nrows - 1
     auto prefetch = [&](int row0, int nrows) {
         const float* o = obs + (int64_t)row0 * N;
 #pragma unroll
-        for (int tt = 0; tt < KS; ++tt, o += N) onx[tt] = tt < nrows ? ld_obs(o) : f2(qnan);
+        for (int tt = 0; tt < KS; ++tt, o += N) onx[tt] = ld_obs(o, tt < nrows);
     };
     if (LOSS) prefetch(1, min(KS, steps));
     // checkpoint rows the consumer reads: the gap (idm_backward); + displacement (fused
@@ -189,7 +204,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? 3 : 4))) fwd_kernel(
         if ((tid & 31) == 0) __stcs(sgp, make_uint4(nz0, ps0, nz1, ps1));
         sgp += kSgnWords / 4;
     };
-    if (LOSS) loss_step(ld_obs(obs), p0);
+    if (LOSS) loss_step(ld_obs(obs, true), p0);
     else put(orow, p0);
     if (RECV) put(vrow, v);
     __stcs(vtp, v);
