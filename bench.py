@@ -67,10 +67,11 @@ def alg_bytes(K: int, k: int, path: str) -> dict:
             "bwd": 8.0 + 4.0 / k + (24 + 24 + 8 + 1) / K,       # speed + dL/dP rows, ckpt, params
             "adam": 6 * 28.0 / K,                               # x, g, m, v in; x, m, v out
         }
+    # fused L1 (the headline): the forward sums Eq. 4 and records -sign(obs - P) as 2 bits
     return {
-        "fwd": 8.0 + 8.0 / k + (4 * 4 + 24 + 1) / K,            # obs in, speed rows out, ckpt
-        # speed + obs rows, ckpt, params + p0, Adam (x, m, v in and out, grads out)
-        "bwd": 8.0 + 8.0 / k + (24 + 4 + 1 + 24 + 8 + 6 * 20) / K,
+        "fwd": 4.0 + 4.0 + 4.0 / k + 0.25 + (4 * 4 + 24 + 1) / K,  # obs in; speeds, gap, bits out
+        # speed rows, sign bits, gap checkpoint; params, Adam (x, m, v in and out), grads out
+        "bwd": 4.0 + 0.25 + 4.0 / k + (24 + 1 + 24 + 8 + 6 * 20) / K,
     }
 
 

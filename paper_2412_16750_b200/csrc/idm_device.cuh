@@ -284,9 +284,11 @@ struct RecT {
 template <bool D4, class T>
 __device__ __forceinline__ RecT<T> jac_record(const CoreT<T>& c, T s, T v, const VehPT<T>& p,
                                               const VehBT<T>& b, const Consts& k) {
-    const T hs = vcopysign(vadd(rcp(c.ones), -0.5f), c.s_opt2);
+    // 1/ones and 1/onea from ONE reciprocal (both in [1, 2], product in [1, 4])
+    const T rp = rcp(vmul(c.ones, c.onea));
+    const T hs = vcopysign(vfma(c.onea, rp, splat<T>(-0.5f)), c.s_opt2);
     const T sig_s = vadd(hs, 0.5f);                                  // d s*/d s_opt
-    const T ha = vcopysign(vadd(rcp(c.onea), -0.5f), c.z2);
+    const T ha = vcopysign(vfma(c.ones, rp, splat<T>(-0.5f)), c.z2);
     const T sig_a = vadd(ha, 0.5f);                                  // d a*/d a_raw
     const T omsa = vsub(0.5f, ha);                                   // d a*/d a_lb
     const T As = vmul(vmul(b.nam2ln2, c.qr), c.idp);                // d a_raw/d s*
@@ -344,9 +346,10 @@ template <bool D4, class T>
 __device__ __forceinline__ void bwd_vl(const CoreT<T>& c, T dp, T v, const VehPT<T>& p,
                                        const VehBT<T>& b, const Consts& k, T& lv, T lD,
                                        GradAccT<T>& g, T& gdp, T& gdv) {
-    const T hs = vcopysign(vadd(rcp(c.ones), -0.5f), c.s_opt2);
+    const T rp = rcp(vmul(c.ones, c.onea));
+    const T hs = vcopysign(vfma(c.onea, rp, splat<T>(-0.5f)), c.s_opt2);
     const T sig_s = vadd(hs, 0.5f);
-    const T ha = vcopysign(vadd(rcp(c.onea), -0.5f), c.z2);
+    const T ha = vcopysign(vfma(c.ones, rp, splat<T>(-0.5f)), c.z2);
     const T sig_a = vadd(ha, 0.5f);
     const T omsa = vsub(0.5f, ha);
     const T As = vmul(vmul(b.nam2ln2, c.qr), c.idp);            // d a_raw/d s*
