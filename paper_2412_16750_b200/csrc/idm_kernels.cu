@@ -96,6 +96,58 @@ __device__ __forceinline__ void block_sum_to(double x, double* out) {
     }
 }
 
+// ------------------------------------------------------------------------------ async copies
+// 1-D bulk copies (global -> shared, completion counted on an mbarrier in bytes): the
+// tile-local rows are 16-byte aligned and contiguous, so one elected thread moves a whole
+// 2 KB row per instruction and no register holds data in flight.
+namespace {
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "IDM_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra IDM_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// per-thread 4-byte async copy global -> shared (src_size 0: zero-fill, nothing read)
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool on) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(on ? 4 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+}  // namespace
+
 // ------------------------------------------------------------------------------ NK1
 // One CTA = one lane tile; thread t owns the adjacent local vehicles 2t, 2t + 1 as one float2
 // lane pair (packed f32x2 arithmetic).  Vehicle 2t's leader is 2t + 1 (same thread); vehicle
@@ -110,7 +162,7 @@ __device__ __forceinline__ void block_sum_to(double x, double* out) {
 // CK = checkpoint interval (the backward's segment length); the forward's own prefetch
 // segment is KS = max(4, CK) steps, so CK | KS and checkpoints fall at static positions.
 template <bool D4, bool KAHAN, bool RECV, int LOSS, int CK>
-__global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? 3 : 4))) fwd_kernel(FwdArgs a) {
+__global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
     constexpr int KS = CK > 4 ? CK : 4;
     __shared__ float xv[2][kT + 1];  // speed of each thread's first vehicle; [kT] = 0 sentinel
     const int tid = threadIdx.x;
@@ -162,19 +214,37 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? 3 : 4))) fwd_kernel(
     constexpr int kR2 = kCap / 2;  // one row in float2 units
     const float* obs = LOSS ? a.obs + i0 : nullptr;
     const float qnan = __int_as_float(0x7fc00000);
-    float2 onx[KS];      // LOSS: observation rows of the next segment (registers)
+    // LOSS: observation rows staged two segments ahead in a 3-buffer shared-memory ring by
+    // per-thread cp.async (zero-fill for absent vehicles, masked at use); one commit group per
+    // segment (empty past the end) keeps cp.async.wait_group<1> exact
+    __shared__ __align__(16) float obuf[LOSS ? 3 : 1][LOSS ? KS : 1][kCap];
     float2 lseg = f2(0.f);  // loss of this thread's vehicles in this segment (fp32)
     double lacc = 0.0;   // and across segments (fp64)
     auto ld_obs = [&](const float* o, bool on) {  // absent vehicles observe NaN (= missing)
         return make_float2(ld_cs_if(o, on && val[0], qnan), ld_cs_if(o + 1, on && val[1], qnan));
     };
-    // prefetch the observation rows row0 .. row0 + nrows - 1
-    auto prefetch = [&](int row0, int nrows) {
-        const float* o = obs + (int64_t)row0 * N;
+    // segment seg observes rows seg*KS + 1 .. seg*KS + KS
+    auto fetch_obs = [&](int seg) {
+        const int r0 = seg * KS + 1;
+        const float* o = obs + (int64_t)min(r0, steps) * N;
+        float* dst = &obuf[seg % 3][0][2 * tid];
 #pragma unroll
-        for (int tt = 0; tt < KS; ++tt, o += N) onx[tt] = ld_obs(o, tt < nrows);
+        for (int tt = 0; tt < KS; ++tt) {
+            const bool on = r0 + tt <= steps;
+            cp_async4(dst + tt * kCap, o, on && val[0]);
+            cp_async4(dst + tt * kCap + 1, o + 1, on && val[1]);
+            if (r0 + tt < steps) o += N;
+        }
+        cp_async_commit();
     };
-    if (LOSS) prefetch(1, min(KS, steps));
+    auto obs_at = [&](int seg, int tt) {  // this thread's pair of row seg*KS + 1 + tt
+        const float2 o = *reinterpret_cast<const float2*>(&obuf[seg % 3][tt][2 * tid]);
+        return make_float2(val[0] ? o.x : qnan, val[1] ? o.y : qnan);
+    };
+    if (LOSS) {
+        fetch_obs(0);
+        fetch_obs(1);
+    }
     // checkpoint rows the consumer reads: the gap (idm_backward); + displacement (fused
     // backward rebuilds positions); + compensation (and that with Kahan)
     auto put_ck = [&] {
@@ -245,19 +315,19 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? 3 : 4))) fwd_kernel(
         put_ck();
         finite2(t0);
     };
+    auto obs_ready = [&](int seg) {
+        if (LOSS) {
+            cp_async_wait<1>();  // this segment's group; seg + 1's may stay in flight
+            fetch_obs(seg + 2);
+        }
+    };
     for (int seg = 0; seg < nfull; ++seg) {
         const int t0 = seg * KS;
-        float2 ocur[KS];
-        if (LOSS) {
-#pragma unroll
-            for (int tt = 0; tt < KS; ++tt) ocur[tt] = onx[tt];
-            const int nxt = (seg + 1) * KS;  // the next segment observes rows nxt+1 ..
-            if (nxt < steps) prefetch(nxt + 1, min(KS, steps - nxt));
-        }
+        obs_ready(seg);
 #pragma unroll
         for (int tt = 0; tt < KS; ++tt) {
             if (tt % CK == 0 && (tt > 0 || seg > 0)) checkpoint(t0 + tt);
-            step(ocur[tt]);
+            step(LOSS ? obs_at(seg, tt) : f2(0.f));
         }
         if (LOSS) {
             lacc += (double)lseg.x + (double)lseg.y;
@@ -265,14 +335,16 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? 3 : 4))) fwd_kernel(
         }
     }
     if (tail > 0) {
+        obs_ready(nfull);
 #pragma unroll
         for (int tt = 0; tt < KS; ++tt) {
             if (tt < tail) {  // CTA-uniform predicate
                 if (tt % CK == 0 && (tt > 0 || nfull > 0)) checkpoint(nfull * KS + tt);
-                step(onx[tt]);
+                step(LOSS ? obs_at(nfull, tt) : f2(0.f));
             }
         }
     }
+    if (LOSS) cp_async_wait<0>();  // no copy outlives the CTA
     finite2(steps);
     if (a.state_out) {
         put(a.state_out + i0, vadd(p0, D));
@@ -280,58 +352,6 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? 3 : 4))) fwd_kernel(
     }
     if (LOSS) block_sum_to(lacc + (double)lseg.x + (double)lseg.y, a.loss_partials);
 }
-
-// ------------------------------------------------------------------------------ async copies
-// 1-D bulk copies (global -> shared, completion counted on an mbarrier in bytes): the
-// tile-local rows are 16-byte aligned and contiguous, so one elected thread moves a whole
-// 2 KB row per instruction and no register holds data in flight.
-namespace {
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_fence_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "IDM_WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra IDM_WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// per-thread 4-byte async copy global -> shared (src_size 0: zero-fill, nothing read)
-__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool on) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src),
-                 "r"(on ? 4 : 0)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-    asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-}  // namespace
 
 // ------------------------------------------------------------------------------ NK3
 // Per CTA (lane tile, thread t = vehicles 2t, 2t + 1 as in NK1), segments of KS steps from last
