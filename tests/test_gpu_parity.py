@@ -652,20 +652,47 @@ def test_degenerate_starts(idm, oracle):
 
 
 def test_fused_long_horizon_kahan(idm, oracle):
-    """idm_fit_step beyond 2,000 steps (compensated displacement in the fused forward) equals
-    the separate calls bit for bit."""
+    """idm_fit_step beyond 2,000 steps (compensated displacement in the fused forward; the L2
+    backward rebuilds compensated positions) equals the separate calls bit for bit."""
     w = synth.make_workload("C3", lane_sizes=[60, 60], K=2500, seed=3)
     obs = torch.as_tensor(synth.kinematic_obs(w), device="cuda")
-    a = idm.from_workload(w, w.theta_true, max_steps=w.K)
-    b = idm.from_workload(w, w.theta_true, max_steps=w.K)
-    a.forward(w.K)
-    La = a.loss_grad(obs)
-    a.backward()
-    a.adam_step(0)
-    Lb = b.fit_step(obs, iteration=0, sync=True)
-    torch.cuda.synchronize()
-    assert abs(La - Lb) <= 1e-6 * La
-    assert torch.equal(a.params, b.params)
+    for kind in ("l1", "l2"):
+        a = idm.from_workload(w, w.theta_true, max_steps=w.K)
+        b = idm.from_workload(w, w.theta_true, max_steps=w.K)
+        a.forward(w.K)
+        La = a.loss_grad(obs, kind=kind)
+        a.backward()
+        a.adam_step(0)
+        Lb = b.fit_step(obs, kind=kind, iteration=0, sync=True)
+        torch.cuda.synchronize()
+        assert abs(La - Lb) <= 1e-6 * La
+        assert torch.equal(a.params, b.params)
+        assert torch.equal(a.grad_params, b.grad_params)
+
+
+@pytest.mark.parametrize("K", [1, 3, 5])
+def test_fit_step_short_horizons(idm, K):
+    """Rollouts shorter than one segment (or one segment plus a tail): the fused kernels'
+    partial-segment paths (sign rows incl. the last step, gap rebuild) equal the separate calls."""
+    cap = idm.load_library().idm_max_lane_vehicles()
+    w = synth.make_workload("C2", lane_sizes=[1, 2, 37, cap - 1, 64, 3], K=K, seed=40 + K)
+    obs = synth.kinematic_obs(w)
+    obs[np.random.default_rng(K).random(obs.shape) < 0.3] = np.nan
+    o = torch.as_tensor(obs, device="cuda")
+    for kind in ("l1", "l2"):
+        a = idm.from_workload(w, None, max_steps=8)
+        b = idm.from_workload(w, None, max_steps=8)
+        for it in range(3):
+            a.forward(K)
+            La = a.loss_grad(o, kind=kind)
+            a.backward()
+            a.adam_step(it)
+            Lb = b.fit_step(o, kind=kind, iteration=it, steps=K, sync=True)
+            torch.cuda.synchronize()
+            assert abs(La - Lb) <= 1e-6 * max(abs(La), 1e-30)
+            assert torch.equal(a.grad_params, b.grad_params)
+            assert torch.equal(a.grad_state0, b.grad_state0)
+            assert torch.equal(a.params, b.params)
 
 
 def test_empty_and_malformed_inputs(idm):
