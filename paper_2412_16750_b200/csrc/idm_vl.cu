@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kVT) vl_fwd_kernel(VlArgs a) {
 
 // ------------------------------------------------------------------------------ backward
 template <bool D4, bool ADAM, int KS>
-__global__ void __launch_bounds__(kVT) vl_bwd_kernel(VlArgs a) {
+__global__ void __launch_bounds__(kVT, 2) vl_bwd_kernel(VlArgs a) {
     const int tid = threadIdx.x;
     const int64_t N = a.n;
     const int steps = a.steps;
