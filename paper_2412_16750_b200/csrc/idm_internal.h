@@ -166,16 +166,21 @@ __device__ __forceinline__ void adam_update(const AdamArgs& a, int q, int64_t e,
 }
 
 
-// Adam on one unconstrained leaf (virtual-leader lists), explicit roundings so the separate
-// kernel and the fused backward produce the same bits.
+// Adam on one scalar (parameters and virtual-leader leaves), explicit roundings so the separate
+// kernels, the fused backward and the whole-fit kernel produce the same bits.  The update
+//   x - step m1 / (sqrt(m2) / c + eps)  ==  x - (step c) m1 / (sqrt(m2) + eps c),  c = sqrt(bc2)
+// uses the MUFU sqrt and reciprocal (a few ulp on a step of size ~lr) instead of IEEE divide and
+// square root, whose slow paths dominated the virtual-leader backward's instruction count.
 __device__ __forceinline__ float leaf_adam(float x, float g, float& m, float& v, float step_size,
                                            float sqrt_bc2, float b1, float b2, float eps) {
     const float m1 = __fmaf_rn(__fsub_rn(1.f, b1), g, __fmul_rn(m, b1));
     const float m2 = __fmaf_rn(__fmul_rn(__fsub_rn(1.f, b2), g), g, __fmul_rn(v, b2));
     m = m1;
     v = m2;
-    const float denom = __fadd_rn(__fdiv_rn(__fsqrt_rn(m2), sqrt_bc2), eps);
-    return __fmaf_rn(-step_size, __fdiv_rn(m1, denom), x);
+    float sq;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(m2));
+    const float den = __fmaf_rn(eps, sqrt_bc2, sq);
+    return __fmaf_rn(-__fmul_rn(step_size, sqrt_bc2), __fmul_rn(m1, rcp(den)), x);
 }
 #endif
 
