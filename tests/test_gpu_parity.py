@@ -670,6 +670,28 @@ def test_fused_long_horizon_kahan(idm, oracle):
         assert torch.equal(a.grad_params, b.grad_params)
 
 
+@pytest.mark.parametrize("kind", ["l1", "l2"])
+def test_fit_step_deterministic(idm, kind):
+    """The fused iteration (bulk-copy / cp.async staging rings, mbarriers, ballot sign words,
+    shared-memory exchanges) is bitwise reproducible across runs at C2 scale with missing
+    observations: a race in any of them would show up here."""
+    w = synth.make_workload("C2", seed=77)
+    obs = synth.kinematic_obs(w)
+    obs[np.random.default_rng(77).random(obs.shape) < 0.1] = np.nan
+    o = torch.as_tensor(obs, device="cuda")
+    runs = []
+    for _ in range(2):
+        sim = idm.from_workload(w, None, max_steps=w.K)
+        losses = [sim.fit_step(o, kind=kind, iteration=it, sync=True) for it in range(3)]
+        torch.cuda.synchronize()
+        runs.append((losses, sim.params.clone(), sim.grad_params.clone(),
+                     sim.grad_state0.clone(), sim.adam_m.clone(), sim.adam_v.clone()))
+    (la, *ta), (lb, *tb) = runs
+    assert la == lb
+    for x, y in zip(ta, tb):
+        assert torch.equal(x, y)
+
+
 @pytest.mark.parametrize("K", [1, 3, 5])
 def test_fit_step_short_horizons(idm, K):
     """Rollouts shorter than one segment (or one segment plus a tail): the fused kernels'
