@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "../../include/idm.h"
@@ -78,19 +79,74 @@ int64_t max_tiles_for(const idm_desc* d) {
     return d->n_lanes < by_size ? d->n_lanes : by_size;
 }
 
-bool layout_for(const idm_desc* d, Layout* L) {
+// Lane-tile plan (cold path, host): whole lanes per tile, <= kCap vehicles; greedy, so two
+// consecutive tiles always hold > kCap vehicles (tiles <= 2N/kCap + 1).  Fills tile starts and
+// leader flags (if given); returns the tile count, or -1 with *err set.
+int64_t plan_tiles(const std::vector<int32_t>& off, int32_t n_lanes, int64_t n,
+                   std::vector<int64_t>* tiles, std::vector<uint8_t>* lead, std::string* err) {
+    char buf[256];
+    if (off[0] != 0 || off.back() != n) {
+        std::snprintf(buf, sizeof buf, "lane_offsets must start at 0 and end at N=%lld (got %d..%d)",
+                      (long long)n, off[0], off.back());
+        *err = buf;
+        return -1;
+    }
+    int64_t count = 1, cur = 0;  // cur: vehicles in the open tile
+    if (tiles) tiles->assign(1, 0);
+    for (int32_t l = 0; l < n_lanes; ++l) {
+        const int64_t a = off[l], b = off[l + 1];
+        if (b < a) {
+            std::snprintf(buf, sizeof buf, "lane_offsets decrease at lane %d", l);
+            *err = buf;
+            return -1;
+        }
+        const int64_t sz = b - a;
+        if (sz == 0) continue;
+        if (sz > kCap) {
+            std::snprintf(buf, sizeof buf,
+                          "lane %d has %lld vehicles; at most %d per lane are supported", l,
+                          (long long)sz, kCap);
+            *err = buf;
+            return -1;
+        }
+        if (cur + sz > kCap) {
+            if (tiles) tiles->push_back(a);
+            ++count;
+            cur = 0;
+        }
+        cur += sz;
+        if (lead)
+            for (int64_t i = a; i + 1 < b; ++i) (*lead)[(size_t)i] = 1;
+    }
+    if (tiles) tiles->push_back(n);
+    return count;
+}
+
+// Tile count of the descriptor's lane plan (reads lane_offsets), or the bound if unreadable.
+int64_t tiles_of(const idm_desc* d) {
+    if (!d || !d->lane_offsets || d->n_lanes < 1) return -1;
+    std::vector<int32_t> off((size_t)d->n_lanes + 1);
+    if (cudaMemcpy(off.data(), d->lane_offsets, sizeof(int32_t) * off.size(), cudaMemcpyDefault) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    std::string err;
+    return plan_tiles(off, d->n_lanes, d->n_vehicles, nullptr, nullptr, &err);
+}
+
+// ntiles: the plan's tile count (< 0: size for the bound max_tiles_for)
+bool layout_for(const idm_desc* d, int64_t ntiles, Layout* L) {
     if (!d || d->n_vehicles < 1 || d->n_lanes < 1 || d->max_steps < 1 ||
         !ckpt_supported(d->ckpt_every))
         return false;
     int64_t n = d->n_vehicles;
-    int64_t mt = max_tiles_for(d);
+    int64_t mt = ntiles > 0 ? ntiles : max_tiles_for(d);
     int64_t nck = (d->max_steps + d->ckpt_every - 1) / d->ckpt_every;
     size_t off = 0;
     L->tile_start = off; off += align256(sizeof(int64_t) * (mt + 1));
     L->lead = off; off += align256((size_t)n);
-    // lane mode: tile-local state history (idm_internal.h); sized for the worst-case tile
-    // count (the plan is built at idm_init), +64 floats so the leader read of a tile's last
-    // slot stays in bounds
+    // lane mode: tile-local state history (idm_internal.h), sized for the plan's tile count
     L->vt_stride = (int64_t)(d->max_steps + 1) * kCap;
     L->ck_stride = nck * kCkRows * kCap;
     L->vt = off; off += align256(sizeof(float) * ((size_t)(mt * L->vt_stride) + 64));
@@ -224,7 +280,7 @@ extern "C" {
 
 size_t idm_workspace_bytes(const idm_desc* d) {
     Layout L;
-    return layout_for(d, &L) ? L.total : 0;
+    return layout_for(d, tiles_of(d), &L) ? L.total : 0;
 }
 
 int32_t idm_max_lane_vehicles(void) { return kCap; }
@@ -268,7 +324,7 @@ int idm_init(idm_handle** out, const idm_desc* d) {
         Layout L;
         if (!d) { bail(fail(h, IDM_EINVAL, "NULL descriptor")); break; }
         h->d = *d;
-        if (!layout_for(d, &L)) {
+        if (!layout_for(d, -1, &L)) {
             bail(fail(h, IDM_EINVAL, "malformed descriptor (need N >= 1, L >= 1, max_steps >= 1, "
                                      "ckpt_every in {2, 4, 8})"));
             break;
@@ -298,13 +354,34 @@ int idm_init(idm_handle** out, const idm_desc* d) {
             bail(fail(h, IDM_EINVAL, "required device array is NULL"));
             break;
         }
+        // ---- lane plan on the host (cold path); the workspace is sized for its tile count
+        std::vector<int32_t> off((size_t)d->n_lanes + 1);
+        cudaError_t ce = cudaMemcpyAsync(off.data(), d->lane_offsets, sizeof(int32_t) * off.size(),
+                                         cudaMemcpyDefault, (cudaStream_t)d->stream);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize((cudaStream_t)d->stream);
+        if (ce != cudaSuccess) {
+            bail(fail(h, IDM_ECUDA, "reading lane_offsets: %s", cudaGetErrorString(ce)));
+            break;
+        }
+        std::vector<int64_t> tiles;
+        std::vector<uint8_t> lead((size_t)d->n_vehicles, 0);
+        std::string perr;
+        const int64_t nt = plan_tiles(off, d->n_lanes, d->n_vehicles, &tiles, &lead, &perr);
+        if (nt < 0) {
+            bail(fail(h, IDM_EINVAL, "%s", perr.c_str()));
+            break;
+        }
+        if (nt > max_tiles_for(d) || !layout_for(d, nt, &L)) {
+            bail(fail(h, IDM_EINVAL, "internal: tile plan exceeds bound"));
+            break;
+        }
         if (!d->workspace || d->workspace_bytes < L.total || ((uintptr_t)d->workspace & 255)) {
             bail(fail(h, IDM_EINVAL, "workspace must be >= %zu bytes and 256-byte aligned",
                       L.total));
             break;
         }
         int dev = -1;
-        cudaError_t ce = cudaGetDevice(&dev);
+        ce = cudaGetDevice(&dev);
         cudaDeviceProp prop;
         if (ce == cudaSuccess) ce = cudaGetDeviceProperties(&prop, dev);
         if (ce != cudaSuccess) {
@@ -338,54 +415,7 @@ int idm_init(idm_handle** out, const idm_desc* d) {
 
         h->nck = (int)((d->max_steps + d->ckpt_every - 1) / d->ckpt_every);
 
-        // ---- lane plan on the host (cold path): whole lanes per tile, <= kCap vehicles
-        std::vector<int32_t> off((size_t)d->n_lanes + 1);
-        ce = cudaMemcpyAsync(off.data(), d->lane_offsets, sizeof(int32_t) * off.size(),
-                             cudaMemcpyDeviceToHost, h->st);
-        if (ce == cudaSuccess) ce = cudaStreamSynchronize(h->st);
-        if (ce != cudaSuccess) {
-            bail(fail(h, IDM_ECUDA, "reading lane_offsets: %s", cudaGetErrorString(ce)));
-            break;
-        }
-        if (off[0] != 0 || off.back() != d->n_vehicles) {
-            bail(fail(h, IDM_EINVAL, "lane_offsets must start at 0 and end at N=%lld (got %d..%d)",
-                      (long long)d->n_vehicles, off[0], off.back()));
-            break;
-        }
-        std::vector<int64_t> tiles;
-        std::vector<uint8_t> lead((size_t)d->n_vehicles, 0);
-        tiles.push_back(0);
-        int64_t cur = 0;  // vehicles in the open tile
-        bool bad = false;
-        for (int32_t l = 0; l < d->n_lanes; ++l) {
-            int64_t a = off[l], b = off[l + 1];
-            if (b < a) {
-                bail(fail(h, IDM_EINVAL, "lane_offsets decrease at lane %d", l));
-                bad = true;
-                break;
-            }
-            int64_t sz = b - a;
-            if (sz == 0) continue;
-            if (sz > kCap) {
-                bail(fail(h, IDM_EINVAL, "lane %d has %lld vehicles; at most %d per lane are "
-                                         "supported", l, (long long)sz, kCap));
-                bad = true;
-                break;
-            }
-            if (cur + sz > kCap) {
-                tiles.push_back(a);
-                cur = 0;
-            }
-            cur += sz;
-            for (int64_t i = a; i + 1 < b; ++i) lead[(size_t)i] = 1;
-        }
-        if (bad) break;
-        tiles.push_back(d->n_vehicles);
-        h->ntiles = (int)tiles.size() - 1;
-        if ((int64_t)h->ntiles > max_tiles_for(d)) {
-            bail(fail(h, IDM_EINVAL, "internal: tile plan exceeds bound"));
-            break;
-        }
+        h->ntiles = (int)nt;
         const char* what = "upload tile plan";
         ce = cudaMemcpyAsync(h->tile_start, tiles.data(), sizeof(int64_t) * tiles.size(),
                              cudaMemcpyHostToDevice, h->st);

@@ -48,8 +48,9 @@ def test_workspace_bytes_and_descriptor_checks(lib):
     d.max_steps = 300
     d.ckpt_every = 4
     ws = lib.idm_workspace_bytes(C.byref(d))
-    # checkpoints (gap, speed) fp32 for ceil(300/4) = 75 segments dominate
-    assert ws >= 75 * 2 * 4 * 1000
+    # the speed history dominates: every vehicle slot at every step, fp32 (tile-local; with
+    # lane_offsets unreadable the size is for the worst-case tile count)
+    assert ws >= 301 * 4 * 1000
     assert ws % 256 == 0
     for bad in (0, 1, 3, 5, 16):
         d.ckpt_every = bad
