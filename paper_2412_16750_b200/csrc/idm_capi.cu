@@ -33,6 +33,9 @@ struct idm_handle {
     // host-side resources for idm_step_host / synchronous reads
     cudaStream_t copy_st;
     cudaEvent_t ev_obs, ev_loss_done;
+    // fused iteration in tile chunks: backward of chunk c on st2 overlaps forward of chunk c+1
+    cudaStream_t st2;
+    cudaEvent_t ev_fork, ev_join, ev_chunk[16];
     double* pinned;  // [0] loss, [1] status (as bits), [2] flags
     int stage;       // 0 = initialised, 1 = forward done, 2 = loss done, 3 = backward done
     int32_t steps;
@@ -214,21 +217,33 @@ cudaEvent_t pool_event(idm_handle* h) {
 struct TimedLaunch {
     idm_handle* h;
     int kind;
+    cudaStream_t st;
     cudaEvent_t a = nullptr, b = nullptr;
-    TimedLaunch(idm_handle* h_, int kind_) : h(h_), kind(kind_) {
+    TimedLaunch(idm_handle* h_, int kind_, cudaStream_t st_ = nullptr)
+        : h(h_), kind(kind_), st(st_ ? st_ : h_->st) {
         if (h->timing) {
             a = pool_event(h);
             b = pool_event(h);
-            cudaEventRecord(a, h->st);
+            cudaEventRecord(a, st);
         }
     }
     ~TimedLaunch() {
         if (h->timing && a && b) {
-            cudaEventRecord(b, h->st);
+            cudaEventRecord(b, st);
             h->ev_rec->push_back({kind, {a, b}});
         }
     }
 };
+
+// Tile chunks of the fused iteration (IDM_FUSED_CHUNKS, default 1 = no split).
+int fused_chunks(const idm_handle* h) {
+    static const int env = [] {
+        const char* e = std::getenv("IDM_FUSED_CHUNKS");
+        return e ? std::atoi(e) : 1;
+    }();
+    int c = env < 1 ? 1 : (env > 16 ? 16 : env);
+    return c > h->ntiles ? h->ntiles : c;
+}
 
 int sync_status(idm_handle* h) {
     CK(h, cudaMemcpyAsync(&h->pinned[1], h->status, sizeof(unsigned long long),
@@ -304,6 +319,11 @@ void idm_destroy(idm_handle* h) {
         delete h->ev_pool;
     }
     if (h->copy_st) cudaStreamDestroy(h->copy_st);
+    if (h->st2) cudaStreamDestroy(h->st2);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
+    for (cudaEvent_t e : h->ev_chunk)
+        if (e) cudaEventDestroy(e);
     if (h->ev_obs) cudaEventDestroy(h->ev_obs);
     if (h->ev_loss_done) cudaEventDestroy(h->ev_loss_done);
     if (h->pinned) cudaFreeHost(h->pinned);
@@ -437,6 +457,14 @@ int idm_init(idm_handle** out, const idm_desc* d) {
         }
         if (ce == cudaSuccess)
             ce = cudaEventCreateWithFlags(&h->ev_loss_done, cudaEventDisableTiming);
+        if (ce == cudaSuccess) {
+            what = "chunk stream / events";
+            ce = cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking);
+            if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
+            if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
+            for (cudaEvent_t& e : h->ev_chunk)
+                if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        }
         if (ce == cudaSuccess) {
             what = "pinned buffer";
             ce = cudaMallocHost((void**)&h->pinned, 4 * sizeof(double));
@@ -769,28 +797,52 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
     var.kahan = steps > 2000;
     var.rec_v = false;
     var.loss = 1 + kind;
-    {
-        TimedLaunch tl(h, IDM_K_FWD);
-        CK(h, launch_fwd(f, h->ntiles, var, h->st));
-    }
-    {
-        TimedLaunch tl(h, IDM_K_REDUCE);
-        CK(h, launch_reduce(h->loss_partials, h->ntiles, 1, h->loss_scalar, nullptr, h->st));
-    }
-    h->launches += 2;
     h->steps = steps;
-    // backward: dL/dP re-derived from obs and the rebuilt positions; per-vehicle parameters
-    // get Adam in the same kernel's epilogue
+    // backward: dL/dP from the forward's sign words (L1) or re-derived from obs and rebuilt
+    // positions (L2); per-vehicle parameters get Adam in the same kernel's epilogue
     BwdArgs b = bwd_args(h, steps);
     b.obs = obs;
     b.pos0 = h->d.pos0;
     b.adam = make_adam(h, iter, total_iters, lr0, lr1);
     const bool shared = h->d.param_mode == IDM_PARAMS_SHARED;
+    // Tiles are independent, so the iteration can run in tile chunks: the backward of chunk c
+    // (second stream) overlaps the forward of chunk c + 1; every chunk does the same
+    // arithmetic on the same tiles, so the results do not depend on the chunking.
+    const int nch = fused_chunks(h);
+    cudaStream_t sb = nch > 1 ? h->st2 : h->st;
+    if (nch > 1) {
+        CK(h, cudaEventRecord(h->ev_fork, h->st));
+        CK(h, cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
+    }
+    for (int c = 0; c < nch; ++c) {
+        const int t0 = (int)((int64_t)h->ntiles * c / nch);
+        const int t1 = (int)((int64_t)h->ntiles * (c + 1) / nch);
+        if (t1 <= t0) continue;
+        f.tile0 = t0;
+        b.tile0 = t0;
+        {
+            TimedLaunch tl(h, IDM_K_FWD);
+            CK(h, launch_fwd(f, t1 - t0, var, h->st));
+        }
+        if (nch > 1) {
+            CK(h, cudaEventRecord(h->ev_chunk[c], h->st));
+            CK(h, cudaStreamWaitEvent(h->st2, h->ev_chunk[c], 0));
+        }
+        {
+            TimedLaunch tl(h, IDM_K_BWD, sb);
+            CK(h, launch_bwd(b, t1 - t0, h->delta4, shared, !shared, 1 + kind, var.kahan, sb));
+        }
+        h->launches += 2;
+    }
     {
-        TimedLaunch tl(h, IDM_K_BWD);
-        CK(h, launch_bwd(b, h->ntiles, h->delta4, shared, !shared, 1 + kind, var.kahan, h->st));
+        TimedLaunch tl(h, IDM_K_REDUCE);
+        CK(h, launch_reduce(h->loss_partials, h->ntiles, 1, h->loss_scalar, nullptr, h->st));
     }
     h->launches++;
+    if (nch > 1) {
+        CK(h, cudaEventRecord(h->ev_join, h->st2));
+        CK(h, cudaStreamWaitEvent(h->st, h->ev_join, 0));
+    }
     if (shared) {
         {
             TimedLaunch tl(h, IDM_K_REDUCE);

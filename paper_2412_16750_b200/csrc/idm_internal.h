@@ -48,6 +48,7 @@ struct FwdArgs {
     int64_t vt_stride, ck_stride;  // floats per tile
     uint32_t* sgn;                 // fused L1: sign words
     int64_t sg_stride;             // words per tile
+    int tile0;                     // first tile of this launch (grid = a chunk of the tiles)
     int steps, ckpt_every;
     Consts k;
     unsigned long long* status;
@@ -77,6 +78,7 @@ struct BwdArgs {
     int64_t vt_stride, ck_stride;
     const uint32_t* sgn;
     int64_t sg_stride;
+    int tile0;  // first tile of this launch
     float *grad_params, *grad_state0;
     double* shared_partials;  // [ntiles][6] (shared mode)
     int steps, ckpt_every;

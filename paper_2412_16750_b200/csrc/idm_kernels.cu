@@ -82,7 +82,7 @@ __device__ __forceinline__ RawP dummy_raw() { return RawP{1.f, 1.f, 1.f, 1.f, 1.
 constexpr int kVpt = 2;          // vehicles per thread (one float2 lane pair)
 constexpr int kT = kCap / kVpt;   // 256 threads per CTA
 
-// fixed-order CTA reduction of one double per thread -> out[blockIdx.x] (deterministic)
+// fixed-order CTA reduction of one double per thread -> *out (deterministic)
 __device__ __forceinline__ void block_sum_to(double x, double* out) {
     __shared__ double red[kT / 32];
 #pragma unroll
@@ -92,7 +92,7 @@ __device__ __forceinline__ void block_sum_to(double x, double* out) {
     if (threadIdx.x == 0) {
         double y = 0.0;
         for (int w = 0; w < kT / 32; ++w) y += red[w];
-        out[blockIdx.x] = y;
+        *out = y;
     }
 }
 
@@ -166,8 +166,9 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
     constexpr int KS = CK > 4 ? CK : 4;
     __shared__ float xv[2][kT + 1];  // speed of each thread's first vehicle; [kT] = 0 sentinel
     const int tid = threadIdx.x;
-    const int64_t base = a.tile_start[blockIdx.x];
-    const int n_loc = (int)(a.tile_start[blockIdx.x + 1] - base);
+    const int tile = a.tile0 + (int)blockIdx.x;  // launches may cover a chunk of the tiles
+    const int64_t base = a.tile_start[tile];
+    const int n_loc = (int)(a.tile_start[tile + 1] - base);
     const Consts k = a.k;
     const int64_t N = a.n;
     const int steps = a.steps;
@@ -209,8 +210,8 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
     float* orow = LOSS ? nullptr : a.traj + i0;
     float* vrow = RECV ? a.vel_traj + i0 : nullptr;
     // tile-local state history: speed row of every step, (gap, D, compensation) every CK steps
-    float2* vtp = reinterpret_cast<float2*>(a.vt + blockIdx.x * a.vt_stride) + tid;
-    float2* ckp = reinterpret_cast<float2*>(a.ckt + blockIdx.x * a.ck_stride) + tid;
+    float2* vtp = reinterpret_cast<float2*>(a.vt + tile * a.vt_stride) + tid;
+    float2* ckp = reinterpret_cast<float2*>(a.ckt + tile * a.ck_stride) + tid;
     constexpr int kR2 = kCap / 2;  // one row in float2 units
     const float* obs = LOSS ? a.obs + i0 : nullptr;
     const float qnan = __int_as_float(0x7fc00000);
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
     };
     // fused L1: dL/dP = -sign(obs - P) of each vehicle as two ballot bits (nonzero, +1); lane 0
     // of each warp stores the warp's four words of the step (16 B)
-    uint4* sgp = LOSS == 1 ? reinterpret_cast<uint4*>(a.sgn + blockIdx.x * a.sg_stride) +
+    uint4* sgp = LOSS == 1 ? reinterpret_cast<uint4*>(a.sgn + tile * a.sg_stride) +
                                  (tid >> 5)
                            : nullptr;
     // Eq. 4 term of the fused forward: L2 sums r^2; L1 sums |r| and records -sign(r) as the
@@ -350,7 +351,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
         put(a.state_out + i0, vadd(p0, D));
         put(a.state_out + N + i0, v);
     }
-    if (LOSS) block_sum_to(lacc + (double)lseg.x + (double)lseg.y, a.loss_partials);
+    if (LOSS) block_sum_to(lacc + (double)lseg.x + (double)lseg.y, a.loss_partials + tile);
 }
 
 // ------------------------------------------------------------------------------ NK3
@@ -377,8 +378,9 @@ template <bool D4, bool SHARED, bool ADAM, int KS, int GOBS, bool KAHAN>
 __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(BwdArgs a) {
     __shared__ float fx[2][kT + 1];
     const int tid = threadIdx.x;
-    const int64_t base = a.tile_start[blockIdx.x];
-    const int n_loc = (int)(a.tile_start[blockIdx.x + 1] - base);
+    const int tile = a.tile0 + (int)blockIdx.x;  // launches may cover a chunk of the tiles
+    const int64_t base = a.tile_start[tile];
+    const int n_loc = (int)(a.tile_start[tile + 1] - base);
     const Consts k = a.k;
     const int64_t N = a.n;
     const int steps = a.steps;
@@ -455,13 +457,13 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
             mbar_expect_tx(&mbar[b], bytes);
             if (SGN)
                 bulk_g2s(sbuf + b * KO * (kSgnWords / 4),
-                         a.sgn + blockIdx.x * a.sg_stride + t0 * kSgnWords,
+                         a.sgn + tile * a.sg_stride + t0 * kSgnWords,
                          srows * kSgnWords * sizeof(uint32_t), &mbar[b]);
-            const float* src = a.vt + blockIdx.x * a.vt_stride + t0 * kCap;
+            const float* src = a.vt + tile * a.vt_stride + t0 * kCap;
             for (int tt = 0; tt < len; ++tt)
                 bulk_g2s(vrow + (b * KS + tt) * VP, src + tt * kCap, kCap * sizeof(float), &mbar[b]);
             bulk_g2s(ckrow + b * kCkRows * kCap,
-                     a.ckt + blockIdx.x * a.ck_stride + (int64_t)seg * kCkRows * kCap,
+                     a.ckt + tile * a.ck_stride + (int64_t)seg * kCkRows * kCap,
                      nckr * kCap * sizeof(float), &mbar[b]);
         }
         if (!SGN) {
@@ -636,7 +638,7 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
         if (tid < 6) {
             double x = 0.0;
             for (int w = 0; w < kT / 32; ++w) x += red[w][tid];
-            a.shared_partials[(int64_t)blockIdx.x * 6 + tid] = x;
+            a.shared_partials[(int64_t)tile * 6 + tid] = x;
         }
     }
 }
