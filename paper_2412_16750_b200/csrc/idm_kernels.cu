@@ -224,22 +224,35 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
     auto ld_obs = [&](const float* o, bool on) {  // absent vehicles observe NaN (= missing)
         return make_float2(ld_cs_if(o, on && val[0], qnan), ld_cs_if(o + 1, on && val[1], qnan));
     };
-    // segment seg observes rows seg*KS + 1 .. seg*KS + KS
+    // segment seg observes rows seg*KS + 1 .. seg*KS + KS; fetches run two segments ahead of
+    // use, slots rotate 0, 1, 2 (fslot: next fetch, cslot: current use)
+    const float* onext = LOSS ? obs + N : nullptr;  // first row of the next fetch
+    int fslot = 0, cslot = 0;
     auto fetch_obs = [&](int seg) {
         const int r0 = seg * KS + 1;
-        const float* o = obs + (int64_t)min(r0, steps) * N;
-        float* dst = &obuf[seg % 3][0][2 * tid];
+        float* dst = &obuf[fslot][0][2 * tid];
+        fslot = fslot == 2 ? 0 : fslot + 1;
+        if (r0 + KS - 1 <= steps) {  // whole segment inside the rollout (CTA-uniform)
+            const float* o = onext;
 #pragma unroll
-        for (int tt = 0; tt < KS; ++tt) {
-            const bool on = r0 + tt <= steps;
-            cp_async4(dst + tt * kCap, o, on && val[0]);
-            cp_async4(dst + tt * kCap + 1, o + 1, on && val[1]);
-            if (r0 + tt < steps) o += N;
+            for (int tt = 0; tt < KS; ++tt, o += N) {
+                cp_async4(dst + tt * kCap, o, val[0]);
+                cp_async4(dst + tt * kCap + 1, o + 1, val[1]);
+            }
+            onext = o;
+        } else {  // the tail / past the end: predicated, addresses kept inside the array
+#pragma unroll
+            for (int tt = 0; tt < KS; ++tt) {
+                const bool on = r0 + tt <= steps;
+                const float* o = on ? onext + (int64_t)tt * N : obs;
+                cp_async4(dst + tt * kCap, o, on && val[0]);
+                cp_async4(dst + tt * kCap + 1, o + 1, on && val[1]);
+            }
         }
         cp_async_commit();
     };
-    auto obs_at = [&](int seg, int tt) {  // this thread's pair of row seg*KS + 1 + tt
-        const float2 o = *reinterpret_cast<const float2*>(&obuf[seg % 3][tt][2 * tid]);
+    auto obs_at = [&](int tt) {  // this thread's pair of row seg*KS + 1 + tt (current segment)
+        const float2 o = *reinterpret_cast<const float2*>(&obuf[cslot][tt][2 * tid]);
         return make_float2(val[0] ? o.x : qnan, val[1] ? o.y : qnan);
     };
     if (LOSS) {
@@ -322,14 +335,16 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
             fetch_obs(seg + 2);
         }
     };
+    auto obs_done = [&] { cslot = cslot == 2 ? 0 : cslot + 1; };
     for (int seg = 0; seg < nfull; ++seg) {
         const int t0 = seg * KS;
         obs_ready(seg);
 #pragma unroll
         for (int tt = 0; tt < KS; ++tt) {
             if (tt % CK == 0 && (tt > 0 || seg > 0)) checkpoint(t0 + tt);
-            step(LOSS ? obs_at(seg, tt) : f2(0.f));
+            step(LOSS ? obs_at(tt) : f2(0.f));
         }
+        obs_done();
         if (LOSS) {
             lacc += (double)lseg.x + (double)lseg.y;
             lseg = f2(0.f);
@@ -341,7 +356,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
         for (int tt = 0; tt < KS; ++tt) {
             if (tt < tail) {  // CTA-uniform predicate
                 if (tt % CK == 0 && (tt > 0 || nfull > 0)) checkpoint(nfull * KS + tt);
-                step(LOSS ? obs_at(nfull, tt) : f2(0.f));
+                step(LOSS ? obs_at(tt) : f2(0.f));
             }
         }
     }
