@@ -372,20 +372,22 @@ def run_ours(args, rank, world, local_rank):
                              f"MEASURED_PEAKS hbm_gbs ({peak_src})"}
     else:
         issue_peak = ISSUE_PER_CLK * sm_mhz_max * 1e6 / 1e12  # Tinstr/s
-        achieved = ALG_INSTR["bwd" if dom == "bwd" else "fwd"] * n_veh_steps / \
-            (kms[dom] * 1e-3) / 1e12
+        kk = "bwd" if dom == "bwd" else "fwd"
+        # essential issue slots of THIS (f32x2-packed) implementation: SURVEY 8(d) addendum
+        achieved = PACKED_INSTR[kk] * n_veh_steps / (kms[dom] * 1e-3) / 1e12
+        frozen = ALG_INSTR[kk] * n_veh_steps / (kms[dom] * 1e-3) / 1e12
         traffic = load_traffic().get(f"{dom}_kernel")
-        packed = PACKED_INSTR["bwd" if dom == "bwd" else "fwd"] * n_veh_steps / \
-            (kms[dom] * 1e-3) / 1e12
         roofline = {"bound": "alu", "kernel": f"{dom}_kernel (fused path)", "achieved": achieved,
                     "peak": issue_peak, "unit": "Tinstr/s", "frac": achieved / issue_peak,
                     "traffic": traffic,
-                    "frac_packed_slots": packed / issue_peak,
-                    "basis": f"{ALG_INSTR[dom]:.0f} essential thread-instr per vehicle-step x "
-                             f"{n_veh_steps:.3g} vehicle-steps per launch / CUDA-event launch "
-                             f"time; peak = 148 SM x 4 issue/clk x 32 lanes x {sm_mhz_max:.0f} "
-                             f"MHz (MEASURED_PEAKS sm_max, {peak_src}); traffic = ncu dram "
-                             f"bytes/launch (profiles/traffic.json)"}
+                    "frac_frozen_scalar_count": frozen / issue_peak,
+                    "basis": f"{PACKED_INSTR[kk]} essential issue slots per vehicle-step (packed "
+                             f"f32x2 implementation; SURVEY 8(d) addendum) x {n_veh_steps:.3g} "
+                             f"vehicle-steps per launch / CUDA-event launch time; peak = 148 SM "
+                             f"x 4 issue/clk x 32 lanes x {sm_mhz_max:.0f} MHz (MEASURED_PEAKS "
+                             f"sm_max, {peak_src}); frac_frozen_scalar_count uses the round-1 "
+                             f"scalar count {ALG_INSTR[kk]:.0f}, which a packed kernel can exceed; "
+                             f"traffic = ncu dram bytes/launch (profiles/traffic.json)"}
 
     def hbm_of(p, path):
         ab = alg_bytes(K, k, path)
