@@ -120,8 +120,9 @@ size_t idm_workspace_bytes(const idm_desc* d);
 int idm_init(idm_handle** out, const idm_desc* d);
 
 /* Simulate `steps` (1..max_steps) synchronous steps from (pos0, vel0) (Eqs. 1-3, Sec. III-B/C,
-   PAPER.md:106-152): one fused launch, state in registers, gap/speed checkpoints every
-   ckpt_every steps, traj rows 0..steps (and vel_traj, state_out if given).
+   PAPER.md:106-152): one fused launch, state in registers; traj rows 0..steps (and vel_traj,
+   state_out if given); the workspace gets every vehicle's speed at every step and its gap every
+   ckpt_every steps, which idm_backward reads back.
    Non-finite states are detected at checkpoints and reported by the next synchronizing call. */
 int idm_forward(idm_handle* h, int32_t steps);
 

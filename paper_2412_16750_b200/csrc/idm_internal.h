@@ -23,7 +23,7 @@ struct FwdVariant {
     bool delta4;  // every delta == 4 (two squarings instead of ex2/lg2)
     bool kahan;   // compensated displacement
     bool rec_v;   // record speeds
-    int loss;     // 0, or fused Eq. 4 (1 = L1, 2 = L2): read obs, write dL/dP (idm_fit_step)
+    int loss;     // 0, or fused Eq. 4 (1 = L1, 2 = L2): read obs, sum the loss (idm_fit_step)
 };
 
 // Lane-mode state history in HBM, TILE-LOCAL layout (internal workspace):
@@ -135,7 +135,6 @@ struct LossArgs {
 cudaError_t launch_validate(const ValidateArgs& a, cudaStream_t st);
 cudaError_t launch_fwd(const FwdArgs& a, int ntiles, const FwdVariant& var, cudaStream_t st);
 cudaError_t kernels_configure(int ckpt_every);
-size_t bwd_smem_bytes(int ckpt_every);
 // gobs = 0: dL/dP from grad_traj; 1: L1 from the forward's sign words; 2: L2 re-derived from obs
 // and the rebuilt positions (gobs != 0: fused idm_fit_step, ckpt_every == 4)
 cudaError_t launch_bwd(const BwdArgs& a, int ntiles, bool delta4, bool shared, bool adam,

@@ -1,18 +1,20 @@
 // idm_kernels.cu -- sm_100a kernels of the differentiable IDM hot path (arXiv 2412.16750).
 //
 //   NK0 validate_kernel   input checks (finite, v >= 0, params > 0)            once per init
-//   NK1 fwd_kernel        K fused steps per lane tile, state in registers       Eqs. 1-3, III-C
+//   NK1 fwd_kernel        K fused steps per lane tile, state in registers;     Eqs. 1-3, III-C
+//                         stores the speed history (+ fused Eq. 4 value, L1 sign bits)
 //   NK2 loss_kernel       Eq. 4 L1/L2 + dL/dP, fixed-order fp64 partials
-//   NK3 bwd_kernel        checkpoint recompute + reverse sweep per lane tile    adjoint of NK1
+//   NK3 bwd_kernel        rebuild gaps from the stored history, local Jacobians, adjoint of NK1
+//                         reverse sweep per lane tile (+ fused Adam epilogue)
 //   NK4 reduce_kernel     fixed-order sum of per-block fp64 partials (loss / shared grads)
 //   NK5 adam_kernel       Adam + linear lr + box clamp
 //
 // A lane tile is a run of WHOLE lanes of at most kCap = 512 vehicles (lanes are independent, so
-// no tile ever needs another tile's data).  A CTA of kT = 256 threads owns one tile; local
-// vehicle id = j * kT + threadIdx.x (j < kVpt = 2), so every global access of a warp is 32
-// consecutive floats and the leader of local vehicle id is id + 1, exchanged through shared
-// memory (one barrier per step).  Checkpoint segments are KS steps (compile-time, unrolled);
-// step-major rows (observations, dL/dP) are prefetched a segment ahead into registers.
+// no tile ever needs another tile's data).  A CTA of kT = 256 threads owns one tile; thread t
+// owns the adjacent local vehicles 2t, 2t + 1 as one float2 pair (packed f32x2 arithmetic), so
+// vehicle 2t's leader is in the thread and 2t + 1's is thread t + 1's first vehicle (one
+// shared-memory word and one barrier per step).  Segments are KS steps (compile-time,
+// unrolled).  Lane-mode state history and its layout: idm_internal.h, DESIGN.md section 3.
 #include <cstdint>
 #include <type_traits>
 #include <cuda_runtime.h>
@@ -156,9 +158,9 @@ __device__ __forceinline__ void cp_async_wait() {
 // its interaction term whatever "leader" speed it reads.
 // All `steps` steps run in one launch, in segments of KS steps (compile-time, fully unrolled;
 // the K mod KS tail runs as one predicated segment).  LOSS = 0: record P (idm_forward).
-// LOSS = 1 (L1) / 2 (L2): fused Eq. 4 for idm_fit_step -- the observation rows of the next
-// segment are prefetched into registers while the current one runs; each step evaluates Eq. 4
-// against the fresh positions and writes dL/dP instead of P.
+// LOSS = 1 (L1) / 2 (L2): fused Eq. 4 for idm_fit_step -- observation rows staged two segments
+// ahead (cp.async ring); each step sums Eq. 4 against the fresh positions and, for L1, records
+// dL/dP = -sign(obs - P) as ballot bits; P and dL/dP are not written.
 // CK = checkpoint interval (the backward's segment length); the forward's own prefetch
 // segment is KS = max(4, CK) steps, so CK | KS and checkpoints fall at static positions.
 template <bool D4, bool KAHAN, bool RECV, int LOSS, int CK>
@@ -769,8 +771,6 @@ cudaError_t launch_validate(const ValidateArgs& a, cudaStream_t st) {
 }
 
 bool ckpt_supported(int k) { return k == 2 || k == 4 || k == 8; }
-
-size_t bwd_smem_bytes(int) { return 0; }  // the backward uses static shared memory only
 
 template <bool D4, bool KH, int KS>
 static void launch_fwd_k(const FwdArgs& a, int ntiles, const FwdVariant& var, cudaStream_t st) {
