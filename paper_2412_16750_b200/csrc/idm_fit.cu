@@ -4,9 +4,14 @@
 // 1-second history (10 steps of 0.1 s) before rolling out.  With K <= kFitMaxSteps the whole
 // state history, the observations and the Adam moments of a 512-vehicle lane tile fit on chip,
 // so fit_kernel runs `iters` complete iterations (forward + Eq. 4 + reverse sweep + Adam) in
-// one launch with no HBM traffic between iterations.  Arithmetic is the same device code as
-// fwd_kernel<LOSS> / bwd_kernel<ADAM> (core, jac_record, bwd_from_record, loss term, Adam), in
-// the same order, so the parameters come out bit-identical to `iters` idm_fit_step calls.
+// one launch with no HBM traffic between iterations.
+//
+// Layout as the lane kernels: 256 threads, thread t owns the adjacent vehicles 2t, 2t + 1 as
+// one float2 pair (packed f32x2 arithmetic); the Adam state of both vehicles stays in registers
+// across iterations, the per-step history (speeds, gaps, dL/dP) and the observations live in
+// this CTA's shared memory.  Arithmetic is the same device code as fwd_kernel<LOSS> /
+// bwd_kernel<ADAM> (core, jac_record, bwd_from_record, loss term, Adam), in the same order, so
+// the parameters come out bit-identical to `iters` idm_fit_step calls.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -15,12 +20,23 @@
 
 namespace idm {
 
-constexpr int kFT = kCap;  // one vehicle per thread, 512 threads per CTA
+namespace {
+constexpr int kFT = kCap / 2;  // 256 threads, two vehicles each
+
+template <int KM>
+constexpr size_t fit_smem_of() {  // speed pairs (+ sentinel) | gaps | dL/dP | observations
+    return (size_t)(KM * (kFT + 1) + KM * kFT + 2 * (KM + 1) * kFT) * sizeof(float2);
+}
+}  // namespace
 
 template <int KM, bool D4, int KIND>
-__global__ void __launch_bounds__(kFT, 1) fit_kernel(FitArgs a) {
-    __shared__ float hv[KM][kCap + 1];  // speeds per step (leader reads)
-    __shared__ float fx[2][kCap + 1];   // follower -> leader adjoint term
+__global__ void __launch_bounds__(kFT, 2) fit_kernel(FitArgs a) {
+    extern __shared__ __align__(16) float2 smem_fit[];
+    float2* hv = smem_fit;                        // [KM][kFT + 1] speed pairs; [kFT] = 0
+    float2* sg = hv + KM * (kFT + 1);             // [KM][kFT]     gap pairs
+    float2* gg = sg + KM * kFT;                   // [KM + 1][kFT] dL/dP pairs
+    float2* ob = gg + (KM + 1) * kFT;             // [KM + 1][kFT] observation pairs
+    __shared__ float fx[2][kFT + 1];              // follower -> leader adjoint term
     __shared__ double red[kFT / 32];
     const int tid = threadIdx.x;
     const int64_t base = a.tile_start[blockIdx.x];
@@ -28,124 +44,152 @@ __global__ void __launch_bounds__(kFT, 1) fit_kernel(FitArgs a) {
     const int64_t N = a.n;
     const int K = a.steps;
     const Consts k = a.k;
-    const bool valid = tid < n_loc;
-    const int64_t i = base + tid;
+    const int id0 = 2 * tid;
+    const int64_t i0 = base + id0;
+    const bool val[2] = {id0 < n_loc, id0 + 1 < n_loc};
+    const float qnan = __int_as_float(0x7fc00000);
 
-    float p0 = 0.f, v0 = 0.f, s0 = 0.f, leadf = 0.f;
-    float x[6] = {1.f, 1.f, 1.f, 1.f, 1.f, 4.f}, m1[6], m2[6];
-    float ob[KM + 1];
-    if (valid) {
-        p0 = a.pos0[i];
-        v0 = a.vel0[i];
-        const bool lead = a.lead[i] != 0;
-        leadf = lead ? 1.f : 0.f;
-        s0 = lead ? (a.pos0[i + 1] - p0) - a.length[i + 1] : 0.f;
+    float pj[2] = {0.f, 0.f}, vj[2] = {0.f, 0.f}, sj[2] = {0.f, 0.f}, lf[2] = {0.f, 0.f};
+    float x[2][6], m1[2][6], m2[2][6];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int64_t i = i0 + j;
 #pragma unroll
         for (int q = 0; q < 6; ++q) {
-            x[q] = a.params[q * N + i];
-            m1[q] = a.adam_m[q * N + i];
-            m2[q] = a.adam_v[q * N + i];
+            x[j][q] = q == 5 ? 4.f : 1.f;
+            m1[j][q] = 0.f;
+            m2[j][q] = 0.f;
         }
-    } else {
+        if (val[j]) {
+            pj[j] = a.pos0[i];
+            vj[j] = a.vel0[i];
+            const bool lead = a.lead[i] != 0;
+            lf[j] = lead ? 1.f : 0.f;
+            sj[j] = lead ? (a.pos0[i + 1] - pj[j]) - a.length[i + 1] : 0.f;
 #pragma unroll
-        for (int q = 0; q < 6; ++q) { m1[q] = 0.f; m2[q] = 0.f; }
+            for (int q = 0; q < 6; ++q) {
+                x[j][q] = a.params[q * N + i];
+                m1[j][q] = a.adam_m[q * N + i];
+                m2[j][q] = a.adam_v[q * N + i];
+            }
+            if (D4 && x[j][5] != 4.f)
+                atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
+        }
     }
-#pragma unroll
-    for (int t = 0; t <= KM; ++t)  // absent vehicles observe NaN (= missing)
-        ob[t] = (valid && t <= K) ? a.obs[(int64_t)t * N + i] : __int_as_float(0x7fc00000);
+    const float2 p0 = make_float2(pj[0], pj[1]), v0 = make_float2(vj[0], vj[1]);
+    const float2 s0 = make_float2(sj[0], sj[1]), leadf = make_float2(lf[0], lf[1]);
+    for (int t = 0; t <= KM; ++t) {  // absent vehicles observe NaN (= missing)
+        const float* o = a.obs + (int64_t)min(t, K) * N + i0;
+        ob[t * kFT + tid] = make_float2((val[0] && t <= K) ? o[0] : qnan,
+                                        (val[1] && t <= K) ? o[1] : qnan);
+    }
     if (tid == 0) {
         fx[0][0] = 0.f;
         fx[1][0] = 0.f;
     }
-    if (tid < KM) hv[tid][kCap] = 0.f;  // leader-read sentinel of the last thread
-    if (D4 && valid && x[5] != 4.f)
-        atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
+    if (tid < KM) hv[tid * (kFT + 1) + kFT] = f2(0.f);  // leader-read sentinel of thread kFT-1
+    __syncthreads();
 
-    float st[KM], vt[KM], g[KM + 1];
-    float lsum = 0.f;
+    float2 lsum = f2(0.f);
     int par = 0;
     for (int it = 0; it < a.iters; ++it) {
-        const VehP P = make_vehp(x[0], x[1], x[2], x[3], x[4], x[5]);
-        const VehB B = make_vehb(x[0], x[1], x[4], x[5]);
+        const VehPT<float2> P =
+            pack(make_vehp(x[0][0], x[0][1], x[0][2], x[0][3], x[0][4], x[0][5]),
+                 make_vehp(x[1][0], x[1][1], x[1][2], x[1][3], x[1][4], x[1][5]));
+        const VehBT<float2> B = pack(make_vehb(x[0][0], x[0][1], x[0][4], x[0][5]),
+                                     make_vehb(x[1][0], x[1][1], x[1][4], x[1][5]));
         // ---- forward + Eq. 4 (as fwd_kernel<LOSS>)
-        float s = s0, v = v0, D = 0.f;
-        lsum = 0.f;
-        g[0] = loss_term<KIND>(ob[0], p0, lsum);
+        float2 s = s0, v = v0, D = f2(0.f);
+        lsum = f2(0.f);
+        gg[tid] = loss_term<KIND>(ob[tid], p0, lsum);
 #pragma unroll
         for (int t = 0; t < KM; ++t) {
             if (t < K) {
-                st[t] = s;
-                vt[t] = v;
-                hv[t][tid] = v;
+                sg[t * kFT + tid] = s;
+                hv[t * (kFT + 1) + tid] = v;
                 __syncthreads();
-                const float vl = hv[t][tid + 1];
+                const float2 vl = make_float2(v.y, hv[t * (kFT + 1) + tid + 1].x);
                 D = vfma(v, k.dt, D);
                 fwd_step<D4>(s, v, vl, leadf, P, k);
-                g[t + 1] = loss_term<KIND>(ob[t + 1], vadd(p0, D), lsum);
+                gg[(t + 1) * kFT + tid] =
+                    loss_term<KIND>(ob[(t + 1) * kFT + tid], vadd(p0, D), lsum);
             }
         }
         // ---- reverse sweep (as bwd_kernel: local Jacobian of each step, then the update)
-        float ls = 0.f, lv = 0.f, lD = 0.f;
-        GradAcc G = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int t = KM; t >= 0; --t)
-            if (t == K) lD = g[t];  // lambda_D^K = dL/dP(K)
+        float2 ls = f2(0.f), lv = f2(0.f), lD = gg[K * kFT + tid];  // lambda_D^K = dL/dP(K)
+        GradAccT<float2> G = {f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
 #pragma unroll
         for (int t = KM - 1; t >= 0; --t) {
             if (t < K) {
-                const float vl = hv[t][tid + 1];
-                Core c;
-                core<D4>(st[t], vt[t], vl, leadf, P, k, c);
-                const RecT<float> R = jac_record<D4>(c, st[t], vt[t], P, B, k);
-                const float F = bwd_from_record<D4>(R, vt[t], vl, P, B, k, ls, lv, lD, G);
-                fx[par][tid + 1] = F;
+                const float2 vv = hv[t * (kFT + 1) + tid];
+                const float2 vl = make_float2(vv.y, hv[t * (kFT + 1) + tid + 1].x);
+                const float2 sv = sg[t * kFT + tid];
+                CoreT<float2> c;
+                core<D4>(sv, vv, vl, leadf, P, k, c);
+                const RecT<float2> R = jac_record<D4>(c, sv, vv, P, B, k);
+                const float2 F = bwd_from_record<D4>(R, vv, vl, P, B, k, ls, lv, lD, G);
+                fx[par][tid + 1] = F.y;  // vehicle 2t + 1 -> its leader 2t + 2 (thread t + 1)
                 __syncthreads();
-                lv = vadd(lv, fx[par][tid]);
-                lD = vadd(lD, g[t]);
+                lv = vadd(lv, make_float2(fx[par][tid], F.x));
+                lD = vadd(lD, gg[t * kFT + tid]);
                 par ^= 1;
             }
         }
         // ---- gradients (as bwd_kernel's epilogue) + Adam (as adam_update)
-        const float c = 0.5f / sqrtf(x[0] * x[1]);
-        float gr[6];
-        gr[0] = G.S1 - c * (0.5f / x[0]) * G.S2;
-        gr[1] = -c * (0.5f / x[1]) * G.S2;
-        gr[2] = G.S3;
-        gr[3] = G.S4;
-        gr[4] = x[0] * x[5] / x[4] * G.S5;
-        gr[5] = -x[0] * kLn2 * G.S6;
+        const float Sj[6][2] = {{G.S1.x, G.S1.y}, {G.S2.x, G.S2.y}, {G.S3.x, G.S3.y},
+                                {G.S4.x, G.S4.y}, {G.S5.x, G.S5.y}, {G.S6.x, G.S6.y}};
         const float step_size = a.adam_table[2 * it], sqrt_bc2 = a.adam_table[2 * it + 1];
+        float gr[2][6];
 #pragma unroll
-        for (int q = 0; q < 6; ++q) {
-            if (!((a.opt_mask >> q) & 1u)) continue;
-            float xn = leaf_adam(x[q], gr[q], m1[q], m2[q], step_size, sqrt_bc2, a.beta1,
-                                 a.beta2, a.eps);
-            if (q < 5) xn = fminf(fmaxf(xn, a.lo[q]), a.hi[q]);
-            x[q] = xn;
-        }
-        if (it + 1 == a.iters && valid) {
+        for (int j = 0; j < 2; ++j) {
+            const float c = 0.5f / sqrtf(x[j][0] * x[j][1]);
+            gr[j][0] = Sj[0][j] - c * (0.5f / x[j][0]) * Sj[1][j];
+            gr[j][1] = -c * (0.5f / x[j][1]) * Sj[1][j];
+            gr[j][2] = Sj[2][j];
+            gr[j][3] = Sj[3][j];
+            gr[j][4] = x[j][0] * x[j][5] / x[j][4] * Sj[4][j];
+            gr[j][5] = -x[j][0] * kLn2 * Sj[5][j];
 #pragma unroll
-            for (int q = 0; q < 6; ++q) a.grad_params[q * N + i] = gr[q];
-            if (a.grad_state0) fx[par][tid + 1] = vmul(ls, leadf);
+            for (int q = 0; q < 6; ++q) {
+                if (!((a.opt_mask >> q) & 1u)) continue;
+                float xn = leaf_adam(x[j][q], gr[j][q], m1[j][q], m2[j][q], step_size, sqrt_bc2,
+                                     a.beta1, a.beta2, a.eps);
+                if (q < 5) xn = fminf(fmaxf(xn, a.lo[q]), a.hi[q]);
+                x[j][q] = xn;
+            }
         }
         if (it + 1 == a.iters) {
+            const float2 lsl = vmul(ls, leadf);
+            fx[par][tid + 1] = lsl.y;
             __syncthreads();
-            if (a.grad_state0 && valid) {
-                a.grad_state0[i] = vadd(vsub(lD, vmul(ls, leadf)), fx[par][tid]);
-                a.grad_state0[N + i] = lv;
+            const float2 gp0 = vadd(vsub(lD, lsl), make_float2(fx[par][tid], lsl.x));
+            const float gpj[2] = {gp0.x, gp0.y}, lvj[2] = {lv.x, lv.y};
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                if (!val[j]) continue;
+                const int64_t i = i0 + j;
+#pragma unroll
+                for (int q = 0; q < 6; ++q) a.grad_params[q * N + i] = gr[j][q];
+                if (a.grad_state0) {
+                    a.grad_state0[i] = gpj[j];
+                    a.grad_state0[N + i] = lvj[j];
+                }
             }
         }
     }
-    if (valid) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        if (!val[j]) continue;
+        const int64_t i = i0 + j;
 #pragma unroll
         for (int q = 0; q < 6; ++q) {
-            a.params[q * N + i] = x[q];
-            a.adam_m[q * N + i] = m1[q];
-            a.adam_v[q * N + i] = m2[q];
+            a.params[q * N + i] = x[j][q];
+            a.adam_m[q * N + i] = m1[j][q];
+            a.adam_v[q * N + i] = m2[j][q];
         }
     }
     // loss of the last iteration: fixed-order CTA sum -> partials[tile]
-    double y = (double)lsum;
+    double y = (double)lsum.x + (double)lsum.y;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
     if ((tid & 31) == 0) red[tid >> 5] = y;
@@ -157,15 +201,26 @@ __global__ void __launch_bounds__(kFT, 1) fit_kernel(FitArgs a) {
     }
 }
 
+template <bool D4, int KIND>
+static void launch_fit_v(const FitArgs& a, int ntiles, cudaStream_t st) {
+    constexpr size_t smem = fit_smem_of<kFitMaxSteps>();
+    static bool configured = false;  // one opt-in per instantiation (one device per process)
+    if (!configured) {
+        cudaFuncSetAttribute(fit_kernel<kFitMaxSteps, D4, KIND>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    fit_kernel<kFitMaxSteps, D4, KIND><<<ntiles, kFT, smem, st>>>(a);
+}
+
 cudaError_t launch_fit(const FitArgs& a, int ntiles, bool delta4, int kind, cudaStream_t st) {
     if (a.steps < 1 || a.steps > kFitMaxSteps) return cudaErrorInvalidValue;
-    dim3 g(ntiles), b(kFT);
     if (delta4) {
-        if (kind == 0) fit_kernel<kFitMaxSteps, true, 0><<<g, b, 0, st>>>(a);
-        else fit_kernel<kFitMaxSteps, true, 1><<<g, b, 0, st>>>(a);
+        if (kind == 0) launch_fit_v<true, 0>(a, ntiles, st);
+        else launch_fit_v<true, 1>(a, ntiles, st);
     } else {
-        if (kind == 0) fit_kernel<kFitMaxSteps, false, 0><<<g, b, 0, st>>>(a);
-        else fit_kernel<kFitMaxSteps, false, 1><<<g, b, 0, st>>>(a);
+        if (kind == 0) launch_fit_v<false, 0>(a, ntiles, st);
+        else launch_fit_v<false, 1>(a, ntiles, st);
     }
     return cudaGetLastError();
 }
