@@ -99,7 +99,7 @@ REASONS = ["gpu_idle", "applications_clocks_setting", "sw_power_cap", "hw_slowdo
 
 
 class ClockSampler:
-    """nvidia-smi sampled every 50 ms while the timed region runs."""
+    """nvidia-smi sampled every 20 ms while the timed region runs."""
 
     def __init__(self, gpu_index: int):
         self.samples = []
@@ -108,7 +108,7 @@ class ClockSampler:
         try:
             self.p = subprocess.Popen(
                 ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -442,7 +442,7 @@ def run_ours(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
