@@ -15,6 +15,7 @@
 // vehicle 2t's leader is in the thread and 2t + 1's is thread t + 1's first vehicle (one
 // shared-memory word and one barrier per step).  Segments are KS steps (compile-time,
 // unrolled).  Lane-mode state history and its layout: idm_internal.h, DESIGN.md section 3.
+#include <climits>
 #include <cstdint>
 #include <type_traits>
 #include <cuda_runtime.h>
@@ -320,11 +321,14 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
         __stcs(vtp, v);
         if (RECV) put(vrow, v);
     };
+    // first checkpoint step at which each vehicle's state was non-finite (INT_MAX: none); kept
+    // in registers and reported once at the end, no branch or atomic per checkpoint
+    int bad0 = INT_MAX, bad1 = INT_MAX;
     auto finite2 = [&](int t0) {
         const bool ok0 = isfinite(s.x) && isfinite(v.x) && isfinite(D.x);
         const bool ok1 = isfinite(s.y) && isfinite(v.y) && isfinite(D.y);
-        if (val[0] && !ok0) report_nonfinite(a.status, t0, i0);
-        if (val[1] && !ok1) report_nonfinite(a.status, t0, i0 + 1);
+        bad0 = (!ok0 && bad0 == INT_MAX) ? t0 : bad0;
+        bad1 = (!ok1 && bad1 == INT_MAX) ? t0 : bad1;
     };
     auto checkpoint = [&](int t0) {  // (gap, D, compensation) at step t0 > 0 + finiteness check
         ckp += kCkRows * kR2;
@@ -364,6 +368,8 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
     }
     if (LOSS) cp_async_wait<0>();  // no copy outlives the CTA
     finite2(steps);
+    if (val[0] && bad0 != INT_MAX) report_nonfinite(a.status, bad0, i0);
+    if (val[1] && bad1 != INT_MAX) report_nonfinite(a.status, bad1, i0 + 1);
     if (a.state_out) {
         put(a.state_out + i0, vadd(p0, D));
         put(a.state_out + N + i0, v);
