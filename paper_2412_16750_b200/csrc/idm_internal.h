@@ -154,6 +154,21 @@ cudaError_t launch_fit(const FitArgs& a, int ntiles, bool delta4, int kind, cuda
 // Adam (Kingma & Ba, bias-corrected) + box clamp of one scalar;
 // shared by adam_kernel and the fused backward epilogue so both paths agree bitwise.
 #ifdef __CUDACC__
+// Predicated streaming load / store (one instruction each, no branch: the compiler otherwise
+// branches around guarded accesses and rebuilds every 64-bit row address from scratch).
+__device__ __forceinline__ float ld_cs_if(const float* p, bool on, float dflt) {
+    float r = dflt;
+    asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.global.cs.f32 %0, [%1];\n}"
+        : "+f"(r)
+        : "l"(p), "r"((int)on));
+    return r;
+}
+__device__ __forceinline__ void st_cs_if(float* p, bool on, float x) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.cs.f32 [%0], %1;\n}"
+                 ::"l"(p), "f"(x), "r"((int)on)
+                 : "memory");
+}
+
 __device__ __forceinline__ float leaf_adam(float x, float g, float& m, float& v, float step_size,
                                            float sqrt_bc2, float b1, float b2, float eps);
 

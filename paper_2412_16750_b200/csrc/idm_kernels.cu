@@ -48,21 +48,6 @@ __device__ __forceinline__ void report_nonfinite(unsigned long long* status, int
     atomicMin(status, (unsigned long long)(unsigned)step << 32 | (uint64_t)(uint32_t)veh);
 }
 
-// Predicated streaming load / store (one instruction each, no branch: the compiler otherwise
-// branches around guarded accesses and rebuilds every 64-bit row address from scratch).
-__device__ __forceinline__ float ld_cs_if(const float* p, bool on, float dflt) {
-    float r = dflt;
-    asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.global.cs.f32 %0, [%1];\n}"
-        : "+f"(r)
-        : "l"(p), "r"((int)on));
-    return r;
-}
-__device__ __forceinline__ void st_cs_if(float* p, bool on, float x) {
-    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.cs.f32 [%0], %1;\n}"
-                 ::"l"(p), "f"(x), "r"((int)on)
-                 : "memory");
-}
-
 struct RawP {
     float a_max, a_pref, s_min, T, v_targ, delta;
 };

@@ -2,15 +2,17 @@
 //
 // The paper fits each trajectory on its own: the leader terms of vehicle i at step k are free
 // variables (Delta p_k, Delta v_k), initialised to 10 and 0 and optimised with Adam alongside
-// the five IDM parameters.  Every vehicle is independent, so a CTA is 256 threads x 2 vehicles
-// with no exchange and no barrier; the per-step leaf rows are prefetched a segment ahead into
-// registers.  The mode is HBM-bound (per vehicle-step: dp, dv in the forward; dp, dv, dL/dP in
-// and the two leaf gradients out in the backward; Adam over 2 N K leaves).
+// the five IDM parameters.  Every vehicle is independent, so a CTA is 256 threads, thread t
+// owning the adjacent vehicles 2t, 2t + 1 as one float2 pair (packed f32x2 arithmetic, as the
+// lane kernels), with no exchange and no barrier; the per-step leaf rows are loaded a segment
+// at a time into registers.  The mode is HBM-bound (per vehicle-step: dp, dv in the forward;
+// dp, dv, dL/dP in and the two leaf gradients out in the backward; Adam over 2 N K leaves).
 //
 //   vl_fwd_kernel    K steps per vehicle from (p0, v0); records P (or fused Eq. 4: dL/dP)
 //   vl_bwd_kernel    per segment: recompute speeds from the checkpoint, reverse sweep writing
 //                    dL/d(dp_k), dL/d(dv_k); parameter gradients (+ Adam epilogue when fused)
 //   adam_free_kernel Adam over the unconstrained leaf lists (PAPER.md:208 gives them no box)
+#include <climits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -21,21 +23,8 @@ namespace idm {
 
 namespace {
 constexpr int kVT = 256;  // threads per CTA
-constexpr int kVV = 2;    // vehicles per thread
+constexpr int kVV = 2;    // vehicles per thread (one adjacent pair)
 constexpr int kVB = kVT * kVV;
-
-__device__ __forceinline__ float vl_loss_term(int kind, float o, float P, bool valid,
-                                              float& acc) {
-    const float r = o - P;
-    const bool ok = valid && fabsf(o) <= 3.4e38f;
-    if (kind == 0) {
-        acc += ok ? fabsf(r) : 0.f;
-        const float sg = r > 0.f ? -1.f : (r < 0.f ? 1.f : 0.f);
-        return ok ? sg : 0.f;
-    }
-    acc = ok ? fmaf(r, r, acc) : acc;
-    return ok ? -2.f * r : 0.f;
-}
 
 __device__ __forceinline__ void vl_block_sum(double x, double* out) {
     __shared__ double red[kVT / 32];
@@ -55,6 +44,15 @@ __device__ __forceinline__ void vl_params(const float* prm, int64_t n_par, int64
 #pragma unroll
     for (int q = 0; q < 6; ++q) r[q] = prm[q * n_par + j];
 }
+
+// predicated pair access at p (vehicles i0, i0 + 1)
+__device__ __forceinline__ float2 ld_pair(const float* p, bool on0, bool on1, float dflt) {
+    return make_float2(ld_cs_if(p, on0, dflt), ld_cs_if(p + 1, on1, dflt));
+}
+__device__ __forceinline__ void st_pair(float* p, bool on0, bool on1, float2 x) {
+    st_cs_if(p, on0, x.x);
+    st_cs_if(p + 1, on1, x.y);
+}
 }  // namespace
 
 // ------------------------------------------------------------------------------ forward
@@ -63,110 +61,99 @@ __global__ void __launch_bounds__(kVT) vl_fwd_kernel(VlArgs a) {
     const int tid = threadIdx.x;
     const int64_t N = a.n;
     const int steps = a.steps;
-    const int64_t base = (int64_t)blockIdx.x * kVB + tid;
-    float v[kVV], D[kVV], p0[kVV];
-    bool valid[kVV];
-    VehP P[kVV];
+    const int64_t i0 = (int64_t)blockIdx.x * kVB + 2 * tid;
+    const bool val0 = i0 < N, val1 = i0 + 1 < N;
+    const float qnan = __int_as_float(0x7fc00000);
+    float pj[2] = {0.f, 0.f}, vj[2] = {0.f, 0.f};
+    VehP Pj[2];
 #pragma unroll
-    for (int j = 0; j < kVV; ++j) {
-        const int64_t i = base + j * kVT;
-        valid[j] = i < N;
+    for (int j = 0; j < 2; ++j) {
+        const int64_t i = i0 + j;
         float r[6] = {1.f, 1.f, 1.f, 1.f, 1.f, 4.f};
-        p0[j] = 0.f;
-        v[j] = 0.f;
-        if (valid[j]) {
-            p0[j] = a.pos0[i];
-            v[j] = a.vel0[i];
+        if (i < N) {
+            pj[j] = a.pos0[i];
+            vj[j] = a.vel0[i];
             vl_params(a.params, a.n_par, i, r);
             if (D4 && r[5] != 4.f)
                 atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
         }
-        D[j] = 0.f;
-        P[j] = make_vehp(r[0], r[1], r[2], r[3], r[4], r[5]);
+        Pj[j] = make_vehp(r[0], r[1], r[2], r[3], r[4], r[5]);
     }
+    const VehPT<float2> P = pack(Pj[0], Pj[1]);
+    const float2 p0 = make_float2(pj[0], pj[1]);
+    float2 v = make_float2(vj[0], vj[1]), D = f2(0.f);
     const Consts k = a.k;
-    float* orow = (LOSS ? a.grad_traj : a.traj) + base;
-    float* vrow = (!LOSS && a.vel_traj) ? a.vel_traj + base : nullptr;
-    float* ckv = a.ckpt_v + base;
-    const float* dpr = a.vl_dp + base;
-    const float* dvr = a.vl_dv + base;
-    const float* obs = LOSS ? a.obs + base : nullptr;
-    float lseg = 0.f;
+    float* orow = (LOSS ? a.grad_traj : a.traj) + i0;
+    float* vrow = (!LOSS && a.vel_traj) ? a.vel_traj + i0 : nullptr;
+    float* ckv = a.ckpt_v + i0;
+    const float* dpr = a.vl_dp + i0;
+    const float* dvr = a.vl_dv + i0;
+    const float* obs = LOSS ? a.obs + i0 : nullptr;
+    float2 lseg = f2(0.f);
     double lacc = 0.0;
-#pragma unroll
-    for (int j = 0; j < kVV; ++j) {
-        if (!valid[j]) continue;
-        __stcs(orow + j * kVT,
-               LOSS ? vl_loss_term(LOSS - 1, obs[j * kVT], p0[j], true, lseg) : p0[j]);
-        if (vrow) vrow[j * kVT] = v[j];
-        ckv[j * kVT] = v[j];
-    }
+    st_pair(orow, val0, val1,
+            LOSS ? loss_term<LOSS - 1>(ld_pair(obs, val0, val1, qnan), p0, lseg) : p0);
+    if (vrow) st_pair(vrow, val0, val1, v);
+    st_pair(ckv, val0, val1, v);
+    int bad0 = INT_MAX, bad1 = INT_MAX;  // first non-finite checkpoint (reported at the end)
     const int nseg = (steps + KS - 1) / KS;
     for (int seg = 0; seg < nseg; ++seg) {
         const int t0 = seg * KS;
         const int len = min(KS, steps - t0);
         if (seg > 0) {
             ckv += N;
-#pragma unroll
-            for (int j = 0; j < kVV; ++j) {
-                if (!valid[j]) continue;
-                ckv[j * kVT] = v[j];
-                if (!(isfinite(v[j]) && isfinite(D[j])))
-                    atomicMin(a.status, (unsigned long long)(unsigned)t0 << 32 |
-                                            (uint64_t)(uint32_t)(base + j * kVT));
-            }
+            st_pair(ckv, val0, val1, v);
+            bad0 = (!(isfinite(v.x) && isfinite(D.x)) && bad0 == INT_MAX) ? t0 : bad0;
+            bad1 = (!(isfinite(v.y) && isfinite(D.y)) && bad1 == INT_MAX) ? t0 : bad1;
         }
         // this segment's leaf rows (and observation rows) into registers
-        float dp[KS][kVV], dv[KS][kVV], ob[LOSS ? KS : 1][kVV];
+        float2 dp[KS], dv[KS], ob[LOSS ? KS : 1];
 #pragma unroll
-        for (int tt = 0; tt < KS; ++tt)
-#pragma unroll
-            for (int j = 0; j < kVV; ++j) {
-                const bool ok = valid[j] && tt < len;
-                const int64_t off = (int64_t)(t0 + tt) * N + j * kVT;
-                dp[tt][j] = ok ? __ldcs(dpr + off) : 10.f;
-                dv[tt][j] = ok ? __ldcs(dvr + off) : 0.f;
-                if (LOSS) ob[tt][j] = ok ? __ldcs(obs + off + N) : 0.f;
-            }
+        for (int tt = 0; tt < KS; ++tt) {
+            const bool on = tt < len;
+            const int64_t off = (int64_t)(t0 + (on ? tt : 0)) * N;
+            dp[tt] = ld_pair(dpr + off, on && val0, on && val1, 10.f);
+            dv[tt] = ld_pair(dvr + off, on && val0, on && val1, 0.f);
+            if (LOSS) ob[tt] = ld_pair(obs + off + N, on && val0, on && val1, qnan);
+        }
 #pragma unroll
         for (int tt = 0; tt < KS; ++tt) {
             if (tt < len) {
                 orow += N;
                 if (vrow) vrow += N;
-#pragma unroll
-                for (int j = 0; j < kVV; ++j) {
-                    D[j] = __fmaf_rn(k.dt, v[j], D[j]);
-                    Core c;
-                    core_dv<D4>(dp[tt][j], v[j], dv[tt][j], 1.f, P[j], k, c);
-                    float sdummy = 0.f;
-                    advance(c, sdummy, v[j], k);
-                    const float Pv = __fadd_rn(p0[j], D[j]);
-                    const float out =
-                        LOSS ? vl_loss_term(LOSS - 1, ob[tt][j], Pv, valid[j], lseg) : Pv;
-                    if (valid[j]) {
-                        __stcs(orow + j * kVT, out);
-                        if (vrow) vrow[j * kVT] = v[j];
-                    }
-                }
+                D = vfma(v, k.dt, D);
+                CoreT<float2> c;
+                core_dv<D4>(dp[tt], v, dv[tt], f2(1.f), P, k, c);
+                float2 sdummy = f2(0.f);
+                advance(c, sdummy, v, k);
+                const float2 Pv = vadd(p0, D);
+                st_pair(orow, val0, val1, LOSS ? loss_term<LOSS - 1>(ob[tt], Pv, lseg) : Pv);
+                if (vrow) st_pair(vrow, val0, val1, v);
             }
         }
         if (LOSS) {
-            lacc += (double)lseg;
-            lseg = 0.f;
+            lacc += (double)lseg.x + (double)lseg.y;
+            lseg = f2(0.f);
         }
     }
+    bad0 = (!(isfinite(v.x) && isfinite(D.x)) && bad0 == INT_MAX) ? steps : bad0;
+    bad1 = (!(isfinite(v.y) && isfinite(D.y)) && bad1 == INT_MAX) ? steps : bad1;
+    const float2 Pend = vadd(p0, D);
+    const int badj[2] = {bad0, bad1};
+    const float pend[2] = {Pend.x, Pend.y}, vend[2] = {v.x, v.y};
 #pragma unroll
-    for (int j = 0; j < kVV; ++j) {
-        if (!valid[j]) continue;
-        const int64_t i = base + j * kVT;
-        if (!(isfinite(v[j]) && isfinite(D[j])))
-            atomicMin(a.status, (unsigned long long)(unsigned)steps << 32 | (uint64_t)(uint32_t)i);
+    for (int j = 0; j < 2; ++j) {
+        const int64_t i = i0 + j;
+        if (i >= N) continue;
+        if (badj[j] != INT_MAX)
+            atomicMin(a.status,
+                      (unsigned long long)(unsigned)badj[j] << 32 | (uint64_t)(uint32_t)i);
         if (a.state_out) {
-            a.state_out[i] = __fadd_rn(p0[j], D[j]);
-            a.state_out[N + i] = v[j];
+            a.state_out[i] = pend[j];
+            a.state_out[N + i] = vend[j];
         }
     }
-    if (LOSS) vl_block_sum(lacc + (double)lseg, a.loss_partials);
+    if (LOSS) vl_block_sum(lacc + (double)lseg.x + (double)lseg.y, a.loss_partials);
 }
 
 // ------------------------------------------------------------------------------ backward
@@ -175,126 +162,120 @@ __global__ void __launch_bounds__(kVT, 2) vl_bwd_kernel(VlArgs a) {
     const int tid = threadIdx.x;
     const int64_t N = a.n;
     const int steps = a.steps;
-    const int64_t base = (int64_t)blockIdx.x * kVB + tid;
+    const int64_t i0 = (int64_t)blockIdx.x * kVB + 2 * tid;
+    const bool val0 = i0 < N, val1 = i0 + 1 < N;
     const Consts k = a.k;
     const int64_t KN = (int64_t)a.max_steps * N;  // leaf plane stride
-    float lv[kVV], lD[kVV];
-    bool valid[kVV];
-    VehP P[kVV];
-    VehB B[kVV];
-    GradAcc G[kVV];
+    float ldj[2] = {0.f, 0.f};
+    VehP Pj[2];
+    VehB Bj[2];
 #pragma unroll
-    for (int j = 0; j < kVV; ++j) {
-        const int64_t i = base + j * kVT;
-        valid[j] = i < N;
+    for (int j = 0; j < 2; ++j) {
+        const int64_t i = i0 + j;
         float r[6] = {1.f, 1.f, 1.f, 1.f, 1.f, 4.f};
-        lv[j] = 0.f;
-        lD[j] = 0.f;
-        if (valid[j]) {
+        if (i < N) {
             vl_params(a.params, a.n_par, i, r);
-            lD[j] = a.grad_traj[(int64_t)steps * N + i];  // lambda_P^K = dL/dP(K)
+            ldj[j] = a.grad_traj[(int64_t)steps * N + i];  // lambda_P^K = dL/dP(K)
         }
-        P[j] = make_vehp(r[0], r[1], r[2], r[3], r[4], r[5]);
-        B[j] = make_vehb(r[0], r[1], r[4], r[5]);
-        G[j] = GradAcc{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        Pj[j] = make_vehp(r[0], r[1], r[2], r[3], r[4], r[5]);
+        Bj[j] = make_vehb(r[0], r[1], r[4], r[5]);
     }
+    const VehPT<float2> P = pack(Pj[0], Pj[1]);
+    const VehBT<float2> B = pack(Bj[0], Bj[1]);
+    float2 lv = f2(0.f), lD = make_float2(ldj[0], ldj[1]);
+    GradAccT<float2> G = {f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
     const int nseg = (steps + KS - 1) / KS;
     for (int seg = nseg - 1; seg >= 0; --seg) {
         const int t0 = seg * KS;
         const int len = min(KS, steps - t0);
-        float dp[KS][kVV], dv[KS][kVV], gr[KS][kVV], vt[KS][kVV];
+        float2 dp[KS], dv[KS], gr[KS], vt[KS];
         // ADAM (fused iteration): the leaves' Adam moments of this segment, updated in place
-        float am[ADAM ? KS : 1][kVV][2], av[ADAM ? KS : 1][kVV][2];
+        float2 am[ADAM ? KS : 1][2], av[ADAM ? KS : 1][2];
 #pragma unroll
-        for (int tt = 0; tt < KS; ++tt)
+        for (int tt = 0; tt < KS; ++tt) {
+            const bool on = tt < len;
+            const bool o0 = on && val0, o1 = on && val1;
+            const int64_t off = (int64_t)(t0 + (on ? tt : 0)) * N + i0;
+            dp[tt] = ld_pair(a.vl_dp + off, o0, o1, 10.f);
+            dv[tt] = ld_pair(a.vl_dv + off, o0, o1, 0.f);
+            gr[tt] = ld_pair(a.grad_traj + off, o0, o1, 0.f);
+            if (ADAM) {
 #pragma unroll
-            for (int j = 0; j < kVV; ++j) {
-                const bool ok = valid[j] && tt < len;
-                const int64_t off = (int64_t)(t0 + tt) * N + base + j * kVT;
-                dp[tt][j] = ok ? __ldcs(a.vl_dp + off) : 10.f;
-                dv[tt][j] = ok ? __ldcs(a.vl_dv + off) : 0.f;
-                gr[tt][j] = ok ? __ldcs(a.grad_traj + off) : 0.f;
-                if (ADAM) {
-#pragma unroll
-                    for (int pl = 0; pl < 2; ++pl) {
-                        am[tt][j][pl] = ok ? __ldcs(a.vl_adam_m + pl * KN + off) : 0.f;
-                        av[tt][j][pl] = ok ? __ldcs(a.vl_adam_v + pl * KN + off) : 0.f;
-                    }
+                for (int pl = 0; pl < 2; ++pl) {
+                    am[tt][pl] = ld_pair(a.vl_adam_m + pl * KN + off, o0, o1, 0.f);
+                    av[tt][pl] = ld_pair(a.vl_adam_v + pl * KN + off, o0, o1, 0.f);
                 }
             }
+        }
         // recompute the segment's speeds from its checkpoint (bit-identical to the forward)
-#pragma unroll
-        for (int j = 0; j < kVV; ++j)
-            vt[0][j] = valid[j] ? a.ckpt_v[(int64_t)seg * N + base + j * kVT] : 0.f;
+        vt[0] = ld_pair(a.ckpt_v + (int64_t)seg * N + i0, val0, val1, 0.f);
 #pragma unroll
         for (int tt = 0; tt + 1 < KS; ++tt) {
             if (tt + 1 < len) {
-#pragma unroll
-                for (int j = 0; j < kVV; ++j) {
-                    Core c;
-                    core_dv<D4>(dp[tt][j], vt[tt][j], dv[tt][j], 1.f, P[j], k, c);
-                    float sdummy = 0.f, vn = vt[tt][j];
-                    advance(c, sdummy, vn, k);
-                    vt[tt + 1][j] = vn;
-                }
+                CoreT<float2> c;
+                core_dv<D4>(dp[tt], vt[tt], dv[tt], f2(1.f), P, k, c);
+                float2 sdummy = f2(0.f), vn = vt[tt];
+                advance(c, sdummy, vn, k);
+                vt[tt + 1] = vn;
             }
         }
         // reverse sweep
 #pragma unroll
         for (int tt = KS - 1; tt >= 0; --tt) {
             if (tt < len) {
-                const int64_t off = (int64_t)(t0 + tt) * N + base;
+                const int64_t off = (int64_t)(t0 + tt) * N + i0;
+                CoreT<float2> c;
+                core_dv<D4>(dp[tt], vt[tt], dv[tt], f2(1.f), P, k, c);
+                float2 gdp, gdv;
+                bwd_vl<D4>(c, dp[tt], vt[tt], P, B, k, lv, lD, G, gdp, gdv);
+                lD = vadd(lD, gr[tt]);  // lambda_P^t = g^t + lambda_P^{t+1}
+                if (ADAM) {  // Adam on the two leaves of step t, in place (no box)
+                    const float gg[2][2] = {{gdp.x, gdp.y}, {gdv.x, gdv.y}};
+                    const float x0[2][2] = {{dp[tt].x, dp[tt].y}, {dv[tt].x, dv[tt].y}};
+                    float* xs[2] = {const_cast<float*>(a.vl_dp), const_cast<float*>(a.vl_dv)};
 #pragma unroll
-                for (int j = 0; j < kVV; ++j) {
-                    Core c;
-                    core_dv<D4>(dp[tt][j], vt[tt][j], dv[tt][j], 1.f, P[j], k, c);
-                    float gdp, gdv;
-                    bwd_vl<D4>(c, dp[tt][j], vt[tt][j], P[j], B[j], k, lv[j], lD[j], G[j], gdp,
-                               gdv);
-                    lD[j] += gr[tt][j];  // lambda_P^t = g^t + lambda_P^{t+1}
-                    if (valid[j]) {
-                        if (ADAM) {  // Adam on the two leaves of step t, in place (no box)
-                            const float gg[2] = {gdp, gdv};
-                            float* xs[2] = {const_cast<float*>(a.vl_dp), const_cast<float*>(a.vl_dv)};
-                            const float x0[2] = {dp[tt][j], dv[tt][j]};
+                    for (int pl = 0; pl < 2; ++pl) {
+                        float mm[2] = {am[tt][pl].x, am[tt][pl].y};
+                        float vv[2] = {av[tt][pl].x, av[tt][pl].y};
+                        float xn[2];
 #pragma unroll
-                            for (int pl = 0; pl < 2; ++pl) {
-                                float mm = am[tt][j][pl], vv = av[tt][j][pl];
-                                const float xn = leaf_adam(x0[pl], gg[pl], mm, vv,
-                                                           a.adam.step_size, a.adam.sqrt_bc2,
-                                                           a.adam.beta1, a.adam.beta2, a.adam.eps);
-                                __stcs(a.vl_adam_m + pl * KN + off + j * kVT, mm);
-                                __stcs(a.vl_adam_v + pl * KN + off + j * kVT, vv);
-                                __stcs(xs[pl] + off + j * kVT, xn);
-                            }
-                        } else {
-                            __stcs(a.vl_grad + off + j * kVT, gdp);
-                            __stcs(a.vl_grad + KN + off + j * kVT, gdv);
-                        }
+                        for (int j = 0; j < 2; ++j)
+                            xn[j] = leaf_adam(x0[pl][j], gg[pl][j], mm[j], vv[j],
+                                              a.adam.step_size, a.adam.sqrt_bc2, a.adam.beta1,
+                                              a.adam.beta2, a.adam.eps);
+                        st_pair(a.vl_adam_m + pl * KN + off, val0, val1, make_float2(mm[0], mm[1]));
+                        st_pair(a.vl_adam_v + pl * KN + off, val0, val1, make_float2(vv[0], vv[1]));
+                        st_pair(xs[pl] + off, val0, val1, make_float2(xn[0], xn[1]));
                     }
+                } else {
+                    st_pair(a.vl_grad + off, val0, val1, gdp);
+                    st_pair(a.vl_grad + KN + off, val0, val1, gdv);
                 }
             }
         }
     }
+    const float Sj[6][2] = {{G.S1.x, G.S1.y}, {G.S2.x, G.S2.y}, {G.S3.x, G.S3.y},
+                            {G.S4.x, G.S4.y}, {G.S5.x, G.S5.y}, {G.S6.x, G.S6.y}};
+    const float lvj[2] = {lv.x, lv.y}, lDj[2] = {lD.x, lD.y};
 #pragma unroll
-    for (int j = 0; j < kVV; ++j) {
-        if (!valid[j]) continue;
-        const int64_t i = base + j * kVT;
+    for (int j = 0; j < 2; ++j) {
+        const int64_t i = i0 + j;
+        if (i >= N) continue;
         float r[6];
         vl_params(a.params, a.n_par, i, r);
         const float c = 0.5f / sqrtf(r[0] * r[1]);
         float gr6[6];
-        gr6[0] = G[j].S1 - c * (0.5f / r[0]) * G[j].S2;
-        gr6[1] = -c * (0.5f / r[1]) * G[j].S2;
-        gr6[2] = G[j].S3;
-        gr6[3] = G[j].S4;
-        gr6[4] = r[0] * r[5] / r[4] * G[j].S5;
-        gr6[5] = -r[0] * kLn2 * G[j].S6;
+        gr6[0] = Sj[0][j] - c * (0.5f / r[0]) * Sj[1][j];
+        gr6[1] = -c * (0.5f / r[1]) * Sj[1][j];
+        gr6[2] = Sj[2][j];
+        gr6[3] = Sj[3][j];
+        gr6[4] = r[0] * r[5] / r[4] * Sj[4][j];
+        gr6[5] = -r[0] * kLn2 * Sj[5][j];
         if (a.grad_state0) {
-            a.grad_state0[i] = lD[j];  // dL/dp0: position enters every later P
-            a.grad_state0[N + i] = lv[j];
+            a.grad_state0[i] = lDj[j];  // dL/dp0: position enters every later P
+            a.grad_state0[N + i] = lvj[j];
         }
-        if (!(isfinite(lv[j]) && isfinite(lD[j])))
+        if (!(isfinite(lvj[j]) && isfinite(lDj[j])))
             atomicMin(a.status, (unsigned long long)0 << 32 | (uint64_t)(uint32_t)i);
 #pragma unroll
         for (int q = 0; q < 6; ++q) {
