@@ -177,6 +177,17 @@ int idm_fit(idm_handle* h, int32_t steps, const float* obs, int32_t kind, int32_
 /* Largest horizon idm_fit accepts. */
 int32_t idm_fit_max_steps(void);
 
+/* Iterations iter0 .. iter0+iters-1 of idm_fit_step(steps, obs, kind, it, total_iters, lr0, lr1)
+   for any horizon, launched as ONE CUDA graph: the calls are captured on the handle's stream
+   (each iteration's Adam step size baked into its kernel nodes) and the graph is launched once,
+   which removes the per-launch host overhead that dominates small configurations.  Same
+   kernels, same order: parameters, moments and gradients are bit-identical to the loop of
+   idm_fit_step calls.  The loss of the last iteration goes to *loss_dev / *loss_host.  The
+   instantiated graph is kept by the handle until the next call or idm_destroy. */
+int idm_fit_steps(idm_handle* h, int32_t steps, const float* obs, int32_t kind, int32_t iter0,
+                  int32_t iters, int32_t total_iters, float lr0, float lr1, double* loss_dev,
+                  double* loss_host);
+
 /* One whole optimizer iteration from HOST buffers (end-to-end path): async-copies pos0/vel0
    (nullable = keep), obs (required) and mask (nullable = all observed) from host memory
    (pinned for overlap) into desc->pos0/vel0/obs_stage/mask_stage, runs forward(steps) ->

@@ -36,6 +36,9 @@ struct idm_handle {
     // fused iteration in tile chunks: backward of chunk c on st2 overlaps forward of chunk c+1
     cudaStream_t st2;
     cudaEvent_t ev_fork, ev_join, ev_chunk[16];
+    cudaGraphExec_t graph_exec;  // last idm_fit_steps graph (kept until the next call / destroy)
+    cudaStream_t cap_st;         // capture stream (capture is not allowed on the legacy stream)
+    cudaEvent_t ev_gfork, ev_gjoin;
     double* pinned;  // [0] loss, [1] status (as bits), [2] flags
     int stage;       // 0 = initialised, 1 = forward done, 2 = loss done, 3 = backward done
     int32_t steps;
@@ -319,6 +322,10 @@ void idm_destroy(idm_handle* h) {
         delete h->ev_pool;
     }
     if (h->copy_st) cudaStreamDestroy(h->copy_st);
+    if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+    if (h->cap_st) cudaStreamDestroy(h->cap_st);
+    if (h->ev_gfork) cudaEventDestroy(h->ev_gfork);
+    if (h->ev_gjoin) cudaEventDestroy(h->ev_gjoin);
     if (h->st2) cudaStreamDestroy(h->st2);
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
@@ -464,6 +471,9 @@ int idm_init(idm_handle** out, const idm_desc* d) {
             if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
             for (cudaEvent_t& e : h->ev_chunk)
                 if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+            if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&h->cap_st, cudaStreamNonBlocking);
+            if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&h->ev_gfork, cudaEventDisableTiming);
+            if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&h->ev_gjoin, cudaEventDisableTiming);
         }
         if (ce == cudaSuccess) {
             what = "pinned buffer";
@@ -870,6 +880,63 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
 }
 
 int32_t idm_fit_max_steps(void) { return kFitMaxSteps; }
+
+int idm_fit_steps(idm_handle* h, int32_t steps, const float* obs, int32_t kind, int32_t iter0,
+                  int32_t iters, int32_t total_iters, float lr0, float lr1, double* loss_dev,
+                  double* loss_host) {
+    if (!h) return IDM_EINVAL;
+    if (iters < 1 || iter0 < 0 || (int64_t)iter0 + iters > total_iters)
+        return fail(h, IDM_EINVAL, "idm_fit_steps: iterations %d..%d outside [0, %d)", iter0,
+                    iter0 + iters - 1, total_iters);
+    // the iteration loop as ONE CUDA graph: capture `iters` idm_fit_step calls on the handle's
+    // stream (each with its own schedule step baked into its kernel nodes), launch it once
+    if (h->graph_exec) {
+        CK(h, cudaStreamSynchronize(h->cap_st));  // the previous graph may still be running
+        cudaGraphExecDestroy(h->graph_exec);
+        h->graph_exec = nullptr;
+    }
+    // capture on the handle's private stream, ordered after the work already queued on the
+    // handle's stream (fork before the capture), and order the handle's stream after the
+    // graph (join)
+    cudaStream_t orig = h->st;
+    CK(h, cudaEventRecord(h->ev_gfork, orig));
+    CK(h, cudaStreamWaitEvent(h->cap_st, h->ev_gfork, 0));
+    const bool timing = h->timing;
+    h->timing = false;  // no timing events inside a capture
+    h->st = h->cap_st;
+    cudaError_t ce = cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal);
+    if (ce != cudaSuccess) {
+        h->st = orig;
+        h->timing = timing;
+        return fail(h, IDM_ECUDA, "graph capture: %s", cudaGetErrorString(ce));
+    }
+    int rc = IDM_OK;
+    for (int32_t it = iter0; it < iter0 + iters && rc == IDM_OK; ++it)
+        rc = idm_fit_step(h, steps, obs, nullptr, kind, it, total_iters, lr0, lr1,
+                          it + 1 == iter0 + iters ? loss_dev : nullptr, nullptr);
+    cudaGraph_t graph = nullptr;
+    ce = cudaStreamEndCapture(h->st, &graph);
+    h->st = orig;
+    h->timing = timing;
+    if (rc != IDM_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+    }
+    if (ce == cudaSuccess) ce = cudaGraphInstantiate(&h->graph_exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    if (ce == cudaSuccess) ce = cudaGraphLaunch(h->graph_exec, h->cap_st);
+    if (ce == cudaSuccess) ce = cudaEventRecord(h->ev_gjoin, h->cap_st);
+    if (ce == cudaSuccess) ce = cudaStreamWaitEvent(orig, h->ev_gjoin, 0);
+    if (ce != cudaSuccess) return fail(h, IDM_ECUDA, "graph launch: %s", cudaGetErrorString(ce));
+    if (loss_host) {
+        CK(h, cudaMemcpyAsync(&h->pinned[0], h->loss_scalar, sizeof(double),
+                              cudaMemcpyDeviceToHost, h->st));
+        int st2 = sync_status(h);
+        *loss_host = h->pinned[0];
+        if (st2 != IDM_OK) return st2;
+    }
+    return IDM_OK;
+}
 
 int idm_fit(idm_handle* h, int32_t steps, const float* obs, int32_t kind, int32_t iter0,
             int32_t iters, int32_t total_iters, float lr0, float lr1, double* loss_dev,

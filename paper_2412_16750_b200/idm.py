@@ -114,6 +114,9 @@ def load_library(path: str | None = None):
     L.idm_fit.restype = C.c_int
     L.idm_fit.argtypes = [vp, i32, vp, i32, i32, i32, i32, C.c_float, C.c_float, vp,
                           C.POINTER(C.c_double)]
+    L.idm_fit_steps.restype = C.c_int
+    L.idm_fit_steps.argtypes = [vp, i32, vp, i32, i32, i32, i32, C.c_float, C.c_float, vp,
+                                C.POINTER(C.c_double)]
     L.idm_fit_max_steps.restype = i32
     L.idm_fit_max_steps.argtypes = []
     L.idm_step_host.restype = C.c_int
@@ -314,6 +317,21 @@ class IdmSim:
         self._check(self._lib.idm_fit(self.handle, steps, _ptr(obs), LOSS_KINDS[kind], iter0,
                                       iters, total, lr0, lr1, _ptr(self.loss_dev),
                                       C.byref(out) if sync else None))
+        self.steps = steps
+        return out.value if sync else None
+
+    def fit_steps(self, obs: torch.Tensor, iters: int, kind: str = "l1", iter0: int = 0,
+                  total: int = 500, lr0: float = 0.1, lr1: float = 0.01,
+                  steps: int | None = None, sync: bool = False):
+        """`iters` fused iterations (any horizon) launched as ONE CUDA graph (idm_fit_steps):
+        bit-identical to calling fit_step for iterations iter0 .. iter0+iters-1."""
+        steps = self.max_steps if steps is None else int(steps)
+        assert obs.dtype == torch.float32 and obs.is_contiguous() and obs.device == self.device
+        assert obs.numel() >= (steps + 1) * self.n
+        out = C.c_double(0.0)
+        self._check(self._lib.idm_fit_steps(self.handle, steps, _ptr(obs), LOSS_KINDS[kind],
+                                            iter0, iters, total, lr0, lr1, _ptr(self.loss_dev),
+                                            C.byref(out) if sync else None))
         self.steps = steps
         return out.value if sync else None
 

@@ -692,6 +692,37 @@ def test_fit_step_deterministic(idm, kind):
         assert torch.equal(x, y)
 
 
+@pytest.mark.parametrize("kind", ["l1", "l2"])
+def test_fit_steps_graph_equals_loop(idm, kind):
+    """idm_fit_steps (the iteration loop captured as one CUDA graph) == the idm_fit_step loop,
+    bit for bit in parameters, Adam moments, gradients and the last loss; lane mode with a
+    partial last segment, and virtual-leader mode."""
+    w = synth.make_workload("C2", lane_sizes=[100] * 20 + [7, 1], K=90, seed=13)
+    obs = synth.kinematic_obs(w)
+    obs[np.random.default_rng(13).random(obs.shape) < 0.1] = np.nan
+    o = torch.as_tensor(obs, device="cuda")
+    for vl in (False, True):
+        kw = dict(max_steps=w.K, virtual_leader=True) if vl else dict(max_steps=w.K)
+        a = idm.from_workload(w, None, **kw)
+        b = idm.from_workload(w, None, **kw)
+        for it in range(7):
+            La = a.fit_step(o, kind=kind, iteration=it, total=100, sync=True)
+        Lb = b.fit_steps(o, iters=7, kind=kind, iter0=0, total=100, sync=True)
+        torch.cuda.synchronize()
+        assert La == Lb
+        assert torch.equal(a.params, b.params)
+        assert torch.equal(a.adam_m, b.adam_m) and torch.equal(a.adam_v, b.adam_v)
+        assert torch.equal(a.grad_params, b.grad_params)
+        if vl:
+            assert torch.equal(a.vl_dp, b.vl_dp) and torch.equal(a.vl_dv, b.vl_dv)
+        # a second graph continues the schedule
+        Lc = b.fit_steps(o, iters=3, kind=kind, iter0=7, total=100, sync=True)
+        for it in range(7, 10):
+            La = a.fit_step(o, kind=kind, iteration=it, total=100, sync=True)
+        torch.cuda.synchronize()
+        assert La == Lc and torch.equal(a.params, b.params)
+
+
 @pytest.mark.parametrize("K", [1, 3, 5])
 def test_fit_step_short_horizons(idm, K):
     """Rollouts shorter than one segment (or one segment plus a tail): the fused kernels'
