@@ -7,8 +7,10 @@ from __future__ import annotations
 
 import glob
 import os
+import shutil
 import subprocess
 import sys
+import tempfile
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
@@ -41,23 +43,41 @@ def _stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None,
           defines: tuple = ()) -> str:
-    """Build libidm.so (or a variant at `out` with extra -D defines, for tuning sweeps)."""
+    """Build libidm.so (or a variant at `out` with extra -D defines, for tuning sweeps): each
+    .cu compiled to an object in parallel, then one link."""
     lib = out or LIB
     if out is None and not force and not _stale():
         return LIB
     tmp = lib + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-shared", "-Xlinker",
-           "--exclude-libs,ALL", "-I", os.path.join(ROOT, "include"), *sources(), "-o", tmp,
-           "-lcudart_static"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    objdir = tempfile.mkdtemp(prefix="idm_build_")
+    inc = ["-I", os.path.join(ROOT, "include")]
+    dflags = [f"-D{d}" for d in defines]
+    jobs = []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [NVCC, *NVCC_FLAGS, *dflags, *inc, "-c", src, "-o", obj]
+        jobs.append((cmd, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE,
+                                                stderr=subprocess.PIPE, text=True)))
+    logtxt, failed = [], False
+    for cmd, _, proc in jobs:
+        so, se = proc.communicate()
+        logtxt.append(" ".join(cmd) + "\n" + so + se)
+        failed |= proc.returncode != 0
+    if not failed:
+        link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xlinker",
+                "--exclude-libs,ALL", *[o for _, o, _ in jobs], "-o", tmp, "-lcudart_static"]
+        res = subprocess.run(link, capture_output=True, text=True)
+        logtxt.append(" ".join(link) + "\n" + res.stdout + res.stderr)
+        failed = res.returncode != 0
+    shutil.rmtree(objdir, ignore_errors=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
+        f.write("\n".join(logtxt))
+    if failed:
+        sys.stderr.write("\n".join(logtxt)[-20000:])
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write("\n".join(logtxt))
     os.replace(tmp, lib)
     return lib
 
