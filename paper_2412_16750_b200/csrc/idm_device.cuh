@@ -55,6 +55,11 @@ __device__ __forceinline__ float rcp(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+__device__ __forceinline__ float rsqrt_a(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ float2 ex2(float2 x) { return make_float2(ex2(x.x), ex2(x.y)); }
 __device__ __forceinline__ float2 lg2(float2 x) { return make_float2(lg2(x.x), lg2(x.y)); }
 __device__ __forceinline__ float2 rcp(float2 x) { return make_float2(rcp(x.x), rcp(x.y)); }
@@ -132,11 +137,12 @@ using VehP = VehPT<float>;
 __device__ __forceinline__ VehP make_vehp(float a_max, float a_pref, float s_min, float T,
                                           float v_targ, float delta) {
     VehP p;
-    float c = 0.5f / sqrtf(a_max * a_pref);  // 1 / (2 sqrt(a_max a_pref))  (Eq. 1)
+    // per-vehicle reciprocals with the MUFU (a few ulp; every path shares these constants)
+    const float c = __fmul_rn(0.5f, rsqrt_a(__fmul_rn(a_max, a_pref)));  // 1/(2 sqrt(a b)), Eq. 1
     p.sm2 = s_min * kLog2e;
     p.T2 = T * kLog2e;
     p.c2 = c * kLog2e;
-    p.ivt = 1.f / v_targ;
+    p.ivt = rcp(v_targ);
     p.am2 = a_max * kLog2e;
     p.amln2 = a_max * kLn2;
     p.delta = delta;
@@ -250,9 +256,23 @@ using VehB = VehBT<float>;
 __device__ __forceinline__ VehB make_vehb(float a_max, float a_pref, float v_targ, float delta) {
     VehB b;
     b.nam2ln2 = -2.f * a_max * kLn2;
-    b.ndamivt = -delta * a_max / v_targ;
-    b.nc = -0.5f / sqrtf(a_max * a_pref);
+    b.ndamivt = __fmul_rn(__fmul_rn(-delta, a_max), rcp(v_targ));
+    b.nc = __fmul_rn(-0.5f, rsqrt_a(__fmul_rn(a_max, a_pref)));
     return b;
+}
+
+// dL/d(a_max, a_pref, s_min, T_pref, v_targ, delta) of one vehicle from its factored
+// accumulators (GradAcc) and raw parameters r; shared by every backward so they agree bitwise:
+//   c = 1/(2 sqrt(a b)),  ds_opt/da = -c/(2a) v dv,  ds_opt/db = -c/(2b) v dv,
+//   dw/dv_targ = -delta w / v_targ,  dw/ddelta = w ln x
+__device__ __forceinline__ void param_grads(const float r[6], const float S[6], float gr[6]) {
+    const float c = __fmul_rn(0.5f, rsqrt_a(__fmul_rn(r[0], r[1])));
+    gr[0] = __fmaf_rn(-__fmul_rn(c, __fmul_rn(0.5f, rcp(r[0]))), S[1], S[0]);       // a_max
+    gr[1] = __fmul_rn(-__fmul_rn(c, __fmul_rn(0.5f, rcp(r[1]))), S[1]);             // a_pref
+    gr[2] = S[2];                                                                    // s_min
+    gr[3] = S[3];                                                                    // T_pref
+    gr[4] = __fmul_rn(__fmul_rn(__fmul_rn(r[0], r[5]), rcp(r[4])), S[4]);            // v_targ
+    gr[5] = __fmul_rn(__fmul_rn(-r[0], kLn2), S[5]);                                  // delta
 }
 
 __device__ __forceinline__ VehBT<float2> pack(const VehB& a, const VehB& b) {

@@ -142,13 +142,8 @@ __global__ void __launch_bounds__(kFT, 2) fit_kernel(FitArgs a) {
         float gr[2][6];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-            const float c = 0.5f / sqrtf(x[j][0] * x[j][1]);
-            gr[j][0] = Sj[0][j] - c * (0.5f / x[j][0]) * Sj[1][j];
-            gr[j][1] = -c * (0.5f / x[j][1]) * Sj[1][j];
-            gr[j][2] = Sj[2][j];
-            gr[j][3] = Sj[3][j];
-            gr[j][4] = x[j][0] * x[j][5] / x[j][4] * Sj[4][j];
-            gr[j][5] = -x[j][0] * kLn2 * Sj[5][j];
+            const float Sv[6] = {Sj[0][j], Sj[1][j], Sj[2][j], Sj[3][j], Sj[4][j], Sj[5][j]};
+            param_grads(x[j], Sv, gr[j]);
 #pragma unroll
             for (int q = 0; q < 6; ++q) {
                 if (!((a.opt_mask >> q) & 1u)) continue;

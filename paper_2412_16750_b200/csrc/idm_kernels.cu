@@ -601,13 +601,9 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
         if (!val[j]) continue;
         const int64_t i = i0 + j;
         const RawP r = load_raw(a.params, a.n_par, i);
-        const float c = 0.5f / sqrtf(r.a_max * r.a_pref);
-        gr[j][0] = Sj[0][j] - c * (0.5f / r.a_max) * Sj[1][j];           // a_max
-        gr[j][1] = -c * (0.5f / r.a_pref) * Sj[1][j];                     // a_pref
-        gr[j][2] = Sj[2][j];                                              // s_min
-        gr[j][3] = Sj[3][j];                                              // T_pref
-        gr[j][4] = r.a_max * r.delta / r.v_targ * Sj[4][j];               // v_targ
-        gr[j][5] = -r.a_max * kLn2 * Sj[5][j];                            // delta
+        const float rr[6] = {r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta};
+        const float Sv[6] = {Sj[0][j], Sj[1][j], Sj[2][j], Sj[3][j], Sj[4][j], Sj[5][j]};
+        param_grads(rr, Sv, gr[j]);
         if (a.grad_state0) {
             a.grad_state0[i] = gpj[j];
             a.grad_state0[N + i] = lvj[j];

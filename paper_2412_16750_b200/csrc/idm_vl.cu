@@ -263,14 +263,9 @@ __global__ void __launch_bounds__(kVT, 2) vl_bwd_kernel(VlArgs a) {
         if (i >= N) continue;
         float r[6];
         vl_params(a.params, a.n_par, i, r);
-        const float c = 0.5f / sqrtf(r[0] * r[1]);
+        const float Sv[6] = {Sj[0][j], Sj[1][j], Sj[2][j], Sj[3][j], Sj[4][j], Sj[5][j]};
         float gr6[6];
-        gr6[0] = Sj[0][j] - c * (0.5f / r[0]) * Sj[1][j];
-        gr6[1] = -c * (0.5f / r[1]) * Sj[1][j];
-        gr6[2] = Sj[2][j];
-        gr6[3] = Sj[3][j];
-        gr6[4] = r[0] * r[5] / r[4] * Sj[4][j];
-        gr6[5] = -r[0] * kLn2 * Sj[5][j];
+        param_grads(r, Sv, gr6);
         if (a.grad_state0) {
             a.grad_state0[i] = lDj[j];  // dL/dp0: position enters every later P
             a.grad_state0[N + i] = lvj[j];
