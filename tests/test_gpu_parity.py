@@ -237,6 +237,14 @@ def test_gradients_c4_subset(idm, oracle):
     worst, plain = grad_check(gg, g["g_params"], g["g_abs"])
     print(f"C4 subset grad worst/tol = {worst:.3f}, plain pass = {plain:.4f}")
     assert worst <= 1.0
+    # the launch configuration bench.py times (idm_fit_step: fused forward with sign words,
+    # backward with the staging ring and Adam) gives the oracle-checked gradients bit for bit
+    # on all 2M vehicles
+    fused = idm.from_workload(w, prm, max_steps=w.K, ckpt_every=DEFAULT_CKPT)
+    fused.fit_step(torch.as_tensor(obs, device="cuda"), kind="l1", iteration=0, sync=True)
+    torch.cuda.synchronize()
+    assert torch.equal(fused.grad_params, sim.grad_params)
+    assert torch.equal(fused.grad_state0, sim.grad_state0)
 
 
 # ---------------------------------------------------------------------- Adam / fit
