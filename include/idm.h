@@ -112,6 +112,15 @@ typedef struct {
    Returns 0 if the descriptor is malformed. */
 size_t idm_workspace_bytes(const idm_desc* d);
 
+/* The lane -> CTA tile plan idm_init builds (host only, no device needed): whole lanes per
+   tile, at most idm_max_lane_vehicles() vehicles per tile, packed greedily in lane order, so two
+   consecutive tiles always hold more than that many vehicles.  lane_offsets: HOST [n_lanes+1].
+   Writes the n_tiles+1 tile starts (vehicle indices, last = n_vehicles) to tile_start (HOST,
+   nullable: count only) and returns n_tiles, or -1 for malformed offsets or a lane longer than
+   a tile. */
+int64_t idm_plan_tiles(const int32_t* lane_offsets, int32_t n_lanes, int64_t n_vehicles,
+                       int64_t* tile_start);
+
 /* Validate the descriptor and input data (finite, v(0) >= 0, lengths >= 0, a_max, a_pref,
    v_targ, delta > 0, lane offsets well formed, every lane fits one lane tile of
    idm_max_lane_vehicles() vehicles), build the lane -> CTA tile plan and leader flags in the

@@ -296,6 +296,17 @@ bool is_vl(const idm_handle* h) { return h->d.leader_mode == IDM_LEADER_VIRTUAL;
 
 extern "C" {
 
+int64_t idm_plan_tiles(const int32_t* lane_offsets, int32_t n_lanes, int64_t n_vehicles,
+                       int64_t* tile_start) {
+    if (!lane_offsets || n_lanes < 1 || n_vehicles < 1) return -1;
+    std::vector<int32_t> off(lane_offsets, lane_offsets + (size_t)n_lanes + 1);
+    std::vector<int64_t> tiles;
+    std::string err;
+    const int64_t nt = plan_tiles(off, n_lanes, n_vehicles, &tiles, nullptr, &err);
+    if (nt >= 0 && tile_start) std::memcpy(tile_start, tiles.data(), sizeof(int64_t) * tiles.size());
+    return nt;
+}
+
 size_t idm_workspace_bytes(const idm_desc* d) {
     Layout L;
     return layout_for(d, tiles_of(d), &L) ? L.total : 0;

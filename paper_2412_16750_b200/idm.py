@@ -117,6 +117,8 @@ def load_library(path: str | None = None):
     L.idm_fit_steps.restype = C.c_int
     L.idm_fit_steps.argtypes = [vp, i32, vp, i32, i32, i32, i32, C.c_float, C.c_float, vp,
                                 C.POINTER(C.c_double)]
+    L.idm_plan_tiles.restype = C.c_int64
+    L.idm_plan_tiles.argtypes = [vp, i32, C.c_int64, vp]
     L.idm_fit_max_steps.restype = i32
     L.idm_fit_max_steps.argtypes = []
     L.idm_step_host.restype = C.c_int
@@ -402,6 +404,20 @@ def idm_adam_step(sim: IdmSim, iteration: int, total: int = 500, lr0=0.1, lr1=0.
 def idm_fit_step(sim: IdmSim, obs, kind="l1", iteration=0, total=500, lr0=0.1, lr1=0.01,
                  sync=False):
     return sim.fit_step(obs, kind, iteration, total, lr0, lr1, sync=sync)
+
+
+def idm_plan_tiles(lane_offsets) -> "np.ndarray":
+    """The lane -> CTA tile plan (host only): tile start vehicle indices, [n_tiles + 1]."""
+    import numpy as np
+    off = np.ascontiguousarray(np.asarray(lane_offsets, np.int32))
+    lib = load_library()
+    n_lanes, n = len(off) - 1, int(off[-1])
+    nt = lib.idm_plan_tiles(off.ctypes.data, n_lanes, n, None)
+    if nt < 0:
+        raise IdmError(IDM_EINVAL, "malformed lane offsets or a lane longer than a tile")
+    out = np.zeros(nt + 1, np.int64)
+    lib.idm_plan_tiles(off.ctypes.data, n_lanes, n, out.ctypes.data)
+    return out
 
 
 def from_workload(w, params=None, **kw) -> IdmSim:

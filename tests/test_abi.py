@@ -84,3 +84,38 @@ def test_init_without_gpu_fails_loudly(lib):
     assert rc == idm.IDM_ECUDA and not h.value
     with pytest.raises(idm.IdmError):
         idm.IdmSim([0, 4], np.zeros(4), np.ones(4), np.full(4, 4.0), max_steps=10)
+
+
+def test_tile_plan_properties(lib):
+    """The host tile planner (idm_plan_tiles, what idm_init uploads and idm_workspace_bytes
+    sizes for): whole lanes per tile, at most the tile capacity per tile, greedy (consecutive
+    tiles hold more than a tile's capacity), within the 2N/cap + 1 bound, and equal to a plain
+    greedy packing written here; malformed offsets and over-long lanes are rejected."""
+    import numpy as np
+    from paper_2412_16750_b200 import idm
+    cap = lib.idm_max_lane_vehicles()
+    rng = np.random.default_rng(0)
+    cases = [[100] * 2000, [1, 7, cap, 3, cap, 1], list(rng.integers(1, cap + 1, 3000)),
+             [cap] * 5, [1] * 9000]
+    for sizes in cases:
+        off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+        tiles = idm.idm_plan_tiles(off)
+        n = int(off[-1])
+        assert tiles[0] == 0 and tiles[-1] == n
+        lens = np.diff(tiles)
+        assert np.all(lens > 0) and np.all(lens <= cap)
+        assert set(tiles).issubset(set(off.tolist()))          # whole lanes only
+        assert np.all(lens[:-1] + lens[1:] > cap)               # greedy
+        assert len(lens) <= 2 * ((n + cap - 1) // cap) + 1
+        expect, cur = [0], 0                                    # plain greedy packing
+        for a, b in zip(off[:-1], off[1:]):
+            if cur + (b - a) > cap:
+                expect.append(int(a))
+                cur = 0
+            cur += int(b - a)
+        expect.append(n)
+        assert tiles.tolist() == expect
+    with pytest.raises(idm.IdmError):
+        idm.idm_plan_tiles([0, cap + 1])
+    with pytest.raises(idm.IdmError):
+        idm.idm_plan_tiles([0, 5, 3])
