@@ -159,7 +159,9 @@ int idm_adam_step(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, f
 
 /* One whole optimizer iteration, fused: exactly forward(steps) -> loss_grad(obs, kind) ->
    backward -> adam_step(iter, ...) (same arithmetic; grad_params, grad_state0, Adam moments and
-   parameters bit for bit), in three launches when ckpt_every == 4: the forward kernel sums
+   parameters bit for bit -- except grad_params row 5, dL/d delta, which is written as 0 when
+   delta is frozen (opt_mask bit 5 clear): the optimizer never reads it, and the delta = 4
+   kernels skip the per-step log2 it needs), in three launches when ckpt_every == 4: the forward kernel sums
    Eq. 4 against each fresh position row (writing only the internal state history), a
    fixed-order reduction of the loss, and the backward kernel, which re-derives dL/dP from obs
    and the rebuilt positions and whose epilogue applies Adam + box clamp per vehicle (shared
@@ -173,8 +175,8 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
 
 /* Whole fit in one launch for short horizons (Waymo-shaped prediction histories of 10 steps,
    PAPER.md:218, :329-331): iterations iter0 .. iter0+iters-1 of exactly idm_fit_step(steps,
-   obs, kind, it, total_iters, lr0, lr1) -- parameters, Adam moments and gradients come out
-   bit-identical -- with the state history, observations and Adam moments of each lane tile
+   obs, kind, it, total_iters, lr0, lr1) -- parameters, Adam moments and gradients (incl. the
+   zero delta row of a frozen delta) come out bit-identical -- with the state history, observations and Adam moments of each lane tile
    kept on chip (no HBM traffic between iterations).  steps <= idm_fit_max_steps(); lane-leader
    mode with per-vehicle parameters; iters <= 4096 per call; grad_traj is not written.  The
    loss of the last iteration (same Eq. 4, summed in a different fixed order) goes to

@@ -798,6 +798,9 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
         if (s == IDM_OK) s = idm_backward(h);
         if (s == IDM_OK) s = idm_adam_step(h, iter, total_iters, lr0, lr1);
         if (s != IDM_OK) return s;
+        if (!((h->d.opt_mask >> 5) & 1u))  // dL/d delta of a frozen delta is not reported
+            CK(h, cudaMemsetAsync(h->d.grad_params + 5 * h->n_par, 0, h->n_par * sizeof(float),
+                                  h->st));
         if (loss_host) {
             CK(h, cudaMemcpyAsync(&h->pinned[0], h->loss_scalar, sizeof(double),
                                   cudaMemcpyDeviceToHost, h->st));

@@ -301,7 +301,9 @@ struct RecT {
     T w, dv;  // (v/v_targ)^delta and v - v_h, reused by the reverse step
 };
 
-template <bool D4, class T>
+//   GD = false: dL/d delta is not wanted (delta frozen at 4 on an optimizer path): r2 = 0, and the
+//   delta = 4 step skips the log2 x it would need.
+template <bool D4, bool GD = true, class T>
 __device__ __forceinline__ RecT<T> jac_record(const CoreT<T>& c, T s, T v, const VehPT<T>& p,
                                               const VehBT<T>& b, const Consts& k) {
     // 1/ones and 1/onea from ONE reciprocal (both in [1, 2], product in [1, 4])
@@ -327,9 +329,13 @@ __device__ __forceinline__ RecT<T> jac_record(const CoreT<T>& c, T s, T v, const
     R.Jv = vsel(lb_act, vfma(omsa, -k.inv_dt, Jv), Jv);
     R.Js = vsel(vge(s, k.eps), vmul(vmul(sAs, c.qr), -kLn2), splat<T>(0.f));
     // log2 x (x = 0: w = 0 makes w log2 x = 0 with log2 of the smallest normal)
-    const T lx = D4 ? lg2(vmax(c.x, 1.17549435e-38f)) : c.lx;
     R.r1 = vfma(c.inter2, -kLn2Sq, c.t1);
-    R.r2 = vmul(c.w, lx);
+    if (GD) {
+        const T lx = D4 ? lg2(vmax(c.x, 1.17549435e-38f)) : c.lx;
+        R.r2 = vmul(c.w, lx);
+    } else {
+        R.r2 = splat<T>(0.f);
+    }
     return R;
 }
 
@@ -337,7 +343,7 @@ __device__ __forceinline__ RecT<T> jac_record(const CoreT<T>& c, T s, T v, const
 // (this vehicle's term for its LEADER's lambda_v), updates ls, lv (the follower's F_in is added
 // by the caller) and the gradient accumulators.  ls = 0 and beta = 0 for a lane head, so no
 // leader predicates are needed (vl only has to be finite there).
-template <bool D4, class T>
+template <bool D4, bool GD = true, class T>
 __device__ __forceinline__ T bwd_from_record(const RecT<T>& R, T v, T vl, const VehPT<T>& p,
                                              const VehBT<T>& b, const Consts& k, T& ls, T& lv,
                                              T lD, GradAccT<T>& g) {
@@ -354,7 +360,7 @@ __device__ __forceinline__ T bwd_from_record(const RecT<T>& R, T v, T vl, const 
     g.S3 = vadd(g.S3, qb);
     g.S4 = vadd(g.S4, qbv);
     g.S5 = vfma(qa, R.w, g.S5);
-    g.S6 = vfma(qa, R.r2, g.S6);
+    if (GD) g.S6 = vfma(qa, R.r2, g.S6);
     return F_out;
 }
 

@@ -126,8 +126,8 @@ __global__ void __launch_bounds__(kFT, 2) fit_kernel(FitArgs a) {
                 const float2 sv = sg[t * kFT + tid];
                 CoreT<float2> c;
                 core<D4>(sv, vv, vl, leadf, P, k, c);
-                const RecT<float2> R = jac_record<D4>(c, sv, vv, P, B, k);
-                const float2 F = bwd_from_record<D4>(R, vv, vl, P, B, k, ls, lv, lD, G);
+                const RecT<float2> R = jac_record<D4, !D4>(c, sv, vv, P, B, k);
+                const float2 F = bwd_from_record<D4, !D4>(R, vv, vl, P, B, k, ls, lv, lD, G);
                 fx[par][tid + 1] = F.y;  // vehicle 2t + 1 -> its leader 2t + 2 (thread t + 1)
                 __syncthreads();
                 lv = vadd(lv, make_float2(fx[par][tid], F.x));
@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(kFT, 2) fit_kernel(FitArgs a) {
         for (int j = 0; j < 2; ++j) {
             const float Sv[6] = {Sj[0][j], Sj[1][j], Sj[2][j], Sj[3][j], Sj[4][j], Sj[5][j]};
             param_grads(x[j], Sv, gr[j]);
+            if (!((a.opt_mask >> 5) & 1u)) gr[j][5] = 0.f;  // delta frozen: not computed
 #pragma unroll
             for (int q = 0; q < 6; ++q) {
                 if (!((a.opt_mask >> q) & 1u)) continue;

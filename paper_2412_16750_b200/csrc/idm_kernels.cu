@@ -436,6 +436,8 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
     constexpr int NB = 3;
     constexpr int VP = kCap + 4;  // speed row pitch: [kCap] = 0 is the leader read of slot 511
     constexpr bool SGN = GOBS == 1, OBS = GOBS == 2;
+    // fused iteration with delta frozen at 4: dL/d delta is not computed (row 5 written as 0)
+    constexpr bool GD = !(D4 && GOBS != 0);
     constexpr int KO = GOBS ? KS + 1 : KS;             // + the rollout's last step (fused)
     float* vrow = smem_b;                              // [NB][KS][VP]
     float* ckrow = vrow + NB * KS * VP;                // [NB][3][kCap]
@@ -569,8 +571,8 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
             if (kFull || tt < len) {  // CTA-uniform
                 CoreT<float2> c;
                 core<D4>(sg[tt], v[tt], vl[tt], leadf, P, k, c);
-                const RecT<float2> R = jac_record<D4>(c, sg[tt], v[tt], P, B, k);
-                const float2 F = bwd_from_record<D4>(R, v[tt], vl[tt], P, B, k, ls, lv, lD, G);
+                const RecT<float2> R = jac_record<D4, GD>(c, sg[tt], v[tt], P, B, k);
+                const float2 F = bwd_from_record<D4, GD>(R, v[tt], vl[tt], P, B, k, ls, lv, lD, G);
                 fx[par][tid + 1] = F.y;  // vehicle 2t + 1 -> its leader 2t + 2 (thread t + 1)
                 __syncthreads();
                 // F from the follower: 2t - 1 (thread t - 1) for 2t, 2t (this thread) for 2t + 1
@@ -604,6 +606,7 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
         const float rr[6] = {r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta};
         const float Sv[6] = {Sj[0][j], Sj[1][j], Sj[2][j], Sj[3][j], Sj[4][j], Sj[5][j]};
         param_grads(rr, Sv, gr[j]);
+        if (GOBS && !((a.adam.opt_mask >> 5) & 1u)) gr[j][5] = 0.f;  // delta frozen: not computed
         if (a.grad_state0) {
             a.grad_state0[i] = gpj[j];
             a.grad_state0[N + i] = lvj[j];

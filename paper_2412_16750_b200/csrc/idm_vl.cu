@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(kVT, 2) vl_bwd_kernel(VlArgs a) {
         const float Sv[6] = {Sj[0][j], Sj[1][j], Sj[2][j], Sj[3][j], Sj[4][j], Sj[5][j]};
         float gr6[6];
         param_grads(r, Sv, gr6);
+        if (ADAM && !((a.adam.opt_mask >> 5) & 1u)) gr6[5] = 0.f;  // delta frozen: not reported
         if (a.grad_state0) {
             a.grad_state0[i] = lDj[j];  // dL/dp0: position enters every later P
             a.grad_state0[N + i] = lvj[j];
