@@ -22,7 +22,7 @@ struct idm_handle {
     int64_t* tile_start;
     uint8_t* lead;
     float *vt, *ckt, *ckpt_v;     // lane-mode state history (tile-local), VL speed checkpoints
-    uint32_t* sgn;                // fused L1 sign words (tile-local)
+    uint32_t* sgn;                // fused L1 sign codes (tile-local)
     int64_t vt_stride, ck_stride, sg_stride;
     double *loss_partials, *loss_scalar, *shared_partials;
     unsigned long long* status;
@@ -157,7 +157,7 @@ bool layout_for(const idm_desc* d, int64_t ntiles, Layout* L) {
     L->ck_stride = nck * kCkRows * kCap;
     L->vt = off; off += align256(sizeof(float) * ((size_t)(mt * L->vt_stride) + 64));
     L->ckt = off; off += align256(sizeof(float) * (size_t)(mt * L->ck_stride));
-    L->sg_stride = (int64_t)(d->max_steps + 1) * kSgnWords;
+    L->sg_stride = sgn_words_per_tile(d->max_steps);
     L->sgn = off; off += align256(sizeof(uint32_t) * (size_t)(mt * L->sg_stride));
     // virtual-leader mode: speed checkpoints every 4 steps
     L->ckpt_v = off; off += align256(sizeof(float) * (size_t)(nck * n));

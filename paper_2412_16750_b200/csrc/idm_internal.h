@@ -34,9 +34,13 @@ struct FwdVariant {
 // aligned 8-byte access at an immediate offset, and slots past the tile's vehicles are
 // private padding (stores need no predicate).
 constexpr int kCkRows = 3;
-//   sgn [tile][max_steps + 1][kSgnWords] fused L1 only: dL/dP = -sign(obs - P) as two ballot
-//                                       bits per vehicle (observed-and-nonzero, negative)
-constexpr int kSgnWords = 32;  // per step per tile: 8 warps x (nz, neg) x 2 vehicles per thread
+//   sgn [tile][max_steps / 4 + 1][kCap / 2] u16, fused L1 only: dL/dP = -sign(obs - P) of a
+//                                       thread's two vehicles as a 4-bit code per step (bits 0 / 2:
+//                                       r != 0, bits 1 / 3: r < 0), steps 4j .. 4j + 3 in word j
+constexpr int kSgnSteps = 4;  // steps per u16 code word
+__host__ __device__ constexpr int64_t sgn_words_per_tile(int max_steps) {  // in u32 units
+    return (int64_t)(max_steps / kSgnSteps + 1) * (kCap / 2) / 2;
+}
 
 struct FwdArgs {
     const int64_t* tile_start;
@@ -46,7 +50,7 @@ struct FwdArgs {
     float *traj, *vel_traj, *state_out;
     float *vt, *ckt;
     int64_t vt_stride, ck_stride;  // floats per tile
-    uint32_t* sgn;                 // fused L1: sign words
+    uint32_t* sgn;                 // fused L1: sign codes (u16 words, see above)
     int64_t sg_stride;             // words per tile
     int tile0;                     // first tile of this launch (grid = a chunk of the tiles)
     int steps, ckpt_every;

@@ -18,12 +18,24 @@
 #include <climits>
 #include <cstdint>
 #include <type_traits>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "idm_device.cuh"
 #include "idm_internal.h"
 
 namespace idm {
+
+// f(integral_constant<int, 0>) ... f(integral_constant<int, N - 1>): an unrolled loop whose index
+// is a compile-time constant inside the body
+template <class F, int... I>
+__device__ __forceinline__ void static_for_impl(F& f, std::integer_sequence<int, I...>) {
+    (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+    static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
 
 // ------------------------------------------------------------------------------ NK0
 __global__ void validate_kernel(ValidateArgs a) {
@@ -146,7 +158,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // the K mod KS tail runs as one predicated segment).  LOSS = 0: record P (idm_forward).
 // LOSS = 1 (L1) / 2 (L2): fused Eq. 4 for idm_fit_step -- observation rows staged two segments
 // ahead (cp.async ring); each step sums Eq. 4 against the fresh positions and, for L1, records
-// dL/dP = -sign(obs - P) as ballot bits; P and dL/dP are not written.
+// dL/dP = -sign(obs - P) as a 4-bit code per thread-step; P and dL/dP are not written.
 // CK = checkpoint interval (the backward's segment length); the forward's own prefetch
 // segment is KS = max(4, CK) steps, so CK | KS and checkpoints fall at static positions.
 template <bool D4, bool KAHAN, bool RECV, int LOSS, int CK>
@@ -254,36 +266,41 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
         if (LOSS == 2) __stcs(ckp + kR2, D);
         if (LOSS == 2 && KAHAN) __stcs(ckp + 2 * kR2, cmp);
     };
-    // fused L1: dL/dP = -sign(obs - P) of each vehicle as two ballot bits (nonzero, +1); lane 0
-    // of each warp stores the warp's four words of the step (16 B)
-    uint4* sgp = LOSS == 1 ? reinterpret_cast<uint4*>(a.sgn + tile * a.sg_stride) +
-                                 (tid >> 5)
-                           : nullptr;
-    // Eq. 4 term of the fused forward: L2 sums r^2; L1 sums |r| and records -sign(r) as the
-    // bits (r != 0, r < 0) of the masked residual r (0 where unobserved), i.e. exactly
-    // loss_term<0>'s dL/dP
-    auto loss_step = [&](float2 o, float2 Pv) {
+    // fused L1: dL/dP = -sign(obs - P) of the thread's two vehicles as a 4-bit code per step
+    // (bits 0 / 2: r != 0, bits 1 / 3: r < 0), collected in a register and stored as one u16
+    // word per 4 steps (steps 4j .. 4j + 3 -> word j; 64 B per warp)
+    static_assert(LOSS != 1 || KS % kSgnSteps == 0, "code words align with segments");
+    unsigned short* sgp =
+        LOSS == 1 ? reinterpret_cast<unsigned short*>(a.sgn + tile * a.sg_stride) + tid : nullptr;
+    unsigned code = 0;
+    // Eq. 4 term of the fused forward at a step t with t mod 4 = ph (compile-time): L2 sums r^2;
+    // L1 sums |r| and records -sign(r) of the masked residual r (0 where unobserved), i.e.
+    // exactly loss_term<0>'s dL/dP
+    auto loss_step = [&](float2 o, float2 Pv, auto PH) {
+        constexpr int ph = decltype(PH)::value;
         if (LOSS == 2) {
             (void)loss_term<1>(o, Pv, lseg);
             return;
         }
         const float2 rm = vsel(vge(vnabs(o), -3.4e38f), vsub(o, Pv), f2(0.f));
         lseg = vadd(lseg, vabs(rm));
-        const unsigned nz0 = __ballot_sync(0xffffffffu, rm.x != 0.f);
-        const unsigned ps0 = __ballot_sync(0xffffffffu, rm.x < 0.f);
-        const unsigned nz1 = __ballot_sync(0xffffffffu, rm.y != 0.f);
-        const unsigned ps1 = __ballot_sync(0xffffffffu, rm.y < 0.f);
-        if ((tid & 31) == 0) __stcs(sgp, make_uint4(nz0, ps0, nz1, ps1));
-        sgp += kSgnWords / 4;
+        const unsigned nib = (rm.x != 0.f ? 1u : 0u) | (rm.x < 0.f ? 2u : 0u) |
+                             (rm.y != 0.f ? 4u : 0u) | (rm.y < 0.f ? 8u : 0u);
+        code |= nib << (4 * ph);
+        if (ph == kSgnSteps - 1) {
+            __stcs(sgp, (unsigned short)code);
+            sgp += kT;
+            code = 0;
+        }
     };
-    if (LOSS) loss_step(ld_obs(obs, true), p0);
+    if (LOSS) loss_step(ld_obs(obs, true), p0, std::integral_constant<int, 0>{});
     else put(orow, p0);
     if (RECV) put(vrow, v);
     __stcs(vtp, v);
     put_ck();
     int par = 0;
     // one synchronous step of the whole tile; o = this step's observations (LOSS)
-    auto step = [&](float2 o) {
+    auto step = [&](float2 o, auto PH) {  // PH: (index of the step computed) mod 4
         xv[par][tid] = v.x;
         __syncthreads();
         const float2 vl = make_float2(v.y, xv[par][tid + 1]);
@@ -301,7 +318,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
         if (RECV) vrow += N;
         vtp += kR2;
         const float2 Pv = vadd(p0, D);
-        if (LOSS) loss_step(o, Pv);
+        if (LOSS) loss_step(o, Pv, PH);
         else put(orow, Pv);
         __stcs(vtp, v);
         if (RECV) put(vrow, v);
@@ -330,11 +347,11 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
     for (int seg = 0; seg < nfull; ++seg) {
         const int t0 = seg * KS;
         obs_ready(seg);
-#pragma unroll
-        for (int tt = 0; tt < KS; ++tt) {
+        static_for<KS>([&](auto TT) {
+            constexpr int tt = decltype(TT)::value;
             if (tt % CK == 0 && (tt > 0 || seg > 0)) checkpoint(t0 + tt);
-            step(LOSS ? obs_at(tt) : f2(0.f));
-        }
+            step(LOSS ? obs_at(tt) : f2(0.f), std::integral_constant<int, (tt + 1) % 4>{});
+        });
         obs_done();
         if (LOSS) {
             lacc += (double)lseg.x + (double)lseg.y;
@@ -343,15 +360,17 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
     }
     if (tail > 0) {
         obs_ready(nfull);
-#pragma unroll
-        for (int tt = 0; tt < KS; ++tt) {
+        static_for<KS>([&](auto TT) {
+            constexpr int tt = decltype(TT)::value;
             if (tt < tail) {  // CTA-uniform predicate
                 if (tt % CK == 0 && (tt > 0 || nfull > 0)) checkpoint(nfull * KS + tt);
-                step(LOSS ? obs_at(tt) : f2(0.f));
+                step(LOSS ? obs_at(tt) : f2(0.f), std::integral_constant<int, (tt + 1) % 4>{});
             }
-        }
+        });
     }
     if (LOSS) cp_async_wait<0>();  // no copy outlives the CTA
+    if (LOSS == 1 && steps % kSgnSteps != kSgnSteps - 1)
+        __stcs(sgp, (unsigned short)code);  // the last, partial code word (holds step K)
     finite2(steps);
     if (val[0] && bad0 != INT_MAX) report_nonfinite(a.status, bad0, i0);
     if (val[1] && bad1 != INT_MAX) report_nonfinite(a.status, bad1, i0 + 1);
@@ -373,8 +392,8 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
 // 2t + 1, passed to thread t + 1 through shared memory (one barrier per step).  The next
 // segment's rows are prefetched into registers while the current one is swept.
 //   GOBS = 0:      dL/dP rows from grad_traj (idm_backward after idm_loss_grad);
-//   GOBS = 1:      fused idm_fit_step, L1 -- dL/dP = -sign(obs - P) from the forward's ballot
-//                  words (2 bits per vehicle-step);
+//   GOBS = 1:      fused idm_fit_step, L1 -- dL/dP = -sign(obs - P) from the forward's sign
+//                  codes (2 bits per vehicle-step);
 //   GOBS = 2:      fused idm_fit_step, L2 -- dL/dP re-derived from obs and the rebuilt positions
 //                  P = p0 + D with the forward's loss term (same bits as idm_loss_grad).
 // Gradient accumulators stay in registers for the whole rollout; ADAM: per-vehicle Adam in the
@@ -442,10 +461,16 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
     float* vrow = smem_b;                              // [NB][KS][VP]
     float* ckrow = vrow + NB * KS * VP;                // [NB][3][kCap]
     float* orow = ckrow + NB * kCkRows * kCap;         // [NB][KO][kCap] (dL/dP or obs rows)
-    uint4* sbuf = reinterpret_cast<uint4*>(orow);      // [NB][KO][8 warps] (SGN: sign words)
+    // SGN: [NB][2][kT] u16 code words (the segment's steps; + the next word, which holds step K
+    // when the last segment is a whole one) and the 16-entry decode table code -> dL/dP pair
+    unsigned short* sbuf = reinterpret_cast<unsigned short*>(orow);
+    __shared__ float2 glut[16];
+    if (SGN && tid < 16) {
+        auto gv = [](unsigned nz, unsigned neg) { return nz ? (neg ? 1.f : -1.f) : 0.f; };
+        glut[tid] = make_float2(gv(tid & 1u, tid & 2u), gv(tid & 4u, tid & 8u));
+    }
     __shared__ __align__(8) uint64_t mbar[NB];
     constexpr int nckr = OBS ? (KAHAN ? 3 : 2) : 1;    // checkpoint rows used
-    const unsigned lmask = 1u << (tid & 31);
     if (tid == 0) {
 #pragma unroll
         for (int q = 0; q < NB; ++q) mbar_init(&mbar[q], 1);
@@ -461,14 +486,16 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
             // buffer b was last read (generic proxy) before the barriers of an earlier
             // segment; order those reads before the async-proxy writes
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            const int srows = len + (seg == nseg - 1 ? 1 : 0);  // SGN: + row K
+            // SGN: code word seg, + word seg + 1 (step K) when the last segment is whole
+            const int swords = (seg == nseg - 1 && len == KS) ? 2 : 1;
             const uint32_t bytes = (uint32_t)(len + nckr) * kCap * sizeof(float) +
-                                   (SGN ? (uint32_t)srows * kSgnWords * sizeof(uint32_t) : 0u);
+                                   (SGN ? (uint32_t)swords * kT * sizeof(unsigned short) : 0u);
             mbar_expect_tx(&mbar[b], bytes);
             if (SGN)
-                bulk_g2s(sbuf + b * KO * (kSgnWords / 4),
-                         a.sgn + tile * a.sg_stride + t0 * kSgnWords,
-                         srows * kSgnWords * sizeof(uint32_t), &mbar[b]);
+                bulk_g2s(sbuf + b * 2 * kT,
+                         reinterpret_cast<const unsigned short*>(a.sgn + tile * a.sg_stride) +
+                             (int64_t)seg * kT,
+                         swords * kT * sizeof(unsigned short), &mbar[b]);
             const float* src = a.vt + tile * a.vt_stride + t0 * kCap;
             for (int tt = 0; tt < len; ++tt)
                 bulk_g2s(vrow + (b * KS + tt) * VP, src + tt * kCap, kCap * sizeof(float), &mbar[b]);
@@ -513,14 +540,17 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
                 vl[tt] = f2(0.f);
             }
         }
+        unsigned cw0 = 0, cw1 = 0;  // SGN: this thread's code words (steps t0 .. t0 + 4)
+        if (SGN) {
+            static_assert(!SGN || KS == kSgnSteps, "one code word per segment");
+            cw0 = sbuf[b * 2 * kT + tid];
+            if (seg == nseg - 1 && len == KS) cw1 = sbuf[b * 2 * kT + kT + tid];
+        }
 #pragma unroll
         for (int tt = 0; tt < KO; ++tt) {
-            if (SGN) {  // -sign(obs - P): (nonzero, +1) bits of this thread's two vehicles
-                const uint4 w = sbuf[(b * KO + tt) * (kSgnWords / 4) + (tid >> 5)];
-                auto gv = [&](unsigned nz, unsigned ps) {
-                    return (nz & lmask) ? ((ps & lmask) ? 1.f : -1.f) : 0.f;
-                };
-                g[tt] = (kFull || tt <= len) ? make_float2(gv(w.x, w.y), gv(w.z, w.w)) : f2(0.f);
+            if (SGN) {  // -sign(obs - P) of this thread's two vehicles: 4-bit code -> table
+                const unsigned c = ((tt < KS ? cw0 : cw1) >> (4 * (tt % KS))) & 15u;
+                g[tt] = (kFull || tt <= len) ? glut[c] : f2(0.f);
             } else {
                 g[tt] = (kFull || tt <= len) ? *reinterpret_cast<const float2*>(orr + tt * kCap)
                                              : f2(0.f);
@@ -802,7 +832,7 @@ template <int KS, int GOBS>
 constexpr size_t bwd_smem_of() {  // ring of 3: speed + checkpoint + dL/dP/obs (or sign) rows
     return (size_t)3 *
            (KS * (kCap + 4) + kCkRows * kCap +
-            (GOBS == 1 ? (KS + 1) * kSgnWords : (GOBS ? KS + 1 : KS) * kCap)) *
+            (GOBS == 1 ? kCap / 2 : (GOBS ? KS + 1 : KS) * kCap)) *
            sizeof(float);
 }
 
