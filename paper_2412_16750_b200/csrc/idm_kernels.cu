@@ -139,6 +139,13 @@ __device__ __forceinline__ void cp_async4(float* dst, const float* src, bool on)
                  "r"(on ? 4 : 0)
                  : "memory");
 }
+// 4-byte cp.async issued only when `on` (no zero-fill: the destination keeps its value)
+__device__ __forceinline__ void cp_async4_if(float* dst, const float* src, bool on) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n"
+                 " @q cp.async.ca.shared.global [%0], [%1], 4;\n}" ::"r"(smem_u32(dst)),
+                 "l"(src), "r"((int)on)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() {
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -161,8 +168,12 @@ __device__ __forceinline__ void cp_async_wait() {
 // dL/dP = -sign(obs - P) as a 4-bit code per thread-step; P and dL/dP are not written.
 // CK = checkpoint interval (the backward's segment length); the forward's own prefetch
 // segment is KS = max(4, CK) steps, so CK | KS and checkpoints fall at static positions.
+#ifndef IDM_FWD_LOSS_MINB
+#define IDM_FWD_LOSS_MINB 4  // CTAs per SM the fused (LOSS) forward is register-budgeted for
+#endif
 template <bool D4, bool KAHAN, bool RECV, int LOSS, int CK>
-__global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
+__global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 4)))
+    fwd_kernel(FwdArgs a) {
     constexpr int KS = CK > 4 ? CK : 4;
     __shared__ float xv[2][kT + 1];  // speed of each thread's first vehicle; [kT] = 0 sentinel
     const int tid = threadIdx.x;
@@ -216,8 +227,9 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
     const float* obs = LOSS ? a.obs + i0 : nullptr;
     const float qnan = __int_as_float(0x7fc00000);
     // LOSS: observation rows staged two segments ahead in a 3-buffer shared-memory ring by
-    // per-thread cp.async (zero-fill for absent vehicles, masked at use); one commit group per
-    // segment (empty past the end) keeps cp.async.wait_group<1> exact
+    // per-thread cp.async; the slots of absent vehicles hold NaN (= missing) from the start and
+    // are never copied to; one commit group per segment (empty past the end) keeps
+    // cp.async.wait_group<1> exact
     __shared__ __align__(16) float obuf[LOSS ? 3 : 1][LOSS ? KS : 1][kCap];
     float2 lseg = f2(0.f);  // loss of this thread's vehicles in this segment (fp32)
     double lacc = 0.0;   // and across segments (fp64)
@@ -236,8 +248,8 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
             const float* o = onext;
 #pragma unroll
             for (int tt = 0; tt < KS; ++tt, o += N) {
-                cp_async4(dst + tt * kCap, o, val[0]);
-                cp_async4(dst + tt * kCap + 1, o + 1, val[1]);
+                cp_async4_if(dst + tt * kCap, o, val[0]);
+                cp_async4_if(dst + tt * kCap + 1, o + 1, val[1]);
             }
             onext = o;
         } else {  // the tail / past the end: predicated, addresses kept inside the array
@@ -245,17 +257,22 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : 4)) fwd_kernel(FwdArgs a) {
             for (int tt = 0; tt < KS; ++tt) {
                 const bool on = r0 + tt <= steps;
                 const float* o = on ? onext + (int64_t)tt * N : obs;
-                cp_async4(dst + tt * kCap, o, on && val[0]);
-                cp_async4(dst + tt * kCap + 1, o + 1, on && val[1]);
+                cp_async4_if(dst + tt * kCap, o, on && val[0]);
+                cp_async4_if(dst + tt * kCap + 1, o + 1, on && val[1]);
             }
         }
         cp_async_commit();
     };
     auto obs_at = [&](int tt) {  // this thread's pair of row seg*KS + 1 + tt (current segment)
-        const float2 o = *reinterpret_cast<const float2*>(&obuf[cslot][tt][2 * tid]);
-        return make_float2(val[0] ? o.x : qnan, val[1] ? o.y : qnan);
+        return *reinterpret_cast<const float2*>(&obuf[cslot][tt][2 * tid]);
     };
     if (LOSS) {
+        float* ob = &obuf[0][0][0];
+#pragma unroll
+        for (int q = 0; q < 3 * KS; ++q) {  // own slots only: no barrier needed
+            if (!val[0]) ob[q * kCap + 2 * tid] = qnan;
+            if (!val[1]) ob[q * kCap + 2 * tid + 1] = qnan;
+        }
         fetch_obs(0);
         fetch_obs(1);
     }
