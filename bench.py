@@ -39,7 +39,10 @@ ALG_INSTR = {"fwd": 36.0, "bwd": 114.0}  # SURVEY.md 8(d) frozen essential-op co
 # The same essential math counted in issue slots of THIS implementation, where two vehicles'
 # FP32 multiply-adds issue as one f32x2 instruction: the frozen scalar
 # counts over-credit a packed kernel, so both fractions are reported.
-PACKED_INSTR = {"fwd": 21.0, "bwd": 45.5}
+# "bwd_fit": the optimizer-path backward with delta frozen at 4 (the paper's five parameters,
+# PAPER.md:208), which does not compute dL/d delta (one log2, one max, one multiply, one FMA per
+# vehicle-step fewer: 3 slots per vehicle-step; R#1).
+PACKED_INSTR = {"fwd": 21.0, "bwd": 45.5, "bwd_fit": 42.5}
 ISSUE_PER_CLK = 148 * 4 * 32  # SMs x schedulers x lanes (thread-instr / clk)
 
 
@@ -389,15 +392,16 @@ def run_ours(args, rank, world, local_rank):
     else:
         issue_peak = ISSUE_PER_CLK * sm_mhz_max * 1e6 / 1e12  # Tinstr/s
         kk = "bwd" if dom == "bwd" else "fwd"
+        kp = "bwd_fit" if kk == "bwd" else kk  # the headline path is idm_fit_step, delta frozen
         # essential issue slots of THIS (f32x2-packed) implementation: SURVEY 8(d) addendum
-        achieved = PACKED_INSTR[kk] * n_veh_steps / (kms[dom] * 1e-3) / 1e12
+        achieved = PACKED_INSTR[kp] * n_veh_steps / (kms[dom] * 1e-3) / 1e12
         frozen = ALG_INSTR[kk] * n_veh_steps / (kms[dom] * 1e-3) / 1e12
         traffic = load_traffic().get(f"{dom}_kernel")
         roofline = {"bound": "alu", "kernel": f"{dom}_kernel (fused path)", "achieved": achieved,
                     "peak": issue_peak, "unit": "Tinstr/s", "frac": achieved / issue_peak,
                     "traffic": traffic,
                     "frac_frozen_scalar_count": frozen / issue_peak,
-                    "basis": f"{PACKED_INSTR[kk]} essential issue slots per vehicle-step (packed "
+                    "basis": f"{PACKED_INSTR[kp]} essential issue slots per vehicle-step (packed "
                              f"f32x2 implementation; SURVEY 8(d) addendum) x {n_veh_steps:.3g} "
                              f"vehicle-steps per launch / CUDA-event launch time; peak = 148 SM "
                              f"x 4 issue/clk x 32 lanes x {sm_mhz_max:.0f} MHz (MEASURED_PEAKS "
