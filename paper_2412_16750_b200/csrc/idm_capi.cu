@@ -184,6 +184,7 @@ Consts consts_of(const idm_desc& d) {
     k.a_min2 = (float)((double)d.a_min * 1.4426950408889634);
     k.ninv_dt2 = (float)(-1.4426950408889634 / (double)d.dt);
     k.dt_amin = d.dt * d.a_min;  // fp32 product, as the device would round it
+    k.dt2 = d.dt * d.dt;
     return k;
 }
 

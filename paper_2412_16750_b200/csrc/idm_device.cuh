@@ -33,6 +33,7 @@ struct Consts {
     float a_min2;     // a_min log2 e
     float ninv_dt2;   // -log2(e) / dt
     float dt_amin;    // dt a_min (fp32 product)
+    float dt2;        // dt^2 (fp32 product): scale of the lane adjoint's lambda_D
 };
 
 // ------------------------------------------------------------------ lane arithmetic
@@ -168,13 +169,14 @@ using Core = CoreT<float>;
 // Eqs. 1-2 with the Sec. III-C bounds, exact free road
 // without a leader (R#8), gap clamped at eps (R#7), given the approach rate dv = v_i - v_h
 // directly (the virtual-leader mode, passes its free variable).
-//   leadf: 1 with a leader, 0 without (folded into 1/Delta p: the interaction term and every
-//   derivative through it vanish exactly for a lane head).
+// A vehicle without a leader (lane head, or an empty slot of a tile) carries the gap s = +inf:
+// 1/Delta p = rcp(inf) = 0 makes the interaction term and every derivative through it vanish
+// exactly, and s + dt (v_h - v) stays +inf.
 // Explicit _rn intrinsics: the forward kernel and the backward recompute produce bitwise
 // identical states.
-template <bool D4, class T, class LF>
-__device__ __forceinline__ void core_dv(T s, T v, T dv, LF leadf, const VehPT<T>& p,
-                                        const Consts& k, CoreT<T>& c) {
+template <bool D4, class T>
+__device__ __forceinline__ void core_dv(T s, T v, T dv, const VehPT<T>& p, const Consts& k,
+                                        CoreT<T>& c) {
     c.x = vmul(v, p.ivt);
     c.x2 = vmul(c.x, c.x);
     if (D4) {
@@ -191,7 +193,7 @@ __device__ __forceinline__ void core_dv(T s, T v, T dv, LF leadf, const VehPT<T>
     c.es = ex2(vnabs(c.s_opt2));
     c.ones = vadd(c.es, 1.f);
     c.ss2 = vadd(vmax(c.s_opt2, 0.f), lg2(c.ones));            // softplus(s_opt) log2 e
-    c.idp = vmul(rcp(vmax(s, k.eps)), leadf);                  // lead / Delta p
+    c.idp = rcp(vmax(s, k.eps));                               // 1 / Delta p (0: no leader)
     c.qr = vmul(c.ss2, c.idp);                                 // (s*/Delta p) log2 e
     c.inter2 = vmul(c.qr, c.qr);
     c.t1 = vsub(1.f, c.w);
@@ -204,10 +206,10 @@ __device__ __forceinline__ void core_dv(T s, T v, T dv, LF leadf, const VehPT<T>
     c.onea = vadd(c.ea, 1.f);
 }
 
-template <bool D4, class T, class LF>
-__device__ __forceinline__ void core(T s, T v, T vl, LF leadf, const VehPT<T>& p,
-                                     const Consts& k, CoreT<T>& c) {
-    core_dv<D4>(s, v, vsub(v, vl), leadf, p, k, c);  // Delta v = v_i - v_h
+template <bool D4, class T>
+__device__ __forceinline__ void core(T s, T v, T vl, const VehPT<T>& p, const Consts& k,
+                                     CoreT<T>& c) {
+    core_dv<D4>(s, v, vsub(v, vl), p, k, c);  // Delta v = v_i - v_h
 }
 
 // State update of one vehicle from its step core (Eq. 3).  v' = v + dt a* computed as
@@ -222,11 +224,10 @@ __device__ __forceinline__ void advance(const CoreT<T>& c, T& s, T& v, const Con
 }
 
 // One synchronous IDM + Euler step (Eqs. 1-3, Sec. III-C).
-template <bool D4, class T, class LF>
-__device__ __forceinline__ void fwd_step(T& s, T& v, T vl, LF leadf, const VehPT<T>& p,
-                                         const Consts& k) {
+template <bool D4, class T>
+__device__ __forceinline__ void fwd_step(T& s, T& v, T vl, const VehPT<T>& p, const Consts& k) {
     CoreT<T> c;
-    core<D4>(s, v, vl, leadf, p, k, c);
+    core<D4>(s, v, vl, p, k, c);
     advance(c, s, v, k);
 }
 
@@ -261,6 +262,32 @@ __device__ __forceinline__ VehB make_vehb(float a_max, float a_pref, float v_tar
     return b;
 }
 
+// Backward constants of the LANE adjoint, scaled: the reverse
+// sweep carries u = dt lambda_v (= q), m = -dt lambda_s and e = dt^2 lambda_D, so the per-step
+// factors dt and ln 2 live in these constants instead of in multiplies:
+//   Kb = -2 a_max ln2^2 dt    (d a_raw/d s* = nam2ln2 qr idp, times ln2 dt)
+//   ndvt = -delta a_max dt / v_targ
+//   ncl = -c / ln2            (d s_opt/d v_h over ln2)
+template <class T>
+struct VehAT {
+    T Kb, ndvt, ncl;
+};
+using VehA = VehAT<float>;
+
+__device__ __forceinline__ VehA make_veha(float a_max, float a_pref, float v_targ, float delta,
+                                          const Consts& k) {
+    VehA b;
+    b.Kb = __fmul_rn(__fmul_rn(-2.f * a_max, kLn2Sq), k.dt);
+    b.ndvt = __fmul_rn(__fmul_rn(__fmul_rn(-delta, a_max), rcp(v_targ)), k.dt);
+    b.ncl = __fmul_rn(-0.5f * kLog2e, rsqrt_a(__fmul_rn(a_max, a_pref)));
+    return b;
+}
+
+__device__ __forceinline__ VehAT<float2> pack(const VehA& a, const VehA& b) {
+    return VehAT<float2>{make_float2(a.Kb, b.Kb), make_float2(a.ndvt, b.ndvt),
+                         make_float2(a.ncl, b.ncl)};
+}
+
 // dL/d(a_max, a_pref, s_min, T_pref, v_targ, delta) of one vehicle from its factored
 // accumulators (GradAcc) and raw parameters r; shared by every backward so they agree bitwise:
 //   c = 1/(2 sqrt(a b)),  ds_opt/da = -c/(2a) v dv,  ds_opt/db = -c/(2b) v dv,
@@ -290,11 +317,12 @@ struct GradAccT {
 };
 using GradAcc = GradAccT<float>;
 
-// Local Jacobian of one vehicle-step (derivation: DESIGN.md "Adjoint (gap form)"), 24 bytes per
-// vehicle: (sigma_a, beta = d a*/d s_opt, J_v = d a*/d v |_{v_h}, J_s = d a*/d s,
-// r1 = 1 - w - r^2, r2 = w log2 x) with w = (v/v_targ)^delta, r = s*/dp.
-// sigma_a = d a*/d a_raw, d s*/d s_opt = sigmoid(s_opt) (:148); beta = 0 without
-// a leader (idp = 0, R#8) and J_s = 0 while the gap is clamped (R#7).
+// Local Jacobian of one vehicle-step of the LANE adjoint (derivation: DESIGN.md "Adjoint (gap
+// form)" and "Adjoint scaling"): sigma_a = d a*/d a_raw; beta = (d a*/d s_opt) ln2 dt
+// with d s*/d s_opt = sigmoid(s_opt) (:148); J_v = dt d a*/d v |_{v_h}; J_s = -dt^2 (d a*/d s)
+// ln 2 / ln 2 = sAs qr (see jac_record); r1 = 1 - w - r^2, r2 = w log2 x with w = (v/v_targ)^delta,
+// r = s*/dp.  beta = J_s = 0 without a leader (idp = 0, R#8) and J_s = 0 while the gap is clamped
+// (R#7).
 template <class T>
 struct RecT {
     T sig_a, beta, Jv, Js, r1, r2;
@@ -305,7 +333,7 @@ struct RecT {
 //   delta = 4 step skips the log2 x it would need.
 template <bool D4, bool GD = true, class T>
 __device__ __forceinline__ RecT<T> jac_record(const CoreT<T>& c, T s, T v, const VehPT<T>& p,
-                                              const VehBT<T>& b, const Consts& k) {
+                                              const VehAT<T>& b, const Consts& k) {
     // 1/ones and 1/onea from ONE reciprocal (both in [1, 2], product in [1, 4])
     const T rp = rcp(vmul(c.ones, c.onea));
     const T hs = vcopysign(vfma(c.onea, rp, splat<T>(-0.5f)), c.s_opt2);
@@ -313,21 +341,23 @@ __device__ __forceinline__ RecT<T> jac_record(const CoreT<T>& c, T s, T v, const
     const T ha = vcopysign(vfma(c.ones, rp, splat<T>(-0.5f)), c.z2);
     const T sig_a = vadd(ha, 0.5f);                                  // d a*/d a_raw
     const T omsa = vsub(0.5f, ha);                                   // d a*/d a_lb
-    const T As = vmul(vmul(b.nam2ln2, c.qr), c.idp);                // d a_raw/d s*
+    const T As = vmul(vmul(b.Kb, c.qr), c.idp);                     // (d a_raw/d s*) ln2 dt
     const T sAs = vmul(sig_a, As);
     RecT<T> R;
     R.w = c.w;
     R.dv = c.dv;
     R.sig_a = sig_a;
-    R.beta = vmul(sAs, sig_s);                                       // d a*/d s_opt
+    R.beta = vmul(sAs, sig_s);                                       // (d a*/d s_opt) ln2 dt
     T xm1;                                                           // x^(delta-1)
     if (D4) xm1 = vmul(c.x2, c.x);
     else xm1 = vsel(vgt(c.x, 0.f), vmul(c.w, rcp(c.x)), splat<T>(0.f));
-    // d a*/d v at fixed leader speed: free term + s_opt term (T + (dv + v) c) + a_lb branch (R#5)
-    const T Jv = vfma(vmul(R.beta, kLn2), vfma(v, p.c2, c.c12), vmul(vmul(sig_a, b.ndamivt), xm1));
+    // dt d a*/d v at fixed leader speed: free term + s_opt term (T + (dv + v) c; c2 = c log2 e
+    // meets beta's ln 2) + a_lb branch (R#5: dt (1 - sigma_a)(-1/dt))
+    const T Jv = vfma(R.beta, vfma(v, p.c2, c.c12), vmul(vmul(sig_a, b.ndvt), xm1));
     const Mask<T> lb_act = vgt(c.vlb2, k.a_min2);                    // a_lb = -v/dt branch
-    R.Jv = vsel(lb_act, vfma(omsa, -k.inv_dt, Jv), Jv);
-    R.Js = vsel(vge(s, k.eps), vmul(vmul(sAs, c.qr), -kLn2), splat<T>(0.f));
+    R.Jv = vsel(lb_act, vsub(Jv, omsa), Jv);
+    // d a*/d Delta p = sig_a (d a_raw/d s*)(-qr ln2) (log2 units): -dt^2 times it is sAs qr
+    R.Js = vsel(vge(s, k.eps), vmul(sAs, c.qr), splat<T>(0.f));
     // log2 x (x = 0: w = 0 makes w log2 x = 0 with log2 of the smallest normal)
     R.r1 = vfma(c.inter2, -kLn2Sq, c.t1);
     if (GD) {
@@ -339,22 +369,25 @@ __device__ __forceinline__ RecT<T> jac_record(const CoreT<T>& c, T s, T v, const
     return R;
 }
 
-// Reverse step from the stored record: consumes lambda^{t+1} = (ls, lv, lD), returns F_out
-// (this vehicle's term for its LEADER's lambda_v), updates ls, lv (the follower's F_in is added
-// by the caller) and the gradient accumulators.  ls = 0 and beta = 0 for a lane head, so no
-// leader predicates are needed (vl only has to be finite there).
+// Reverse step of the lane adjoint from the stored record, in the scaled variables
+//   u = dt lambda_v (= q of the paper's recursion),  m = -dt lambda_s,  e = dt^2 lambda_D:
+//   lambda_v^t = lambda_v + q J_v + dt lambda_D - dt lambda_s   ->  u' = u + u Jv + e - dt^2 lambda_s
+//   lambda_s^t = lambda_s + q J_s                              ->  m' = m + u Js
+// Consumes (u, m, e) of step t + 1; returns dt F_out (this vehicle's term for its LEADER's u:
+// dt (q d a*/d v_h + dt lambda_s)); updates u, m (the follower's term is added by the caller) and
+// the accumulators (S2, S3, S4 scaled by ln2 dt: unscale_acc).  m = 0 and beta = 0 for a lane
+// head, so no leader predicates are needed (vl only has to be finite there).
 template <bool D4, bool GD = true, class T>
 __device__ __forceinline__ T bwd_from_record(const RecT<T>& R, T v, T vl, const VehPT<T>& p,
-                                             const VehBT<T>& b, const Consts& k, T& ls, T& lv,
-                                             T lD, GradAccT<T>& g) {
-    const T q = vmul(lv, k.dt);
-    const T qa = vmul(q, R.sig_a);
-    const T qb = vmul(q, R.beta);
-    const T dtls = vmul(ls, k.dt);
+                                             const VehAT<T>& b, const Consts& k, T& m, T& u,
+                                             T e, GradAccT<T>& g) {
+    const T qa = vmul(u, R.sig_a);
+    const T qb = vmul(u, R.beta);
     const T qbv = vmul(qb, v);
-    const T F_out = vfma(qbv, b.nc, dtls);                       // q d a*/d v_h + dt lambda_s
-    lv = vsub(vfma(lD, k.dt, vfma(q, R.Jv, lv)), dtls);
-    ls = vfma(q, R.Js, ls);
+    const T ndm = vmul(m, -k.dt);                                // dt^2 lambda_s
+    const T F_out = vfma(qbv, b.ncl, ndm);
+    m = vfma(u, R.Js, m);
+    u = vsub(vadd(vfma(u, R.Jv, u), e), ndm);
     g.S1 = vfma(qa, R.r1, g.S1);
     g.S2 = vfma(qbv, R.dv, g.S2);
     g.S3 = vadd(g.S3, qb);
@@ -362,6 +395,24 @@ __device__ __forceinline__ T bwd_from_record(const RecT<T>& R, T v, T vl, const 
     g.S5 = vfma(qa, R.w, g.S5);
     if (GD) g.S6 = vfma(qa, R.r2, g.S6);
     return F_out;
+}
+
+// Undo the lane adjoint's scaling at the end of a rollout: S2, S3, S4 carry a factor ln2 dt
+// (bwd_from_record), the initial-state gradients come from u = dt lambda_v, m = -dt lambda_s,
+// e = dt^2 lambda_D (m_f: the follower's m, 0 without one):
+//   dL/dv0 = lambda_v,  dL/dp0 = lambda_D - lambda_s + lambda_s(follower)   (gap form)
+template <class T>
+__device__ __forceinline__ void unscale_acc(GradAccT<T>& g, const Consts& k) {
+    const float us = __fmul_rn(kLog2e, k.inv_dt);  // 1 / (ln2 dt)
+    g.S2 = vmul(g.S2, us);
+    g.S3 = vmul(g.S3, us);
+    g.S4 = vmul(g.S4, us);
+}
+template <class T>
+__device__ __forceinline__ T grad_v0(T u, const Consts& k) { return vmul(u, k.inv_dt); }
+template <class T>
+__device__ __forceinline__ T grad_p0(T e, T m, T m_f, const Consts& k) {
+    return vmul(vadd(vmul(e, k.inv_dt), vsub(m, m_f)), k.inv_dt);
 }
 
 // Virtual-leader reverse step: at state v with free leader terms (dp, dv) the

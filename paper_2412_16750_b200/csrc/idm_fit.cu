@@ -49,7 +49,8 @@ __global__ void __launch_bounds__(kFT, 2) fit_kernel(FitArgs a) {
     const bool val[2] = {id0 < n_loc, id0 + 1 < n_loc};
     const float qnan = __int_as_float(0x7fc00000);
 
-    float pj[2] = {0.f, 0.f}, vj[2] = {0.f, 0.f}, sj[2] = {0.f, 0.f}, lf[2] = {0.f, 0.f};
+    const float pinf = __int_as_float(0x7f800000);
+    float pj[2] = {0.f, 0.f}, vj[2] = {0.f, 0.f}, sj[2] = {pinf, pinf};  // no leader: gap +inf
     float x[2][6], m1[2][6], m2[2][6];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
@@ -63,9 +64,7 @@ __global__ void __launch_bounds__(kFT, 2) fit_kernel(FitArgs a) {
         if (val[j]) {
             pj[j] = a.pos0[i];
             vj[j] = a.vel0[i];
-            const bool lead = a.lead[i] != 0;
-            lf[j] = lead ? 1.f : 0.f;
-            sj[j] = lead ? (a.pos0[i + 1] - pj[j]) - a.length[i + 1] : 0.f;
+            if (a.lead[i] != 0) sj[j] = (a.pos0[i + 1] - pj[j]) - a.length[i + 1];
 #pragma unroll
             for (int q = 0; q < 6; ++q) {
                 x[j][q] = a.params[q * N + i];
@@ -77,7 +76,7 @@ __global__ void __launch_bounds__(kFT, 2) fit_kernel(FitArgs a) {
         }
     }
     const float2 p0 = make_float2(pj[0], pj[1]), v0 = make_float2(vj[0], vj[1]);
-    const float2 s0 = make_float2(sj[0], sj[1]), leadf = make_float2(lf[0], lf[1]);
+    const float2 s0 = make_float2(sj[0], sj[1]);
     for (int t = 0; t <= KM; ++t) {  // absent vehicles observe NaN (= missing)
         const float* o = a.obs + (int64_t)min(t, K) * N + i0;
         ob[t * kFT + tid] = make_float2((val[0] && t <= K) ? o[0] : qnan,
@@ -96,8 +95,8 @@ __global__ void __launch_bounds__(kFT, 2) fit_kernel(FitArgs a) {
         const VehPT<float2> P =
             pack(make_vehp(x[0][0], x[0][1], x[0][2], x[0][3], x[0][4], x[0][5]),
                  make_vehp(x[1][0], x[1][1], x[1][2], x[1][3], x[1][4], x[1][5]));
-        const VehBT<float2> B = pack(make_vehb(x[0][0], x[0][1], x[0][4], x[0][5]),
-                                     make_vehb(x[1][0], x[1][1], x[1][4], x[1][5]));
+        const VehAT<float2> B = pack(make_veha(x[0][0], x[0][1], x[0][4], x[0][5], k),
+                                     make_veha(x[1][0], x[1][1], x[1][4], x[1][5], k));
         // ---- forward + Eq. 4 (as fwd_kernel<LOSS>)
         float2 s = s0, v = v0, D = f2(0.f);
         lsum = f2(0.f);
@@ -110,13 +109,14 @@ __global__ void __launch_bounds__(kFT, 2) fit_kernel(FitArgs a) {
                 __syncthreads();
                 const float2 vl = make_float2(v.y, hv[t * (kFT + 1) + tid + 1].x);
                 D = vfma(v, k.dt, D);
-                fwd_step<D4>(s, v, vl, leadf, P, k);
+                fwd_step<D4>(s, v, vl, P, k);
                 gg[(t + 1) * kFT + tid] =
                     loss_term<KIND>(ob[(t + 1) * kFT + tid], vadd(p0, D), lsum);
             }
         }
         // ---- reverse sweep (as bwd_kernel: local Jacobian of each step, then the update)
-        float2 ls = f2(0.f), lv = f2(0.f), lD = gg[K * kFT + tid];  // lambda_D^K = dL/dP(K)
+        // scaled adjoint as bwd_kernel: u = dt lambda_v, m = -dt lambda_s, e = dt^2 lambda_D
+        float2 m = f2(0.f), u = f2(0.f), e = vmul(gg[K * kFT + tid], k.dt2);  // lambda_D^K = dL/dP(K)
         GradAccT<float2> G = {f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
 #pragma unroll
         for (int t = KM - 1; t >= 0; --t) {
@@ -125,17 +125,18 @@ __global__ void __launch_bounds__(kFT, 2) fit_kernel(FitArgs a) {
                 const float2 vl = make_float2(vv.y, hv[t * (kFT + 1) + tid + 1].x);
                 const float2 sv = sg[t * kFT + tid];
                 CoreT<float2> c;
-                core<D4>(sv, vv, vl, leadf, P, k, c);
+                core<D4>(sv, vv, vl, P, k, c);
                 const RecT<float2> R = jac_record<D4, !D4>(c, sv, vv, P, B, k);
-                const float2 F = bwd_from_record<D4, !D4>(R, vv, vl, P, B, k, ls, lv, lD, G);
+                const float2 F = bwd_from_record<D4, !D4>(R, vv, vl, P, B, k, m, u, e, G);
                 fx[par][tid + 1] = F.y;  // vehicle 2t + 1 -> its leader 2t + 2 (thread t + 1)
                 __syncthreads();
-                lv = vadd(lv, make_float2(fx[par][tid], F.x));
-                lD = vadd(lD, gg[t * kFT + tid]);
+                u = vadd(u, make_float2(fx[par][tid], F.x));
+                e = vfma(gg[t * kFT + tid], k.dt2, e);
                 par ^= 1;
             }
         }
         // ---- gradients (as bwd_kernel's epilogue) + Adam (as adam_update)
+        unscale_acc(G, k);
         const float Sj[6][2] = {{G.S1.x, G.S1.y}, {G.S2.x, G.S2.y}, {G.S3.x, G.S3.y},
                                 {G.S4.x, G.S4.y}, {G.S5.x, G.S5.y}, {G.S6.x, G.S6.y}};
         const float step_size = a.adam_table[2 * it], sqrt_bc2 = a.adam_table[2 * it + 1];
@@ -155,11 +156,11 @@ __global__ void __launch_bounds__(kFT, 2) fit_kernel(FitArgs a) {
             }
         }
         if (it + 1 == a.iters) {
-            const float2 lsl = vmul(ls, leadf);
-            fx[par][tid + 1] = lsl.y;
+            fx[par][tid + 1] = m.y;
             __syncthreads();
-            const float2 gp0 = vadd(vsub(lD, lsl), make_float2(fx[par][tid], lsl.x));
-            const float gpj[2] = {gp0.x, gp0.y}, lvj[2] = {lv.x, lv.y};
+            const float2 gp0 = grad_p0(e, m, make_float2(fx[par][tid], m.x), k);
+            const float2 gv0 = grad_v0(u, k);
+            const float gpj[2] = {gp0.x, gp0.y}, lvj[2] = {gv0.x, gv0.y};
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 if (!val[j]) continue;

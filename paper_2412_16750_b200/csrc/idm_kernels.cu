@@ -159,8 +159,8 @@ __device__ __forceinline__ void cp_async_wait() {
 // One CTA = one lane tile; thread t owns the adjacent local vehicles 2t, 2t + 1 as one float2
 // lane pair (packed f32x2 arithmetic).  Vehicle 2t's leader is 2t + 1 (same thread); vehicle
 // 2t + 1's leader is 2t + 2, thread t + 1's first vehicle, so one speed per thread crosses shared
-// memory per step (one __syncthreads, double-buffered).  A lane head has leadf = 0, which zeroes
-// its interaction term whatever "leader" speed it reads.
+// memory per step (one __syncthreads, double-buffered).  A lane head carries the gap +inf, which
+// zeroes its interaction term whatever "leader" speed it reads.
 // All `steps` steps run in one launch, in segments of KS steps (compile-time, fully unrolled;
 // the K mod KS tail runs as one predicated segment).  LOSS = 0: record P (idm_forward).
 // LOSS = 1 (L1) / 2 (L2): fused Eq. 4 for idm_fit_step -- observation rows staged two segments
@@ -188,19 +188,18 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     const int64_t i0 = base + id0;
     const bool val[2] = {id0 < n_loc, id0 + 1 < n_loc};
 
-    float sj[2], vj[2], pj[2], lf[2];
+    const float pinf = __int_as_float(0x7f800000);
+    float sj[2], vj[2], pj[2];
     VehP Pj[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
         const int64_t i = i0 + j;
         RawP r = dummy_raw();
-        sj[j] = 0.f; vj[j] = 0.f; pj[j] = 0.f; lf[j] = 0.f;
+        sj[j] = pinf; vj[j] = 0.f; pj[j] = 0.f;  // no leader: gap +inf (see core_dv)
         if (val[j]) {
             pj[j] = a.pos0[i];
             vj[j] = a.vel0[i];
-            const bool lead = a.lead[i] != 0;
-            lf[j] = lead ? 1.f : 0.f;
-            sj[j] = lead ? (a.pos0[i + 1] - pj[j]) - a.length[i + 1] : 0.f;
+            if (a.lead[i] != 0) sj[j] = (a.pos0[i + 1] - pj[j]) - a.length[i + 1];
             r = load_raw(a.params, a.n_par, i);
             if (D4 && r.delta != 4.f)
                 atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
@@ -208,7 +207,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
         Pj[j] = make_vehp(r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta);
     }
     float2 s = make_float2(sj[0], sj[1]), v = make_float2(vj[0], vj[1]);
-    const float2 p0 = make_float2(pj[0], pj[1]), leadf = make_float2(lf[0], lf[1]);
+    const float2 p0 = make_float2(pj[0], pj[1]);
     const VehPT<float2> P = pack(Pj[0], Pj[1]);
     float2 D = f2(0.f), cmp = f2(0.f);
     if (tid == 0) { xv[0][kT] = 0.f; xv[1][kT] = 0.f; }
@@ -330,7 +329,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
         } else {
             D = vfma(v, k.dt, D);
         }
-        fwd_step<D4>(s, v, vl, leadf, P, k);
+        fwd_step<D4>(s, v, vl, P, k);
         if (!LOSS) orow += N;
         if (RECV) vrow += N;
         vtp += kR2;
@@ -343,9 +342,9 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     // first checkpoint step at which each vehicle's state was non-finite (INT_MAX: none); kept
     // in registers and reported once at the end, no branch or atomic per checkpoint
     int bad0 = INT_MAX, bad1 = INT_MAX;
-    auto finite2 = [&](int t0) {
-        const bool ok0 = isfinite(s.x) && isfinite(v.x) && isfinite(D.x);
-        const bool ok1 = isfinite(s.y) && isfinite(v.y) && isfinite(D.y);
+    auto finite2 = [&](int t0) {  // gap: +inf is the no-leader value, only NaN is an error
+        const bool ok0 = !isnan(s.x) && isfinite(v.x) && isfinite(D.x);
+        const bool ok1 = !isnan(s.y) && isfinite(v.y) && isfinite(D.y);
         bad0 = (!ok0 && bad0 == INT_MAX) ? t0 : bad0;
         bad1 = (!ok1 && bad1 == INT_MAX) ? t0 : bad1;
     };
@@ -434,18 +433,16 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
     const int nseg = (steps + KS - 1) / KS;
     const int tail = steps - (nseg - 1) * KS;  // length of the last segment (1..KS)
 
-    float lf[2], ldj[2], pj[2];
+    float ldj[2], pj[2];
     VehP Pj[2];
-    VehB Bj[2];
+    VehA Aj[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
         const int64_t i = i0 + j;
         RawP r = dummy_raw();
-        lf[j] = 0.f;
         ldj[j] = 0.f;
         pj[j] = 0.f;
         if (val[j]) {
-            lf[j] = a.lead[i] != 0 ? 1.f : 0.f;
             r = load_raw(a.params, a.n_par, i);
             if (D4 && r.delta != 4.f)
                 atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
@@ -453,14 +450,14 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
             if (GOBS == 2) pj[j] = a.pos0[i];
         }
         Pj[j] = make_vehp(r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta);
-        Bj[j] = make_vehb(r.a_max, r.a_pref, r.v_targ, r.delta);
+        Aj[j] = make_veha(r.a_max, r.a_pref, r.v_targ, r.delta, k);
     }
-    const float2 leadf = make_float2(lf[0], lf[1]);
     const float2 p0 = make_float2(pj[0], pj[1]);
     const VehPT<float2> P = pack(Pj[0], Pj[1]);
-    const VehBT<float2> B = pack(Bj[0], Bj[1]);
-    float2 lD = make_float2(ldj[0], ldj[1]);
-    float2 ls = f2(0.f), lv = f2(0.f);
+    const VehAT<float2> B = pack(Aj[0], Aj[1]);
+    // scaled adjoint (bwd_from_record): u = dt lambda_v, m = -dt lambda_s, e = dt^2 lambda_D
+    float2 e = vmul(make_float2(ldj[0], ldj[1]), k.dt2);
+    float2 m = f2(0.f), u = f2(0.f);
     GradAccT<float2> G = {f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
     if (tid == 0) { fx[0][0] = 0.f; fx[1][0] = 0.f; }  // never written again (slots t+1 >= 1)
 
@@ -608,7 +605,7 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
         if (GOBS && seg == nseg - 1) {  // lambda_D^K = dL/dP(K) (static selects, no indexing)
 #pragma unroll
             for (int tt = 0; tt < KO; ++tt)
-                if (tt == len) lD = g[tt];
+                if (tt == len) e = vmul(g[tt], k.dt2);
         }
         if (seg > 1) fetch(seg - 2, KS);
         // reverse sweep t = t0 + len - 1 ... t0; the local Jacobian of the next step down is
@@ -617,14 +614,14 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
         for (int tt = KS - 1; tt >= 0; --tt) {
             if (kFull || tt < len) {  // CTA-uniform
                 CoreT<float2> c;
-                core<D4>(sg[tt], v[tt], vl[tt], leadf, P, k, c);
+                core<D4>(sg[tt], v[tt], vl[tt], P, k, c);
                 const RecT<float2> R = jac_record<D4, GD>(c, sg[tt], v[tt], P, B, k);
-                const float2 F = bwd_from_record<D4, GD>(R, v[tt], vl[tt], P, B, k, ls, lv, lD, G);
+                const float2 F = bwd_from_record<D4, GD>(R, v[tt], vl[tt], P, B, k, m, u, e, G);
                 fx[par][tid + 1] = F.y;  // vehicle 2t + 1 -> its leader 2t + 2 (thread t + 1)
                 __syncthreads();
                 // F from the follower: 2t - 1 (thread t - 1) for 2t, 2t (this thread) for 2t + 1
-                lv = vadd(lv, make_float2(fx[par][tid], F.x));
-                lD = vadd(lD, g[tt]);  // lambda_D^t = g^t + lambda_D^{t+1}
+                u = vadd(u, make_float2(fx[par][tid], F.x));
+                e = vfma(g[tt], k.dt2, e);  // lambda_D^t = g^t + lambda_D^{t+1}
                 par ^= 1;
             }
         }
@@ -632,16 +629,17 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
     int seg = nseg - 1;
     if (tail < KS) segment(seg--, tail, std::false_type{});
     for (; seg >= 0; --seg) segment(seg, KS, std::true_type{});
-    // dL/dp0_i = lambda_D - lambda_s_i + lambda_s_{follower}; dL/dv0 = lambda_v
-    const float2 lsl = vmul(ls, leadf);
-    fx[par][tid + 1] = lsl.y;
+    // dL/dp0_i = lambda_D - lambda_s_i + lambda_s_{follower}; dL/dv0 = lambda_v (unscaled)
+    fx[par][tid + 1] = m.y;
     __syncthreads();
-    const float2 gp0 = vadd(vsub(lD, lsl), make_float2(fx[par][tid], lsl.x));
+    const float2 gp0 = grad_p0(e, m, make_float2(fx[par][tid], m.x), k);
+    const float2 gv0 = grad_v0(u, k);
 
     // parameter gradients from the factored accumulators
+    unscale_acc(G, k);
     const float Sj[6][2] = {{G.S1.x, G.S1.y}, {G.S2.x, G.S2.y}, {G.S3.x, G.S3.y},
                             {G.S4.x, G.S4.y}, {G.S5.x, G.S5.y}, {G.S6.x, G.S6.y}};
-    const float lvj[2] = {lv.x, lv.y}, gpj[2] = {gp0.x, gp0.y};
+    const float lvj[2] = {gv0.x, gv0.y}, gpj[2] = {gp0.x, gp0.y};
     float gr[kVpt][6];
 #pragma unroll
     for (int j = 0; j < kVpt; ++j) {

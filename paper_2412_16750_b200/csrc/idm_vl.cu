@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(kVT) vl_fwd_kernel(VlArgs a) {
                 if (vrow) vrow += N;
                 D = vfma(v, k.dt, D);
                 CoreT<float2> c;
-                core_dv<D4>(dp[tt], v, dv[tt], f2(1.f), P, k, c);
+                core_dv<D4>(dp[tt], v, dv[tt], P, k, c);
                 float2 sdummy = f2(0.f);
                 advance(c, sdummy, v, k);
                 const float2 Pv = vadd(p0, D);
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kVT, 2) vl_bwd_kernel(VlArgs a) {
         for (int tt = 0; tt + 1 < KS; ++tt) {
             if (tt + 1 < len) {
                 CoreT<float2> c;
-                core_dv<D4>(dp[tt], vt[tt], dv[tt], f2(1.f), P, k, c);
+                core_dv<D4>(dp[tt], vt[tt], dv[tt], P, k, c);
                 float2 sdummy = f2(0.f), vn = vt[tt];
                 advance(c, sdummy, vn, k);
                 vt[tt + 1] = vn;
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(kVT, 2) vl_bwd_kernel(VlArgs a) {
             if (tt < len) {
                 const int64_t off = (int64_t)(t0 + tt) * N + i0;
                 CoreT<float2> c;
-                core_dv<D4>(dp[tt], vt[tt], dv[tt], f2(1.f), P, k, c);
+                core_dv<D4>(dp[tt], vt[tt], dv[tt], P, k, c);
                 float2 gdp, gdv;
                 bwd_vl<D4>(c, dp[tt], vt[tt], P, B, k, lv, lD, G, gdp, gdv);
                 lD = vadd(lD, gr[tt]);  // lambda_P^t = g^t + lambda_P^{t+1}
