@@ -41,8 +41,10 @@ ALG_INSTR = {"fwd": 36.0, "bwd": 114.0}  # SURVEY.md 8(d) frozen essential-op co
 # counts over-credit a packed kernel, so both fractions are reported.
 # "bwd_fit": the optimizer-path backward with delta frozen at 4 (the paper's five parameters,
 # PAPER.md:208), which does not compute dL/d delta (one log2, one max, one multiply, one FMA per
-# vehicle-step fewer: 3 slots per vehicle-step; R#1).
-PACKED_INSTR = {"fwd": 21.0, "bwd": 45.5, "bwd_fit": 42.5}
+# vehicle-step fewer: 3 slots per vehicle-step; R#1).  The counts are after the
+# constant folding of DESIGN.md "Adjoint scaling" (lane heads at gap +inf: -0.5 slot per
+# vehicle-step forward and backward; dt and ln2 in per-vehicle constants: -1 backward).
+PACKED_INSTR = {"fwd": 20.5, "bwd": 44.0, "bwd_fit": 41.0}
 ISSUE_PER_CLK = 148 * 4 * 32  # SMs x schedulers x lanes (thread-instr / clk)
 
 
