@@ -27,6 +27,8 @@ struct idm_handle {
     double *loss_partials, *loss_scalar, *shared_partials;
     unsigned long long* status;
     unsigned* flags;  // [0] = some delta != 4 (set by the validation kernel)
+    unsigned* tile_ready;  // [ntiles] forward -> backward handoff epochs of idm_fit_step (PDL)
+    unsigned epoch;        // last epoch used
     float* adam_table;  // [kFitMaxIters][2] per-iteration Adam step sizes for idm_fit
     float* adam_table_host;  // pinned staging of the above
     bool delta4;      // all delta == 4 and delta frozen => specialised kernels
@@ -76,7 +78,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
     size_t tile_start, lead, vt, ckt, sgn, ckpt_v, loss_partials, loss_scalar, shared_partials,
-        status, flags, adam_table, total;
+        status, flags, adam_table, tile_ready, total;
     int64_t vt_stride, ck_stride, sg_stride;  // elements per tile
 };
 
@@ -170,6 +172,7 @@ bool layout_for(const idm_desc* d, int64_t ntiles, Layout* L) {
     L->status = off; off += align256(sizeof(unsigned long long));
     L->flags = off; off += align256(sizeof(unsigned));
     L->adam_table = off; off += align256(sizeof(float) * 2 * kFitMaxIters);
+    L->tile_ready = off; off += align256(sizeof(unsigned) * (size_t)mt);  // fused-step handoff
     L->total = off;
     return true;
 }
@@ -247,6 +250,17 @@ int fused_chunks(const idm_handle* h) {
     }();
     int c = env < 1 ? 1 : (env > 16 ? 16 : env);
     return c > h->ntiles ? h->ntiles : c;
+}
+
+// Backward of idm_fit_step as a programmatic dependent launch of the forward (per-tile handoff,
+// idm_kernels.cu "tile handoff"); IDM_PDL=0 turns it off.  Not with tile chunks (the backward runs
+// on the second stream there) nor under launch timing (events between the two kernels).
+bool use_pdl(const idm_handle* h, int nch) {
+    static const bool env = [] {
+        const char* e = std::getenv("IDM_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return env && nch == 1 && !h->timing;
 }
 
 int sync_status(idm_handle* h) {
@@ -451,6 +465,8 @@ int idm_init(idm_handle** out, const idm_desc* d) {
         h->status = (unsigned long long*)(ws + L.status);
         h->flags = (unsigned*)(ws + L.flags);
         h->adam_table = (float*)(ws + L.adam_table);
+        h->tile_ready = (unsigned*)(ws + L.tile_ready);
+        h->epoch = 0;
 
         h->nck = (int)((d->max_steps + d->ckpt_every - 1) / d->ckpt_every);
 
@@ -465,6 +481,10 @@ int idm_init(idm_handle** out, const idm_desc* d) {
         if (ce == cudaSuccess) { what = "memset status"; ce = cudaMemsetAsync(h->status, 0xff, 8, h->st); }
         if (ce == cudaSuccess) { what = "memset loss"; ce = cudaMemsetAsync(h->loss_scalar, 0, 8, h->st); }
         if (ce == cudaSuccess) { what = "memset flags"; ce = cudaMemsetAsync(h->flags, 0, 4, h->st); }
+        if (ce == cudaSuccess) {
+            what = "memset tile handoff";
+            ce = cudaMemsetAsync(h->tile_ready, 0, sizeof(unsigned) * (size_t)nt, h->st);
+        }
         if (ce == cudaSuccess) { what = "smem attributes"; ce = kernels_configure(d->ckpt_every); }
         if (ce == cudaSuccess) {
             what = "copy stream";
@@ -835,6 +855,13 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
     // arithmetic on the same tiles, so the results do not depend on the chunking.
     const int nch = fused_chunks(h);
     cudaStream_t sb = nch > 1 ? h->st2 : h->st;
+    const bool pdl = use_pdl(h, nch);
+    if (pdl) {
+        f.tile_ready = h->tile_ready;
+        b.tile_ready = h->tile_ready;
+        if (++h->epoch == 0) h->epoch = 1;  // 0 = never signalled
+        f.epoch = b.epoch = h->epoch;
+    }
     if (nch > 1) {
         CK(h, cudaEventRecord(h->ev_fork, h->st));
         CK(h, cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
@@ -855,7 +882,7 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
         }
         {
             TimedLaunch tl(h, IDM_K_BWD, sb);
-            CK(h, launch_bwd(b, t1 - t0, h->delta4, shared, !shared, 1 + kind, var.kahan, sb));
+            CK(h, launch_bwd(b, t1 - t0, h->delta4, shared, !shared, 1 + kind, var.kahan, sb, pdl));
         }
         h->launches += 2;
     }

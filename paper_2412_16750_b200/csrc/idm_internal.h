@@ -60,6 +60,10 @@ struct FwdArgs {
     const float* obs;
     int kind;
     double* loss_partials;  // [ntiles]
+    // programmatic dependent launch of the fused backward (nullable): tile_ready[tile] = epoch
+    // (release) once the tile's history is written
+    unsigned* tile_ready;
+    unsigned epoch;
 };
 
 struct AdamArgs {
@@ -89,6 +93,10 @@ struct BwdArgs {
     Consts k;
     unsigned long long* status;
     AdamArgs adam;  // fused Adam epilogue (ADAM variant)
+    // launched as a programmatic dependent of the forward (nullable): wait (acquire) for
+    // tile_ready[tile] == epoch before reading the tile's history
+    const unsigned* tile_ready;
+    unsigned epoch;
 };
 
 // virtual-leader mode (idm_vl.cu)
@@ -141,8 +149,10 @@ cudaError_t launch_fwd(const FwdArgs& a, int ntiles, const FwdVariant& var, cuda
 cudaError_t kernels_configure(int ckpt_every);
 // gobs = 0: dL/dP from grad_traj; 1: L1 from the forward's sign words; 2: L2 re-derived from obs
 // and the rebuilt positions (gobs != 0: fused idm_fit_step, ckpt_every == 4)
+// pdl: launch as a programmatic dependent of the preceding kernel in the stream (the forward of
+// the same tiles, which signals a.tile_ready)
 cudaError_t launch_bwd(const BwdArgs& a, int ntiles, bool delta4, bool shared, bool adam,
-                       int gobs, bool kahan, cudaStream_t st);
+                       int gobs, bool kahan, cudaStream_t st, bool pdl = false);
 bool ckpt_supported(int k);
 cudaError_t launch_loss(const LossArgs& a, int nblocks, cudaStream_t st);
 cudaError_t launch_reduce(const double* partials, int64_t n, int width, double* out, float* out_f,

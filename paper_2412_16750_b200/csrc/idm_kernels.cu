@@ -96,6 +96,30 @@ __device__ __forceinline__ void block_sum_to(double x, double* out) {
     }
 }
 
+// ------------------------------------------------------------------------------ tile handoff
+// The fused backward may start while the forward's last wave drains (programmatic dependent
+// launch, launch_bwd(pdl)): forward CTA j releases tile_ready[j] = epoch after its last global
+// store, backward CTA j acquires it before its first read of the tile's history.  The forward
+// allows the dependent launch at its start, so the backward grid launches only once every forward
+// CTA is resident or done: a waiting backward CTA never blocks the forward it waits for.
+__device__ __forceinline__ void tile_release(unsigned* flag, unsigned epoch) {
+    __threadfence();  // every thread's history stores, at gpu scope
+    __syncthreads();
+    if (threadIdx.x == 0)
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
+}
+__device__ __forceinline__ void tile_acquire(const unsigned* flag, unsigned epoch) {
+    unsigned v;
+    for (long long spins = 0;; ++spins) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if (v == epoch) break;
+        if (spins > (1ll << 24)) __trap();  // a broken handoff fails the launch, never hangs
+        __nanosleep(64);
+    }
+    // order the acquire before the bulk copies (async proxy) that read the history
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // ------------------------------------------------------------------------------ async copies
 // 1-D bulk copies (global -> shared, completion counted on an mbarrier in bytes): the
 // tile-local rows are 16-byte aligned and contiguous, so one elected thread moves a whole
@@ -187,6 +211,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     const int id0 = 2 * tid;
     const int64_t i0 = base + id0;
     const bool val[2] = {id0 < n_loc, id0 + 1 < n_loc};
+    if (LOSS && a.tile_ready) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     const float pinf = __int_as_float(0x7f800000);
     float sj[2], vj[2], pj[2];
@@ -395,6 +420,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
         put(a.state_out + N + i0, v);
     }
     if (LOSS) block_sum_to(lacc + (double)lseg.x + (double)lseg.y, a.loss_partials + tile);
+    if (LOSS && a.tile_ready) tile_release(a.tile_ready + tile, a.epoch);
 }
 
 // ------------------------------------------------------------------------------ NK3
@@ -489,6 +515,8 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
 #pragma unroll
         for (int q = 0; q < NB; ++q) mbar_init(&mbar[q], 1);
         mbar_fence_init();
+        // fused step after a programmatic launch: the tile's history is complete
+        if (GOBS && a.tile_ready) tile_acquire(a.tile_ready + tile, a.epoch);
     }
     if (tid < NB * KS) vrow[tid * VP + kCap] = 0.f;
     __syncthreads();
@@ -852,7 +880,8 @@ constexpr size_t bwd_smem_of() {  // ring of 3: speed + checkpoint + dL/dP/obs (
 }
 
 template <bool D4, bool SH, bool AD, int KS, int GO, bool KH>
-static void launch_bwd_v(const BwdArgs& a, int ntiles, cudaStream_t st) {
+static cudaError_t launch_bwd_v(const BwdArgs& a, int ntiles, cudaStream_t st,
+                                bool pdl = false) {
     constexpr size_t smem = bwd_smem_of<KS, GO>();
     static bool configured = false;  // one opt-in per instantiation (one device per process)
     if (!configured) {
@@ -860,49 +889,62 @@ static void launch_bwd_v(const BwdArgs& a, int ntiles, cudaStream_t st) {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
-    bwd_kernel<D4, SH, AD, KS, GO, KH><<<ntiles, kT, smem, st>>>(a);
+    if (!pdl) {
+        bwd_kernel<D4, SH, AD, KS, GO, KH><<<ntiles, kT, smem, st>>>(a);
+        return cudaSuccess;  // launch errors: cudaGetLastError in launch_bwd
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ntiles);
+    cfg.blockDim = dim3(kT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, bwd_kernel<D4, SH, AD, KS, GO, KH>, a);
 }
 
+// API backward (idm_backward): dL/dP rows from grad_traj, Adam by its own kernel
 template <bool D4, int KS>
-static void launch_bwd_k(const BwdArgs& a, int ntiles, bool shared, bool adam, cudaStream_t st) {
+static void launch_bwd_k(const BwdArgs& a, int ntiles, bool shared, cudaStream_t st) {
     if (shared) launch_bwd_v<D4, true, false, KS, 0, false>(a, ntiles, st);
-    else if (adam) launch_bwd_v<D4, false, true, KS, 0, false>(a, ntiles, st);
     else launch_bwd_v<D4, false, false, KS, 0, false>(a, ntiles, st);
 }
 
 // fused idm_fit_step backward (ckpt_every == 4): dL/dP from obs
 template <bool D4, int GO, bool KH>
-static void launch_bwd_obs(const BwdArgs& a, int ntiles, bool shared, cudaStream_t st) {
-    if (shared) launch_bwd_v<D4, true, false, 4, GO, KH>(a, ntiles, st);
-    else launch_bwd_v<D4, false, true, 4, GO, KH>(a, ntiles, st);
+static cudaError_t launch_bwd_obs(const BwdArgs& a, int ntiles, bool shared, cudaStream_t st,
+                                  bool pdl) {
+    if (shared) return launch_bwd_v<D4, true, false, 4, GO, KH>(a, ntiles, st, pdl);
+    return launch_bwd_v<D4, false, true, 4, GO, KH>(a, ntiles, st, pdl);
 }
 
 template <bool D4>
 static cudaError_t launch_bwd_d(const BwdArgs& a, int ntiles, bool shared, bool adam, int gobs,
-                                bool kahan, cudaStream_t st) {
+                                bool kahan, cudaStream_t st, bool pdl) {
     if (gobs) {
         if (a.ckpt_every != 4) return cudaErrorInvalidValue;
-        if (gobs == 1) {  // sign words: no positions needed, compensation irrelevant
-            launch_bwd_obs<D4, 1, false>(a, ntiles, shared, st);
-        } else {
-            if (kahan) launch_bwd_obs<D4, 2, true>(a, ntiles, shared, st);
-            else launch_bwd_obs<D4, 2, false>(a, ntiles, shared, st);
-        }
-        return cudaSuccess;
+        if (gobs == 1)  // sign codes: no positions needed, compensation irrelevant
+            return launch_bwd_obs<D4, 1, false>(a, ntiles, shared, st, pdl);
+        if (kahan) return launch_bwd_obs<D4, 2, true>(a, ntiles, shared, st, pdl);
+        return launch_bwd_obs<D4, 2, false>(a, ntiles, shared, st, pdl);
     }
+    if (pdl || adam) return cudaErrorInvalidValue;  // API backward: after the loss kernel, no Adam
     switch (a.ckpt_every) {
-        case 2: launch_bwd_k<D4, 2>(a, ntiles, shared, adam, st); break;
-        case 4: launch_bwd_k<D4, 4>(a, ntiles, shared, adam, st); break;
-        case 8: launch_bwd_k<D4, 8>(a, ntiles, shared, adam, st); break;
+        case 2: launch_bwd_k<D4, 2>(a, ntiles, shared, st); break;
+        case 4: launch_bwd_k<D4, 4>(a, ntiles, shared, st); break;
+        case 8: launch_bwd_k<D4, 8>(a, ntiles, shared, st); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaSuccess;
 }
 
 cudaError_t launch_bwd(const BwdArgs& a, int ntiles, bool delta4, bool shared, bool adam,
-                       int gobs, bool kahan, cudaStream_t st) {
-    cudaError_t e = delta4 ? launch_bwd_d<true>(a, ntiles, shared, adam, gobs, kahan, st)
-                           : launch_bwd_d<false>(a, ntiles, shared, adam, gobs, kahan, st);
+                       int gobs, bool kahan, cudaStream_t st, bool pdl) {
+    cudaError_t e = delta4 ? launch_bwd_d<true>(a, ntiles, shared, adam, gobs, kahan, st, pdl)
+                           : launch_bwd_d<false>(a, ntiles, shared, adam, gobs, kahan, st, pdl);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
