@@ -41,6 +41,18 @@ def main(rep):
         rd *= scale[u[h.index("dram__bytes_read.sum")]]
         wr *= scale[u[h.index("dram__bytes_write.sum")]]
         print(f"  traffic (dram read + write) bytes/launch            {rd + wr:20.4e}")
+        stalls = []
+        for i, k in enumerate(h):
+            if k.startswith("smsp__average_warps_issue_stalled_") and \
+                    k.endswith("_per_issue_active.ratio"):
+                try:
+                    stalls.append((float(vals[i].replace(",", "")), k[34:-23]))
+                except ValueError:
+                    pass
+        print("  warp stall reasons (warps per issue-active cycle, >= 0.05):")
+        for v, k in sorted(stalls, reverse=True):
+            if v >= 0.05:
+                print(f"    {k:28s} {v:6.3f}")
     # stall reasons: top SASS lines by warp-stall samples
     src = list(csv.reader(io.StringIO(ncu(rep, "--page", "source", "--csv", "--print-source",
                                           "sass"))))

@@ -766,6 +766,52 @@ def test_fit_step_short_horizons(idm, K):
             assert torch.equal(a.params, b.params)
 
 
+def _ragged_aligned_lanes():
+    """Lane sizes with N % 4 == 0 whose tile plan starts and ends tiles at every residue mod 4
+    (searched over seeds; the planner is the library's own host call)."""
+    for seed in range(200):
+        rng = np.random.default_rng(seed)
+        lanes = [int(x) for x in rng.integers(1, 300, size=24)]
+        lanes[-1] += (4 - sum(lanes) % 4) % 4
+        off = np.concatenate([[0], np.cumsum(lanes)]).astype(np.int32)
+        ts = idm_mod().idm_plan_tiles(off)
+        if {int(t) % 4 for t in ts[:-1]} >= {1, 2, 3} and {int(t) % 4 for t in ts[1:]} >= {1, 2, 3}:
+            return lanes
+    raise AssertionError("no lane set found")
+
+
+def idm_mod():
+    from paper_2412_16750_b200 import idm as m
+    return m
+
+
+@pytest.mark.parametrize("K", [13, 40])
+def test_fit_step_aligned_n_ragged_tiles(idm, K):
+    """N % 4 == 0 with tile starts and ends at every residue mod 4 (the alignment cases of any
+    row-staging scheme for the observation rows): the fused iteration equals the separate calls
+    bit for bit, with missing observations and a partial last segment."""
+    lanes = _ragged_aligned_lanes()
+    w = synth.make_workload("C2", lane_sizes=lanes, K=K, seed=7)
+    assert w.n % 4 == 0
+    obs = synth.kinematic_obs(w)
+    obs[np.random.default_rng(K).random(obs.shape) < 0.2] = np.nan
+    o = torch.as_tensor(obs, device="cuda")
+    for kind in ("l1", "l2"):
+        a = idm.from_workload(w, None, max_steps=w.K)
+        b = idm.from_workload(w, None, max_steps=w.K)
+        for it in range(2):
+            a.forward(w.K)
+            La = a.loss_grad(o, kind=kind)
+            a.backward()
+            a.adam_step(it)
+            Lb = b.fit_step(o, kind=kind, iteration=it, sync=True)
+            torch.cuda.synchronize()
+            assert abs(La - Lb) <= 1e-6 * abs(La)
+            assert_fit_grads(a.grad_params, b.grad_params)
+            assert torch.equal(a.grad_state0, b.grad_state0)
+            assert torch.equal(a.params, b.params)
+
+
 def test_empty_and_malformed_inputs(idm):
     with pytest.raises(idm.IdmError):  # N = 0
         idm.IdmSim(np.array([0], np.int32), np.zeros(0), np.zeros(0), np.zeros(0),
