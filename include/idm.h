@@ -161,11 +161,12 @@ int idm_adam_step(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, f
    backward -> adam_step(iter, ...) (same arithmetic; grad_params, grad_state0, Adam moments and
    parameters bit for bit -- except grad_params row 5, dL/d delta, which is written as 0 when
    delta is frozen (opt_mask bit 5 clear): the optimizer never reads it, and the delta = 4
-   kernels skip the per-step log2 it needs), in three launches when ckpt_every == 4: the forward kernel sums
-   Eq. 4 against each fresh position row (writing only the internal state history), a
-   fixed-order reduction of the loss, and the backward kernel, which re-derives dL/dP from obs
-   and the rebuilt positions and whose epilogue applies Adam + box clamp per vehicle (shared
-   mode: + reduce + Adam launches).  traj and grad_traj are NOT written on this path; with any
+   kernels skip the per-step log2 it needs), in two launches when ckpt_every == 4: the forward
+   kernel sums Eq. 4 against each fresh position row (writing only the internal state history;
+   its last CTA sums the per-tile losses in a fixed order), and the backward kernel -- launched
+   as a programmatic dependent of the forward, each CTA waiting for its own tile's history --
+   re-derives dL/dP from obs and the rebuilt positions and applies Adam + box clamp per vehicle
+   in its epilogue (shared mode: + reduce + Adam launches).  traj and grad_traj are NOT written on this path; with any
    other ckpt_every the defining sequence runs as is (and writes them).
    obs: device [(steps+1)][N]; missing observations are NaN (mask must be NULL).  Loss to
    *loss_dev / *loss_host as in idm_loss_grad. */

@@ -29,6 +29,7 @@ struct idm_handle {
     unsigned* flags;  // [0] = some delta != 4 (set by the validation kernel)
     unsigned* tile_ready;  // [ntiles] forward -> backward handoff epochs of idm_fit_step (PDL)
     unsigned epoch;        // last epoch used
+    unsigned* done_count;  // fused backward's finished-tile ticket (0 between launches)
     float* adam_table;  // [kFitMaxIters][2] per-iteration Adam step sizes for idm_fit
     float* adam_table_host;  // pinned staging of the above
     bool delta4;      // all delta == 4 and delta frozen => specialised kernels
@@ -78,7 +79,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
     size_t tile_start, lead, vt, ckt, sgn, ckpt_v, loss_partials, loss_scalar, shared_partials,
-        status, flags, adam_table, tile_ready, total;
+        status, flags, adam_table, tile_ready, done_count, total;
     int64_t vt_stride, ck_stride, sg_stride;  // elements per tile
 };
 
@@ -173,6 +174,7 @@ bool layout_for(const idm_desc* d, int64_t ntiles, Layout* L) {
     L->flags = off; off += align256(sizeof(unsigned));
     L->adam_table = off; off += align256(sizeof(float) * 2 * kFitMaxIters);
     L->tile_ready = off; off += align256(sizeof(unsigned) * (size_t)mt);  // fused-step handoff
+    L->done_count = off; off += align256(sizeof(unsigned));  // fused-step last-CTA ticket
     L->total = off;
     return true;
 }
@@ -466,6 +468,7 @@ int idm_init(idm_handle** out, const idm_desc* d) {
         h->flags = (unsigned*)(ws + L.flags);
         h->adam_table = (float*)(ws + L.adam_table);
         h->tile_ready = (unsigned*)(ws + L.tile_ready);
+        h->done_count = (unsigned*)(ws + L.done_count);
         h->epoch = 0;
 
         h->nck = (int)((d->max_steps + d->ckpt_every - 1) / d->ckpt_every);
@@ -484,6 +487,10 @@ int idm_init(idm_handle** out, const idm_desc* d) {
         if (ce == cudaSuccess) {
             what = "memset tile handoff";
             ce = cudaMemsetAsync(h->tile_ready, 0, sizeof(unsigned) * (size_t)nt, h->st);
+        }
+        if (ce == cudaSuccess) {
+            what = "memset ticket";
+            ce = cudaMemsetAsync(h->done_count, 0, sizeof(unsigned), h->st);
         }
         if (ce == cudaSuccess) { what = "smem attributes"; ce = kernels_configure(d->ckpt_every); }
         if (ce == cudaSuccess) {
@@ -856,6 +863,10 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
     const int nch = fused_chunks(h);
     cudaStream_t sb = nch > 1 ? h->st2 : h->st;
     const bool pdl = use_pdl(h, nch);
+    // the loss: summed by the forward's last CTA (no reduce launch)
+    f.loss_out = h->loss_scalar;
+    f.done_count = h->done_count;
+    f.n_tiles = h->ntiles;
     if (pdl) {
         f.tile_ready = h->tile_ready;
         b.tile_ready = h->tile_ready;
@@ -886,11 +897,6 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
         }
         h->launches += 2;
     }
-    {
-        TimedLaunch tl(h, IDM_K_REDUCE);
-        CK(h, launch_reduce(h->loss_partials, h->ntiles, 1, h->loss_scalar, nullptr, h->st));
-    }
-    h->launches++;
     if (nch > 1) {
         CK(h, cudaEventRecord(h->ev_join, h->st2));
         CK(h, cudaStreamWaitEvent(h->st, h->ev_join, 0));

@@ -64,6 +64,11 @@ struct FwdArgs {
     // (release) once the tile's history is written
     unsigned* tile_ready;
     unsigned epoch;
+    // fused step (nullable): the last CTA to finish sums loss_partials[0 .. n_tiles) in
+    // reduce_kernel's fixed order into *loss_out (done_count: zero between launches)
+    double* loss_out;
+    unsigned* done_count;
+    int n_tiles;
 };
 
 struct AdamArgs {

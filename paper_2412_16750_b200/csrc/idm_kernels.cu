@@ -420,6 +420,29 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
         put(a.state_out + N + i0, v);
     }
     if (LOSS) block_sum_to(lacc + (double)lseg.x + (double)lseg.y, a.loss_partials + tile);
+    if (LOSS && a.loss_out) {  // the step's Eq. 4 loss, summed by the last CTA to finish
+        bool mine = false;
+        if (tid == 0) {
+            __threadfence();  // this tile's partial precedes its ticket
+            mine = atomicAdd(a.done_count, 1u) == (unsigned)(a.n_tiles - 1);
+        }
+        if (__syncthreads_or(mine)) {
+            __threadfence();
+            double* lred = reinterpret_cast<double*>(&obuf[0][0][0]);  // the ring is idle now
+            double x = 0.0;  // reduce_kernel's order: strided per thread, then a fixed tree
+            for (int r = tid; r < a.n_tiles; r += kT) x += __ldcg(a.loss_partials + r);
+            lred[tid] = x;
+            __syncthreads();
+            for (int st = kT / 2; st > 0; st >>= 1) {
+                if (tid < st) lred[tid] += lred[tid + st];
+                __syncthreads();
+            }
+            if (tid == 0) {
+                *a.loss_out = lred[0];
+                *a.done_count = 0u;
+            }
+        }
+    }
     if (LOSS && a.tile_ready) tile_release(a.tile_ready + tile, a.epoch);
 }
 
