@@ -108,12 +108,16 @@ __device__ __forceinline__ void tile_release(unsigned* flag, unsigned epoch) {
     if (threadIdx.x == 0)
         asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
 }
-__device__ __forceinline__ void tile_acquire(const unsigned* flag, unsigned epoch) {
+// The wait is bounded: a forward CTA that has started finishes within its `steps` steps, so a
+// handoff still missing after ~2^24 + 1024 * steps polls (seconds, orders of magnitude above any
+// forward CTA's duration) is a bug, and it fails the launch instead of hanging the GPU.
+__device__ __forceinline__ void tile_acquire(const unsigned* flag, unsigned epoch, int steps) {
     unsigned v;
+    const long long bound = (1ll << 24) + 1024ll * steps;
     for (long long spins = 0;; ++spins) {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
         if (v == epoch) break;
-        if (spins > (1ll << 24)) __trap();  // a broken handoff fails the launch, never hangs
+        if (spins > bound) __trap();
         __nanosleep(64);
     }
     // order the acquire before the bulk copies (async proxy) that read the history
@@ -539,7 +543,7 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
         for (int q = 0; q < NB; ++q) mbar_init(&mbar[q], 1);
         mbar_fence_init();
         // fused step after a programmatic launch: the tile's history is complete
-        if (GOBS && a.tile_ready) tile_acquire(a.tile_ready + tile, a.epoch);
+        if (GOBS && a.tile_ready) tile_acquire(a.tile_ready + tile, a.epoch, a.steps);
     }
     if (tid < NB * KS) vrow[tid * VP + kCap] = 0.f;
     __syncthreads();
