@@ -72,6 +72,11 @@ def alg_bytes(K: int, k: int, path: str) -> dict:
             "bwd": 8.0 + 4.0 / k + (24 + 24 + 8 + 1) / K,       # speed + dL/dP rows, ckpt, params
             "adam": 6 * 28.0 / K,                               # x, g, m, v in; x, m, v out
         }
+    if path == "fused_l2":  # the forward sums Eq. 4; the backward re-derives dL/dP from obs
+        return {
+            "fwd": 4.0 + 4.0 + 8.0 / k + (4 * 4 + 24 + 1) / K,  # obs in; speeds, gap + D out
+            "bwd": 4.0 + 4.0 + 8.0 / k + (24 + 1 + 4 + 24 + 8 + 6 * 20) / K,  # + obs, p0
+        }
     # fused L1 (the headline): the forward sums Eq. 4 and records -sign(obs - P) as 2 bits
     return {
         "fwd": 4.0 + 4.0 + 4.0 / k + 0.25 + (4 * 4 + 24 + 1) / K,  # obs in; speeds, gap, bits out
@@ -277,13 +282,13 @@ def run_ours(args, rank, world, local_rank):
 
     def step_api(it):
         sim.forward(K)
-        sim.loss_grad(obs, kind="l1", sync=False)
+        sim.loss_grad(obs, kind=args.loss, sync=False)
         parallel.reduce_step(sim.loss_dev)  # total loss: one 8-byte NCCL all-reduce
         sim.backward()
         sim.adam_step(it % 500, 500, 0.1, 0.01)
 
     def step_fused(it):
-        sim.fit_step(obs, kind="l1", iteration=it % 500, total=500, lr0=0.1, lr1=0.01)
+        sim.fit_step(obs, kind=args.loss, iteration=it % 500, total=500, lr0=0.1, lr1=0.01)
         parallel.reduce_step(sim.loss_dev)
 
     clocks = ClockSampler(local_rank)
@@ -436,7 +441,8 @@ def run_ours(args, rank, world, local_rank):
                                                 "vehicle fitted alone with free per-step "
                                                 "(dp, dv) leaves" if vl else ""),
                    "vehicles_per_rank": w.n, "K": K,
-                   "ckpt_every": k, "path": "idm_fit_step (fused fwd+Eq.4 / bwd+Adam)",
+                   "ckpt_every": k, "loss": args.loss,
+                   "path": "idm_fit_step (fused fwd+Eq.4 / bwd+Adam)",
                    "parallelism": f"lane-sharded x{world}",
                    "l2": "no flush: inputs larger than L2 (2.4 GB obs read by both kernels + "
                          "2.4 GB speed history per rank per step vs 126 MB L2)"},
@@ -449,7 +455,8 @@ def run_ours(args, rank, world, local_rank):
         "whole_fit_path": whole,
         "graph_path": graph,
         "roofline": roofline,
-        "hbm": {"fused": hbm_of(fused, "vl" if vl else "fused"),
+        "hbm": {"fused": hbm_of(fused, "vl" if vl else ("fused_l2" if args.loss == "l2" else
+                                                        "fused")),
                 "api": hbm_of(api, "vl_api" if vl else "api"), "peak_source": peak_src},
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -479,6 +486,8 @@ def main():
                     help="BASELINE.json configuration (C4 = the headline)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--ckpt", type=int, default=None, help="checkpoint interval k")
+    ap.add_argument("--loss", choices=["l1", "l2"], default="l1",
+                    help="Eq. 4 as the paper's L1 (headline) or the smooth L2 variant")
     ap.add_argument("--e2e", type=int, default=3, help="end-to-end steps (0 = skip)")
     ap.add_argument("--cpu-lanes", type=int, default=2000,
                     help="C4 lanes in the oracle cpu_baseline sample (0 = skip)")
