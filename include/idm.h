@@ -209,6 +209,20 @@ int idm_step_host(idm_handle* h, int32_t steps, const float* pos0_host, const fl
                   const float* obs_host, const uint8_t* mask_host, int32_t kind, int32_t iter,
                   int32_t total_iters, float lr0, float lr1, double* loss_host);
 
+/* Pipelined form of idm_step_host for a stream of iterations: enqueues the same uploads and
+   kernels plus an asynchronous read of the loss and status, and returns without synchronizing,
+   so the next call's observation upload (which still waits for this step's loss kernel, the
+   staging buffer's last reader) overlaps this step's backward and Adam.  At most two steps may
+   be in flight; idm_step_host_wait retires the oldest.  Same arithmetic as idm_step_host. */
+int idm_step_host_async(idm_handle* h, int32_t steps, const float* pos0_host,
+                        const float* vel0_host, const float* obs_host, const uint8_t* mask_host,
+                        int32_t kind, int32_t iter, int32_t total_iters, float lr0, float lr1);
+
+/* Waits for the oldest idm_step_host_async step; its loss to *loss_host (nullable).  A pending
+   non-finite or invalid status drains the pipeline and is returned as by idm_check.
+   IDM_ESTATE if no step is in flight. */
+int idm_step_host_wait(idm_handle* h, double* loss_host);
+
 /* Kernel classes for idm_timing_read. */
 enum {
     IDM_K_FWD = 0,      /* forward (fused with Eq. 4 in idm_fit_step) */

@@ -36,6 +36,8 @@ struct idm_handle {
     // host-side resources for idm_step_host / synchronous reads
     cudaStream_t copy_st;
     cudaEvent_t ev_obs, ev_loss_done;
+    cudaEvent_t ev_step[2];  // idm_step_host_async: completion of the (up to) two steps in flight
+    int async_head, async_n;
     // fused iteration in tile chunks: backward of chunk c on st2 overlaps forward of chunk c+1
     cudaStream_t st2;
     cudaEvent_t ev_fork, ev_join, ev_chunk[16];
@@ -361,6 +363,8 @@ void idm_destroy(idm_handle* h) {
         if (e) cudaEventDestroy(e);
     if (h->ev_obs) cudaEventDestroy(h->ev_obs);
     if (h->ev_loss_done) cudaEventDestroy(h->ev_loss_done);
+    for (int q = 0; q < 2; ++q)
+        if (h->ev_step[q]) cudaEventDestroy(h->ev_step[q]);
     if (h->pinned) cudaFreeHost(h->pinned);
     if (h->adam_table_host) cudaFreeHost(h->adam_table_host);
     delete h;
@@ -512,11 +516,14 @@ int idm_init(idm_handle** out, const idm_desc* d) {
                 if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
             if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&h->cap_st, cudaStreamNonBlocking);
             if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&h->ev_gfork, cudaEventDisableTiming);
+            for (int q = 0; q < 2 && ce == cudaSuccess; ++q)
+                ce = cudaEventCreateWithFlags(&h->ev_step[q], cudaEventDisableTiming);
             if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&h->ev_gjoin, cudaEventDisableTiming);
         }
         if (ce == cudaSuccess) {
             what = "pinned buffer";
-            ce = cudaMallocHost((void**)&h->pinned, 4 * sizeof(double));
+            // [0] loss, [1] status, [2] flags, [4..5] / [6..7] loss / status of the async ring
+            ce = cudaMallocHost((void**)&h->pinned, 8 * sizeof(double));
         }
         if (ce != cudaSuccess) {
             bail(fail(h, IDM_ECUDA, "init (%s): %s", what, cudaGetErrorString(ce)));
@@ -1095,10 +1102,13 @@ int idm_check(idm_handle* h) {
     return sync_status(h);
 }
 
-int idm_step_host(idm_handle* h, int32_t steps, const float* pos0_host, const float* vel0_host,
-                  const float* obs_host, const uint8_t* mask_host, int32_t kind, int32_t iter,
-                  int32_t total_iters, float lr0, float lr1, double* loss_host) {
-    if (!h) return IDM_EINVAL;
+}  // extern "C"
+
+namespace {
+// idm_step_host without the final read: uploads, then forward -> loss -> backward -> Adam.
+int step_host_enqueue(idm_handle* h, int32_t steps, const float* pos0_host, const float* vel0_host,
+                      const float* obs_host, const uint8_t* mask_host, int32_t kind, int32_t iter,
+                      int32_t total_iters, float lr0, float lr1) {
     if (!obs_host) return fail(h, IDM_EINVAL, "obs_host is NULL");
     if (!h->d.obs_stage || (mask_host && !h->d.mask_stage))
         return fail(h, IDM_EINVAL, "idm_step_host needs desc.obs_stage (and mask_stage)");
@@ -1124,13 +1134,64 @@ int idm_step_host(idm_handle* h, int32_t steps, const float* pos0_host, const fl
     CK(h, cudaEventRecord(h->ev_loss_done, h->st));
     s = idm_backward(h);
     if (s) return s;
-    s = idm_adam_step(h, iter, total_iters, lr0, lr1);
+    return idm_adam_step(h, iter, total_iters, lr0, lr1);
+}
+}  // namespace
+
+extern "C" {
+
+int idm_step_host(idm_handle* h, int32_t steps, const float* pos0_host, const float* vel0_host,
+                  const float* obs_host, const uint8_t* mask_host, int32_t kind, int32_t iter,
+                  int32_t total_iters, float lr0, float lr1, double* loss_host) {
+    if (!h) return IDM_EINVAL;
+    int s = step_host_enqueue(h, steps, pos0_host, vel0_host, obs_host, mask_host, kind, iter,
+                              total_iters, lr0, lr1);
     if (s) return s;
     CK(h, cudaMemcpyAsync(&h->pinned[0], h->loss_scalar, sizeof(double), cudaMemcpyDeviceToHost,
                           h->st));
     s = sync_status(h);
     if (loss_host) *loss_host = h->pinned[0];
     return s;
+}
+
+int idm_step_host_async(idm_handle* h, int32_t steps, const float* pos0_host,
+                        const float* vel0_host, const float* obs_host, const uint8_t* mask_host,
+                        int32_t kind, int32_t iter, int32_t total_iters, float lr0, float lr1) {
+    if (!h) return IDM_EINVAL;
+    if (h->async_n >= 2)
+        return fail(h, IDM_ESTATE, "two idm_step_host_async steps in flight: call "
+                                   "idm_step_host_wait first");
+    int s = step_host_enqueue(h, steps, pos0_host, vel0_host, obs_host, mask_host, kind, iter,
+                              total_iters, lr0, lr1);
+    if (s) return s;
+    const int slot = (h->async_head + h->async_n) % 2;
+    CK(h, cudaMemcpyAsync(&h->pinned[4 + slot], h->loss_scalar, sizeof(double),
+                          cudaMemcpyDeviceToHost, h->st));
+    CK(h, cudaMemcpyAsync(&h->pinned[6 + slot], h->status, sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, h->st));
+    CK(h, cudaEventRecord(h->ev_step[slot], h->st));
+    h->async_n++;
+    return IDM_OK;
+}
+
+int idm_step_host_wait(idm_handle* h, double* loss_host) {
+    if (!h) return IDM_EINVAL;
+    if (h->async_n == 0) return fail(h, IDM_ESTATE, "no idm_step_host_async step in flight");
+    const int slot = h->async_head;
+    CK(h, cudaEventSynchronize(h->ev_step[slot]));
+    h->async_head = (h->async_head + 1) % 2;
+    h->async_n--;
+    if (loss_host) *loss_host = h->pinned[4 + slot];
+    unsigned long long st;
+    std::memcpy(&st, &h->pinned[6 + slot], sizeof(st));
+    if (st != ~0ull) {  // drain the pipeline, then report (and clear) the status as idm_check
+        CK(h, cudaStreamSynchronize(h->st));
+        h->async_n = 0;
+        CK(h, cudaMemsetAsync(h->status, 0xff, sizeof(unsigned long long), h->st));
+        CK(h, cudaStreamSynchronize(h->st));
+        return consume_status(h, st);
+    }
+    return IDM_OK;
 }
 
 }  // extern "C"

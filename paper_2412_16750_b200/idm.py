@@ -121,6 +121,11 @@ def load_library(path: str | None = None):
     L.idm_plan_tiles.argtypes = [vp, i32, C.c_int64, vp]
     L.idm_fit_max_steps.restype = i32
     L.idm_fit_max_steps.argtypes = []
+    L.idm_step_host_async.restype = C.c_int
+    L.idm_step_host_async.argtypes = [vp, i32, vp, vp, vp, vp, i32, i32, i32, C.c_float,
+                                      C.c_float]
+    L.idm_step_host_wait.restype = C.c_int
+    L.idm_step_host_wait.argtypes = [vp, C.POINTER(C.c_double)]
     L.idm_step_host.restype = C.c_int
     L.idm_step_host.argtypes = [vp, i32, vp, vp, vp, vp, i32, i32, i32, C.c_float, C.c_float,
                                 C.POINTER(C.c_double)]
@@ -347,6 +352,23 @@ class IdmSim:
             self.handle, int(steps), _ptr(pos0_host), _ptr(vel0_host), _ptr(obs_host),
             _ptr(mask_host), LOSS_KINDS[kind], iteration, total, lr0, lr1, C.byref(out)))
         self.steps = int(steps)
+        return out.value
+
+    def step_host_async(self, steps, obs_host: torch.Tensor, pos0_host=None, vel0_host=None,
+                        mask_host=None, kind="l1", iteration=0, total=500, lr0=0.1, lr1=0.01):
+        """idm_step_host without the final synchronization (at most two in flight); the host
+        tensors must stay alive and unchanged until the matching step_host_wait."""
+        for t in (obs_host, pos0_host, vel0_host, mask_host):
+            assert t is None or (t.device.type == "cpu" and t.is_contiguous())
+        self._check(self._lib.idm_step_host_async(
+            self.handle, int(steps), _ptr(pos0_host), _ptr(vel0_host), _ptr(obs_host),
+            _ptr(mask_host), LOSS_KINDS[kind], iteration, total, lr0, lr1))
+        self.steps = int(steps)
+
+    def step_host_wait(self) -> float:
+        """Retire the oldest step_host_async step; returns its loss."""
+        out = C.c_double(0.0)
+        self._check(self._lib.idm_step_host_wait(self.handle, C.byref(out)))
         return out.value
 
     def timing(self, enable: bool = True):

@@ -326,6 +326,29 @@ def test_step_host_matches_device_path(idm, oracle):
         assert La == Lb
     torch.cuda.synchronize()
     assert torch.equal(a.params, b.params)
+    # pipelined host steps (two in flight) retire the same losses and parameters
+    c = idm.from_workload(w, None, max_steps=w.K, stage_obs=True)
+    d = idm.from_workload(w, None, max_steps=w.K, stage_obs=True)
+    Ls = [c.step_host(w.K, o_host, iteration=it) for it in range(5)]
+    La = []
+    for it in range(5):
+        d.step_host_async(w.K, o_host, iteration=it)
+        if it > 0:
+            La.append(d.step_host_wait())
+    La.append(d.step_host_wait())
+    assert La == Ls
+    torch.cuda.synchronize()
+    assert torch.equal(c.params, d.params)
+    with pytest.raises(idm.IdmError) as e:
+        d.step_host_wait()  # nothing in flight
+    assert e.value.code == idm.IDM_ESTATE
+    d.step_host_async(w.K, o_host, iteration=5)
+    d.step_host_async(w.K, o_host, iteration=6)
+    with pytest.raises(idm.IdmError) as e:
+        d.step_host_async(w.K, o_host, iteration=7)  # at most two in flight
+    assert e.value.code == idm.IDM_ESTATE
+    d.step_host_wait()
+    d.step_host_wait()
 
 
 # ------------------------------------------------------------------- fused iteration
