@@ -166,7 +166,9 @@ int idm_adam_step(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, f
    its last CTA sums the per-tile losses in a fixed order), and the backward kernel -- launched
    as a programmatic dependent of the forward, each CTA waiting for its own tile's history --
    re-derives dL/dP from obs and the rebuilt positions and applies Adam + box clamp per vehicle
-   in its epilogue (shared mode: + reduce + Adam launches).  traj and grad_traj are NOT written on this path; with any
+   in its epilogue (shared mode: + reduce + Adam launches; the shared gradient is THIS
+   process's sum, so with several ranks use the separate calls and all-reduce between
+   idm_backward and idm_adam_step -- the Python binding refuses the fused calls there).  traj and grad_traj are NOT written on this path; with any
    other ckpt_every the defining sequence runs as is (and writes them).
    obs: device [(steps+1)][N]; missing observations are NaN (mask must be NULL).  Loss to
    *loss_dev / *loss_host as in idm_loss_grad. */

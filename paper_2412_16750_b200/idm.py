@@ -190,6 +190,7 @@ class IdmSim:
                 raise IdmError(IDM_EINVAL, f"{name} has {t.numel()} entries; lane_offsets "
                                            f"describe {n} vehicles")
         n_par = 1 if shared_params else n
+        self.shared_params = bool(shared_params)
         if params is None:
             from .synth import init_params
             params = init_params(n_par)
@@ -296,12 +297,24 @@ class IdmSim:
     def adam_step(self, iteration: int, total: int = 500, lr0: float = 0.1, lr1: float = 0.01):
         self._check(self._lib.idm_adam_step(self.handle, iteration, total, lr0, lr1))
 
+    def _no_sharded_shared(self, what: str):
+        """The fused optimizer calls apply Adam inside the library, on this process's gradient
+        sum: with shared parameters over several ranks that would skip the all-reduce."""
+        import torch.distributed as dist
+        if self.shared_params and dist.is_available() and dist.is_initialized() and \
+                dist.get_world_size() > 1:
+            raise IdmError(IDM_EINVAL, f"{what}: shared parameters over {dist.get_world_size()} "
+                           "ranks need the gradient all-reduce between backward and adam_step "
+                           "(parallel.reduce_step); use the separate calls")
+
     def fit_step(self, obs: torch.Tensor, kind: str = "l1", iteration: int = 0,
                  total: int = 500, lr0: float = 0.1, lr1: float = 0.01, steps: int | None = None,
                  sync: bool = False):
-        """One fused iteration (idm_fit_step): forward + Eq. 4 + backward + Adam in three
+        """One fused iteration (idm_fit_step): forward + Eq. 4 + backward + Adam in two
         launches.  Missing observations are NaN.  Returns the loss if sync, else None (the
-        loss is in self.loss_dev)."""
+        loss is in self.loss_dev).  Shared parameters across several ranks need the gradient
+        all-reduce between backward and Adam: use the separate calls there."""
+        self._no_sharded_shared("fit_step")
         steps = self.max_steps if steps is None else int(steps)
         assert obs.dtype == torch.float32 and obs.is_contiguous() and obs.device == self.device
         assert obs.numel() >= (steps + 1) * self.n
@@ -317,6 +330,7 @@ class IdmSim:
             sync: bool = False):
         """`iters` fused iterations in ONE launch (idm_fit; horizons <= idm_fit_max_steps()):
         bit-identical to calling fit_step for iterations iter0 .. iter0+iters-1."""
+        self._no_sharded_shared("fit")
         steps = self.max_steps if steps is None else int(steps)
         assert obs.dtype == torch.float32 and obs.is_contiguous() and obs.device == self.device
         assert obs.numel() >= (steps + 1) * self.n
@@ -332,6 +346,7 @@ class IdmSim:
                   steps: int | None = None, sync: bool = False):
         """`iters` fused iterations (any horizon) launched as ONE CUDA graph (idm_fit_steps):
         bit-identical to calling fit_step for iterations iter0 .. iter0+iters-1."""
+        self._no_sharded_shared("fit_steps")
         steps = self.max_steps if steps is None else int(steps)
         assert obs.dtype == torch.float32 and obs.is_contiguous() and obs.device == self.device
         assert obs.numel() >= (steps + 1) * self.n

@@ -53,6 +53,16 @@ def _worker(rank, world, port, shared, out_q):
         loss = torch.tensor([L], dtype=torch.float64)
         grads = torch.tensor(g["g_params"][:, 0]) if shared else None
         parallel.reduce_step(loss, grads)
+        # the fused optimizer calls refuse shared parameters across ranks (their in-library
+        # Adam would skip this all-reduce); per-vehicle parameters are fine
+        import types
+        from paper_2412_16750_b200 import idm
+        guard = idm.IdmSim._no_sharded_shared
+        if shared:
+            with pytest.raises(idm.IdmError):
+                guard(types.SimpleNamespace(shared_params=True), "fit_step")
+        else:
+            guard(types.SimpleNamespace(shared_params=False), "fit_step")
         out_q.put((rank, float(loss.item()),
                    None if grads is None else grads.numpy().copy(),
                    None if shared else (vi, g["g_params"])))
