@@ -587,3 +587,44 @@ def test_product_alignment_agrees_with_oracle_alignment():
         got = tasks.nearest_steps(Ts, dt)
         exp = [T.nearest_step(float(t), dt) for t in Ts]
         assert list(got) == exp
+
+
+def test_rollout_converges_to_the_ode_at_first_order(oracle):
+    """The multi-step rollout (leader gather, synchronous update, explicit Euler of Eq. 3,
+    PAPER.md:121-128) against an independent integrator: scipy's adaptive RK45 on the ODE
+    dp/dt = v, dv/dt = a*(v, Delta p, Delta v) of the same lane, with a* from the oracle's
+    scalar accel (pinned on its own above) at a step so small that a_lb = a_min.  Euler is
+    first order, so the error at T = 3 s halves with dt (ratio 2 +- 0.3) and is small."""
+    from scipy.integrate import solve_ivp
+
+    theta = np.array([[7.0, 1.5, 2.5, 1.2, 30.0, 4.0],
+                      [8.5, 2.0, 3.0, 1.0, 33.0, 4.0],
+                      [6.0, 1.8, 2.0, 1.5, 28.0, 4.0]]).T.copy()  # [6][3]
+    length = np.array([4.5, 5.0, 4.2])
+    p0 = np.array([0.0, 22.0, 47.0])   # lane-sorted, vehicle 2 leads
+    v0 = np.array([14.0, 12.0, 10.0])
+    leader = oracle.leader_from_lanes([0, 3])
+    T = 3.0
+
+    def rhs(_, y):
+        p, v = y[:3], y[3:]
+        a = np.empty(3)
+        for i in range(3):
+            h = leader[i]
+            if h < 0:
+                a[i] = oracle.accel(theta[:, i], v[i], 0.0, 0.0, has_leader=False, dt=1e-9)
+            else:
+                a[i] = oracle.accel(theta[:, i], v[i], p[h] - p[i] - length[h], v[i] - v[h],
+                                    has_leader=True, dt=1e-9)
+        return np.concatenate([v, a])
+
+    ref = solve_ivp(rhs, (0.0, T), np.concatenate([p0, v0]), method="RK45", rtol=1e-11,
+                    atol=1e-11).y[:, -1]
+    errs = []
+    for dt in (0.01, 0.005, 0.0025):
+        K = int(round(T / dt))
+        P, V = oracle.rollout(leader, length, p0, v0, theta, K, dt=dt)
+        errs.append(max(np.max(np.abs(P[K] - ref[:3])), np.max(np.abs(V[K] - ref[3:]))))
+    r1, r2 = errs[0] / errs[1], errs[1] / errs[2]
+    assert 1.7 < r1 < 2.3 and 1.7 < r2 < 2.3, (errs, r1, r2)
+    assert errs[2] < 0.05
