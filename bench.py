@@ -255,7 +255,8 @@ def run_ours(args, rank, world, local_rank):
     vl = args.leader == "virtual"
     K, k = w.K, (4 if vl else (args.ckpt or idm.DEFAULT_CKPT))
     # synthetic observations: truth rollout with theta_true (our forward) + N(0, 0.3^2)
-    sim = idm.from_workload(w, w.theta_true, max_steps=K, ckpt_every=k, stage_obs=args.e2e > 0)
+    stage = 2 if args.e2e > 0 else 0  # e2e: two alternating observation staging buffers
+    sim = idm.from_workload(w, w.theta_true, max_steps=K, ckpt_every=k, stage_obs=stage)
     sim.forward(K)
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     obs = sim.traj.clone()
@@ -264,7 +265,7 @@ def run_ours(args, rank, world, local_rank):
         sim.close()
         del sim
         torch.cuda.empty_cache()
-        sim = idm.from_workload(w, None, max_steps=K, ckpt_every=k, stage_obs=args.e2e > 0,
+        sim = idm.from_workload(w, None, max_steps=K, ckpt_every=k, stage_obs=stage,
                                 virtual_leader=True)
     init = torch.as_tensor(synth.init_params(w.n), device=dev)
     stream = sim.stream

@@ -103,6 +103,10 @@ typedef struct {
     float* vl_grad;              /* [2][max_steps][N] dL/dDelta p_k, dL/dDelta v_k */
     float* vl_adam_m;            /* [2][max_steps][N] Adam moments of the leaves (zeroed) */
     float* vl_adam_v;            /* [2][max_steps][N] */
+    float* obs_stage2;           /* [(max_steps+1)][N] second observation staging buffer
+                                    (nullable): idm_step_host(_async) alternate between the two
+                                    when no mask is given, so an upload never waits for the
+                                    previous step's loss kernel */
 } idm_desc;
 
 /* Bytes of device workspace idm_init needs for this descriptor: the lane-mode state history

@@ -35,7 +35,8 @@ struct idm_handle {
     bool delta4;      // all delta == 4 and delta frozen => specialised kernels
     // host-side resources for idm_step_host / synchronous reads
     cudaStream_t copy_st;
-    cudaEvent_t ev_obs, ev_loss_done;
+    cudaEvent_t ev_obs, ev_loss_done, ev_loss_done2;  // last reader of obs_stage / obs_stage2
+    int stage_next;  // staging buffer of the next host step (0 / 1 with obs_stage2)
     cudaEvent_t ev_step[2];  // idm_step_host_async: completion of the (up to) two steps in flight
     int async_head, async_n;
     // fused iteration in tile chunks: backward of chunk c on st2 overlaps forward of chunk c+1
@@ -363,6 +364,7 @@ void idm_destroy(idm_handle* h) {
         if (e) cudaEventDestroy(e);
     if (h->ev_obs) cudaEventDestroy(h->ev_obs);
     if (h->ev_loss_done) cudaEventDestroy(h->ev_loss_done);
+    if (h->ev_loss_done2) cudaEventDestroy(h->ev_loss_done2);
     for (int q = 0; q < 2; ++q)
         if (h->ev_step[q]) cudaEventDestroy(h->ev_step[q]);
     if (h->pinned) cudaFreeHost(h->pinned);
@@ -507,6 +509,8 @@ int idm_init(idm_handle** out, const idm_desc* d) {
         }
         if (ce == cudaSuccess)
             ce = cudaEventCreateWithFlags(&h->ev_loss_done, cudaEventDisableTiming);
+            if (ce == cudaSuccess)
+                ce = cudaEventCreateWithFlags(&h->ev_loss_done2, cudaEventDisableTiming);
         if (ce == cudaSuccess) {
             what = "chunk stream / events";
             ce = cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking);
@@ -1118,9 +1122,14 @@ int step_host_enqueue(idm_handle* h, int32_t steps, const float* pos0_host, cons
     size_t ob = sizeof(float) * (size_t)(steps + 1) * (size_t)h->n;
     if (pos0_host) CK(h, cudaMemcpyAsync(h->d.pos0, pos0_host, nb, cudaMemcpyHostToDevice, h->st));
     if (vel0_host) CK(h, cudaMemcpyAsync(h->d.vel0, vel0_host, nb, cudaMemcpyHostToDevice, h->st));
-    // the obs upload waits for the previous loss kernel (staging reuse), overlaps the forward
-    CK(h, cudaStreamWaitEvent(h->copy_st, h->ev_loss_done, 0));
-    CK(h, cudaMemcpyAsync(h->d.obs_stage, obs_host, ob, cudaMemcpyHostToDevice, h->copy_st));
+    // staging: alternate obs_stage / obs_stage2 when both exist (and no mask: one mask stage);
+    // the upload waits for the last loss kernel that read its buffer, overlaps the forward
+    const int sb = (h->d.obs_stage2 && !mask_host) ? h->stage_next : 0;
+    h->stage_next = h->d.obs_stage2 ? sb ^ 1 : 0;
+    float* stage = sb ? h->d.obs_stage2 : h->d.obs_stage;
+    cudaEvent_t ev_done = sb ? h->ev_loss_done2 : h->ev_loss_done;
+    CK(h, cudaStreamWaitEvent(h->copy_st, ev_done, 0));
+    CK(h, cudaMemcpyAsync(stage, obs_host, ob, cudaMemcpyHostToDevice, h->copy_st));
     if (mask_host)
         CK(h, cudaMemcpyAsync(h->d.mask_stage, mask_host, (size_t)(steps + 1) * (size_t)h->n,
                               cudaMemcpyHostToDevice, h->copy_st));
@@ -1128,10 +1137,9 @@ int step_host_enqueue(idm_handle* h, int32_t steps, const float* pos0_host, cons
     int s = idm_forward(h, steps);
     if (s) return s;
     CK(h, cudaStreamWaitEvent(h->st, h->ev_obs, 0));
-    s = idm_loss_grad(h, h->d.obs_stage, mask_host ? h->d.mask_stage : nullptr, kind, nullptr,
-                      nullptr);
+    s = idm_loss_grad(h, stage, mask_host ? h->d.mask_stage : nullptr, kind, nullptr, nullptr);
     if (s) return s;
-    CK(h, cudaEventRecord(h->ev_loss_done, h->st));
+    CK(h, cudaEventRecord(ev_done, h->st));
     s = idm_backward(h);
     if (s) return s;
     return idm_adam_step(h, iter, total_iters, lr0, lr1);

@@ -67,6 +67,7 @@ class IdmDesc(C.Structure):
         ("vl_grad", C.c_void_p),
         ("vl_adam_m", C.c_void_p),
         ("vl_adam_v", C.c_void_p),
+        ("obs_stage2", C.c_void_p),
     ]
 
 
@@ -168,7 +169,7 @@ class IdmSim:
                  ckpt_every: int = DEFAULT_CKPT, dt: float = 0.1, a_min: float = -10.0,
                  eps_gap: float = 0.1, shared_params: bool = False,
                  opt_mask: int = PAPER_OPT_MASK, record_velocity: bool = False,
-                 stage_obs: bool = False, stage_mask: bool = False, state_out: bool = True,
+                 stage_obs: int = 0, stage_mask: bool = False, state_out: bool = True,
                  virtual_leader: bool = False, vl_dp=None, vl_dv=None,
                  device=None, stream: torch.cuda.Stream | None = None):
         L = load_library()
@@ -204,8 +205,11 @@ class IdmSim:
             if record_velocity else None
         self.grad_traj = torch.empty(max_steps + 1, n, dtype=f32, device=dev)
         self.state_out = torch.empty(2, n, dtype=f32, device=dev) if state_out else None
+        # stage_obs: 0 none, 1 (or True) one staging buffer for step_host, 2 two (alternating)
         self.obs_stage = torch.empty(max_steps + 1, n, dtype=f32, device=dev) \
             if stage_obs else None
+        self.obs_stage2 = torch.empty(max_steps + 1, n, dtype=f32, device=dev) \
+            if int(stage_obs) >= 2 else None
         self.mask_stage = torch.empty(max_steps + 1, n, dtype=torch.uint8, device=dev) \
             if stage_mask else None
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=dev)
@@ -239,6 +243,7 @@ class IdmSim:
         d.grad_traj = self.grad_traj.data_ptr()
         d.state_out = self.state_out.data_ptr() if self.state_out is not None else None
         d.obs_stage = self.obs_stage.data_ptr() if self.obs_stage is not None else None
+        d.obs_stage2 = self.obs_stage2.data_ptr() if self.obs_stage2 is not None else None
         d.mask_stage = self.mask_stage.data_ptr() if self.mask_stage is not None else None
         d.max_steps = max_steps
         d.ckpt_every = ckpt_every

@@ -328,7 +328,7 @@ def test_step_host_matches_device_path(idm, oracle):
     assert torch.equal(a.params, b.params)
     # pipelined host steps (two in flight) retire the same losses and parameters
     c = idm.from_workload(w, None, max_steps=w.K, stage_obs=True)
-    d = idm.from_workload(w, None, max_steps=w.K, stage_obs=True)
+    d = idm.from_workload(w, None, max_steps=w.K, stage_obs=2)  # alternating staging buffers
     Ls = [c.step_host(w.K, o_host, iteration=it) for it in range(5)]
     La = []
     for it in range(5):
