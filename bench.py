@@ -512,7 +512,7 @@ def main():
     ap.add_argument("--ckpt", type=int, default=None, help="checkpoint interval k")
     ap.add_argument("--loss", choices=["l1", "l2"], default="l1",
                     help="Eq. 4 as the paper's L1 (headline) or the smooth L2 variant")
-    ap.add_argument("--e2e", type=int, default=3, help="end-to-end steps (0 = skip)")
+    ap.add_argument("--e2e", type=int, default=8, help="end-to-end steps (0 = skip)")
     ap.add_argument("--cpu-lanes", type=int, default=2000,
                     help="C4 lanes in the oracle cpu_baseline sample (0 = skip)")
     ap.add_argument("--traffic", type=float, default=None,
