@@ -258,7 +258,11 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     // per-thread cp.async; the slots of absent vehicles hold NaN (= missing) from the start and
     // are never copied to; one commit group per segment (empty past the end) keeps
     // cp.async.wait_group<1> exact
-    __shared__ __align__(16) float obuf[LOSS ? 3 : 1][LOSS ? KS : 1][kCap];
+#ifndef IDM_FWD_RING
+#define IDM_FWD_RING 3  // observation ring slots (prefetch distance = slots - 1 segments)
+#endif
+    constexpr int OR = IDM_FWD_RING;
+    __shared__ __align__(16) float obuf[LOSS ? OR : 1][LOSS ? KS : 1][kCap];
     float2 lseg = f2(0.f);  // loss of this thread's vehicles in this segment (fp32)
     double lacc = 0.0;   // and across segments (fp64)
     auto ld_obs = [&](const float* o, bool on) {  // absent vehicles observe NaN (= missing)
@@ -271,7 +275,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     auto fetch_obs = [&](int seg) {
         const int r0 = seg * KS + 1;
         float* dst = &obuf[fslot][0][2 * tid];
-        fslot = fslot == 2 ? 0 : fslot + 1;
+        fslot = fslot == OR - 1 ? 0 : fslot + 1;
         if (r0 + KS - 1 <= steps) {  // whole segment inside the rollout (CTA-uniform)
             const float* o = onext;
 #pragma unroll
@@ -297,12 +301,12 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     if (LOSS) {
         float* ob = &obuf[0][0][0];
 #pragma unroll
-        for (int q = 0; q < 3 * KS; ++q) {  // own slots only: no barrier needed
+        for (int q = 0; q < OR * KS; ++q) {  // own slots only: no barrier needed
             if (!val[0]) ob[q * kCap + 2 * tid] = qnan;
             if (!val[1]) ob[q * kCap + 2 * tid + 1] = qnan;
         }
-        fetch_obs(0);
-        fetch_obs(1);
+#pragma unroll
+        for (int q = 0; q < OR - 1; ++q) fetch_obs(q);
     }
     // checkpoint rows the consumer reads: the gap (idm_backward); + displacement (fused
     // backward rebuilds positions); + compensation (and that with Kahan)
@@ -384,11 +388,11 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     };
     auto obs_ready = [&](int seg) {
         if (LOSS) {
-            cp_async_wait<1>();  // this segment's group; seg + 1's may stay in flight
-            fetch_obs(seg + 2);
+            cp_async_wait<OR - 2>();  // this segment's group; later ones may stay in flight
+            fetch_obs(seg + OR - 1);
         }
     };
-    auto obs_done = [&] { cslot = cslot == 2 ? 0 : cslot + 1; };
+    auto obs_done = [&] { cslot = cslot == OR - 1 ? 0 : cslot + 1; };
     for (int seg = 0; seg < nfull; ++seg) {
         const int t0 = seg * KS;
         obs_ready(seg);
