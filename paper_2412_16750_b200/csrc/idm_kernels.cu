@@ -490,33 +490,6 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
     const int nseg = (steps + KS - 1) / KS;
     const int tail = steps - (nseg - 1) * KS;  // length of the last segment (1..KS)
 
-    float ldj[2], pj[2];
-    VehP Pj[2];
-    VehA Aj[2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const int64_t i = i0 + j;
-        RawP r = dummy_raw();
-        ldj[j] = 0.f;
-        pj[j] = 0.f;
-        if (val[j]) {
-            r = load_raw(a.params, a.n_par, i);
-            if (D4 && r.delta != 4.f)
-                atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
-            if (!GOBS) ldj[j] = a.grad_traj[(int64_t)steps * N + i];  // lambda_D^K = dL/dP(K)
-            if (GOBS == 2) pj[j] = a.pos0[i];
-        }
-        Pj[j] = make_vehp(r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta);
-        Aj[j] = make_veha(r.a_max, r.a_pref, r.v_targ, r.delta, k);
-    }
-    const float2 p0 = make_float2(pj[0], pj[1]);
-    const VehPT<float2> P = pack(Pj[0], Pj[1]);
-    const VehAT<float2> B = pack(Aj[0], Aj[1]);
-    // scaled adjoint (bwd_from_record): u = dt lambda_v, m = -dt lambda_s, e = dt^2 lambda_D
-    float2 e = vmul(make_float2(ldj[0], ldj[1]), k.dt2);
-    float2 m = f2(0.f), u = f2(0.f);
-    GradAccT<float2> G = {f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
-    if (tid == 0) { fx[0][0] = 0.f; fx[1][0] = 0.f; }  // never written again (slots t+1 >= 1)
 
     // Segment rows are staged in shared memory, two segments ahead, in a ring of 3 buffers:
     // speeds and the checkpoint by bulk copy (one thread, mbarrier-counted), dL/dP rows (or the
@@ -591,6 +564,34 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
     int par = 0;
     fetch(nseg - 1, tail);
     if (nseg > 1) fetch(nseg - 2, KS);
+    // per-vehicle constants while the first two segments' rows are in flight
+    float ldj[2], pj[2];
+    VehP Pj[2];
+    VehA Aj[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int64_t i = i0 + j;
+        RawP r = dummy_raw();
+        ldj[j] = 0.f;
+        pj[j] = 0.f;
+        if (val[j]) {
+            r = load_raw(a.params, a.n_par, i);
+            if (D4 && r.delta != 4.f)
+                atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
+            if (!GOBS) ldj[j] = a.grad_traj[(int64_t)steps * N + i];  // lambda_D^K = dL/dP(K)
+            if (GOBS == 2) pj[j] = a.pos0[i];
+        }
+        Pj[j] = make_vehp(r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta);
+        Aj[j] = make_veha(r.a_max, r.a_pref, r.v_targ, r.delta, k);
+    }
+    const float2 p0 = make_float2(pj[0], pj[1]);
+    const VehPT<float2> P = pack(Pj[0], Pj[1]);
+    const VehAT<float2> B = pack(Aj[0], Aj[1]);
+    // scaled adjoint (bwd_from_record): u = dt lambda_v, m = -dt lambda_s, e = dt^2 lambda_D
+    float2 e = vmul(make_float2(ldj[0], ldj[1]), k.dt2);
+    float2 m = f2(0.f), u = f2(0.f);
+    GradAccT<float2> G = {f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
+    if (tid == 0) { fx[0][0] = 0.f; fx[1][0] = 0.f; }  // never written again (slots t+1 >= 1)
     auto segment = [&](const int seg, const int len, auto FULL) {
         constexpr bool kFull = decltype(FULL)::value;
         const int b = seg % NB;
