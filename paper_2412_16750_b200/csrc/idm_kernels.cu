@@ -217,29 +217,6 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     const bool val[2] = {id0 < n_loc, id0 + 1 < n_loc};
     if (LOSS && a.tile_ready) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
-    const float pinf = __int_as_float(0x7f800000);
-    float sj[2], vj[2], pj[2];
-    VehP Pj[2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const int64_t i = i0 + j;
-        RawP r = dummy_raw();
-        sj[j] = pinf; vj[j] = 0.f; pj[j] = 0.f;  // no leader: gap +inf (see core_dv)
-        if (val[j]) {
-            pj[j] = a.pos0[i];
-            vj[j] = a.vel0[i];
-            if (a.lead[i] != 0) sj[j] = (a.pos0[i + 1] - pj[j]) - a.length[i + 1];
-            r = load_raw(a.params, a.n_par, i);
-            if (D4 && r.delta != 4.f)
-                atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
-        }
-        Pj[j] = make_vehp(r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta);
-    }
-    float2 s = make_float2(sj[0], sj[1]), v = make_float2(vj[0], vj[1]);
-    const float2 p0 = make_float2(pj[0], pj[1]);
-    const VehPT<float2> P = pack(Pj[0], Pj[1]);
-    float2 D = f2(0.f), cmp = f2(0.f);
-    if (tid == 0) { xv[0][kT] = 0.f; xv[1][kT] = 0.f; }
 
     auto put = [&](float* row, float2 x) {  // row points at local vehicle 2 tid
         st_cs_if(row, val[0], x.x);
@@ -308,6 +285,30 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
 #pragma unroll
         for (int q = 0; q < OR - 1; ++q) fetch_obs(q);
     }
+    // per-vehicle state and constants while the first observation rows are in flight
+    const float pinf = __int_as_float(0x7f800000);
+    float sj[2], vj[2], pj[2];
+    VehP Pj[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int64_t i = i0 + j;
+        RawP r = dummy_raw();
+        sj[j] = pinf; vj[j] = 0.f; pj[j] = 0.f;  // no leader: gap +inf (see core_dv)
+        if (val[j]) {
+            pj[j] = a.pos0[i];
+            vj[j] = a.vel0[i];
+            if (a.lead[i] != 0) sj[j] = (a.pos0[i + 1] - pj[j]) - a.length[i + 1];
+            r = load_raw(a.params, a.n_par, i);
+            if (D4 && r.delta != 4.f)
+                atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
+        }
+        Pj[j] = make_vehp(r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta);
+    }
+    float2 s = make_float2(sj[0], sj[1]), v = make_float2(vj[0], vj[1]);
+    const float2 p0 = make_float2(pj[0], pj[1]);
+    const VehPT<float2> P = pack(Pj[0], Pj[1]);
+    float2 D = f2(0.f), cmp = f2(0.f);
+    if (tid == 0) { xv[0][kT] = 0.f; xv[1][kT] = 0.f; }
     // checkpoint rows the consumer reads: the gap (idm_backward); + displacement (fused
     // backward rebuilds positions); + compensation (and that with Kahan)
     auto put_ck = [&] {
