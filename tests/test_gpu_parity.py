@@ -516,6 +516,44 @@ def test_virtual_leader_forward_and_gradients(idm, oracle):
     assert vg[0][5, 3] == 0.0  # clamped gap: zero gradient
 
 
+def test_virtual_leader_c4_full_size_sampled(idm, oracle):
+    """Virtual-leader mode at the C4 geometry bench.py --leader virtual times (2M trajectories,
+    K = 300, the paper's leaf initialisation Delta p = 10, Delta v = 0): trajectories fit alone,
+    so 2,000 sampled trajectories are exactly the oracle's problem.  Positions, parameter and
+    leaf gradients of those against the fp64 oracle (the GPU's dL/dP given, as above)."""
+    w = synth.make_workload("C4")
+    lane = idm.from_workload(w, w.theta_true, max_steps=w.K)
+    lane.forward(w.K)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    obs = lane.traj.clone()
+    obs[1:].add_(torch.randn(obs[1:].shape, device="cuda", generator=gen), alpha=0.3)
+    lane.close()
+    del lane
+    prm = synth.init_params(w.n)
+    sim = idm.from_workload(w, prm, max_steps=w.K, ckpt_every=4, virtual_leader=True)
+    sim.forward(w.K)
+    sim.loss_grad(obs, kind="l2")
+    sim.backward()
+    torch.cuda.synchronize()
+    vi = np.sort(np.random.default_rng(1).choice(w.n, 2000, replace=False))
+    idx = torch.as_tensor(vi, device="cuda")
+    dp = np.full((w.K, vi.size), idm.VL_INIT[0])
+    dv = np.full((w.K, vi.size), idm.VL_INIT[1])
+    p = prm[:, vi].astype(np.float64)
+    P_o, V_o = oracle.rollout_vl(w.p0[vi], w.v0[vi], p, dp, dv)
+    assert state_violation(sim.traj.index_select(1, idx).cpu().numpy(), P_o) <= 1.0
+    gP = sim.grad_traj.index_select(1, idx).cpu().numpy().astype(np.float64)
+    g = oracle.backward_vl(p, dp, dv, P_o, V_o, gP)
+    worst, plain = grad_check(sim.grad_params.index_select(1, idx).cpu().numpy(), g["g_params"],
+                              g["g_abs"])
+    print(f"VL C4 sample grad worst/tol = {worst:.3f}, plain pass = {plain:.4f}")
+    assert worst <= 1.0
+    vg = sim.vl_grad.index_select(2, idx).cpu().numpy().astype(np.float64)
+    for got, ref in ((vg[0], g["g_dp"]), (vg[1], g["g_dv"])):
+        scale = np.abs(ref).max(axis=0, keepdims=True)  # per trajectory
+        assert np.all(np.abs(got - ref) <= 1e-3 * np.abs(ref) + 1e-3 * scale)
+
+
 def test_virtual_leader_fit_step_equals_api_and_adam(idm, oracle):
     """Fused and separate calls agree bitwise in virtual-leader mode; the leaves get the
     paper's Adam schedule without a box (oracle Adam as reference)."""
