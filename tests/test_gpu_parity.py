@@ -963,6 +963,35 @@ def test_prediction_pipeline_c5_shape(idm, oracle):
     assert np.isfinite(ade) and ade < cv.mean() and fde < cv[-1].mean()
 
 
+@pytest.mark.parametrize("kind", ["l2", "l1"])
+def test_whole_fit_c5_full_size_sampled(idm, oracle, kind):
+    """idm_fit (the one-launch whole fit bench.py times for C5) at the full C5 size, one
+    iteration: its gradients at the initial parameters for 400 sampled lanes against the fp64
+    oracle on those lanes (the GPU's L1 sign pattern given)."""
+    w = synth.make_workload("C5")
+    obs = synth.kinematic_obs(w, sigma=0.1)
+    sim = idm.from_workload(w, None, max_steps=w.K)
+    prm = sim.params.cpu().numpy().astype(np.float64)
+    sim.fit(torch.as_tensor(obs, device="cuda"), iters=1, kind=kind, total=500)
+    torch.cuda.synchronize()
+    lanes = np.sort(np.random.default_rng(2).choice(w.n_lanes, 400, replace=False))
+    sub = synth.lane_subset(w, lanes)
+    vi = sub.meta["vehicle_index"]
+    # the fused iteration's dL/dP signs are those of the same forward: rebuild them with the
+    # API forward on the full problem (same bits as the fit's forward)
+    api = idm.from_workload(w, None, max_steps=w.K)
+    api.forward(w.K)
+    api.loss_grad(torch.as_tensor(obs, device="cuda"), kind=kind)
+    torch.cuda.synchronize()
+    gt = api.grad_traj.cpu().numpy()[:, vi].astype(np.float64)
+    _, _, _, g = oracle_grads(oracle, sub, prm[:, vi], w.K, obs[:, vi].astype(np.float64), kind,
+                              gt)
+    gg = sim.grad_params.cpu().numpy()[:, vi]
+    worst, plain = grad_check(gg[:5], g["g_params"][:5], g["g_abs"][:5])
+    print(f"C5 whole-fit {kind} grad worst/tol = {worst:.3f}, plain pass = {plain:.4f}")
+    assert worst <= 1.0
+
+
 _PDL_CHILD = r"""
 import sys, numpy as np, torch
 sys.path.insert(0, sys.argv[1])
