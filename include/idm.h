@@ -165,12 +165,14 @@ int idm_adam_step(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, f
    backward -> adam_step(iter, ...) (same arithmetic; grad_params, grad_state0, Adam moments and
    parameters bit for bit -- except grad_params row 5, dL/d delta, which is written as 0 when
    delta is frozen (opt_mask bit 5 clear): the optimizer never reads it, and the delta = 4
-   kernels skip the per-step log2 it needs), in two launches when ckpt_every == 4: the forward
-   kernel sums Eq. 4 against each fresh position row (writing only the internal state history;
-   its last CTA sums the per-tile losses in a fixed order), and the backward kernel -- launched
-   as a programmatic dependent of the forward, each CTA waiting for its own tile's history --
-   re-derives dL/dP from obs and the rebuilt positions and applies Adam + box clamp per vehicle
-   in its epilogue (shared mode: + reduce + Adam launches; the shared gradient is THIS
+   kernels skip the per-step log2 it needs), when ckpt_every == 4 in two kernels writing only
+   the internal state history, the backward launched as a programmatic dependent of the forward
+   (each CTA waits for its own tile's history) and applying Adam + box clamp per vehicle in its
+   epilogue.  L1: the forward sums Eq. 4 against each fresh position row and records
+   dL/dP = -sign as 2 bits per vehicle-step; its last CTA sums the per-tile losses (2 launches).
+   L2: the forward only records the history; the backward derives the loss terms and dL/dP
+   from obs and the rebuilt positions, and one fixed-order reduction sums the losses (3
+   launches) (shared mode: + reduce + Adam launches; the shared gradient is THIS
    process's sum, so with several ranks use the separate calls and all-reduce between
    idm_backward and idm_adam_step -- the Python binding refuses the fused calls there).  traj and grad_traj are NOT written on this path; with any
    other ckpt_every the defining sequence runs as is (and writes them).

@@ -859,7 +859,18 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
     var.delta4 = h->delta4;
     var.kahan = steps > 2000;
     var.rec_v = false;
-    var.loss = 1 + kind;
+    // Two schemes, same arithmetic: the forward sums Eq. 4 and records the L1 sign codes (L1
+    // default: 2 bits per vehicle-step cross to the backward), or the forward writes only the
+    // tile history and the backward derives Eq. 4 from obs and the rebuilt positions (L2
+    // default: L2's dL/dP needs the residual, so obs would otherwise be read twice).  C4: L1
+    // 2.71 vs 2.70 ms, L2 3.13 vs 2.67 ms.  IDM_FUSED_OBS_BWD=0/1 forces one for both kinds.
+    static const int obs_env = [] {
+        const char* e = std::getenv("IDM_FUSED_OBS_BWD");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    const bool obs_bwd = obs_env >= 0 ? obs_env == 1 : kind == 1;
+    var.loss = obs_bwd ? 3 : 1 + kind;
+    const int gobs = obs_bwd ? (kind == 0 ? 3 : 2) : 1 + kind;
     h->steps = steps;
     // backward: dL/dP from the forward's sign words (L1) or re-derived from obs and rebuilt
     // positions (L2); per-vehicle parameters get Adam in the same kernel's epilogue
@@ -874,10 +885,13 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
     const int nch = fused_chunks(h);
     cudaStream_t sb = nch > 1 ? h->st2 : h->st;
     const bool pdl = use_pdl(h, nch);
-    // the loss: summed by the forward's last CTA (no reduce launch)
-    f.loss_out = h->loss_scalar;
-    f.done_count = h->done_count;
-    f.n_tiles = h->ntiles;
+    if (!obs_bwd) {  // the loss: summed by the forward's last CTA (no reduce launch)
+        f.loss_out = h->loss_scalar;
+        f.done_count = h->done_count;
+        f.n_tiles = h->ntiles;
+    } else {  // per-tile losses from the backward, then one fixed-order reduction
+        b.loss_partials = h->loss_partials;
+    }
     if (pdl) {
         f.tile_ready = h->tile_ready;
         b.tile_ready = h->tile_ready;
@@ -904,13 +918,18 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
         }
         {
             TimedLaunch tl(h, IDM_K_BWD, sb);
-            CK(h, launch_bwd(b, t1 - t0, h->delta4, shared, !shared, 1 + kind, var.kahan, sb, pdl));
+            CK(h, launch_bwd(b, t1 - t0, h->delta4, shared, !shared, gobs, var.kahan, sb, pdl));
         }
         h->launches += 2;
     }
     if (nch > 1) {
         CK(h, cudaEventRecord(h->ev_join, h->st2));
         CK(h, cudaStreamWaitEvent(h->st, h->ev_join, 0));
+    }
+    if (obs_bwd) {
+        TimedLaunch tl(h, IDM_K_REDUCE);
+        CK(h, launch_reduce(h->loss_partials, h->ntiles, 1, h->loss_scalar, nullptr, h->st));
+        h->launches++;
     }
     if (shared) {
         {

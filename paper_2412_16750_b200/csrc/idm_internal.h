@@ -102,6 +102,8 @@ struct BwdArgs {
     // tile_ready[tile] == epoch before reading the tile's history
     const unsigned* tile_ready;
     unsigned epoch;
+    // GOBS >= 2 (nullable): this tile's Eq. 4 loss -> loss_partials[tile] (the forward did not)
+    double* loss_partials;
 };
 
 // virtual-leader mode (idm_vl.cu)
@@ -152,8 +154,8 @@ struct LossArgs {
 cudaError_t launch_validate(const ValidateArgs& a, cudaStream_t st);
 cudaError_t launch_fwd(const FwdArgs& a, int ntiles, const FwdVariant& var, cudaStream_t st);
 cudaError_t kernels_configure(int ckpt_every);
-// gobs = 0: dL/dP from grad_traj; 1: L1 from the forward's sign words; 2: L2 re-derived from obs
-// and the rebuilt positions (gobs != 0: fused idm_fit_step, ckpt_every == 4)
+// gobs = 0: dL/dP from grad_traj; 1: L1 from the forward's sign codes; 2 / 3: L2 / L1 re-derived
+// from obs and the rebuilt positions (gobs != 0: fused idm_fit_step, ckpt_every == 4)
 // pdl: launch as a programmatic dependent of the preceding kernel in the stream (the forward of
 // the same tiles, which signals a.tile_ready)
 cudaError_t launch_bwd(const BwdArgs& a, int ntiles, bool delta4, bool shared, bool adam,

@@ -203,6 +203,10 @@ template <bool D4, bool KAHAN, bool RECV, int LOSS, int CK>
 __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 4)))
     fwd_kernel(FwdArgs a) {
     constexpr int KS = CK > 4 ? CK : 4;
+    // LOSS = 3: the fused iteration whose backward derives Eq. 4 itself (from obs and the
+    // rebuilt positions): only the tile history (speeds; gap + displacement checkpoints)
+    constexpr bool OBSV = LOSS == 1 || LOSS == 2;  // reads the observations here
+    constexpr bool DCK = LOSS == 2 || LOSS == 3;   // displacement checkpoints for the backward
     __shared__ float xv[2][kT + 1];  // speed of each thread's first vehicle; [kT] = 0 sentinel
     const int tid = threadIdx.x;
     const int tile = a.tile0 + (int)blockIdx.x;  // launches may cover a chunk of the tiles
@@ -229,7 +233,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     float2* vtp = reinterpret_cast<float2*>(a.vt + tile * a.vt_stride) + tid;
     float2* ckp = reinterpret_cast<float2*>(a.ckt + tile * a.ck_stride) + tid;
     constexpr int kR2 = kCap / 2;  // one row in float2 units
-    const float* obs = LOSS ? a.obs + i0 : nullptr;
+    const float* obs = OBSV ? a.obs + i0 : nullptr;
     const float qnan = __int_as_float(0x7fc00000);
     // LOSS: observation rows staged two segments ahead in a 3-buffer shared-memory ring by
     // per-thread cp.async; the slots of absent vehicles hold NaN (= missing) from the start and
@@ -239,7 +243,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
 #define IDM_FWD_RING 3  // observation ring slots (prefetch distance = slots - 1 segments)
 #endif
     constexpr int OR = IDM_FWD_RING;
-    __shared__ __align__(16) float obuf[LOSS ? OR : 1][LOSS ? KS : 1][kCap];
+    __shared__ __align__(16) float obuf[OBSV ? OR : 1][OBSV ? KS : 1][kCap];
     float2 lseg = f2(0.f);  // loss of this thread's vehicles in this segment (fp32)
     double lacc = 0.0;   // and across segments (fp64)
     auto ld_obs = [&](const float* o, bool on) {  // absent vehicles observe NaN (= missing)
@@ -247,7 +251,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     };
     // segment seg observes rows seg*KS + 1 .. seg*KS + KS; fetches run two segments ahead of
     // use, slots rotate 0, 1, 2 (fslot: next fetch, cslot: current use)
-    const float* onext = LOSS ? obs + N : nullptr;  // first row of the next fetch
+    const float* onext = OBSV ? obs + N : nullptr;  // first row of the next fetch
     int fslot = 0, cslot = 0;
     auto fetch_obs = [&](int seg) {
         const int r0 = seg * KS + 1;
@@ -275,7 +279,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     auto obs_at = [&](int tt) {  // this thread's pair of row seg*KS + 1 + tt (current segment)
         return *reinterpret_cast<const float2*>(&obuf[cslot][tt][2 * tid]);
     };
-    if (LOSS) {
+    if (OBSV) {
         float* ob = &obuf[0][0][0];
 #pragma unroll
         for (int q = 0; q < OR * KS; ++q) {  // own slots only: no barrier needed
@@ -313,8 +317,8 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     // backward rebuilds positions); + compensation (and that with Kahan)
     auto put_ck = [&] {
         __stcs(ckp, s);
-        if (LOSS == 2) __stcs(ckp + kR2, D);
-        if (LOSS == 2 && KAHAN) __stcs(ckp + 2 * kR2, cmp);
+        if (DCK) __stcs(ckp + kR2, D);
+        if (DCK && KAHAN) __stcs(ckp + 2 * kR2, cmp);
     };
     // fused L1: dL/dP = -sign(obs - P) of the thread's two vehicles as a 4-bit code per step
     // (bits 0 / 2: r != 0, bits 1 / 3: r < 0), collected in a register and stored as one u16
@@ -343,8 +347,8 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
             code = 0;
         }
     };
-    if (LOSS) loss_step(ld_obs(obs, true), p0, std::integral_constant<int, 0>{});
-    else put(orow, p0);
+    if (OBSV) loss_step(ld_obs(obs, true), p0, std::integral_constant<int, 0>{});
+    else if (!LOSS) put(orow, p0);
     if (RECV) put(vrow, v);
     __stcs(vtp, v);
     put_ck();
@@ -368,8 +372,8 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
         if (RECV) vrow += N;
         vtp += kR2;
         const float2 Pv = vadd(p0, D);
-        if (LOSS) loss_step(o, Pv, PH);
-        else put(orow, Pv);
+        if (OBSV) loss_step(o, Pv, PH);
+        else if (!LOSS) put(orow, Pv);
         __stcs(vtp, v);
         if (RECV) put(vrow, v);
     };
@@ -388,7 +392,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
         finite2(t0);
     };
     auto obs_ready = [&](int seg) {
-        if (LOSS) {
+        if (OBSV) {
             cp_async_wait<OR - 2>();  // this segment's group; later ones may stay in flight
             fetch_obs(seg + OR - 1);
         }
@@ -400,10 +404,10 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
         static_for<KS>([&](auto TT) {
             constexpr int tt = decltype(TT)::value;
             if (tt % CK == 0 && (tt > 0 || seg > 0)) checkpoint(t0 + tt);
-            step(LOSS ? obs_at(tt) : f2(0.f), std::integral_constant<int, (tt + 1) % 4>{});
+            step(OBSV ? obs_at(tt) : f2(0.f), std::integral_constant<int, (tt + 1) % 4>{});
         });
         obs_done();
-        if (LOSS) {
+        if (OBSV) {
             lacc += (double)lseg.x + (double)lseg.y;
             lseg = f2(0.f);
         }
@@ -414,11 +418,11 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
             constexpr int tt = decltype(TT)::value;
             if (tt < tail) {  // CTA-uniform predicate
                 if (tt % CK == 0 && (tt > 0 || nfull > 0)) checkpoint(nfull * KS + tt);
-                step(LOSS ? obs_at(tt) : f2(0.f), std::integral_constant<int, (tt + 1) % 4>{});
+                step(OBSV ? obs_at(tt) : f2(0.f), std::integral_constant<int, (tt + 1) % 4>{});
             }
         });
     }
-    if (LOSS) cp_async_wait<0>();  // no copy outlives the CTA
+    if (OBSV) cp_async_wait<0>();  // no copy outlives the CTA
     if (LOSS == 1 && steps % kSgnSteps != kSgnSteps - 1)
         __stcs(sgp, (unsigned short)code);  // the last, partial code word (holds step K)
     finite2(steps);
@@ -428,8 +432,8 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
         put(a.state_out + i0, vadd(p0, D));
         put(a.state_out + N + i0, v);
     }
-    if (LOSS) block_sum_to(lacc + (double)lseg.x + (double)lseg.y, a.loss_partials + tile);
-    if (LOSS && a.loss_out) {  // the step's Eq. 4 loss, summed by the last CTA to finish
+    if (OBSV) block_sum_to(lacc + (double)lseg.x + (double)lseg.y, a.loss_partials + tile);
+    if (OBSV && a.loss_out) {  // the step's Eq. 4 loss, summed by the last CTA to finish
         bool mine = false;
         if (tid == 0) {
             __threadfence();  // this tile's partial precedes its ticket
@@ -499,7 +503,9 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
     extern __shared__ __align__(16) float smem_b[];
     constexpr int NB = 3;
     constexpr int VP = kCap + 4;  // speed row pitch: [kCap] = 0 is the leader read of slot 511
-    constexpr bool SGN = GOBS == 1, OBS = GOBS == 2;
+    constexpr bool SGN = GOBS == 1, OBS = GOBS >= 2;
+    constexpr int OKIND = GOBS == 3 ? 0 : 1;  // OBS: Eq. 4 as L1 (GOBS 3) or L2 (GOBS 2)
+    double lacc = 0.0;  // OBS: this thread's Eq. 4 terms (fp32 per segment, fp64 across)
     // fused iteration with delta frozen at 4: dL/d delta is not computed (row 5 written as 0)
     constexpr bool GD = !(D4 && GOBS != 0);
     constexpr int KO = GOBS ? KS + 1 : KS;             // + the rollout's last step (fused)
@@ -580,7 +586,7 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
             if (D4 && r.delta != 4.f)
                 atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
             if (!GOBS) ldj[j] = a.grad_traj[(int64_t)steps * N + i];  // lambda_D^K = dL/dP(K)
-            if (GOBS == 2) pj[j] = a.pos0[i];
+            if (GOBS >= 2) pj[j] = a.pos0[i];
         }
         Pj[j] = make_vehp(r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta);
         Aj[j] = make_veha(r.a_max, r.a_pref, r.v_targ, r.delta, k);
@@ -635,16 +641,18 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
         // checkpoint, bitwise
         const float* cr = ckrow + b * kCkRows * kCap + 2 * tid;
         float2 s = *reinterpret_cast<const float2*>(cr);
-        float2 D = f2(0.f), cmp = f2(0.f);
+        float2 D = f2(0.f), cmp = f2(0.f), lsum = f2(0.f);
         if (OBS) D = *reinterpret_cast<const float2*>(cr + kCap);
         if (OBS && KAHAN) cmp = *reinterpret_cast<const float2*>(cr + 2 * kCap);
 #pragma unroll
         for (int tt = 0; tt < KO; ++tt) {
             if (OBS) {
                 // dL/dP at step t0 + tt (the forward's loss term on the same P bits); the
-                // rollout's last step K adds its term to lambda_D^K below
-                float2 dummy = f2(0.f);
-                if (kFull || tt <= len) g[tt] = loss_term<1>(g[tt], vadd(p0, D), dummy);
+                // rollout's last step K adds its term to lambda_D^K below.  Each row's Eq. 4
+                // term is counted once: rows t0 .. t0 + len - 1, and row K in the last segment
+                float2 lt = f2(0.f);
+                if (kFull || tt <= len) g[tt] = loss_term<OKIND>(g[tt], vadd(p0, D), lt);
+                if (tt < len || (tt == len && seg == nseg - 1)) lsum = vadd(lsum, lt);
             }
             if (tt < KS) {
                 sg[tt] = s;
@@ -662,6 +670,9 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
                     }
                 }
             }
+        }
+        if (OBS) {  // absent vehicles' slots are zero-filled, not NaN: their terms drop here
+            lacc += (val[0] ? (double)lsum.x : 0.0) + (val[1] ? (double)lsum.y : 0.0);
         }
         if (GOBS && seg == nseg - 1) {  // lambda_D^K = dL/dP(K) (static selects, no indexing)
 #pragma unroll
@@ -754,6 +765,7 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
             a.shared_partials[(int64_t)tile * 6 + tid] = x;
         }
     }
+    if (OBS && a.loss_partials) block_sum_to(lacc, a.loss_partials + tile);  // Eq. 4 here
 }
 
 // ------------------------------------------------------------------------------ NK2
@@ -874,6 +886,7 @@ static void launch_fwd_k(const FwdArgs& a, int ntiles, const FwdVariant& var, cu
     if constexpr (KS == 4) {  // the fused idm_fit_step forward exists for 4-step segments
         if (var.loss == 1) { fwd_kernel<D4, KH, false, 1, KS><<<g, b, 0, st>>>(a); return; }
         if (var.loss == 2) { fwd_kernel<D4, KH, false, 2, KS><<<g, b, 0, st>>>(a); return; }
+        if (var.loss == 3) { fwd_kernel<D4, KH, false, 3, KS><<<g, b, 0, st>>>(a); return; }
     }
     if (var.rec_v) fwd_kernel<D4, KH, true, 0, KS><<<g, b, 0, st>>>(a);
     else fwd_kernel<D4, KH, false, 0, KS><<<g, b, 0, st>>>(a);
@@ -961,6 +974,10 @@ static cudaError_t launch_bwd_d(const BwdArgs& a, int ntiles, bool shared, bool 
         if (a.ckpt_every != 4) return cudaErrorInvalidValue;
         if (gobs == 1)  // sign codes: no positions needed, compensation irrelevant
             return launch_bwd_obs<D4, 1, false>(a, ntiles, shared, st, pdl);
+        if (gobs == 3) {  // L1 re-derived from obs and the rebuilt positions
+            if (kahan) return launch_bwd_obs<D4, 3, true>(a, ntiles, shared, st, pdl);
+            return launch_bwd_obs<D4, 3, false>(a, ntiles, shared, st, pdl);
+        }
         if (kahan) return launch_bwd_obs<D4, 2, true>(a, ntiles, shared, st, pdl);
         return launch_bwd_obs<D4, 2, false>(a, ntiles, shared, st, pdl);
     }

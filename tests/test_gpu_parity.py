@@ -476,7 +476,10 @@ def test_launch_count(idm):
     assert sim.launch_count - n0 == 5  # fwd, loss, loss-reduce, bwd, adam
     n1 = sim.launch_count
     sim.fit_step(torch.zeros(w.K + 1, w.n, device="cuda"))
-    assert sim.launch_count - n1 == 2  # fwd+loss (its last CTA sums the loss), bwd+adam
+    assert sim.launch_count - n1 == 2  # L1: fwd+loss (its last CTA sums the loss), bwd+adam
+    n2 = sim.launch_count
+    sim.fit_step(torch.zeros(w.K + 1, w.n, device="cuda"), kind="l2")
+    assert sim.launch_count - n2 == 3  # L2: fwd (history), bwd+loss+adam, loss-reduce
 
 
 # ------------------------------------------------------------- virtual-leader mode
