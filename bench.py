@@ -50,11 +50,12 @@ ISSUE_PER_CLK = 148 * 4 * 32  # SMs x schedulers x lanes (thread-instr / clk)
 
 def alg_bytes(K: int, k: int, path: str) -> dict:
     """Algorithmic HBM bytes per vehicle-step of each kernel."""
-    if path == "vl":  # virtual leader, fused: leaves dp, dv in fwd and bwd; leaf Adam in bwd
+    if path == "vl":  # virtual leader, fused: the forward writes only speed + displacement
+        # checkpoints; the backward derives Eq. 4 from obs; leaf Adam in the backward
         return {
-            "fwd": 8.0 + 4.0 + 4.0 + 4.0 / k + (4 * 2 + 24) / K,  # dp, dv, obs in; dL/dP out
-            # dp, dv, dL/dP, 2x(m, v) in; 2x(x, m, v) out; ckpt; params + Adam per vehicle
-            "bwd": 8.0 + 4.0 + 16.0 + 24.0 + 4.0 / k + (24 + 24 + 8 + 120) / K,
+            "fwd": 8.0 + 8.0 / k + (4 * 2 + 24) / K,  # dp, dv in; (v, D) checkpoints out
+            # dp, dv, obs, 2x(m, v) in; 2x(x, m, v) out; checkpoints; params + Adam per vehicle
+            "bwd": 8.0 + 4.0 + 16.0 + 24.0 + 8.0 / k + (4 + 24 + 24 + 8 + 120) / K,
         }
     if path == "vl_api":
         return {

@@ -22,6 +22,7 @@ struct idm_handle {
     int64_t* tile_start;
     uint8_t* lead;
     float *vt, *ckt, *ckpt_v;     // lane-mode state history (tile-local), VL speed checkpoints
+    float* ckpt_d;                // VL displacement checkpoints (fused iteration)
     uint32_t* sgn;                // fused L1 sign codes (tile-local)
     int64_t vt_stride, ck_stride, sg_stride;
     double *loss_partials, *loss_scalar, *shared_partials;
@@ -81,7 +82,7 @@ int fail(idm_handle* h, int code, const char* fmt, ...) {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-    size_t tile_start, lead, vt, ckt, sgn, ckpt_v, loss_partials, loss_scalar, shared_partials,
+    size_t tile_start, lead, vt, ckt, sgn, ckpt_v, ckpt_d, loss_partials, loss_scalar, shared_partials,
         status, flags, adam_table, tile_ready, done_count, total;
     int64_t vt_stride, ck_stride, sg_stride;  // elements per tile
 };
@@ -167,6 +168,8 @@ bool layout_for(const idm_desc* d, int64_t ntiles, Layout* L) {
     L->sgn = off; off += align256(sizeof(uint32_t) * (size_t)(mt * L->sg_stride));
     // virtual-leader mode: speed checkpoints every 4 steps
     L->ckpt_v = off; off += align256(sizeof(float) * (size_t)(nck * n));
+    L->ckpt_d = off;  // virtual-leader mode: + displacement checkpoints
+    if (d->leader_mode == IDM_LEADER_VIRTUAL) off += align256(sizeof(float) * (size_t)(nck * n));
     L->loss_partials = off;
     int64_t np_ = kLossBlocks > mt ? kLossBlocks : mt;
     if (vl_blocks(n) > np_) np_ = vl_blocks(n);
@@ -303,6 +306,7 @@ VlArgs vl_args(idm_handle* h, int32_t steps) {
     a.grad_traj = h->d.grad_traj;
     a.state_out = h->d.state_out;
     a.ckpt_v = h->ckpt_v;
+    a.ckpt_d = h->ckpt_d;
     a.grad_params = h->d.grad_params;
     a.grad_state0 = h->d.grad_state0;
     a.loss_partials = h->loss_partials;
@@ -467,6 +471,7 @@ int idm_init(idm_handle** out, const idm_desc* d) {
         h->sgn = (uint32_t*)(ws + L.sgn);
         h->sg_stride = L.sg_stride;
         h->ckpt_v = (float*)(ws + L.ckpt_v);
+        h->ckpt_d = (float*)(ws + L.ckpt_d);
         h->loss_partials = (double*)(ws + L.loss_partials);
         h->loss_scalar = (double*)(ws + L.loss_scalar);
         h->shared_partials = (double*)(ws + L.shared_partials);
@@ -801,18 +806,20 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
         VlArgs va = vl_args(h, steps);
         va.obs = obs;
         va.adam = make_adam(h, iter, total_iters, lr0, lr1);
+        // the forward writes only speed and displacement checkpoints; the backward derives
+        // Eq. 4 and dL/dP from obs and the rebuilt positions (no dL/dP rows through HBM)
         {
             TimedLaunch tl(h, IDM_K_FWD);
-            CK(h, launch_vl_fwd(va, h->delta4, 1 + kind, h->st));
+            CK(h, launch_vl_fwd(va, h->delta4, 3, h->st));
+        }
+        {
+            TimedLaunch tl(h, IDM_K_BWD);
+            CK(h, launch_vl_bwd(va, h->delta4, true, h->st, kind));
         }
         {
             TimedLaunch tl(h, IDM_K_REDUCE);
             CK(h, launch_reduce(h->loss_partials, vl_blocks(h->n), 1, h->loss_scalar, nullptr,
                                 h->st));
-        }
-        {
-            TimedLaunch tl(h, IDM_K_BWD);
-            CK(h, launch_vl_bwd(va, h->delta4, true, h->st));
         }
         h->launches += 3;  // the leaves' Adam runs in the backward's reverse sweep
         h->steps = steps;

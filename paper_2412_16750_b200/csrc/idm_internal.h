@@ -116,6 +116,7 @@ struct VlArgs {
     float *vl_grad;  // [2][max_steps][N]
     float *vl_adam_m, *vl_adam_v;  // [2][max_steps][N] (fused leaf Adam)
     float *traj, *grad_traj, *state_out, *ckpt_v, *grad_params, *grad_state0;
+    float* ckpt_d;  // [nseg][N] displacement checkpoints (history-only forward, loss = 3)
     float* vel_traj;  // nullable: record speeds
     const float* obs;
     double* loss_partials;
@@ -166,7 +167,10 @@ cudaError_t launch_reduce(const double* partials, int64_t n, int width, double* 
                           cudaStream_t st);
 cudaError_t launch_adam(const AdamArgs& a, cudaStream_t st);
 cudaError_t launch_vl_fwd(const VlArgs& a, bool delta4, int loss, cudaStream_t st);
-cudaError_t launch_vl_bwd(const VlArgs& a, bool delta4, bool adam, cudaStream_t st);
+// obs_kind = -1: dL/dP rows from grad_traj; 0 / 1: L1 / L2 derived from obs after the
+// history-only forward (loss = 3), fused iteration (adam) only
+cudaError_t launch_vl_bwd(const VlArgs& a, bool delta4, bool adam, cudaStream_t st,
+                          int obs_kind = -1);
 cudaError_t launch_adam_free(float* x, const float* g, float* m, float* v, int64_t n,
                              const AdamArgs& hp, cudaStream_t st);
 int64_t vl_blocks(int64_t n);

@@ -83,18 +83,26 @@ __global__ void __launch_bounds__(kVT) vl_fwd_kernel(VlArgs a) {
     const float2 p0 = make_float2(pj[0], pj[1]);
     float2 v = make_float2(vj[0], vj[1]), D = f2(0.f);
     const Consts k = a.k;
-    float* orow = (LOSS ? a.grad_traj : a.traj) + i0;
+    // LOSS = 3: only the history for a backward that derives Eq. 4 itself -- speed and
+    // displacement checkpoints, no per-step row
+    constexpr bool ROWS = LOSS != 3;
+    constexpr bool OBSV = LOSS == 1 || LOSS == 2;
+    float* orow = ROWS ? (LOSS ? a.grad_traj : a.traj) + i0 : nullptr;
     float* vrow = (!LOSS && a.vel_traj) ? a.vel_traj + i0 : nullptr;
     float* ckv = a.ckpt_v + i0;
+    float* ckd = LOSS == 3 ? a.ckpt_d + i0 : nullptr;
     const float* dpr = a.vl_dp + i0;
     const float* dvr = a.vl_dv + i0;
-    const float* obs = LOSS ? a.obs + i0 : nullptr;
+    const float* obs = OBSV ? a.obs + i0 : nullptr;
     float2 lseg = f2(0.f);
     double lacc = 0.0;
-    st_pair(orow, val0, val1,
-            LOSS ? loss_term<LOSS - 1>(ld_pair(obs, val0, val1, qnan), p0, lseg) : p0);
+    if (ROWS)
+        st_pair(orow, val0, val1,
+                OBSV ? loss_term<(LOSS == 2 ? 1 : 0)>(ld_pair(obs, val0, val1, qnan), p0, lseg)
+                     : p0);
     if (vrow) st_pair(vrow, val0, val1, v);
     st_pair(ckv, val0, val1, v);
+    if (LOSS == 3) st_pair(ckd, val0, val1, D);
     int bad0 = INT_MAX, bad1 = INT_MAX;  // first non-finite checkpoint (reported at the end)
     const int nseg = (steps + KS - 1) / KS;
     for (int seg = 0; seg < nseg; ++seg) {
@@ -103,23 +111,27 @@ __global__ void __launch_bounds__(kVT) vl_fwd_kernel(VlArgs a) {
         if (seg > 0) {
             ckv += N;
             st_pair(ckv, val0, val1, v);
+            if (LOSS == 3) {
+                ckd += N;
+                st_pair(ckd, val0, val1, D);
+            }
             bad0 = (!(isfinite(v.x) && isfinite(D.x)) && bad0 == INT_MAX) ? t0 : bad0;
             bad1 = (!(isfinite(v.y) && isfinite(D.y)) && bad1 == INT_MAX) ? t0 : bad1;
         }
         // this segment's leaf rows (and observation rows) into registers
-        float2 dp[KS], dv[KS], ob[LOSS ? KS : 1];
+        float2 dp[KS], dv[KS], ob[OBSV ? KS : 1];
 #pragma unroll
         for (int tt = 0; tt < KS; ++tt) {
             const bool on = tt < len;
             const int64_t off = (int64_t)(t0 + (on ? tt : 0)) * N;
             dp[tt] = ld_pair(dpr + off, on && val0, on && val1, 10.f);
             dv[tt] = ld_pair(dvr + off, on && val0, on && val1, 0.f);
-            if (LOSS) ob[tt] = ld_pair(obs + off + N, on && val0, on && val1, qnan);
+            if (OBSV) ob[tt] = ld_pair(obs + off + N, on && val0, on && val1, qnan);
         }
 #pragma unroll
         for (int tt = 0; tt < KS; ++tt) {
             if (tt < len) {
-                orow += N;
+                if (ROWS) orow += N;
                 if (vrow) vrow += N;
                 D = vfma(v, k.dt, D);
                 CoreT<float2> c;
@@ -127,11 +139,13 @@ __global__ void __launch_bounds__(kVT) vl_fwd_kernel(VlArgs a) {
                 float2 sdummy = f2(0.f);
                 advance(c, sdummy, v, k);
                 const float2 Pv = vadd(p0, D);
-                st_pair(orow, val0, val1, LOSS ? loss_term<LOSS - 1>(ob[tt], Pv, lseg) : Pv);
+                if (ROWS)
+                    st_pair(orow, val0, val1,
+                            OBSV ? loss_term<(LOSS == 2 ? 1 : 0)>(ob[tt], Pv, lseg) : Pv);
                 if (vrow) st_pair(vrow, val0, val1, v);
             }
         }
-        if (LOSS) {
+        if (OBSV) {
             lacc += (double)lseg.x + (double)lseg.y;
             lseg = f2(0.f);
         }
@@ -153,11 +167,14 @@ __global__ void __launch_bounds__(kVT) vl_fwd_kernel(VlArgs a) {
             a.state_out[N + i] = vend[j];
         }
     }
-    if (LOSS) vl_block_sum(lacc + (double)lseg.x + (double)lseg.y, a.loss_partials);
+    if (OBSV) vl_block_sum(lacc + (double)lseg.x + (double)lseg.y, a.loss_partials);
 }
 
 // ------------------------------------------------------------------------------ backward
-template <bool D4, bool ADAM, int KS>
+// OK = -1: dL/dP rows from grad_traj; 0 / 1 (fused iteration after the history-only forward):
+// the Eq. 4 terms (L1 / L2) and dL/dP from obs and the positions rebuilt from the displacement
+// checkpoints (the forward's own recurrence, bitwise), the loss per block to loss_partials
+template <bool D4, bool ADAM, int KS, int OK>
 __global__ void __launch_bounds__(kVT, 2) vl_bwd_kernel(VlArgs a) {
     const int tid = threadIdx.x;
     const int64_t N = a.n;
@@ -166,7 +183,8 @@ __global__ void __launch_bounds__(kVT, 2) vl_bwd_kernel(VlArgs a) {
     const bool val0 = i0 < N, val1 = i0 + 1 < N;
     const Consts k = a.k;
     const int64_t KN = (int64_t)a.max_steps * N;  // leaf plane stride
-    float ldj[2] = {0.f, 0.f};
+    const float qnan = __int_as_float(0x7fc00000);
+    float ldj[2] = {0.f, 0.f}, pj[2] = {0.f, 0.f};
     VehP Pj[2];
     VehB Bj[2];
 #pragma unroll
@@ -175,7 +193,8 @@ __global__ void __launch_bounds__(kVT, 2) vl_bwd_kernel(VlArgs a) {
         float r[6] = {1.f, 1.f, 1.f, 1.f, 1.f, 4.f};
         if (i < N) {
             vl_params(a.params, a.n_par, i, r);
-            ldj[j] = a.grad_traj[(int64_t)steps * N + i];  // lambda_P^K = dL/dP(K)
+            if (OK < 0) ldj[j] = a.grad_traj[(int64_t)steps * N + i];  // lambda_P^K = dL/dP(K)
+            else pj[j] = a.pos0[i];
         }
         Pj[j] = make_vehp(r[0], r[1], r[2], r[3], r[4], r[5]);
         Bj[j] = make_vehb(r[0], r[1], r[4], r[5]);
@@ -183,6 +202,8 @@ __global__ void __launch_bounds__(kVT, 2) vl_bwd_kernel(VlArgs a) {
     const VehPT<float2> P = pack(Pj[0], Pj[1]);
     const VehBT<float2> B = pack(Bj[0], Bj[1]);
     float2 lv = f2(0.f), lD = make_float2(ldj[0], ldj[1]);
+    const float2 p0 = make_float2(pj[0], pj[1]);
+    double lacc = 0.0;
     GradAccT<float2> G = {f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
     const int nseg = (steps + KS - 1) / KS;
     for (int seg = nseg - 1; seg >= 0; --seg) {
@@ -198,7 +219,8 @@ __global__ void __launch_bounds__(kVT, 2) vl_bwd_kernel(VlArgs a) {
             const int64_t off = (int64_t)(t0 + (on ? tt : 0)) * N + i0;
             dp[tt] = ld_pair(a.vl_dp + off, o0, o1, 10.f);
             dv[tt] = ld_pair(a.vl_dv + off, o0, o1, 0.f);
-            gr[tt] = ld_pair(a.grad_traj + off, o0, o1, 0.f);
+            if (OK < 0) gr[tt] = ld_pair(a.grad_traj + off, o0, o1, 0.f);
+            else gr[tt] = ld_pair(a.obs + off, o0, o1, qnan);  // absent vehicles: missing
             if (ADAM) {
 #pragma unroll
                 for (int pl = 0; pl < 2; ++pl) {
@@ -218,6 +240,22 @@ __global__ void __launch_bounds__(kVT, 2) vl_bwd_kernel(VlArgs a) {
                 advance(c, sdummy, vn, k);
                 vt[tt + 1] = vn;
             }
+        }
+        if (OK >= 0) {  // positions by the forward's recurrence, then Eq. 4 and dL/dP
+            float2 D = ld_pair(a.ckpt_d + (int64_t)seg * N + i0, val0, val1, 0.f);
+            float2 lsum = f2(0.f);
+#pragma unroll
+            for (int tt = 0; tt < KS; ++tt) {
+                if (tt < len) {
+                    gr[tt] = loss_term<(OK > 0 ? 1 : 0)>(gr[tt], vadd(p0, D), lsum);
+                    D = vfma(vt[tt], k.dt, D);
+                }
+            }
+            if (seg == nseg - 1)  // lambda_P^K = dL/dP(K), the rollout's last row
+                lD = loss_term<(OK > 0 ? 1 : 0)>(
+                    ld_pair(a.obs + (int64_t)steps * N + i0, val0, val1, qnan), vadd(p0, D),
+                    lsum);
+            lacc += (double)lsum.x + (double)lsum.y;
         }
         // reverse sweep
 #pragma unroll
@@ -279,6 +317,7 @@ __global__ void __launch_bounds__(kVT, 2) vl_bwd_kernel(VlArgs a) {
             if (ADAM && ((a.adam.opt_mask >> q) & 1u)) adam_update(a.adam, q, q * N + i, gr6[q]);
         }
     }
+    if (OK >= 0) vl_block_sum(lacc, a.loss_partials);  // this block's Eq. 4 loss
 }
 
 // Adam over unconstrained leaves (same update as adam_update, no box).
@@ -303,6 +342,7 @@ static void vl_fwd_d(const VlArgs& a, int loss, cudaStream_t st) {
     dim3 g((unsigned)vl_blocks(a.n)), b(kVT);
     if (loss == 1) vl_fwd_kernel<D4, 1, 4><<<g, b, 0, st>>>(a);
     else if (loss == 2) vl_fwd_kernel<D4, 2, 4><<<g, b, 0, st>>>(a);
+    else if (loss == 3) vl_fwd_kernel<D4, 3, 4><<<g, b, 0, st>>>(a);
     else vl_fwd_kernel<D4, 0, 4><<<g, b, 0, st>>>(a);
 }
 
@@ -313,16 +353,21 @@ cudaError_t launch_vl_fwd(const VlArgs& a, bool delta4, int loss, cudaStream_t s
     return cudaGetLastError();
 }
 
-cudaError_t launch_vl_bwd(const VlArgs& a, bool delta4, bool adam, cudaStream_t st) {
-    if (a.ckpt_every != 4) return cudaErrorInvalidValue;
+template <bool D4>
+static void vl_bwd_d(const VlArgs& a, bool adam, int obs_kind, cudaStream_t st) {
     dim3 g((unsigned)vl_blocks(a.n)), b(kVT);
-    if (delta4) {
-        if (adam) vl_bwd_kernel<true, true, 4><<<g, b, 0, st>>>(a);
-        else vl_bwd_kernel<true, false, 4><<<g, b, 0, st>>>(a);
-    } else {
-        if (adam) vl_bwd_kernel<false, true, 4><<<g, b, 0, st>>>(a);
-        else vl_bwd_kernel<false, false, 4><<<g, b, 0, st>>>(a);
-    }
+    if (!adam) vl_bwd_kernel<D4, false, 4, -1><<<g, b, 0, st>>>(a);
+    else if (obs_kind == 0) vl_bwd_kernel<D4, true, 4, 0><<<g, b, 0, st>>>(a);
+    else if (obs_kind == 1) vl_bwd_kernel<D4, true, 4, 1><<<g, b, 0, st>>>(a);
+    else vl_bwd_kernel<D4, true, 4, -1><<<g, b, 0, st>>>(a);
+}
+
+cudaError_t launch_vl_bwd(const VlArgs& a, bool delta4, bool adam, cudaStream_t st,
+                          int obs_kind) {
+    if (a.ckpt_every != 4) return cudaErrorInvalidValue;
+    if (obs_kind >= 0 && !adam) return cudaErrorInvalidValue;  // the fused iteration only
+    if (delta4) vl_bwd_d<true>(a, adam, obs_kind, st);
+    else vl_bwd_d<false>(a, adam, obs_kind, st);
     return cudaGetLastError();
 }
 
