@@ -174,8 +174,11 @@ int idm_adam_step(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, f
    from obs and the rebuilt positions, and one fixed-order reduction sums the losses (3
    launches) (shared mode: + reduce + Adam launches; the shared gradient is THIS
    process's sum, so with several ranks use the separate calls and all-reduce between
-   idm_backward and idm_adam_step -- the Python binding refuses the fused calls there).  traj and grad_traj are NOT written on this path; with any
-   other ckpt_every the defining sequence runs as is (and writes them).
+   idm_backward and idm_adam_step -- the Python binding refuses the fused calls there).  traj
+   and grad_traj are NOT written on this path.  With any other ckpt_every, and for
+   latency-bound shapes (lane tiles <= half the SMs and >= 1000 steps, e.g. C3's 6 tiles x
+   27,000 steps, where the separate kernels are faster), the defining sequence runs as is (and
+   writes them); IDM_FUSED_ALWAYS=1 disables the latter.
    obs: device [(steps+1)][N]; missing observations are NaN (mask must be NULL).  Loss to
    *loss_dev / *loss_host as in idm_loss_grad. */
 int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* mask,

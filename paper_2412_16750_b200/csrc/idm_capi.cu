@@ -18,6 +18,7 @@ struct idm_handle {
     cudaStream_t st;
     int64_t n, n_par;
     int ntiles, nck;
+    int num_sms;  // of the handle's device
     // workspace carve-outs
     int64_t* tile_start;
     uint8_t* lead;
@@ -505,6 +506,13 @@ int idm_init(idm_handle** out, const idm_desc* d) {
         }
         if (ce == cudaSuccess) { what = "smem attributes"; ce = kernels_configure(d->ckpt_every); }
         if (ce == cudaSuccess) {
+            what = "device attributes";
+            int dev = 0;
+            ce = cudaGetDevice(&dev);
+            if (ce == cudaSuccess)
+                ce = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        if (ce == cudaSuccess) {
             what = "copy stream";
             ce = cudaStreamCreateWithFlags(&h->copy_st, cudaStreamNonBlocking);
         }
@@ -836,9 +844,14 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
         }
         return IDM_OK;
     }
-    if (h->d.ckpt_every != 4) {
-        // the fused kernels are specialised to 4-step segments; any other interval runs the
-        // defining sequence itself (same arithmetic, same bits)
+    // Latency-bound shapes (a few lane tiles, long horizon: C3's 6 tiles x 27,000 steps) run
+    // faster as the defining sequence: there each warp's in-order instruction stream sets the
+    // pace, and the fused forward's Eq. 4 work lengthens it (C3: 11.8 vs 12.6 ms).
+    const bool latency_bound = 2 * h->ntiles <= h->num_sms && steps >= 1000 && h->d.traj &&
+                               h->d.grad_traj && !std::getenv("IDM_FUSED_ALWAYS");
+    if (h->d.ckpt_every != 4 || latency_bound) {
+        // the fused kernels are specialised to 4-step segments; any other interval (and a
+        // latency-bound shape) runs the defining sequence itself (same arithmetic, same bits)
         int s = idm_forward(h, steps);
         if (s == IDM_OK) s = idm_loss_grad(h, obs, nullptr, kind, loss_dev, nullptr);
         if (s == IDM_OK) s = idm_backward(h);

@@ -753,9 +753,14 @@ def test_degenerate_starts(idm, oracle):
     assert worst <= 1.0
 
 
-def test_fused_long_horizon_kahan(idm, oracle):
+@pytest.mark.parametrize("fused", [True, False])
+def test_fused_long_horizon_kahan(idm, oracle, fused, monkeypatch):
     """idm_fit_step beyond 2,000 steps (compensated displacement in the fused forward; the L2
-    backward rebuilds compensated positions) equals the separate calls bit for bit."""
+    backward rebuilds compensated positions) equals the separate calls bit for bit -- with the
+    fused kernels forced (IDM_FUSED_ALWAYS: one tile over 2,500 steps is a latency-bound shape)
+    and with the library's own choice (the defining sequence there)."""
+    if fused:
+        monkeypatch.setenv("IDM_FUSED_ALWAYS", "1")
     w = synth.make_workload("C3", lane_sizes=[60, 60], K=2500, seed=3)
     obs = torch.as_tensor(synth.kinematic_obs(w), device="cuda")
     for kind in ("l1", "l2"):
