@@ -194,6 +194,8 @@ __device__ __forceinline__ void cp_async_wait() {
 // LOSS = 1 (L1) / 2 (L2): fused Eq. 4 for idm_fit_step -- observation rows staged two segments
 // ahead (cp.async ring); each step sums Eq. 4 against the fresh positions and, for L1, records
 // dL/dP = -sign(obs - P) as a 4-bit code per thread-step; P and dL/dP are not written.
+// LOSS = 3: fused iteration whose backward derives Eq. 4 from obs (L2 by default): only the
+// tile history -- speeds, and gap + displacement checkpoints.
 // CK = checkpoint interval (the backward's segment length); the forward's own prefetch
 // segment is KS = max(4, CK) steps, so CK | KS and checkpoints fall at static positions.
 #ifndef IDM_FWD_LOSS_MINB
@@ -472,8 +474,9 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
 //   GOBS = 0:      dL/dP rows from grad_traj (idm_backward after idm_loss_grad);
 //   GOBS = 1:      fused idm_fit_step, L1 -- dL/dP = -sign(obs - P) from the forward's sign
 //                  codes (2 bits per vehicle-step);
-//   GOBS = 2:      fused idm_fit_step, L2 -- dL/dP re-derived from obs and the rebuilt positions
-//                  P = p0 + D with the forward's loss term (same bits as idm_loss_grad).
+//   GOBS = 2 / 3:  fused idm_fit_step, L2 / L1 -- dL/dP re-derived from obs and the rebuilt
+//                  positions P = p0 + D with the loss kernel's term (same bits as idm_loss_grad);
+//                  with loss_partials set, this tile's Eq. 4 loss as well (LOSS = 3 forward).
 // Gradient accumulators stay in registers for the whole rollout; ADAM: per-vehicle Adam in the
 // epilogue (idm_fit_step).
 template <bool D4, bool SHARED, bool ADAM, int KS, int GOBS, bool KAHAN>
