@@ -499,7 +499,8 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
     const int tail = steps - (nseg - 1) * KS;  // length of the last segment (1..KS)
 
 
-    // Segment rows are staged in shared memory, two segments ahead, in a ring of 3 buffers:
+    // Segment rows are staged in shared memory, one to two segments ahead, in a ring of 3
+    // buffers (each refill is issued at the end of a segment):
     // speeds and the checkpoint by bulk copy (one thread, mbarrier-counted), dL/dP rows (or the
     // observation rows, plus one for the rollout's last step) by per-thread cp.async.  No
     // register holds data in flight.
@@ -682,7 +683,6 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
             for (int tt = 0; tt < KO; ++tt)
                 if (tt == len) e = vmul(g[tt], k.dt2);
         }
-        if (seg > 1) fetch(seg - 2, KS);
         // reverse sweep t = t0 + len - 1 ... t0; the local Jacobian of the next step down is
         // independent of the adjoint chain, so the scheduler overlaps it with this one
 #pragma unroll
@@ -700,6 +700,10 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
                 par ^= 1;
             }
         }
+        // refill the ring after the sweep: the elected thread's bulk-copy issue (~20
+        // instructions) sits off the first step's barrier, where it held every warp
+        // (backward 1.61 -> 1.51 ms); the rows still arrive a segment ahead of their use
+        if (seg > 1) fetch(seg - 2, KS);
     };
     int seg = nseg - 1;
     if (tail < KS) segment(seg--, tail, std::false_type{});
