@@ -396,7 +396,6 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     auto obs_ready = [&](int seg) {
         if (OBSV) {
             cp_async_wait<OR - 2>();  // this segment's group; later ones may stay in flight
-            fetch_obs(seg + OR - 1);
         }
     };
     auto obs_done = [&] { cslot = cslot == OR - 1 ? 0 : cslot + 1; };
@@ -413,6 +412,8 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
             lacc += (double)lseg.x + (double)lseg.y;
             lseg = f2(0.f);
         }
+        // refill after the segment's steps (its reads of the refilled slot are long done)
+        if (OBSV) fetch_obs(seg + OR - 1);
     }
     if (tail > 0) {
         obs_ready(nfull);
