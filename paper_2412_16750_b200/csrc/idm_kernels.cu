@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     constexpr int kR2 = kCap / 2;  // one row in float2 units
     const float* obs = OBSV ? a.obs + i0 : nullptr;
     const float qnan = __int_as_float(0x7fc00000);
-    // LOSS: observation rows staged two segments ahead in a 3-buffer shared-memory ring by
+    // LOSS: observation rows staged ahead (refilled after each segment) in a 3-buffer ring by
     // per-thread cp.async; the slots of absent vehicles hold NaN (= missing) from the start and
     // are never copied to; one commit group per segment (empty past the end) keeps
     // cp.async.wait_group<1> exact
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     auto ld_obs = [&](const float* o, bool on) {  // absent vehicles observe NaN (= missing)
         return make_float2(ld_cs_if(o, on && val[0], qnan), ld_cs_if(o + 1, on && val[1], qnan));
     };
-    // segment seg observes rows seg*KS + 1 .. seg*KS + KS; fetches run two segments ahead of
+    // segment seg observes rows seg*KS + 1 .. seg*KS + KS; fetches run up to two segments ahead of
     // use, slots rotate 0, 1, 2 (fslot: next fetch, cslot: current use)
     const float* onext = OBSV ? obs + N : nullptr;  // first row of the next fetch
     int fslot = 0, cslot = 0;
