@@ -506,7 +506,10 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
     // observation rows, plus one for the rollout's last step) by per-thread cp.async.  No
     // register holds data in flight.
     extern __shared__ __align__(16) float smem_b[];
-    constexpr int NB = 3;
+#ifndef IDM_BWD_RING
+#define IDM_BWD_RING 3  // staging ring buffers of the backward (rows NB - 1 segments ahead)
+#endif
+    constexpr int NB = IDM_BWD_RING;
     constexpr int VP = kCap + 4;  // speed row pitch: [kCap] = 0 is the leader read of slot 511
     constexpr bool SGN = GOBS == 1, OBS = GOBS >= 2;
     constexpr int OKIND = GOBS == 3 ? 0 : 1;  // OBS: Eq. 4 as L1 (GOBS 3) or L2 (GOBS 2)
@@ -575,7 +578,9 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
     };
     int par = 0;
     fetch(nseg - 1, tail);
-    if (nseg > 1) fetch(nseg - 2, KS);
+#pragma unroll
+    for (int q = 2; q <= NB - 1; ++q)
+        if (nseg >= q) fetch(nseg - q, KS);
     // per-vehicle constants while the first two segments' rows are in flight
     float ldj[2], pj[2];
     VehP Pj[2];
@@ -610,7 +615,9 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
         mbar_wait(&mbar[b], (phase >> b) & 1u);
         phase ^= 1u << b;
         if (!SGN) {
-            if (seg > 0) cp_async_wait<1>();  // this segment's rows; seg - 1's may stay in flight
+            // this segment's rows; the (up to NB - 2) later segments' may stay in flight
+            if (NB >= 4 && seg >= 2) cp_async_wait<(NB >= 4 ? 2 : 1)>();
+            else if (seg >= 1) cp_async_wait<1>();
             else cp_async_wait<0>();
         }
         const float* orr = orow + b * KO * kCap + 2 * tid;
@@ -704,7 +711,7 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
         // refill the ring after the sweep: the elected thread's bulk-copy issue (~20
         // instructions) sits off the first step's barrier, where it held every warp
         // (backward 1.61 -> 1.51 ms); the rows still arrive a segment ahead of their use
-        if (seg > 1) fetch(seg - 2, KS);
+        if (seg > NB - 2) fetch(seg - (NB - 1), KS);
     };
     int seg = nseg - 1;
     if (tail < KS) segment(seg--, tail, std::false_type{});
@@ -926,8 +933,8 @@ cudaError_t kernels_configure(int ckpt_every) {
 }
 
 template <int KS, int GOBS>
-constexpr size_t bwd_smem_of() {  // ring of 3: speed + checkpoint + dL/dP/obs (or sign) rows
-    return (size_t)3 *
+constexpr size_t bwd_smem_of() {  // ring of NB: speed + checkpoint + dL/dP/obs (or sign) rows
+    return (size_t)IDM_BWD_RING *
            (KS * (kCap + 4) + kCkRows * kCap +
             (GOBS == 1 ? kCap / 2 : (GOBS ? KS + 1 : KS) * kCap)) *
            sizeof(float);
