@@ -883,7 +883,7 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
     // default: 2 bits per vehicle-step cross to the backward), or the forward writes only the
     // tile history and the backward derives Eq. 4 from obs and the rebuilt positions (L2
     // default: L2's dL/dP needs the residual, so obs would otherwise be read twice).  C4: L1
-    // 2.71 vs 2.70 ms, L2 3.13 vs 2.67 ms.  IDM_FUSED_OBS_BWD=0/1 forces one for both kinds.
+    // 2.61 (codes) vs 2.75 ms, L2 3.13 vs 2.70 ms (obs).  IDM_FUSED_OBS_BWD=0/1 forces one.
     static const int obs_env = [] {
         const char* e = std::getenv("IDM_FUSED_OBS_BWD");
         return e ? (e[0] == '1' ? 1 : 0) : -1;
