@@ -174,6 +174,13 @@ __device__ __forceinline__ void cp_async4_if(float* dst, const float* src, bool 
                  "l"(src), "r"((int)on)
                  : "memory");
 }
+// 8-byte cp.async issued only when `on` (both addresses 8-byte aligned)
+__device__ __forceinline__ void cp_async8_if(float* dst, const float* src, bool on) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n"
+                 " @q cp.async.ca.shared.global [%0], [%1], 8;\n}" ::"r"(smem_u32(dst)),
+                 "l"(src), "r"((int)on)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() {
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -255,16 +262,27 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     // use, slots rotate 0, 1, 2 (fslot: next fetch, cslot: current use)
     const float* onext = OBSV ? obs + N : nullptr;  // first row of the next fetch
     int fslot = 0, cslot = 0;
+    // pairs are 8-byte aligned in every row when the tile starts at an even vehicle, N is even
+    // and the array is 8-byte aligned (CTA-uniform)
+    const bool pair8 = OBSV && ((base | N) & 1) == 0 && ((uintptr_t)a.obs & 7) == 0;
     auto fetch_obs = [&](int seg) {
         const int r0 = seg * KS + 1;
         float* dst = &obuf[fslot][0][2 * tid];
         fslot = fslot == OR - 1 ? 0 : fslot + 1;
         if (r0 + KS - 1 <= steps) {  // whole segment inside the rollout (CTA-uniform)
             const float* o = onext;
+            if (pair8) {  // both vehicles in one 8-byte copy (the lone last vehicle: 4 bytes)
 #pragma unroll
-            for (int tt = 0; tt < KS; ++tt, o += N) {
-                cp_async4_if(dst + tt * kCap, o, val[0]);
-                cp_async4_if(dst + tt * kCap + 1, o + 1, val[1]);
+                for (int tt = 0; tt < KS; ++tt, o += N) {
+                    cp_async8_if(dst + tt * kCap, o, val[1]);
+                    cp_async4_if(dst + tt * kCap, o, val[0] && !val[1]);
+                }
+            } else {
+#pragma unroll
+                for (int tt = 0; tt < KS; ++tt, o += N) {
+                    cp_async4_if(dst + tt * kCap, o, val[0]);
+                    cp_async4_if(dst + tt * kCap + 1, o + 1, val[1]);
+                }
             }
             onext = o;
         } else {  // the tail / past the end: predicated, addresses kept inside the array
