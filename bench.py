@@ -1,22 +1,31 @@
 #!/usr/bin/env python
 """Benchmark of the B200 IDM hot path (arXiv 2412.16750) -- one JSON line on rank 0.
 
-A "step" is one pass of the whole hot path over one batch: idm_forward(K) -> idm_loss_grad
-(Eq. 4, L1) -> idm_backward -> idm_adam_step, on config C4 of BASELINE.json (2M vehicles in
-20,000 lanes x 100, K = 300 steps of dt = 0.1 s, per-vehicle parameters, checkpoint k = 16).
-value = vehicle-steps/s over all ranks = ranks * N * K / max-over-ranks(step time).
+A "step" is one pass of the whole hot path over one batch: forward(K) -> Eq. 4 (L1) -> backward
+-> Adam, on config C4 of BASELINE.json (2M vehicles in 20,000 lanes x 100, K = 300 steps of
+dt = 0.1 s, per-vehicle parameters).  The headline path is the fused idm_fit_step (2 launches,
+checkpoint interval k = 4, the library default); the 5-call API path, the forward alone, the
+CUDA-graph loop, the end-to-end host path and the virtual-leader mode are reported beside it.
+value = vehicle-steps/s over all ranks = (sum of the ranks' N) * K / max-over-ranks(step time).
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--scaling weak|strong]
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--scaling strong|weak]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
+With --gpus N > 1 and no torchrun environment, bench.py launches the N ranks itself (torchrun,
+127.0.0.1) -- or fails loudly if this host has fewer than N GPUs.  At N > 1 the headline is the
+2M-vehicle strong split (BASELINE.json: "at 2M vehicles, 1/2/4/8 B200"); the weak-scaling
+number (2M vehicles per rank) is a secondary field.
+
 --impl reference times the fp64 CPU oracle (oracle/, the only other program of this method
-here) on the host cores, on a bounded sample of the same workload.
+here) on all host cores, on a bounded sample of the same workload.
 """
 from __future__ import annotations
 
 import argparse
+import concurrent.futures as cf
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -30,26 +39,24 @@ sys.path.insert(0, ROOT)
 
 from paper_2412_16750_b200 import parallel, synth  # noqa: E402
 
-LANE_VEH = 100
 WORKLOAD = "C4"  # the headline configuration (BASELINE.json configs[3]); --config selects others
-# Frozen algorithmic counts: thread-instructions (issue slots) per
-# vehicle-step that any implementation of the kernel's math must issue, and HBM bytes per
-# vehicle-step the method must move at k = 16, K = 300.
-ALG_INSTR = {"fwd": 36.0, "bwd": 114.0}  # SURVEY.md 8(d) frozen essential-op counts
-# The same essential math counted in issue slots of THIS implementation, where two vehicles'
-# FP32 multiply-adds issue as one f32x2 instruction: the frozen scalar
-# counts over-credit a packed kernel, so both fractions are reported.
-# "bwd_fit": the optimizer-path backward with delta frozen at 4 (the paper's five parameters,
-# PAPER.md:208), which does not compute dL/d delta (one log2, one max, one multiply, one FMA per
-# vehicle-step fewer: 3 slots per vehicle-step; R#1).  The counts are after the
-# constant folding of DESIGN.md "Adjoint scaling" (lane heads at gap +inf: -0.5 slot per
-# vehicle-step forward and backward; dt and ln2 in per-vehicle constants: -1 backward).
+# Essential issue slots (thread-instructions) per vehicle-step:
+# SURVEY.md 8(d)'s frozen scalar counts (the survey commit: 36 forward, 114 backward, 150 both)
+# and the same essential math counted for THIS implementation, where two vehicles' FP32
+# multiply-adds issue as one f32x2 instruction (SURVEY 8(d) addendum).  "bwd_fit": the
+# optimizer-path backward with delta frozen at 4 (no dL/d delta, R#1).
+ALG_INSTR = {"fwd": 36.0, "bwd": 114.0}
 PACKED_INSTR = {"fwd": 20.5, "bwd": 44.0, "bwd_fit": 41.0}
 ISSUE_PER_CLK = 148 * 4 * 32  # SMs x schedulers x lanes (thread-instr / clk)
+# SURVEY.md 8(d) algorithmic HBM bytes per vehicle-step of the method's variants (k = 32 there):
+# forward with the trajectory record 4.5; fwd+bwd through the API 21.0; with the loss inside the
+# kernels (obs read twice) 9.0 -- the variant the fused idm_fit_step implements; single launch 4.2
+SURVEY_BYTES = {"fwd": 4.5, "api": 21.0, "fused": 9.0, "single_launch": 4.2}
 
 
 def alg_bytes(K: int, k: int, path: str) -> dict:
-    """Algorithmic HBM bytes per vehicle-step of each kernel."""
+    """HBM bytes per vehicle-step each kernel of this implementation moves by design
+    (DESIGN.md section 4): the method's bytes plus the speed history the design stores."""
     if path == "vl":  # virtual leader, fused: the forward writes only speed + displacement
         # checkpoints; the backward derives Eq. 4 from obs; leaf Adam in the backward
         return {
@@ -73,6 +80,8 @@ def alg_bytes(K: int, k: int, path: str) -> dict:
             "bwd": 8.0 + 4.0 / k + (24 + 24 + 8 + 1) / K,       # speed + dL/dP rows, ckpt, params
             "adam": 6 * 28.0 / K,                               # x, g, m, v in; x, m, v out
         }
+    if path == "fwd_only":  # prediction rollout (IDM_FWD_NO_HISTORY): P rows only
+        return {"fwd": 4.0 + (4 * 4 + 24 + 1) / K}
     if path == "fused_l2":  # the forward sums Eq. 4; the backward re-derives dL/dP from obs
         return {
             "fwd": 4.0 + 4.0 + 8.0 / k + (4 * 4 + 24 + 1) / K,  # obs in; speeds, gap + D out
@@ -86,10 +95,9 @@ def alg_bytes(K: int, k: int, path: str) -> dict:
     }
 
 
-def load_traffic():
-    """ncu dram bytes per launch of the dominant kernel, from the committed capture summary."""
+def _load_json(rel):
     try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+        with open(os.path.join(ROOT, rel)) as f:
             return json.load(f)
     except Exception:
         return {}
@@ -114,7 +122,6 @@ class ClockSampler:
 
     def __init__(self, gpu_index: int):
         self.samples = []
-        self.window = None
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active")
         try:
             self.p = subprocess.Popen(
@@ -164,30 +171,101 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------- workload
 def make_rank_workload(rank: int, world: int, scaling: str):
+    """strong: the 2M-vehicle C4 workload split in contiguous whole-lane shards;
+    weak: every rank its own C4-sized workload (seed per rank)."""
     if scaling == "weak" or world == 1:
-        w = synth.make_workload(WORKLOAD, seed=synth.CONFIGS[WORKLOAD]["seed"] + 1000 * rank)
-    else:
-        full = synth.make_workload(WORKLOAD)
-        l0, l1 = parallel.shard_lanes(full.n_lanes, world, rank)
-        w = synth.lane_subset(full, np.arange(l0, l1))
-    return w
+        return synth.make_workload(WORKLOAD, seed=synth.CONFIGS[WORKLOAD]["seed"] + 1000 * rank)
+    full = synth.make_workload(WORKLOAD)
+    l0, l1 = parallel.shard_lanes(full.n_lanes, world, rank)
+    return synth.lane_subset(full, np.arange(l0, l1))
 
 
-def cpu_baseline(lanes: int, K: int, seed: int = 99):
-    """The fp64 oracle as it stands, single-threaded, one full step (rollout, Eq. 4 L1 loss,
-    adjoint, Adam) on the first `lanes` lanes of the configured workload."""
+# ------------------------------------------------------------------ oracle on the host cores
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def _oracle_inputs(full, lanes, K):
     from oracle import oracle as O
-    full = synth.make_workload(WORKLOAD, seed=seed)
-    w = synth.lane_subset(full, np.arange(min(lanes, full.n_lanes)))
+    w = synth.lane_subset(full, lanes)
     w.K = K
     obs = synth.kinematic_obs(w).astype(np.float64)
     st = dict(leader=O.leader_from_lanes(w.lane_offsets), length=w.length, p0=w.p0, v0=w.v0,
               params=synth.init_params(w.n).astype(np.float64), m1=np.zeros((6, w.n)),
               m2=np.zeros((6, w.n)))
+    return w.n * K, st, obs
+
+
+def oracle_step(lanes: int, K: int, threads: int, seed: int = 99):
+    """The fp64 oracle as it stands (oracle.fit_iteration: rollout, Eq. 4 L1, adjoint, Adam) on
+    the first `lanes` lanes of the workload, one full step, over `threads` host threads: whole
+    lanes per task (the adjoint scatters into leaders, so lanes are the unit of parallelism;
+    the C oracle releases the GIL).  Inputs are prepared before the timed region.
+    Returns (vehicle-steps, seconds)."""
+    from oracle import oracle as O
+    full = synth.make_workload(WORKLOAD, seed=seed)
+    lanes = min(lanes, full.n_lanes)
+    chunks = [c for c in np.array_split(np.arange(lanes), max(1, 4 * threads)) if len(c)]
+    work = [_oracle_inputs(full, c, K) for c in chunks]
     t0 = time.perf_counter()
-    O.fit_iteration(st, obs, 0)
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(lambda x: O.fit_iteration(x[1], x[2], 0), work))
     dt = time.perf_counter() - t0
-    return w.n * K, dt
+    return sum(x[0] for x in work), dt
+
+
+def oracle_c1_fit_seconds() -> float:
+    """The paper's whole 500-iteration fit of C1 by the oracle."""
+    from oracle import oracle as O
+    w = synth.make_workload("C1")
+    obs = synth.kinematic_obs(w).astype(np.float64)
+    st = dict(leader=O.leader_from_lanes(w.lane_offsets), length=w.length, p0=w.p0, v0=w.v0,
+              params=synth.init_params(w.n).astype(np.float64), m1=np.zeros((6, w.n)),
+              m2=np.zeros((6, w.n)))
+    t0 = time.perf_counter()
+    for it in range(500):
+        O.fit_iteration(st, obs, it)
+    return time.perf_counter() - t0
+
+
+def sample_lanes(K: int, cpu_seconds: float) -> int:
+    """Lanes of the workload that take about `cpu_seconds` of single-core oracle work."""
+    vs, t = oracle_step(8, K, 1)
+    per_lane = t / 8
+    return int(max(1, min(synth.CONFIGS[WORKLOAD].get("lanes", 10 ** 9), cpu_seconds / per_lane)))
+
+
+def cpu_baseline(K: int, cpu_seconds: float) -> dict:
+    cores = host_cores()
+    lanes = sample_lanes(K, cpu_seconds)
+    vs, t = oracle_step(lanes, K, cores)
+    out = {"value": vs / t, "unit": "vehicle-steps/s", "cores": cores, "kind": "oracle",
+           "cpu_model": cpu_model(),
+           "sample": f"first {lanes} lanes x {K} steps of {WORKLOAD} ({vs:.3g} vehicle-steps), "
+                     f"one full step (fp64 rollout + Eq.4 L1 + adjoint + Adam), whole lanes over "
+                     f"{cores} threads, {t:.2f} s wall"}
+    if cores >= 16:  # the paper's CPU setting: 16 threads (PAPER.md:253, Xeon W-2255)
+        vs16, t16 = oracle_step(lanes, K, 16)
+        out["threads_16"] = {"value": vs16 / t16, "seconds": t16}
+    else:
+        out["threads_16"] = f"not run: the host has {cores} cores"
+    vs1, t1 = oracle_step(max(1, lanes // max(1, cores)), K, 1)
+    out["threads_1"] = {"value": vs1 / t1, "seconds": t1}
+    out["c1_full_fit_s"] = oracle_c1_fit_seconds()
+    return out
 
 
 def run_reference(args, rank, world):
@@ -195,27 +273,31 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     K = synth.CONFIGS[WORKLOAD]["K"]
-    vs, t = cpu_baseline(4, K)
-    per_lane = t / min(4, synth.make_workload(WORKLOAD).n_lanes)
-    budget = args.ref_budget  # seconds for the whole --warmup + --steps run
-    lanes = int(max(1, min(20000, budget / max(1, args.steps + args.warmup) / per_lane)))
+    cores = host_cores()
+    # each step a bounded sample sized so the whole --warmup + --steps run ends in ~ref_budget s
+    vs, t = oracle_step(8, K, 1)
+    per_lane_core = t / 8
+    per_step = args.ref_budget / max(1, args.steps + args.warmup)
+    lanes = int(max(1, min(synth.CONFIGS[WORKLOAD].get("lanes", 10 ** 9),
+                           per_step * 0.8 * cores / per_lane_core)))
     for _ in range(args.warmup):
-        cpu_baseline(lanes, K)
+        oracle_step(lanes, K, cores)
     tot_vs, tot_t = 0, 0.0
     for i in range(args.steps):
-        vs, t = cpu_baseline(lanes, K, seed=100 + i)
+        vs, t = oracle_step(lanes, K, cores, seed=100 + i)
         tot_vs += vs
         tot_t += t
     value = tot_vs / tot_t
-    sample = (f"first {lanes} lanes x {K} steps of {WORKLOAD} per step "
-              f"(rollout + Eq.4 L1 + adjoint + Adam, fp64, single thread)")
+    sample = (f"first {lanes} lanes x {K} steps of {WORKLOAD} per step (rollout + Eq.4 L1 + "
+              f"adjoint + Adam, fp64), whole lanes over {cores} host threads ({cpu_model()})")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "vehicle-steps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * tot_t / max(1, args.steps), "higher_is_better": True,
+        "scaling": "strong" if args.gpus > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD_DESC, "sample": sample},
-        "cpu_baseline": {"value": value, "unit": "vehicle-steps/s", "cores": 1,
+        "cpu_baseline": {"value": value, "unit": "vehicle-steps/s", "cores": cores,
                          "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "vehicle-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -245,6 +327,11 @@ def set_config(name: str):
         METRIC = "vehicle-steps/s, forward+loss+backward+Adam (" + name + ")"
 
 
+# ------------------------------------------------------------------------------- our arm
+def _events(torch):
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -252,91 +339,100 @@ def run_ours(args, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank % torch.cuda.device_count())
     torch.cuda.set_device(dev)
-    w = make_rank_workload(rank, world, args.scaling)
+    scaling = args.scaling or ("strong" if world > 1 else "weak")
+    w = make_rank_workload(rank, world, scaling)
     vl = args.leader == "virtual"
     K, k = w.K, (4 if vl else (args.ckpt or idm.DEFAULT_CKPT))
-    # synthetic observations: truth rollout with theta_true (our forward) + N(0, 0.3^2)
-    stage = 2 if args.e2e > 0 else 0  # e2e: two alternating observation staging buffers
-    sim = idm.from_workload(w, w.theta_true, max_steps=K, ckpt_every=k, stage_obs=stage)
-    sim.forward(K)
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    obs = sim.traj.clone()
-    obs[1:].add_(torch.randn(obs[1:].shape, device=dev, generator=gen), alpha=0.3)
-    if vl:  # the paper's per-trajectory fit: free leader terms
-        sim.close()
-        del sim
-        torch.cuda.empty_cache()
-        sim = idm.from_workload(w, None, max_steps=K, ckpt_every=k, stage_obs=stage,
-                                virtual_leader=True)
-    init = torch.as_tensor(synth.init_params(w.n), device=dev)
-    stream = sim.stream
-    vsteps = float(w.n) * K * world
+    n_total = parallel.sum_over_ranks(w.n)
+    vsteps = float(n_total) * K  # whole job, per step
+    clocks = ClockSampler(local_rank)
+    clocks.wait_first()
 
-    def reset():
-        sim.params.copy_(init)
-        sim.adam_m.zero_()
-        sim.adam_v.zero_()
-        if vl:
-            sim.vl_dp.fill_(idm.VL_INIT[0])
-            sim.vl_dv.fill_(idm.VL_INIT[1])
-            sim.vl_adam_m.zero_()
-            sim.vl_adam_v.zero_()
+    def build(wl, virtual):
+        """A handle on workload wl with synthetic observations: the truth rollout with
+        theta_true (our forward) + N(0, 0.3^2)."""
+        stage = 2 if args.e2e > 0 and not virtual else 0
+        s = idm.from_workload(wl, wl.theta_true, max_steps=wl.K, ckpt_every=k, stage_obs=stage)
+        s.forward(wl.K)
+        gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+        o = s.traj.clone()
+        o[1:].add_(torch.randn(o[1:].shape, device=dev, generator=gen), alpha=0.3)
+        if virtual:  # the paper's per-trajectory fit: free leader terms (PAPER.md:208)
+            s.close()
+            del s
+            torch.cuda.empty_cache()
+            s = idm.from_workload(wl, None, max_steps=wl.K, ckpt_every=4, virtual_leader=True)
+        return s, o
+
+    def reset(s):
+        s.params.copy_(torch.as_tensor(synth.init_params(s.n), device=dev))
+        s.adam_m.zero_()
+        s.adam_v.zero_()
+        if s.virtual_leader:
+            s.vl_dp.fill_(idm.VL_INIT[0])
+            s.vl_dv.fill_(idm.VL_INIT[1])
+            s.vl_adam_m.zero_()
+            s.vl_adam_v.zero_()
+
+    def run_path(s, step_fn, n_vs, per_kernel=True):
+        reset(s)
+        for i in range(args.warmup):
+            step_fn(i)
+        torch.cuda.synchronize()
+        parallel.barrier()
+        start, stop = _events(torch)
+        n0 = s.launch_count
+        tw0 = time.time()
+        start.record(s.stream)
+        for i in range(args.steps):
+            step_fn(args.warmup + i)
+        stop.record(s.stream)
+        torch.cuda.synchronize()
+        tw1 = time.time()
+        launches = s.launch_count - n0
+        ms = parallel.max_over_ranks(start.elapsed_time(stop), dev) / args.steps
+        kms = {}
+        if per_kernel:  # the same steps again with per-launch events in the library
+            s.timing(True)
+            s.timing_read()
+            for i in range(args.steps):
+                step_fn(args.warmup + args.steps + i)
+            kt = s.timing_read()
+            s.timing(False)
+            kms = {kk: parallel.max_over_ranks(v[0], dev) / args.steps for kk, v in kt.items()
+                   if v[1] > 0}
+        return {"ms_per_step": ms, "value": n_vs / (ms * 1e-3), "kernel_ms": kms,
+                "launches_per_step": launches / args.steps, "window": (tw0, tw1)}
+
+    sim, obs = build(w, vl)
 
     def step_api(it):
         sim.forward(K)
         sim.loss_grad(obs, kind=args.loss, sync=False)
-        parallel.reduce_step(sim.loss_dev)  # total loss: one 8-byte NCCL all-reduce
+        parallel.reduce_loss(sim.loss_dev)  # total loss: one 8-byte NCCL all-reduce
         sim.backward()
         sim.adam_step(it % 500, 500, 0.1, 0.01)
 
     def step_fused(it):
         sim.fit_step(obs, kind=args.loss, iteration=it % 500, total=500, lr0=0.1, lr1=0.01)
-        parallel.reduce_step(sim.loss_dev)
+        parallel.reduce_loss(sim.loss_dev)
 
-    clocks = ClockSampler(local_rank)
-    clocks.wait_first()
-
-    def run_path(step_fn):
-        reset()
-        for i in range(args.warmup):
-            step_fn(i)
-        torch.cuda.synchronize()
-        parallel.barrier()
-        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n0 = sim.launch_count
-        tw0 = time.time()
-        start.record(stream)
-        for i in range(args.steps):
-            step_fn(args.warmup + i)
-        stop.record(stream)
-        torch.cuda.synchronize()
-        tw1 = time.time()
-        launches = sim.launch_count - n0
-        ms = parallel.max_over_ranks(start.elapsed_time(stop), dev) / args.steps
-        # per-kernel device time: the same steps again with per-launch events in the library
-        sim.timing(True)
-        sim.timing_read()
-        for i in range(args.steps):
-            step_fn(args.warmup + args.steps + i)
-        kt = sim.timing_read()
-        sim.timing(False)
-        kms = {kk: parallel.max_over_ranks(v[0], dev) / args.steps for kk, v in kt.items()
-               if v[1] > 0}
-        return {"ms_per_step": ms, "value": vsteps / (ms * 1e-3), "kernel_ms": kms,
-                "launches_per_step": launches / args.steps, "window": (tw0, tw1)}
-
-    api = run_path(step_api)
-    fused = run_path(step_fused)
+    api = run_path(sim, step_api, vsteps)
+    fused = run_path(sim, step_fused, vsteps)
+    # the forward alone (BASELINE.json's fwd metric): the prediction rollout, P rows only
+    fwd_only = None
+    if not vl:
+        fwd_only = run_path(sim, lambda it: sim.forward(K, history=False), vsteps)
     # the same iterations as ONE CUDA graph (idm_fit_steps): capture + instantiate + launch, all
     # inside the timed region (the host capture is part of what a user pays)
-    reset()
+    reset(sim)
     sim.fit_steps(obs, iters=2, total=max(args.steps, 2) + 2)
     torch.cuda.synchronize()
-    reset()
-    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    g0.record(stream)
+    reset(sim)
+    g0, g1 = _events(torch)
+    g0.record(sim.stream)
     sim.fit_steps(obs, iters=args.steps, total=args.steps)
-    g1.record(stream)
+    g1.record(sim.stream)
     torch.cuda.synchronize()
     t_g = parallel.max_over_ranks(g0.elapsed_time(g1), dev)
     graph = {"iters": args.steps, "ms_per_step": t_g / args.steps,
@@ -346,24 +442,24 @@ def run_ours(args, rank, world, local_rank):
     whole = None
     if not vl and K <= idm.load_library().idm_fit_max_steps():
         # short horizons (C1-like, C5): every iteration of a 500-iteration fit in ONE launch
-        reset()
+        reset(sim)
         sim.fit(obs, iters=10, total=500)
         torch.cuda.synchronize()
-        reset()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        reset(sim)
+        e0, e1 = _events(torch)
+        e0.record(sim.stream)
         sim.fit(obs, iters=500, total=500)
-        e1.record(stream)
+        e1.record(sim.stream)
         torch.cuda.synchronize()
         t_fit = parallel.max_over_ranks(e0.elapsed_time(e1), dev)
         whole = {"iters": 500, "ms_total": t_fit, "ms_per_iteration": t_fit / 500,
                  "value": vsteps * 500 / (t_fit * 1e-3), "unit": "vehicle-steps/s",
                  "launches": 2, "path": "idm_fit (fwd+Eq.4+bwd+Adam x 500 on chip)"}
-    clocks.stop()
+    clocks_main = clocks.summary(*fused["window"])
 
     # ---- end to end through the C-ABI with HOST buffers (idm_step_host)
     e2e = None
-    if args.e2e > 0:
+    if args.e2e > 0 and not vl:
         obs_h = obs.cpu().pin_memory()
         p0_h = sim.pos0.cpu().pin_memory()
         v0_h = sim.vel0.cpu().pin_memory()
@@ -384,14 +480,14 @@ def run_ours(args, rank, world, local_rank):
         scratch = torch.empty_like(obs)
         scratch.copy_(obs_h, non_blocking=True)
         torch.cuda.synchronize()
-        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0, c1 = _events(torch)
         c0.record()
         for _ in range(2):
             scratch.copy_(obs_h, non_blocking=True)
         c1.record()
         torch.cuda.synchronize()
         copy_gbps = 2 * obs_h.numel() * 4 / (c0.elapsed_time(c1) * 1e-3) / 1e9
-        del scratch
+        del scratch, obs_h
         e2e = {"value": vsteps * args.e2e / te, "unit": "vehicle-steps/s",
                "h2d_bytes_per_step": h2d,
                "h2d_GBps": h2d * args.e2e / te / 1e9,
@@ -404,6 +500,30 @@ def run_ours(args, rank, world, local_rank):
                        "backward), fwd, loss, bwd, adam, loss -> host every step; wall clock, "
                        "max over ranks"}
 
+    # ---- secondary measurements of the same metric: weak scaling (N > 1), virtual leader (N = 1)
+    weak = None
+    vl_line = None
+    if world > 1 and scaling == "strong" and args.weak_also:
+        sim.close()
+        del sim, obs
+        torch.cuda.empty_cache()
+        ww = make_rank_workload(rank, world, "weak")
+        sim, obs = build(ww, False)
+        wr = run_path(sim, step_fused, float(parallel.sum_over_ranks(ww.n)) * K, per_kernel=False)
+        weak = {"value": wr["value"], "ms_per_step": wr["ms_per_step"], "scaling": "weak",
+                "vehicles_per_rank": ww.n, "path": "idm_fit_step"}
+    if world == 1 and not vl and args.vl_also:
+        sim.close()
+        del sim, obs
+        torch.cuda.empty_cache()
+        sim, obs = build(w, True)
+        vr = run_path(sim, step_fused, vsteps)
+        vl_line = {"ms_per_step": vr["ms_per_step"], "value": vr["value"],
+                   "kernel_ms": vr["kernel_ms"], "clocks": clocks.summary(*vr["window"]),
+                   "what": "virtual-leader fit step (PAPER.md:208): every vehicle fitted alone "
+                           "with free per-step (dp, dv) leaves updated by Adam"}
+    clocks.stop()
+
     if rank != 0:
         return
     hbm_gbs, sm_mhz_max, peak_src = load_peaks()
@@ -411,13 +531,14 @@ def run_ours(args, rank, world, local_rank):
     head = fused
     kms = head["kernel_ms"]
     dom = max(kms, key=kms.get)
+    ncu = _load_json("profiles/ncu_metrics.json")
     if vl:  # HBM-bound mode: roofline against the measured copy bandwidth
         ab = alg_bytes(K, k, "vl")
         achieved = ab[dom] * n_veh_steps / (kms[dom] * 1e-3) / 1e9
-        traffic = load_traffic().get(f"vl_{dom}_kernel")
         roofline = {"bound": "hbm", "kernel": f"vl_{dom}_kernel (fused path)",
                     "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s",
-                    "frac": achieved / hbm_gbs, "traffic": traffic,
+                    "frac": achieved / hbm_gbs,
+                    "traffic": ncu.get(f"vl_{dom}_kernel", {}).get("dram_bytes"),
                     "basis": f"{ab[dom]:.2f} algorithmic bytes per vehicle-step x "
                              f"{n_veh_steps:.3g} per launch / CUDA-event launch time; peak = "
                              f"MEASURED_PEAKS hbm_gbs ({peak_src})"}
@@ -428,70 +549,98 @@ def run_ours(args, rank, world, local_rank):
         # essential issue slots of THIS (f32x2-packed) implementation: SURVEY 8(d) addendum
         achieved = PACKED_INSTR[kp] * n_veh_steps / (kms[dom] * 1e-3) / 1e12
         frozen = ALG_INSTR[kk] * n_veh_steps / (kms[dom] * 1e-3) / 1e12
-        traffic = load_traffic().get(f"{dom}_kernel")
+        nm = ncu.get(f"{dom}_kernel", {})
         roofline = {"bound": "alu", "kernel": f"{dom}_kernel (fused path)", "achieved": achieved,
                     "peak": issue_peak, "unit": "Tinstr/s", "frac": achieved / issue_peak,
-                    "traffic": traffic,
-                    "frac_frozen_scalar_count": frozen / issue_peak,
+                    "traffic": nm.get("dram_bytes"),
+                    "frac_survey": frozen / issue_peak,
+                    "ncu": {key: nm.get(key) for key in (
+                        "issue_active_pct", "fma_pipe_pct", "xu_pipe_pct", "alu_pipe_pct",
+                        "warp_instr_per_unit", "registers", "source")} if nm else None,
                     "basis": f"{PACKED_INSTR[kp]} essential issue slots per vehicle-step (packed "
                              f"f32x2 implementation; SURVEY 8(d) addendum) x {n_veh_steps:.3g} "
                              f"vehicle-steps per launch / CUDA-event launch time; peak = 148 SM "
                              f"x 4 issue/clk x 32 lanes x {sm_mhz_max:.0f} MHz (MEASURED_PEAKS "
-                             f"sm_max, {peak_src}); frac_frozen_scalar_count uses the round-1 "
+                             f"sm_max, {peak_src}; issue and pipe rates measured by "
+                             f"profiles/pipe_bench.cu); frac_survey uses SURVEY 8(d)'s frozen "
                              f"scalar count {ALG_INSTR[kk]:.0f}, which a packed kernel can exceed; "
-                             f"traffic = ncu dram bytes/launch (profiles/traffic.json)"}
+                             f"ncu = the kernel's pipe utilisation (profiles/ncu_metrics.json); "
+                             f"traffic = its ncu dram bytes per launch"}
 
-    def hbm_of(p, path):
+    def hbm_of(p, path, survey_key=None):
         ab = alg_bytes(K, k, path)
         tot = sum(ab.values()) * n_veh_steps
-        return {"bytes_per_vehicle_step": round(sum(ab.values()), 3),
-                "achieved_GBps": tot / (p["ms_per_step"] * 1e-3) / 1e9, "peak_GBps": hbm_gbs,
-                "frac": tot / (p["ms_per_step"] * 1e-3) / 1e9 / hbm_gbs,
-                "per_kernel_frac": {kk: ab[kk] * n_veh_steps / (p["kernel_ms"][kk] * 1e-3) / 1e9
-                                    / hbm_gbs for kk in ab if kk in p["kernel_ms"]}}
+        r = {"bytes_per_vehicle_step": round(sum(ab.values()), 3),
+             "achieved_GBps": tot / (p["ms_per_step"] * 1e-3) / 1e9, "peak_GBps": hbm_gbs,
+             "frac": tot / (p["ms_per_step"] * 1e-3) / 1e9 / hbm_gbs,
+             "per_kernel_frac": {kk: ab[kk] * n_veh_steps / (p["kernel_ms"][kk] * 1e-3) / 1e9
+                                 / hbm_gbs for kk in ab if kk in p["kernel_ms"]}}
+        if survey_key:  # the same time on the METHOD's algorithmic bytes
+            b = SURVEY_BYTES[survey_key]
+            r["survey_bytes_per_vehicle_step"] = b
+            r["frac_survey_bytes"] = b * n_veh_steps / (p["ms_per_step"] * 1e-3) / 1e9 / hbm_gbs
+        return r
 
     cpu = None
-    if world == 1 and args.cpu_lanes > 0:
-        vs_c, t_c = cpu_baseline(args.cpu_lanes, K)
-        cpu = {"value": vs_c / t_c, "unit": "vehicle-steps/s", "cores": 1, "kind": "oracle",
-               "sample": f"first {args.cpu_lanes} lanes x {K} steps of {WORKLOAD}, one "
-                         f"full step (fp64 rollout + Eq.4 L1 + adjoint + Adam), 1 thread, "
-                         f"{t_c:.1f} s"}
+    if world == 1 and args.cpu_seconds > 0:
+        cpu = cpu_baseline(K, args.cpu_seconds)
+    fwd_line = None
+    if fwd_only is not None:
+        fwd_line = {"value": fwd_only["value"], "unit": "vehicle-steps/s",
+                    "ms": fwd_only["ms_per_step"],
+                    "what": "idm_forward_ex(IDM_FWD_NO_HISTORY): the K-step rollout writing P "
+                            "(the prediction path)",
+                    "hbm": hbm_of(fwd_only, "fwd_only", "fwd"),
+                    "with_history": {"value": vsteps / (api["kernel_ms"]["fwd"] * 1e-3),
+                                     "ms": api["kernel_ms"]["fwd"],
+                                     "what": "idm_forward (P + the state history a backward "
+                                             "reads)"}}
     line = {
         "metric": METRIC, "value": head["value"], "unit": "vehicle-steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
-        "higher_is_better": True, "scaling": args.scaling if world > 1 else "weak",
+        "higher_is_better": True, "scaling": scaling if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD_DESC + ("; virtual-leader mode (PAPER.md:208): every "
                                                 "vehicle fitted alone with free per-step "
                                                 "(dp, dv) leaves" if vl else ""),
-                   "vehicles_per_rank": w.n, "K": K,
+                   "vehicles_total": n_total, "vehicles_rank0": w.n, "K": K,
                    "ckpt_every": k, "loss": args.loss,
                    "path": "idm_fit_step (fused fwd+Eq.4 / bwd+Adam)",
-                   "parallelism": f"lane-sharded x{world}",
+                   "parallelism": f"lane-sharded x{world} ({scaling})",
                    "l2": "no flush: inputs larger than L2 (2.4 GB obs read by both kernels + "
                          "2.4 GB speed history per rank per step vs 126 MB L2)"},
-        "fwd": {"value": vsteps / (api["kernel_ms"]["fwd"] * 1e-3), "unit": "vehicle-steps/s",
-                "ms": api["kernel_ms"]["fwd"], "what": "idm_forward, trajectory record on"},
+        "fwd": fwd_line,
         "fused_path": {kk: head[kk] for kk in ("ms_per_step", "value", "kernel_ms",
                                                "launches_per_step")},
         "api_path": {kk: api[kk] for kk in ("ms_per_step", "value", "kernel_ms",
                                             "launches_per_step")},
         "whole_fit_path": whole,
         "graph_path": graph,
+        "weak_scaling": weak,
+        "virtual_leader": vl_line,
         "roofline": roofline,
         "hbm": {"fused": hbm_of(fused, "vl" if vl else ("fused_l2" if args.loss == "l2" else
-                                                        "fused")),
-                "api": hbm_of(api, "vl_api" if vl else "api"), "peak_source": peak_src},
+                                                        "fused"),
+                                None if vl else "fused"),
+                "api": hbm_of(api, "vl_api" if vl else "api", None if vl else "api"),
+                "peak_source": peak_src},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(round(head["launches_per_step"] * args.steps)),
-        "clocks": clocks.summary(*head["window"]),
+        "clocks": clocks_main,
         "paper_context": "< 30 ms per timestep per pass at 2M vehicles on 16-thread Xeon "
                          "W-2255 or one RTX A5000 (PAPER.md:36, :253) = > 6.7e7 vehicle-steps/s "
                          "per pass",
     }
     print(json.dumps(line), flush=True)
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
 
 
 def main():
@@ -509,23 +658,38 @@ def main():
                     help="lane leader (default) or the paper's virtual-leader fit (PAPER.md:208)")
     ap.add_argument("--config", choices=["C1", "C2", "C3", "C4", "C5"], default="C4",
                     help="BASELINE.json configuration (C4 = the headline)")
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                    help="N > 1: strong (default; the 2M vehicles split over the ranks) or weak")
+    ap.add_argument("--weak-also", type=int, default=1,
+                    help="N > 1 strong: also measure weak scaling (secondary field)")
+    ap.add_argument("--vl-also", type=int, default=1,
+                    help="N = 1: also measure the virtual-leader fit step (secondary field)")
     ap.add_argument("--ckpt", type=int, default=None, help="checkpoint interval k")
     ap.add_argument("--loss", choices=["l1", "l2"], default="l1",
                     help="Eq. 4 as the paper's L1 (headline) or the smooth L2 variant")
     ap.add_argument("--e2e", type=int, default=8, help="end-to-end steps (0 = skip)")
-    ap.add_argument("--cpu-lanes", type=int, default=2000,
-                    help="C4 lanes in the oracle cpu_baseline sample (0 = skip)")
-    ap.add_argument("--traffic", type=float, default=None,
-                    help="ncu dram bytes per launch of the dominant kernel (from profiles/)")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0,
+                    help="core-seconds of oracle work in the cpu_baseline sample (0 = skip)")
     args = ap.parse_args()
     set_config(args.config)
     if args.leader == "virtual":
         global METRIC
         METRIC = METRIC.replace("forward+loss+backward+Adam", "virtual-leader fit step")
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launch the N ranks here (one process per GPU, NCCL) -- or fail loudly
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus and args.backend == "nccl":
+            sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this host has {have}")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and args.impl == "ours":
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":
@@ -537,6 +701,9 @@ def main():
         dev = torch.device("cuda", local_rank % torch.cuda.device_count())
         torch.cuda.set_device(dev)
         if args.backend == "nccl":
+            # communicator set-up logged to stderr (which transport, NVLS or not)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:  # host-logic check of the multi-rank path on fewer GPUs than ranks
             dist.init_process_group("gloo")

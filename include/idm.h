@@ -107,6 +107,11 @@ typedef struct {
                                     (nullable): idm_step_host(_async) alternate between the two
                                     when no mask is given, so an upload never waits for the
                                     previous step's loss kernel */
+    double* lane_grads;          /* shared mode: [n_lanes][6] fp64, row l = the sum of lane l's
+                                    vehicles' dL/dtheta in vehicle order, written by
+                                    idm_backward / idm_fit_step (empty lanes: 0) -- the unit of
+                                    the shard-count-invariant reduction (idm_reduce_shared).
+                                    Nullable: then kept in the workspace */
 } idm_desc;
 
 /* Bytes of device workspace idm_init needs for this descriptor: the lane-mode state history
@@ -127,9 +132,15 @@ int64_t idm_plan_tiles(const int32_t* lane_offsets, int32_t n_lanes, int64_t n_v
 
 /* Validate the descriptor and input data (finite, v(0) >= 0, lengths >= 0, a_max, a_pref,
    v_targ, delta > 0, lane offsets well formed, every lane fits one lane tile of
-   idm_max_lane_vehicles() vehicles), build the lane -> CTA tile plan and leader flags in the
-   workspace.  Synchronizes the stream.  *out receives the handle (NULL on failure).
-   The desc is copied; the arrays it points to must stay valid until idm_destroy. */
+   idm_max_lane_vehicles() vehicles, and -- lane mode -- every lane member strictly behind its
+   leader: pos0[i+1] - pos0[i] - length[i+1] > 0, the ordering PAPER.md:106 presumes ("the
+   vehicle directly ahead"); gaps in (0, eps_gap) are valid and clamped, R#7), build the
+   lane -> CTA tile plan and leader flags in the workspace.  IDM_EINVAL on any violation, with
+   the first offending vehicle in the message.  Virtual-leader mode has no lanes: no plan, no
+   lane-size limit, no order check.  Synchronizes the stream.  *out receives the handle (NULL
+   on failure).  The desc is copied; the arrays it points to must stay valid until idm_destroy.
+   The handle belongs to the CUDA device current here; every later call runs on that device
+   (made current for the call, the caller's current device restored after). */
 int idm_init(idm_handle** out, const idm_desc* d);
 
 /* Simulate `steps` (1..max_steps) synchronous steps from (pos0, vel0) (Eqs. 1-3, Sec. III-B/C,
@@ -138,6 +149,16 @@ int idm_init(idm_handle** out, const idm_desc* d);
    ckpt_every steps, which idm_backward reads back.
    Non-finite states are detected at checkpoints and reported by the next synchronizing call. */
 int idm_forward(idm_handle* h, int32_t steps);
+
+/* Flags of idm_forward_ex. */
+enum {
+    IDM_FWD_NO_HISTORY = 1 /* prediction rollout: write traj (and vel_traj, state_out) only, no
+                              state history -- half the HBM bytes of idm_forward; idm_loss_grad
+                              may follow, idm_backward then returns IDM_ESTATE */
+};
+
+/* idm_forward with flags (0 = idm_forward).  The same arithmetic, so traj is bit-identical. */
+int idm_forward_ex(idm_handle* h, int32_t steps, uint32_t flags);
 
 /* Eq. 4 over rows 0..steps of traj:
      L1: L = sum_{observed (t,i)} |obs - P|,  dL/dP = -sign(obs - P), sign(0) = 0 (R#11)
@@ -149,11 +170,29 @@ int idm_forward(idm_handle* h, int32_t steps);
 int idm_loss_grad(idm_handle* h, const float* obs, const uint8_t* mask, int32_t kind,
                   double* loss_dev, double* loss_host);
 
-/* Reverse-mode adjoint of the last idm_forward through grad_traj: rebuilds each checkpoint
-   segment on chip and sweeps it backwards.  Writes grad_params (per vehicle, or in shared
-   mode the sum over this process's vehicles -- the caller all-reduces across ranks) and
-   grad_state0.  No atomics: fixed-order reductions, bitwise deterministic. */
+/* Reverse-mode adjoint of the last idm_forward through grad_traj -- the derivative of the
+   simulator that PAPER.md:134 makes "differentiable" and PAPER.md:227 obtains by autograd:
+   the full coupled BPTT of Eqs. 1-3 with the Sec. III-C bounds (leader states included,
+   R#23), given dL/dP from idm_loss_grad (Eq. 4).  Per lane tile it rebuilds
+   each checkpoint segment's gaps from the stored speeds on chip and sweeps it backwards.
+   Writes
+     grad_params  [6][n_par]  dL/d(a_max, a_pref, s_min, T_pref, v_targ, delta), row 5 = the
+                  true dL/d delta on this call (the fused optimizer calls write 0 there when
+                  delta is frozen, see idm_fit_step);  in shared mode the fixed-order sum of
+                  lane_grads over this handle's lanes (one rank: the whole gradient);
+     lane_grads   (shared mode) the per-lane sums, for idm_reduce_shared across ranks;
+     grad_state0  [2][N]  dL/dp(0), dL/dv(0) (nullable).
+   IDM_ESTATE unless the last forward kept its history (idm_forward, not IDM_FWD_NO_HISTORY)
+   and idm_loss_grad followed it.  No atomics: fixed-order reductions, bitwise deterministic. */
 int idm_backward(idm_handle* h);
+
+/* Shared-parameter mode across ranks (north_star: NCCL only for the shared gradients and the
+   loss): grad_params = the fixed-order fp64 sum over rows 0..n_rows-1 of lane_grads (device
+   [n_rows][6], the rows of ALL ranks' lanes in global lane order, e.g. each rank's own rows
+   placed in a zeroed buffer and all-reduced -- disjoint rows make that all-reduce exact), rounded
+   to fp32.  The result depends only on the global rows, so it is bitwise the same for any
+   number of ranks.  Call between idm_backward and idm_adam_step. */
+int idm_reduce_shared(idm_handle* h, const double* lane_grads, int64_t n_rows);
 
 /* Adam step (Kingma & Ba; beta1 0.9, beta2 0.999, eps 1e-8, bias-corrected, R#14) on the
    parameters selected by opt_mask with lr = lr0 + (lr1 - lr0) * iter / (total_iters - 1)
@@ -163,9 +202,11 @@ int idm_adam_step(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, f
 
 /* One whole optimizer iteration, fused: exactly forward(steps) -> loss_grad(obs, kind) ->
    backward -> adam_step(iter, ...) (same arithmetic; grad_params, grad_state0, Adam moments and
-   parameters bit for bit -- except grad_params row 5, dL/d delta, which is written as 0 when
-   delta is frozen (opt_mask bit 5 clear): the optimizer never reads it, and the delta = 4
-   kernels skip the per-step log2 it needs), when ckpt_every == 4 in two kernels writing only
+   parameters bit for bit -- except grad_params row 5, dL/d delta: on the optimizer calls
+   (idm_fit_step, idm_fit, idm_fit_steps) it is written as 0 when delta is frozen (opt_mask
+   bit 5 clear), because the optimizer never reads it and the delta = 4 kernels skip the
+   per-step log2 it needs; idm_backward always writes the true value), when ckpt_every == 4 in
+   two kernels writing only
    the internal state history, the backward launched as a programmatic dependent of the forward
    (each CTA waits for its own tile's history) and applying Adam + box clamp per vehicle in its
    epilogue.  L1: the forward sums Eq. 4 against each fresh position row and records
@@ -252,7 +293,8 @@ enum {
 int idm_timing_enable(idm_handle* h, int enable);
 int idm_timing_read(idm_handle* h, double* ms, int64_t* launches);
 
-/* Synchronize the stream and report a pending non-finite status (IDM_ENUMERIC) or CUDA error. */
+/* Synchronize the stream and report a pending non-finite status (IDM_ENUMERIC: a non-finite
+   state at a checkpoint, or a non-finite parameter gradient reaching Adam) or CUDA error. */
 int idm_check(idm_handle* h);
 
 /* Number of kernel launches the library issued on this handle since idm_init. */

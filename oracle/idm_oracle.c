@@ -243,21 +243,29 @@ double ora_loss(int kind, int64_t n, int32_t K, const double* P, const double* o
    acceleration also feeds its leader's adjoints.  Terminal lp^K = gP^K, lv^K = 0.
    Outputs: g_params [6][n_par] (accumulated over vehicles when shared),
    g_abs [6][n_par] (nullable) = sum |q da/dtheta| (condition number for parity tolerance),
-   g_p0 = dL/dp(0) = lp^0, g_v0 = dL/dv(0) = lv^0 (nullable).  Returns 0 or 1+t on non-finite. */
+   g_p0 = dL/dp(0) = lp^0, g_v0 = dL/dv(0) = lv^0 (nullable),
+   g_p0_abs, g_v0_abs (nullable) = the sum of |every term added| into lp resp. lv over the
+   sweep (|gP^t|, |dt lp^{t+1}|, |q da/dx|), the state analogue of g_abs: the scale below which
+   a state gradient is a cancellation of larger terms (SURVEY.md 8(c) parity protocol; DESIGN.md
+   section 7).  Returns 0 or 1+t on non-finite. */
 int ora_backward(int64_t n, const int32_t* leader, const double* len, const double* params,
                  int64_t n_par, int32_t K, double dt, double a_min, double eps_gap, const double* P,
                  const double* V, const double* gP, double* g_params, double* g_abs, double* g_p0,
-                 double* g_v0)
+                 double* g_v0, double* g_p0_abs, double* g_v0_abs)
 {
     double* lp = (double*)malloc(sizeof(double) * (size_t)n);
     double* lv = (double*)malloc(sizeof(double) * (size_t)n);
     double* lp_new = (double*)malloc(sizeof(double) * (size_t)n);
     double* lv_new = (double*)malloc(sizeof(double) * (size_t)n);
+    /* running sums of |terms| added into lp, lv (condition scale of the state gradients) */
+    double* pa = (double*)calloc((size_t)n, sizeof(double));
+    double* va = (double*)calloc((size_t)n, sizeof(double));
     memset(g_params, 0, sizeof(double) * NPAR * (size_t)n_par);
     if (g_abs) memset(g_abs, 0, sizeof(double) * NPAR * (size_t)n_par);
     for (int64_t i = 0; i < n; ++i) {
         lp[i] = gP[(int64_t)K * n + i];
         lv[i] = 0.0;
+        pa[i] = fabs(lp[i]);
     }
     int rc = 0;
     for (int32_t t = K - 1; t >= 0; --t) {
@@ -266,6 +274,8 @@ int ora_backward(int64_t n, const int32_t* leader, const double* len, const doub
         for (int64_t i = 0; i < n; ++i) {
             lp_new[i] = gP[(int64_t)t * n + i] + lp[i];
             lv_new[i] = lv[i] + dt * lp[i];
+            pa[i] += fabs(gP[(int64_t)t * n + i]);
+            va[i] += fabs(dt * lp[i]);
         }
         for (int64_t i = 0; i < n; ++i) {
             double th[NPAR], dp, dv, d[10];
@@ -276,11 +286,15 @@ int ora_backward(int64_t n, const int32_t* leader, const double* len, const doub
             double q = dt * lv[i];
             /* v_i enters directly and through dv = v_i - v_h */
             lv_new[i] += q * (d[1] + d[3]);
+            va[i] += fabs(q * (d[1] + d[3]));
             if (hl) {
                 int32_t h = leader[i];
                 lv_new[h] += q * (-d[3]);
                 lp_new[i] += q * (-d[2]);
                 lp_new[h] += q * d[2];
+                va[h] += fabs(q * d[3]);
+                pa[i] += fabs(q * d[2]);
+                pa[h] += fabs(q * d[2]);
             }
             int64_t j = (n_par == 1) ? 0 : i;
             for (int k = 0; k < NPAR; ++k) {
@@ -298,7 +312,9 @@ int ora_backward(int64_t n, const int32_t* leader, const double* len, const doub
     }
     if (g_p0) memcpy(g_p0, lp, sizeof(double) * (size_t)n);
     if (g_v0) memcpy(g_v0, lv, sizeof(double) * (size_t)n);
-    free(lp); free(lv); free(lp_new); free(lv_new);
+    if (g_p0_abs) memcpy(g_p0_abs, pa, sizeof(double) * (size_t)n);
+    if (g_v0_abs) memcpy(g_v0_abs, va, sizeof(double) * (size_t)n);
+    free(lp); free(lv); free(lp_new); free(lv_new); free(pa); free(va);
     return rc;
 }
 
@@ -486,7 +502,8 @@ int ora_rollout_vl(int64_t n, const double* p0, const double* v0, const double* 
 int ora_backward_vl(int64_t n, const double* params, int64_t n_par, int32_t K, double dt,
                     double a_min, double eps_gap, const double* dp, const double* dv,
                     const double* P, const double* V, const double* gP, double* g_params,
-                    double* g_abs, double* g_dp, double* g_dv, double* g_p0, double* g_v0)
+                    double* g_abs, double* g_dp, double* g_dv, double* g_p0, double* g_v0,
+                    double* g_p0_abs, double* g_v0_abs)
 {
     (void)P;
     memset(g_params, 0, sizeof(double) * NPAR * (size_t)n_par);
@@ -494,6 +511,7 @@ int ora_backward_vl(int64_t n, const double* params, int64_t n_par, int32_t K, d
     int rc = 0;
     for (int64_t i = 0; i < n; ++i) {
         double lp = gP[(int64_t)K * n + i], lv = 0.0;
+        double pa = fabs(lp), va = 0.0; /* sums of |terms added| (as ora_backward) */
         double th[NPAR];
         load_theta(params, n_par, i, th);
         int64_t j = (n_par == 1) ? 0 : i;
@@ -506,6 +524,8 @@ int ora_backward_vl(int64_t n, const double* params, int64_t n_par, int32_t K, d
             double q = dt * lv;
             double lp_new = gP[(int64_t)t * n + i] + lp;
             double lv_new = lv + dt * lp + q * d[1];
+            pa += fabs(gP[(int64_t)t * n + i]);
+            va += fabs(dt * lp) + fabs(q * d[1]);
             g_dp[(int64_t)t * n + i] = q * d[2];
             g_dv[(int64_t)t * n + i] = q * d[3];
             for (int k = 0; k < NPAR; ++k) {
@@ -519,6 +539,8 @@ int ora_backward_vl(int64_t n, const double* params, int64_t n_par, int32_t K, d
         if (!isfinite(lp) || !isfinite(lv)) rc = 1;
         if (g_p0) g_p0[i] = lp;
         if (g_v0) g_v0[i] = lv;
+        if (g_p0_abs) g_p0_abs[i] = pa;
+        if (g_v0_abs) g_v0_abs[i] = va;
     }
     return rc;
 }

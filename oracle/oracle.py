@@ -61,7 +61,7 @@ def lib():
         L.ora_loss.argtypes = [C.c_int, i64, i32, _dp, _dp, vp, vp, _dp]
         L.ora_backward.restype = C.c_int
         L.ora_backward.argtypes = [i64, _ip, _dp, _dp, i64, i32, d, d, d, _dp, _dp, _dp, _dp,
-                                   vp, vp, vp]
+                                   vp, vp, vp, vp, vp]
         L.ora_rollout_tangent.restype = C.c_int
         L.ora_rollout_tangent.argtypes = [i64, _ip, _dp, _dp, _dp, _dp, i64, i32, d, d, d,
                                           vp, vp, vp, _dp, _dp]
@@ -69,7 +69,7 @@ def lib():
         L.ora_rollout_vl.argtypes = [i64, _dp, _dp, _dp, i64, i32, d, d, d, _dp, _dp, _dp, _dp]
         L.ora_backward_vl.restype = C.c_int
         L.ora_backward_vl.argtypes = [i64, _dp, i64, i32, d, d, d, _dp, _dp, _dp, _dp, _dp, _dp,
-                                      vp, _dp, _dp, vp, vp]
+                                      vp, _dp, _dp, vp, vp, vp, vp]
         L.ora_rollout_vl_tangent.restype = C.c_int
         L.ora_rollout_vl_tangent.argtypes = [i64, _dp, _dp, _dp, i64, i32, d, d, d, _dp, _dp,
                                              vp, vp, vp, vp, vp, _dp, _dp]
@@ -170,7 +170,8 @@ def loss(P, obs, kind="l1", mask=None, sign_override=None):
 
 
 def backward(leader, length, params, P, V, gP, dt=0.1, a_min=-10.0, eps_gap=0.1):
-    """Reverse-mode adjoint.  Returns dict(g_params [6, n_par], g_abs, g_p0, g_v0)."""
+    """Reverse-mode adjoint.  Returns dict(g_params [6, n_par], g_abs, g_p0, g_v0, g_p0_abs,
+    g_v0_abs); the *_abs arrays are the condition scales (sum of |terms|) of the gradients."""
     leader = np.ascontiguousarray(leader, dtype=np.int32)
     n = leader.shape[0]
     prm = _params2d(params, n)
@@ -179,11 +180,15 @@ def backward(leader, length, params, P, V, gP, dt=0.1, a_min=-10.0, eps_gap=0.1)
     ga = np.empty_like(prm)
     gp0 = np.empty(n)
     gv0 = np.empty(n)
+    gp0a = np.empty(n)
+    gv0a = np.empty(n)
     rc = lib().ora_backward(n, leader, _f64(length), prm, prm.shape[1], K, dt, a_min, eps_gap,
-                            _f64(P), _f64(V), _f64(gP), g, _ptr(ga), _ptr(gp0), _ptr(gv0))
+                            _f64(P), _f64(V), _f64(gP), g, _ptr(ga), _ptr(gp0), _ptr(gv0),
+                            _ptr(gp0a), _ptr(gv0a))
     if rc:
         raise OracleError(f"non-finite adjoint at step {rc - 1}")
-    return {"g_params": g, "g_abs": ga, "g_p0": gp0, "g_v0": gv0}
+    return {"g_params": g, "g_abs": ga, "g_p0": gp0, "g_v0": gv0, "g_p0_abs": gp0a,
+            "g_v0_abs": gv0a}
 
 
 def rollout_tangent(leader, length, p0, v0, params, K, tp0=None, tv0=None, tparams=None,
@@ -232,12 +237,15 @@ def backward_vl(params, dp, dv, P, V, gP, dt=0.1, a_min=-10.0, eps_gap=0.1):
     gdv = np.empty((K, n))
     gp0 = np.empty(n)
     gv0 = np.empty(n)
+    gp0a = np.empty(n)
+    gv0a = np.empty(n)
     rc = lib().ora_backward_vl(n, prm, prm.shape[1], K, dt, a_min, eps_gap, dp, _f64(dv),
                                _f64(P), _f64(V), _f64(gP), g, _ptr(ga), gdp, gdv, _ptr(gp0),
-                               _ptr(gv0))
+                               _ptr(gv0), _ptr(gp0a), _ptr(gv0a))
     if rc:
         raise OracleError("non-finite adjoint")
-    return {"g_params": g, "g_abs": ga, "g_dp": gdp, "g_dv": gdv, "g_p0": gp0, "g_v0": gv0}
+    return {"g_params": g, "g_abs": ga, "g_dp": gdp, "g_dv": gdv, "g_p0": gp0, "g_v0": gv0,
+            "g_p0_abs": gp0a, "g_v0_abs": gv0a}
 
 
 def rollout_vl_tangent(p0, v0, params, dp, dv, tp0=None, tv0=None, tparams=None, tdp=None,

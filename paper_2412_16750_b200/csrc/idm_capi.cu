@@ -15,6 +15,7 @@ using namespace idm;
 
 struct idm_handle {
     idm_desc d;
+    int device;  // the CUDA device current at idm_init; every entry point runs on it
     cudaStream_t st;
     int64_t n, n_par;
     int ntiles, nck;
@@ -26,7 +27,9 @@ struct idm_handle {
     float* ckpt_d;                // VL displacement checkpoints (fused iteration)
     uint32_t* sgn;                // fused L1 sign codes (tile-local)
     int64_t vt_stride, ck_stride, sg_stride;
-    double *loss_partials, *loss_scalar, *shared_partials;
+    double *loss_partials, *loss_scalar;
+    double* lane_grads;  // shared mode: [n_lanes][6] per-lane gradient sums (desc or workspace)
+    bool hist_ok;        // the last forward kept its state history (a backward may follow)
     unsigned long long* status;
     unsigned* flags;  // [0] = some delta != 4 (set by the validation kernel)
     unsigned* tile_ready;  // [ntiles] forward -> backward handoff epochs of idm_fit_step (PDL)
@@ -88,7 +91,10 @@ struct Layout {
     int64_t vt_stride, ck_stride, sg_stride;  // elements per tile
 };
 
+bool lane_mode(const idm_desc* d) { return d->leader_mode != IDM_LEADER_VIRTUAL; }
+
 int64_t max_tiles_for(const idm_desc* d) {
+    if (!lane_mode(d)) return 1;  // virtual leader: independent trajectories, no lane tiles
     int64_t by_size = 2 * ((d->n_vehicles + kCap - 1) / kCap) + 1;
     return d->n_lanes < by_size ? d->n_lanes : by_size;
 }
@@ -139,6 +145,7 @@ int64_t plan_tiles(const std::vector<int32_t>& off, int32_t n_lanes, int64_t n,
 // Tile count of the descriptor's lane plan (reads lane_offsets), or the bound if unreadable.
 int64_t tiles_of(const idm_desc* d) {
     if (!d || !d->lane_offsets || d->n_lanes < 1) return -1;
+    if (!lane_mode(d)) return 1;
     std::vector<int32_t> off((size_t)d->n_lanes + 1);
     if (cudaMemcpy(off.data(), d->lane_offsets, sizeof(int32_t) * off.size(), cudaMemcpyDefault) !=
         cudaSuccess) {
@@ -158,25 +165,27 @@ bool layout_for(const idm_desc* d, int64_t ntiles, Layout* L) {
     int64_t mt = ntiles > 0 ? ntiles : max_tiles_for(d);
     int64_t nck = (d->max_steps + d->ckpt_every - 1) / d->ckpt_every;
     size_t off = 0;
+    const bool lane = lane_mode(d);
     L->tile_start = off; off += align256(sizeof(int64_t) * (mt + 1));
     L->lead = off; off += align256((size_t)n);
-    // lane mode: tile-local state history (idm_internal.h), sized for the plan's tile count
-    L->vt_stride = (int64_t)(d->max_steps + 1) * kCap;
-    L->ck_stride = nck * kCkRows * kCap;
-    L->vt = off; off += align256(sizeof(float) * ((size_t)(mt * L->vt_stride) + 64));
+    // lane mode only: tile-local state history (idm_internal.h), sized for the plan's tiles
+    L->vt_stride = lane ? (int64_t)(d->max_steps + 1) * kCap : 0;
+    L->ck_stride = lane ? nck * kCkRows * kCap : 0;
+    L->sg_stride = lane ? sgn_words_per_tile(d->max_steps) : 0;
+    L->vt = off; if (lane) off += align256(sizeof(float) * ((size_t)(mt * L->vt_stride) + 64));
     L->ckt = off; off += align256(sizeof(float) * (size_t)(mt * L->ck_stride));
-    L->sg_stride = sgn_words_per_tile(d->max_steps);
     L->sgn = off; off += align256(sizeof(uint32_t) * (size_t)(mt * L->sg_stride));
-    // virtual-leader mode: speed checkpoints every 4 steps
-    L->ckpt_v = off; off += align256(sizeof(float) * (size_t)(nck * n));
-    L->ckpt_d = off;  // virtual-leader mode: + displacement checkpoints
-    if (d->leader_mode == IDM_LEADER_VIRTUAL) off += align256(sizeof(float) * (size_t)(nck * n));
+    // virtual-leader mode only: speed and displacement checkpoints every 4 steps
+    L->ckpt_v = off; if (!lane) off += align256(sizeof(float) * (size_t)(nck * n));
+    L->ckpt_d = off; if (!lane) off += align256(sizeof(float) * (size_t)(nck * n));
     L->loss_partials = off;
     int64_t np_ = kLossBlocks > mt ? kLossBlocks : mt;
     if (vl_blocks(n) > np_) np_ = vl_blocks(n);
     off += align256(sizeof(double) * np_);
     L->loss_scalar = off; off += align256(sizeof(double));
-    L->shared_partials = off; off += align256(sizeof(double) * 6 * (size_t)mt);
+    L->shared_partials = off;  // per-lane gradient sums, unless the caller gives lane_grads
+    if (d->param_mode == IDM_PARAMS_SHARED && !d->lane_grads)
+        off += align256(sizeof(double) * 6 * (size_t)d->n_lanes);
     L->status = off; off += align256(sizeof(unsigned long long));
     L->flags = off; off += align256(sizeof(unsigned));
     L->adam_table = off; off += align256(sizeof(float) * 2 * kFitMaxIters);
@@ -215,6 +224,13 @@ int consume_status(idm_handle* h, unsigned long long st) {
         return fail(h, IDM_EINVAL, "invalid IDM parameter %u of vehicle %lld (must be finite "
                                    "and > 0)", (unsigned)(lo / (h->n_par)),
                     (long long)(lo % h->n_par));
+    if (hi == kBadOrder)
+        return fail(h, IDM_EINVAL, "vehicle %u is not strictly behind its leader %u in its lane "
+                                   "(gap pos0[i+1] - pos0[i] - length[i+1] <= 0: lanes must be "
+                                   "sorted by ascending position without overlap)", lo, lo + 1);
+    if (hi == kBadGrad)
+        return fail(h, IDM_ENUMERIC, "non-finite gradient of IDM parameter %u of vehicle %lld",
+                    (unsigned)(lo / (h->n_par)), (long long)(lo % h->n_par));
     return fail(h, IDM_ENUMERIC, "non-finite state detected at step %u (checkpoint), vehicle %u",
                 hi, lo);
 }
@@ -317,6 +333,20 @@ VlArgs vl_args(idm_handle* h, int32_t steps) {
 
 bool is_vl(const idm_handle* h) { return h->d.leader_mode == IDM_LEADER_VIRTUAL; }
 
+// Makes the handle's device current for the duration of one C-ABI call and restores the
+// caller's (the handle's stream, workspace and kernels all belong to that device).
+struct OnDevice {
+    int prev = -1;
+    bool switched = false;
+    explicit OnDevice(const idm_handle* h) {
+        if (h && h->device >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != h->device)
+            switched = cudaSetDevice(h->device) == cudaSuccess;
+    }
+    ~OnDevice() {
+        if (switched) cudaSetDevice(prev);
+    }
+};
+
 }  // namespace
 
 extern "C" {
@@ -345,6 +375,7 @@ int64_t idm_launch_count(const idm_handle* h) { return h ? h->launches : 0; }
 
 void idm_destroy(idm_handle* h) {
     if (!h) return;
+    OnDevice on_dev(h);
     if (h->st) cudaStreamSynchronize(h->st);
     if (h->ev_rec) {
         for (auto& r : *h->ev_rec) {
@@ -420,22 +451,30 @@ int idm_init(idm_handle** out, const idm_desc* d) {
             bail(fail(h, IDM_EINVAL, "required device array is NULL"));
             break;
         }
-        // ---- lane plan on the host (cold path); the workspace is sized for its tile count
-        std::vector<int32_t> off((size_t)d->n_lanes + 1);
-        cudaError_t ce = cudaMemcpyAsync(off.data(), d->lane_offsets, sizeof(int32_t) * off.size(),
-                                         cudaMemcpyDefault, (cudaStream_t)d->stream);
-        if (ce == cudaSuccess) ce = cudaStreamSynchronize((cudaStream_t)d->stream);
-        if (ce != cudaSuccess) {
-            bail(fail(h, IDM_ECUDA, "reading lane_offsets: %s", cudaGetErrorString(ce)));
-            break;
-        }
+        h->device = -1;
+        // ---- lane plan on the host (cold path); the workspace is sized for its tile count.
+        // Virtual-leader mode has no lanes (every trajectory alone): no plan.
+        cudaError_t ce = cudaSuccess;
         std::vector<int64_t> tiles;
         std::vector<uint8_t> lead((size_t)d->n_vehicles, 0);
-        std::string perr;
-        const int64_t nt = plan_tiles(off, d->n_lanes, d->n_vehicles, &tiles, &lead, &perr);
-        if (nt < 0) {
-            bail(fail(h, IDM_EINVAL, "%s", perr.c_str()));
-            break;
+        int64_t nt = 1;
+        if (lane_mode(d)) {
+            std::vector<int32_t> off((size_t)d->n_lanes + 1);
+            ce = cudaMemcpyAsync(off.data(), d->lane_offsets, sizeof(int32_t) * off.size(),
+                                 cudaMemcpyDefault, (cudaStream_t)d->stream);
+            if (ce == cudaSuccess) ce = cudaStreamSynchronize((cudaStream_t)d->stream);
+            if (ce != cudaSuccess) {
+                bail(fail(h, IDM_ECUDA, "reading lane_offsets: %s", cudaGetErrorString(ce)));
+                break;
+            }
+            std::string perr;
+            nt = plan_tiles(off, d->n_lanes, d->n_vehicles, &tiles, &lead, &perr);
+            if (nt < 0) {
+                bail(fail(h, IDM_EINVAL, "%s", perr.c_str()));
+                break;
+            }
+        } else {
+            tiles = {0, d->n_vehicles};
         }
         if (nt > max_tiles_for(d) || !layout_for(d, nt, &L)) {
             bail(fail(h, IDM_EINVAL, "internal: tile plan exceeds bound"));
@@ -459,6 +498,7 @@ int idm_init(idm_handle** out, const idm_desc* d) {
                       prop.name, prop.major, prop.minor));
             break;
         }
+        h->device = dev;
         h->st = (cudaStream_t)d->stream;
         h->n = d->n_vehicles;
         h->n_par = d->param_mode == IDM_PARAMS_SHARED ? 1 : d->n_vehicles;
@@ -475,7 +515,7 @@ int idm_init(idm_handle** out, const idm_desc* d) {
         h->ckpt_d = (float*)(ws + L.ckpt_d);
         h->loss_partials = (double*)(ws + L.loss_partials);
         h->loss_scalar = (double*)(ws + L.loss_scalar);
-        h->shared_partials = (double*)(ws + L.shared_partials);
+        h->lane_grads = d->lane_grads ? d->lane_grads : (double*)(ws + L.shared_partials);
         h->status = (unsigned long long*)(ws + L.status);
         h->flags = (unsigned*)(ws + L.flags);
         h->adam_table = (float*)(ws + L.adam_table);
@@ -546,8 +586,8 @@ int idm_init(idm_handle** out, const idm_desc* d) {
             bail(fail(h, IDM_ECUDA, "init (%s): %s", what, cudaGetErrorString(ce)));
             break;
         }
-        ValidateArgs va{d->pos0, d->vel0, d->length, d->params, h->n, h->n_par, h->status,
-                        h->flags};
+        ValidateArgs va{d->pos0,  d->vel0,      d->length, d->params, lane_mode(d) ? h->lead : nullptr,
+                        h->n,     h->n_par, h->status, h->flags};
         ce = launch_validate(va, h->st);
         h->launches++;
         if (ce != cudaSuccess) {
@@ -619,7 +659,9 @@ BwdArgs bwd_args(idm_handle* h, int32_t steps) {
     a.sg_stride = h->sg_stride;
     a.grad_params = h->d.grad_params;
     a.grad_state0 = h->d.grad_state0;
-    a.shared_partials = h->shared_partials;
+    a.lane_offsets = h->d.lane_offsets;
+    a.n_lanes = h->d.n_lanes;
+    a.lane_grads = h->lane_grads;
     a.steps = steps;
     a.ckpt_every = h->d.ckpt_every;
     a.k = consts_of(h->d);
@@ -628,10 +670,16 @@ BwdArgs bwd_args(idm_handle* h, int32_t steps) {
 }
 }  // namespace
 
-int idm_forward(idm_handle* h, int32_t steps) {
+int idm_forward(idm_handle* h, int32_t steps) { return idm_forward_ex(h, steps, 0u); }
+
+int idm_forward_ex(idm_handle* h, int32_t steps, uint32_t flags) {
     if (!h) return IDM_EINVAL;
+    OnDevice on_dev(h);
     if (steps < 1 || steps > h->d.max_steps)
         return fail(h, IDM_EINVAL, "steps=%d outside [1, max_steps=%d]", steps, h->d.max_steps);
+    if (flags & ~(uint32_t)IDM_FWD_NO_HISTORY)
+        return fail(h, IDM_EINVAL, "unknown idm_forward_ex flags 0x%x", flags);
+    const bool hist = !(flags & IDM_FWD_NO_HISTORY);
     if (is_vl(h)) {
         VlArgs va = vl_args(h, steps);
         {
@@ -641,6 +689,7 @@ int idm_forward(idm_handle* h, int32_t steps) {
         h->launches++;
         h->steps = steps;
         h->stage = 1;
+        h->hist_ok = true;  // (its speed checkpoints are a small fraction of the traffic)
         return IDM_OK;
     }
     FwdArgs a = fwd_args(h, steps);
@@ -651,6 +700,7 @@ int idm_forward(idm_handle* h, int32_t steps) {
     var.kahan = steps > 2000;  // compensated displacement for long horizons (C3)
     var.rec_v = h->d.vel_traj != nullptr;
     var.loss = 0;
+    var.hist = hist;
     {
         TimedLaunch tl(h, IDM_K_FWD);
         CK(h, launch_fwd(a, h->ntiles, var, h->st));
@@ -658,12 +708,14 @@ int idm_forward(idm_handle* h, int32_t steps) {
     h->launches++;
     h->steps = steps;
     h->stage = 1;
+    h->hist_ok = hist;
     return IDM_OK;
 }
 
 int idm_loss_grad(idm_handle* h, const float* obs, const uint8_t* mask, int32_t kind,
                   double* loss_dev, double* loss_host) {
     if (!h) return IDM_EINVAL;
+    OnDevice on_dev(h);
     if (h->stage < 1) return fail(h, IDM_ESTATE, "idm_loss_grad before idm_forward");
     if (!obs) return fail(h, IDM_EINVAL, "obs is NULL");
     if (kind != IDM_LOSS_L1 && kind != IDM_LOSS_L2)
@@ -701,7 +753,11 @@ int idm_loss_grad(idm_handle* h, const float* obs, const uint8_t* mask, int32_t 
 
 int idm_backward(idm_handle* h) {
     if (!h) return IDM_EINVAL;
+    OnDevice on_dev(h);
     if (h->stage < 2) return fail(h, IDM_ESTATE, "idm_backward before idm_loss_grad");
+    if (!h->hist_ok)
+        return fail(h, IDM_ESTATE, "idm_backward after a forward without state history "
+                                   "(IDM_FWD_NO_HISTORY): run idm_forward");
     if (is_vl(h)) {
         VlArgs va = vl_args(h, h->steps);
         {
@@ -716,17 +772,37 @@ int idm_backward(idm_handle* h) {
     a.grad_traj = h->d.grad_traj;
     bool shared = h->d.param_mode == IDM_PARAMS_SHARED;
     std::memset(&a.adam, 0, sizeof(a.adam));
+    if (shared)  // rows of empty lanes stay 0
+        CK(h, cudaMemsetAsync(h->lane_grads, 0, sizeof(double) * 6 * (size_t)h->d.n_lanes, h->st));
     {
         TimedLaunch tl(h, IDM_K_BWD);
         CK(h, launch_bwd(a, h->ntiles, h->delta4, shared, false, 0, false, h->st));
     }
     h->launches++;
-    if (shared) {
+    if (shared) {  // this handle's lanes (one rank: the whole sum; ranks: idm_reduce_shared)
         TimedLaunch tl(h, IDM_K_REDUCE);
-        CK(h, launch_reduce(h->shared_partials, h->ntiles, 6, nullptr, h->d.grad_params, h->st));
+        CK(h, launch_reduce(h->lane_grads, h->d.n_lanes, 6, nullptr, h->d.grad_params, h->st));
         h->launches++;
     }
     h->stage = 3;
+    return IDM_OK;
+}
+
+int idm_reduce_shared(idm_handle* h, const double* lane_grads, int64_t n_rows) {
+    if (!h) return IDM_EINVAL;
+    OnDevice on_dev(h);
+    if (h->d.param_mode != IDM_PARAMS_SHARED)
+        return fail(h, IDM_EINVAL, "idm_reduce_shared needs shared-parameter mode");
+    if (!lane_grads || n_rows < h->d.n_lanes)
+        return fail(h, IDM_EINVAL, "idm_reduce_shared: lane_grads NULL or fewer rows (%lld) "
+                                   "than this handle's lanes (%d)", (long long)n_rows,
+                    h->d.n_lanes);
+    if (h->stage < 3) return fail(h, IDM_ESTATE, "idm_reduce_shared before idm_backward");
+    {
+        TimedLaunch tl(h, IDM_K_REDUCE);
+        CK(h, launch_reduce(lane_grads, n_rows, 6, nullptr, h->d.grad_params, h->st));
+    }
+    h->launches++;
     return IDM_OK;
 }
 
@@ -752,6 +828,7 @@ AdamArgs make_adam(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, 
     a.beta1 = (float)b1;
     a.beta2 = (float)b2;
     a.eps = 1e-8f;
+    a.status = h->status;
     // boxes of PAPER.md:208 in parameter order (a_max, a_pref, s_min, T_pref, v_targ)
     const float lo[5] = {5.f, 0.1f, 1.f, 0.1f, 20.f}, hi[5] = {10.f, 5.f, 10.f, 5.f, 60.f};
     for (int q = 0; q < 5; ++q) { a.lo[q] = lo[q]; a.hi[q] = hi[q]; }
@@ -780,6 +857,7 @@ extern "C" {
 
 int idm_adam_step(idm_handle* h, int32_t iter, int32_t total_iters, float lr0, float lr1) {
     if (!h) return IDM_EINVAL;
+    OnDevice on_dev(h);
     if (h->stage < 3) return fail(h, IDM_ESTATE, "idm_adam_step before idm_backward");
     if (iter < 0 || total_iters < 1 || iter >= total_iters)
         return fail(h, IDM_EINVAL, "iter=%d outside [0, total_iters=%d)", iter, total_iters);
@@ -801,6 +879,7 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
                  int32_t kind, int32_t iter, int32_t total_iters, float lr0, float lr1,
                  double* loss_dev, double* loss_host) {
     if (!h) return IDM_EINVAL;
+    OnDevice on_dev(h);
     if (steps < 1 || steps > h->d.max_steps)
         return fail(h, IDM_EINVAL, "steps=%d outside [1, max_steps=%d]", steps, h->d.max_steps);
     if (!obs) return fail(h, IDM_EINVAL, "obs is NULL");
@@ -918,6 +997,8 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
         if (++h->epoch == 0) h->epoch = 1;  // 0 = never signalled
         f.epoch = b.epoch = h->epoch;
     }
+    if (shared)  // rows of empty lanes stay 0 (before the forward: the backward follows it directly)
+        CK(h, cudaMemsetAsync(h->lane_grads, 0, sizeof(double) * 6 * (size_t)h->d.n_lanes, h->st));
     if (nch > 1) {
         CK(h, cudaEventRecord(h->ev_fork, h->st));
         CK(h, cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
@@ -954,7 +1035,7 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
     if (shared) {
         {
             TimedLaunch tl(h, IDM_K_REDUCE);
-            CK(h, launch_reduce(h->shared_partials, h->ntiles, 6, nullptr, h->d.grad_params,
+            CK(h, launch_reduce(h->lane_grads, h->d.n_lanes, 6, nullptr, h->d.grad_params,
                                 h->st));
         }
         {
@@ -983,6 +1064,7 @@ int idm_fit_steps(idm_handle* h, int32_t steps, const float* obs, int32_t kind, 
                   int32_t iters, int32_t total_iters, float lr0, float lr1, double* loss_dev,
                   double* loss_host) {
     if (!h) return IDM_EINVAL;
+    OnDevice on_dev(h);
     if (iters < 1 || iter0 < 0 || (int64_t)iter0 + iters > total_iters)
         return fail(h, IDM_EINVAL, "idm_fit_steps: iterations %d..%d outside [0, %d)", iter0,
                     iter0 + iters - 1, total_iters);
@@ -1040,6 +1122,7 @@ int idm_fit(idm_handle* h, int32_t steps, const float* obs, int32_t kind, int32_
             int32_t iters, int32_t total_iters, float lr0, float lr1, double* loss_dev,
             double* loss_host) {
     if (!h) return IDM_EINVAL;
+    OnDevice on_dev(h);
     if (steps < 1 || steps > h->d.max_steps || steps > kFitMaxSteps)
         return fail(h, IDM_EINVAL, "idm_fit: steps=%d outside [1, min(max_steps, %d)]", steps,
                     kFitMaxSteps);
@@ -1114,12 +1197,14 @@ int idm_fit(idm_handle* h, int32_t steps, const float* obs, int32_t kind, int32_
 
 int idm_timing_enable(idm_handle* h, int enable) {
     if (!h) return IDM_EINVAL;
+    OnDevice on_dev(h);
     h->timing = enable != 0;
     return IDM_OK;
 }
 
 int idm_timing_read(idm_handle* h, double* ms, int64_t* launches) {
     if (!h) return IDM_EINVAL;
+    OnDevice on_dev(h);
     double acc[IDM_NKERNELS] = {0};
     int64_t cnt[IDM_NKERNELS] = {0};
     for (auto& r : *h->ev_rec) {
@@ -1141,6 +1226,7 @@ int idm_timing_read(idm_handle* h, double* ms, int64_t* launches) {
 
 int idm_check(idm_handle* h) {
     if (!h) return IDM_EINVAL;
+    OnDevice on_dev(h);
     CK(h, cudaGetLastError());
     return sync_status(h);
 }
@@ -1191,6 +1277,7 @@ int idm_step_host(idm_handle* h, int32_t steps, const float* pos0_host, const fl
                   const float* obs_host, const uint8_t* mask_host, int32_t kind, int32_t iter,
                   int32_t total_iters, float lr0, float lr1, double* loss_host) {
     if (!h) return IDM_EINVAL;
+    OnDevice on_dev(h);
     int s = step_host_enqueue(h, steps, pos0_host, vel0_host, obs_host, mask_host, kind, iter,
                               total_iters, lr0, lr1);
     if (s) return s;
@@ -1205,6 +1292,7 @@ int idm_step_host_async(idm_handle* h, int32_t steps, const float* pos0_host,
                         const float* vel0_host, const float* obs_host, const uint8_t* mask_host,
                         int32_t kind, int32_t iter, int32_t total_iters, float lr0, float lr1) {
     if (!h) return IDM_EINVAL;
+    OnDevice on_dev(h);
     if (h->async_n >= 2)
         return fail(h, IDM_ESTATE, "two idm_step_host_async steps in flight: call "
                                    "idm_step_host_wait first");
@@ -1223,6 +1311,7 @@ int idm_step_host_async(idm_handle* h, int32_t steps, const float* pos0_host,
 
 int idm_step_host_wait(idm_handle* h, double* loss_host) {
     if (!h) return IDM_EINVAL;
+    OnDevice on_dev(h);
     if (h->async_n == 0) return fail(h, IDM_ESTATE, "no idm_step_host_async step in flight");
     const int slot = h->async_head;
     CK(h, cudaEventSynchronize(h->ev_step[slot]));

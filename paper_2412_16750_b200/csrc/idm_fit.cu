@@ -12,6 +12,7 @@
 // this CTA's shared memory.  Arithmetic is the same device code as fwd_kernel<LOSS> /
 // bwd_kernel<ADAM> (core, jac_record, bwd_from_record, loss term, Adam), in the same order, so
 // the parameters come out bit-identical to `iters` idm_fit_step calls.
+#include <climits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -52,6 +53,8 @@ __global__ void __launch_bounds__(kFT, 2) fit_kernel(FitArgs a) {
     const float pinf = __int_as_float(0x7f800000);
     float pj[2] = {0.f, 0.f}, vj[2] = {0.f, 0.f}, sj[2] = {pinf, pinf};  // no leader: gap +inf
     float x[2][6], m1[2][6], m2[2][6];
+    int bad_it = INT_MAX;  // first iteration with a non-finite gradient (reported at the end)
+    int64_t bad_e = 0;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
         const int64_t i = i0 + j;
@@ -149,6 +152,11 @@ __global__ void __launch_bounds__(kFT, 2) fit_kernel(FitArgs a) {
 #pragma unroll
             for (int q = 0; q < 6; ++q) {
                 if (!((a.opt_mask >> q) & 1u)) continue;
+                // a NaN gradient would reset the parameter to its bound through the clamp
+                if (val[j] && !isfinite(gr[j][q]) && bad_it == INT_MAX) {
+                    bad_it = it;
+                    bad_e = q * N + i0 + j;
+                }
                 float xn = leaf_adam(x[j][q], gr[j][q], m1[j][q], m2[j][q], step_size, sqrt_bc2,
                                      a.beta1, a.beta2, a.eps);
                 if (q < 5) xn = fminf(fmaxf(xn, a.lo[q]), a.hi[q]);
@@ -185,6 +193,7 @@ __global__ void __launch_bounds__(kFT, 2) fit_kernel(FitArgs a) {
             a.adam_v[q * N + i] = m2[j][q];
         }
     }
+    if (bad_it != INT_MAX) atomicMin(a.status, (unsigned long long)kBadGrad << 32 | (uint64_t)bad_e);
     // loss of the last iteration: fixed-order CTA sum -> partials[tile]
     double y = (double)lsum.x + (double)lsum.y;
 #pragma unroll
@@ -199,26 +208,21 @@ __global__ void __launch_bounds__(kFT, 2) fit_kernel(FitArgs a) {
 }
 
 template <bool D4, int KIND>
-static void launch_fit_v(const FitArgs& a, int ntiles, cudaStream_t st) {
+static cudaError_t launch_fit_v(const FitArgs& a, int ntiles, cudaStream_t st) {
     constexpr size_t smem = fit_smem_of<kFitMaxSteps>();
-    static bool configured = false;  // one opt-in per instantiation (one device per process)
-    if (!configured) {
-        cudaFuncSetAttribute(fit_kernel<kFitMaxSteps, D4, KIND>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    static std::atomic<unsigned long long> optin{0};  // devices opted in (bit per device)
+    cudaError_t e = smem_optin((const void*)fit_kernel<kFitMaxSteps, D4, KIND>, (int)smem, optin);
+    if (e != cudaSuccess) return e;
     fit_kernel<kFitMaxSteps, D4, KIND><<<ntiles, kFT, smem, st>>>(a);
+    return cudaSuccess;
 }
 
 cudaError_t launch_fit(const FitArgs& a, int ntiles, bool delta4, int kind, cudaStream_t st) {
     if (a.steps < 1 || a.steps > kFitMaxSteps) return cudaErrorInvalidValue;
-    if (delta4) {
-        if (kind == 0) launch_fit_v<true, 0>(a, ntiles, st);
-        else launch_fit_v<true, 1>(a, ntiles, st);
-    } else {
-        if (kind == 0) launch_fit_v<false, 0>(a, ntiles, st);
-        else launch_fit_v<false, 1>(a, ntiles, st);
-    }
+    cudaError_t e;
+    if (delta4) e = kind == 0 ? launch_fit_v<true, 0>(a, ntiles, st) : launch_fit_v<true, 1>(a, ntiles, st);
+    else e = kind == 0 ? launch_fit_v<false, 0>(a, ntiles, st) : launch_fit_v<false, 1>(a, ntiles, st);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

@@ -1,5 +1,6 @@
 // idm_internal.h -- kernel argument blocks and launchers shared by idm_kernels.cu and idm_capi.cu.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -11,9 +12,26 @@ namespace idm {
 constexpr unsigned kBadInput = 0xFFFFFFF0u;  // invalid pos0/vel0/length at vehicle index
 constexpr unsigned kBadParam = 0xFFFFFFF1u;  // invalid parameter at flat index
 constexpr unsigned kBadDelta = 0xFFFFFFF2u;  // delta != 4 in a delta=4-specialised kernel
+constexpr unsigned kBadOrder = 0xFFFFFFF3u;  // lane member overlapping / behind its leader
+constexpr unsigned kBadGrad = 0xFFFFFFF4u;   // non-finite parameter gradient (flat index)
+
+// Opt `fn` into `bytes` of dynamic shared memory on the CURRENT device.  The attribute belongs
+// to each device's context, so it is set once per device (bit d of `done`), thread-safely
+// (a race only sets it twice), and its error is returned.
+inline cudaError_t smem_optin(const void* fn, int bytes, std::atomic<unsigned long long>& done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = dev < 64 ? 1ull << dev : 0ull;
+    if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_release);
+    return e;
+}
 
 struct ValidateArgs {
     const float *pos0, *vel0, *length, *params;
+    const uint8_t* lead;  // lane mode: leader flags (order check); nullptr: no lane order
     int64_t n, n_par;
     unsigned long long* status;
     unsigned* delta_not4;
@@ -24,6 +42,7 @@ struct FwdVariant {
     bool kahan;   // compensated displacement
     bool rec_v;   // record speeds
     int loss;     // 0, or fused Eq. 4 (1 = L1, 2 = L2): read obs, sum the loss (idm_fit_step)
+    bool hist = true;  // store the state history for a backward (false: P rows only)
 };
 
 // Lane-mode state history in HBM, TILE-LOCAL layout (internal workspace):
@@ -78,6 +97,7 @@ struct AdamArgs {
     uint32_t opt_mask;
     float step_size, sqrt_bc2, beta1, beta2, eps;
     float lo[5], hi[5];
+    unsigned long long* status;  // a non-finite gradient is reported here (kBadGrad)
 };
 
 struct BwdArgs {
@@ -93,7 +113,11 @@ struct BwdArgs {
     int64_t sg_stride;
     int tile0;  // first tile of this launch
     float *grad_params, *grad_state0;
-    double* shared_partials;  // [ntiles][6] (shared mode)
+    // shared mode: per-lane fp64 gradient sums -> lane_grads[lane][6] (lane = index into
+    // lane_offsets [n_lanes + 1])
+    const int32_t* lane_offsets;
+    int32_t n_lanes;
+    double* lane_grads;
     int steps, ckpt_every;
     Consts k;
     unsigned long long* status;
@@ -197,6 +221,9 @@ __device__ __forceinline__ void st_cs_if(float* p, bool on, float x) {
 __device__ __forceinline__ float leaf_adam(float x, float g, float& m, float& v, float step_size,
                                            float sqrt_bc2, float b1, float b2, float eps);
 
+// The caller reports a non-finite g (report_bad_grad): a NaN gradient would otherwise reset the
+// parameter to its lower bound through the clamp (fminf / fmaxf drop NaN) while the loss still
+// looks finite.
 __device__ __forceinline__ void adam_update(const AdamArgs& a, int q, int64_t e, float g) {
     float m = a.m[e], v = a.v[e];
     float x = leaf_adam(a.x[e], g, m, v, a.step_size, a.sqrt_bc2, a.beta1, a.beta2, a.eps);
@@ -206,6 +233,9 @@ __device__ __forceinline__ void adam_update(const AdamArgs& a, int q, int64_t e,
     a.x[e] = x;
 }
 
+__device__ __forceinline__ void report_bad_grad(unsigned long long* status, int64_t e) {
+    atomicMin(status, (unsigned long long)kBadGrad << 32 | (uint64_t)e);
+}
 
 // Adam on one scalar (parameters and virtual-leader leaves), explicit roundings so the separate
 // kernels, the fused backward and the whole-fit kernel produce the same bits.  The update

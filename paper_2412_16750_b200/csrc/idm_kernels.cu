@@ -46,6 +46,15 @@ __global__ void validate_kernel(ValidateArgs a) {
         bool ok = isfinite(p) && isfinite(v) && isfinite(l) && v >= 0.f && l >= 0.f;
         if (!ok) atomicMin(a.status, (unsigned long long)(kBadInput) << 32 | (uint64_t)i);
     }
+    // lane order (the leader is the vehicle directly ahead in the same lane): a
+    // lane member must be strictly behind its leader with a positive gap, else the input is
+    // out of order or overlapping (gaps in (0, eps_gap) are valid and clamped, R#7)
+    if (a.lead)
+        for (i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
+            if (!a.lead[i]) continue;
+            const float gap = (a.pos0[i + 1] - a.pos0[i]) - a.length[i + 1];  // as fwd_kernel
+            if (!(gap > 0.f)) atomicMin(a.status, (unsigned long long)(kBadOrder) << 32 | (uint64_t)i);
+        }
     int64_t m = 6 * a.n_par;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
         float x = a.params[e];
@@ -208,9 +217,12 @@ __device__ __forceinline__ void cp_async_wait() {
 #ifndef IDM_FWD_LOSS_MINB
 #define IDM_FWD_LOSS_MINB 4  // CTAs per SM the fused (LOSS) forward is register-budgeted for
 #endif
-template <bool D4, bool KAHAN, bool RECV, int LOSS, int CK>
+// HIST = false (LOSS = 0 only): a prediction rollout (idm_forward_ex IDM_FWD_NO_HISTORY) that
+// writes only the P rows -- no speed history or checkpoints, nothing for a backward.
+template <bool D4, bool KAHAN, bool RECV, int LOSS, int CK, bool HIST = true>
 __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 4)))
     fwd_kernel(FwdArgs a) {
+    static_assert(HIST || LOSS == 0, "the fused forward always feeds a backward");
     constexpr int KS = CK > 4 ? CK : 4;
     // LOSS = 3: the fused iteration whose backward derives Eq. 4 itself (from obs and the
     // rebuilt positions): only the tile history (speeds; gap + displacement checkpoints)
@@ -336,6 +348,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     // checkpoint rows the consumer reads: the gap (idm_backward); + displacement (fused
     // backward rebuilds positions); + compensation (and that with Kahan)
     auto put_ck = [&] {
+        if (!HIST) return;
         __stcs(ckp, s);
         if (DCK) __stcs(ckp + kR2, D);
         if (DCK && KAHAN) __stcs(ckp + 2 * kR2, cmp);
@@ -370,7 +383,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     if (OBSV) loss_step(ld_obs(obs, true), p0, std::integral_constant<int, 0>{});
     else if (!LOSS) put(orow, p0);
     if (RECV) put(vrow, v);
-    __stcs(vtp, v);
+    if (HIST) __stcs(vtp, v);
     put_ck();
     int par = 0;
     // one synchronous step of the whole tile; o = this step's observations (LOSS)
@@ -394,7 +407,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
         const float2 Pv = vadd(p0, D);
         if (OBSV) loss_step(o, Pv, PH);
         else if (!LOSS) put(orow, Pv);
-        __stcs(vtp, v);
+        if (HIST) __stcs(vtp, v);
         if (RECV) put(vrow, v);
     };
     // first checkpoint step at which each vehicle's state was non-finite (INT_MAX: none); kept
@@ -407,7 +420,7 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
         bad1 = (!ok1 && bad1 == INT_MAX) ? t0 : bad1;
     };
     auto checkpoint = [&](int t0) {  // (gap, D, compensation) at step t0 > 0 + finiteness check
-        ckp += kCkRows * kR2;
+        if (HIST) ckp += kCkRows * kR2;
         put_ck();
         finite2(t0);
     };
@@ -768,34 +781,49 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
         for (int j = 0; j < kVpt; ++j) {
             if (!val[j]) continue;
             const int64_t i = i0 + j;
+            int bq = -1;  // first optimised parameter with a non-finite gradient
 #pragma unroll
             for (int q = 0; q < 6; ++q) {
                 a.grad_params[q * N + i] = gr[j][q];
                 // fused iteration: Adam on this vehicle's parameters right here (idm_fit_step)
-                if (ADAM && ((a.adam.opt_mask >> q) & 1u)) adam_update(a.adam, q, q * N + i, gr[j][q]);
+                if (ADAM && ((a.adam.opt_mask >> q) & 1u)) {
+                    if (bq < 0 && !isfinite(gr[j][q])) bq = q;
+                    adam_update(a.adam, q, q * N + i, gr[j][q]);
+                }
             }
+            if (ADAM && bq >= 0) report_bad_grad(a.status, bq * N + i);
         }
     } else {
-        // fixed-order block reduction in fp64 -> partial[tile][6]
-        __shared__ double red[kT / 32][6];
-        double acc[6];
+        // Per-LANE fp64 sums in vehicle order -> lane_grads[lane][6]: a lane is whole on every
+        // rank and in every tile plan, so these rows (and their fixed-order sum over the global
+        // lane index, idm_reduce_shared) do not depend on the tiling or the sharding.  The
+        // staging ring is idle after the sweep (the barrier above ordered its last reads).
+        double* vg = reinterpret_cast<double*>(smem_b);  // [kCap][6]
 #pragma unroll
-        for (int q = 0; q < 6; ++q) {
-            double x = 0.0;
+        for (int j = 0; j < kVpt; ++j)
 #pragma unroll
-            for (int j = 0; j < kVpt; ++j) x += (double)gr[j][q];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-            acc[q] = x;
-        }
-        if ((tid & 31) == 0)
-#pragma unroll
-            for (int q = 0; q < 6; ++q) red[tid >> 5][q] = acc[q];
+            for (int q = 0; q < 6; ++q) vg[(id0 + j) * 6 + q] = (double)gr[j][q];
         __syncthreads();
-        if (tid < 6) {
-            double x = 0.0;
-            for (int w = 0; w < kT / 32; ++w) x += red[w][tid];
-            a.shared_partials[(int64_t)tile * 6 + tid] = x;
+#pragma unroll
+        for (int j = 0; j < kVpt; ++j) {
+            const int li = id0 + j;
+            if (!val[j] || !(li == 0 || a.lead[base + li - 1] == 0)) continue;  // lane starts
+            double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            for (int e = li;; ++e) {  // the lane's vehicles up to its head (no leader)
+#pragma unroll
+                for (int q = 0; q < 6; ++q) acc[q] += vg[e * 6 + q];
+                if (a.lead[base + e] == 0) break;
+            }
+            // lane index: the last l with lane_offsets[l] <= i (empty lanes skipped)
+            const int64_t gi = base + li;
+            int lo = 0, hi = a.n_lanes;  // lane_offsets[lo] <= gi < lane_offsets[hi]
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (a.lane_offsets[mid] <= gi) lo = mid;
+                else hi = mid;
+            }
+#pragma unroll
+            for (int q = 0; q < 6; ++q) a.lane_grads[(int64_t)lo * 6 + q] = acc[q];
         }
     }
     if (OBS && a.loss_partials) block_sum_to(lacc, a.loss_partials + tile);  // Eq. 4 here
@@ -874,11 +902,13 @@ __global__ void __launch_bounds__(256) loss_kernel(LossArgs a) {
 }
 
 // ------------------------------------------------------------------------------ NK4
-// Sums `n` rows of `width` fp64 partials in fixed order; out_f (nullable) gets a float copy.
+// Sums `n` rows of `width` fp64 partials in fixed order (per thread strided, then a fixed tree;
+// a function of n only); out_f (nullable) gets a float copy.  Block b sums column b.
 __global__ void reduce_kernel(const double* __restrict__ partials, int64_t n, int width,
                               double* __restrict__ out, float* __restrict__ out_f) {
     __shared__ double red[256];
-    for (int c = 0; c < width; ++c) {
+    {
+        const int c = blockIdx.x;
         double x = 0.0;
         for (int64_t r = threadIdx.x; r < n; r += blockDim.x) x += partials[r * width + c];
         red[threadIdx.x] = x;
@@ -891,7 +921,6 @@ __global__ void reduce_kernel(const double* __restrict__ partials, int64_t n, in
             if (out) out[c] = red[0];
             if (out_f) out_f[c] = (float)red[0];
         }
-        __syncthreads();
     }
 }
 
@@ -901,7 +930,11 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int q = (int)(e / a.n_par);
-        if ((a.opt_mask >> q) & 1u) adam_update(a, q, e, a.grad[e]);
+        if ((a.opt_mask >> q) & 1u) {
+            const float g = a.grad[e];
+            if (!isfinite(g)) report_bad_grad(a.status, e);
+            adam_update(a, q, e, g);
+        }
     }
 }
 
@@ -920,6 +953,11 @@ static void launch_fwd_k(const FwdArgs& a, int ntiles, const FwdVariant& var, cu
         if (var.loss == 1) { fwd_kernel<D4, KH, false, 1, KS><<<g, b, 0, st>>>(a); return; }
         if (var.loss == 2) { fwd_kernel<D4, KH, false, 2, KS><<<g, b, 0, st>>>(a); return; }
         if (var.loss == 3) { fwd_kernel<D4, KH, false, 3, KS><<<g, b, 0, st>>>(a); return; }
+    }
+    if (!var.hist) {  // prediction rollout: P rows only (the segment length is immaterial)
+        if (var.rec_v) fwd_kernel<D4, KH, true, 0, 4, false><<<g, b, 0, st>>>(a);
+        else fwd_kernel<D4, KH, false, 0, 4, false><<<g, b, 0, st>>>(a);
+        return;
     }
     if (var.rec_v) fwd_kernel<D4, KH, true, 0, KS><<<g, b, 0, st>>>(a);
     else fwd_kernel<D4, KH, false, 0, KS><<<g, b, 0, st>>>(a);
@@ -962,12 +1000,9 @@ template <bool D4, bool SH, bool AD, int KS, int GO, bool KH>
 static cudaError_t launch_bwd_v(const BwdArgs& a, int ntiles, cudaStream_t st,
                                 bool pdl = false) {
     constexpr size_t smem = bwd_smem_of<KS, GO>();
-    static bool configured = false;  // one opt-in per instantiation (one device per process)
-    if (!configured) {
-        cudaFuncSetAttribute(bwd_kernel<D4, SH, AD, KS, GO, KH>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    static std::atomic<unsigned long long> optin{0};  // devices opted in (bit per device)
+    cudaError_t e = smem_optin((const void*)bwd_kernel<D4, SH, AD, KS, GO, KH>, (int)smem, optin);
+    if (e != cudaSuccess) return e;
     if (!pdl) {
         bwd_kernel<D4, SH, AD, KS, GO, KH><<<ntiles, kT, smem, st>>>(a);
         return cudaSuccess;  // launch errors: cudaGetLastError in launch_bwd
@@ -987,9 +1022,9 @@ static cudaError_t launch_bwd_v(const BwdArgs& a, int ntiles, cudaStream_t st,
 
 // API backward (idm_backward): dL/dP rows from grad_traj, Adam by its own kernel
 template <bool D4, int KS>
-static void launch_bwd_k(const BwdArgs& a, int ntiles, bool shared, cudaStream_t st) {
-    if (shared) launch_bwd_v<D4, true, false, KS, 0, false>(a, ntiles, st);
-    else launch_bwd_v<D4, false, false, KS, 0, false>(a, ntiles, st);
+static cudaError_t launch_bwd_k(const BwdArgs& a, int ntiles, bool shared, cudaStream_t st) {
+    if (shared) return launch_bwd_v<D4, true, false, KS, 0, false>(a, ntiles, st);
+    return launch_bwd_v<D4, false, false, KS, 0, false>(a, ntiles, st);
 }
 
 // fused idm_fit_step backward (ckpt_every == 4): dL/dP from obs
@@ -1016,12 +1051,11 @@ static cudaError_t launch_bwd_d(const BwdArgs& a, int ntiles, bool shared, bool 
     }
     if (pdl || adam) return cudaErrorInvalidValue;  // API backward: after the loss kernel, no Adam
     switch (a.ckpt_every) {
-        case 2: launch_bwd_k<D4, 2>(a, ntiles, shared, st); break;
-        case 4: launch_bwd_k<D4, 4>(a, ntiles, shared, st); break;
-        case 8: launch_bwd_k<D4, 8>(a, ntiles, shared, st); break;
+        case 2: return launch_bwd_k<D4, 2>(a, ntiles, shared, st);
+        case 4: return launch_bwd_k<D4, 4>(a, ntiles, shared, st);
+        case 8: return launch_bwd_k<D4, 8>(a, ntiles, shared, st);
         default: return cudaErrorInvalidValue;
     }
-    return cudaSuccess;
 }
 
 cudaError_t launch_bwd(const BwdArgs& a, int ntiles, bool delta4, bool shared, bool adam,
@@ -1044,7 +1078,7 @@ cudaError_t launch_loss(const LossArgs& a, int nblocks, cudaStream_t st) {
 
 cudaError_t launch_reduce(const double* partials, int64_t n, int width, double* out,
                           float* out_f, cudaStream_t st) {
-    reduce_kernel<<<1, 256, 0, st>>>(partials, n, width, out, out_f);
+    reduce_kernel<<<width, 256, 0, st>>>(partials, n, width, out, out_f);
     return cudaGetLastError();
 }
 

@@ -311,11 +311,16 @@ __global__ void __launch_bounds__(kVT, 2) vl_bwd_kernel(VlArgs a) {
         }
         if (!(isfinite(lvj[j]) && isfinite(lDj[j])))
             atomicMin(a.status, (unsigned long long)0 << 32 | (uint64_t)(uint32_t)i);
+        int bq = -1;  // first optimised parameter with a non-finite gradient
 #pragma unroll
         for (int q = 0; q < 6; ++q) {
             a.grad_params[q * N + i] = gr6[q];
-            if (ADAM && ((a.adam.opt_mask >> q) & 1u)) adam_update(a.adam, q, q * N + i, gr6[q]);
+            if (ADAM && ((a.adam.opt_mask >> q) & 1u)) {
+                if (bq < 0 && !isfinite(gr6[q])) bq = q;
+                adam_update(a.adam, q, q * N + i, gr6[q]);
+            }
         }
+        if (ADAM && bq >= 0) report_bad_grad(a.status, bq * N + i);
     }
     if (OK >= 0) vl_block_sum(lacc, a.loss_partials);  // this block's Eq. 4 loss
 }

@@ -27,6 +27,7 @@ PARAMS_PER_VEHICLE, PARAMS_SHARED = 0, 1
 LEADER_LANE, LEADER_VIRTUAL = 0, 1
 VL_INIT = (10.0, 0.0)  # initial (Delta p_k, Delta v_k)
 LOSS_KINDS = {"l1": 0, "l2": 1}
+FWD_NO_HISTORY = 1  # idm_forward_ex flag: prediction rollout, no state history
 PAPER_OPT_MASK = 0x1F  # the paper optimizes five parameters; delta frozen
 DEFAULT_CKPT = 4  # backward checkpoint interval k (tuned on B200)
 
@@ -68,6 +69,7 @@ class IdmDesc(C.Structure):
         ("vl_adam_m", C.c_void_p),
         ("vl_adam_v", C.c_void_p),
         ("obs_stage2", C.c_void_p),
+        ("lane_grads", C.c_void_p),
     ]
 
 
@@ -103,6 +105,10 @@ def load_library(path: str | None = None):
     L.idm_init.argtypes = [C.POINTER(vp), C.POINTER(IdmDesc)]
     L.idm_forward.restype = C.c_int
     L.idm_forward.argtypes = [vp, i32]
+    L.idm_forward_ex.restype = C.c_int
+    L.idm_forward_ex.argtypes = [vp, i32, C.c_uint32]
+    L.idm_reduce_shared.restype = C.c_int
+    L.idm_reduce_shared.argtypes = [vp, vp, i64]
     L.idm_loss_grad.restype = C.c_int
     L.idm_loss_grad.argtypes = [vp, vp, vp, i32, vp, C.POINTER(C.c_double)]
     L.idm_backward.restype = C.c_int
@@ -192,6 +198,10 @@ class IdmSim:
                                            f"describe {n} vehicles")
         n_par = 1 if shared_params else n
         self.shared_params = bool(shared_params)
+        # shared mode: per-lane gradient sums [n_lanes, 6] fp64, the unit of the shard-count
+        # invariant cross-rank reduction (parallel.reduce_step -> idm_reduce_shared)
+        self.lane_grads = torch.zeros(self.n_lanes, 6, dtype=torch.float64, device=dev) \
+            if shared_params else None
         if params is None:
             from .synth import init_params
             params = init_params(n_par)
@@ -251,6 +261,7 @@ class IdmSim:
         d.a_min = a_min
         d.eps_gap = eps_gap
         d.param_mode = PARAMS_SHARED if shared_params else PARAMS_PER_VEHICLE
+        d.lane_grads = self.lane_grads.data_ptr() if self.lane_grads is not None else None
         d.opt_mask = opt_mask
         d.stream = self.stream.cuda_stream
         if virtual_leader:
@@ -269,7 +280,8 @@ class IdmSim:
         d.workspace_bytes = nbytes
         self.desc = d
         h = C.c_void_p()
-        rc = L.idm_init(C.byref(h), C.byref(d))
+        with torch.cuda.device(dev):  # the handle belongs to the device current at idm_init
+            rc = L.idm_init(C.byref(h), C.byref(d))
         if rc != IDM_OK:
             raise IdmError(rc, "idm_init failed (message on stderr)")
         self.handle = h
@@ -281,9 +293,22 @@ class IdmSim:
         if rc != IDM_OK:
             raise IdmError(rc, self._lib.idm_last_error(self.handle).decode())
 
-    def forward(self, steps: int):
-        self._check(self._lib.idm_forward(self.handle, int(steps)))
+    def forward(self, steps: int, history: bool = True):
+        """idm_forward (history=False: idm_forward_ex IDM_FWD_NO_HISTORY, a prediction rollout
+        that writes only traj / vel_traj / state_out; no backward may follow)."""
+        if history:
+            self._check(self._lib.idm_forward(self.handle, int(steps)))
+        else:
+            self._check(self._lib.idm_forward_ex(self.handle, int(steps), FWD_NO_HISTORY))
         self.steps = int(steps)
+
+    def reduce_shared(self, lane_grads: torch.Tensor):
+        """idm_reduce_shared: grad_params = the fixed-order sum of the GLOBAL per-lane rows
+        (all ranks' lanes, [n_lanes_total, 6] fp64 on this device)."""
+        assert lane_grads.dtype == torch.float64 and lane_grads.is_contiguous()
+        assert lane_grads.device == self.device and lane_grads.dim() == 2
+        self._check(self._lib.idm_reduce_shared(self.handle, _ptr(lane_grads),
+                                                lane_grads.shape[0]))
 
     def loss_grad(self, obs: torch.Tensor, mask: torch.Tensor | None = None, kind: str = "l1",
                   sync: bool = True):

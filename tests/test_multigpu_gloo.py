@@ -1,6 +1,9 @@
-"""World-size-2 CPU (gloo) tests of the multi-GPU host logic: whole-lane sharding and the one
-per-step all-reduce (loss + shared-parameter gradients).  Per-shard results come from the
-fp64 oracle, so the test checks that sharded-then-reduced equals unsharded."""
+"""Multi-rank host logic on the CPU (gloo, world sizes 2 and 3): whole-lane sharding, the loss
+all-reduce, and the shard-count-invariant shared-gradient reduction (per-lane rows gathered by
+an exact zero-padded all-reduce, then summed in the global lane order).  Per-shard results come
+from the fp64 oracle (lanes are independent, so a lane's shared-mode gradient is the oracle's
+shared-mode gradient of that lane alone), so the test checks sharded-then-reduced against
+unsharded.  The CUDA path under several ranks: tests/test_multirank_gpu.py."""
 import os
 import socket
 
@@ -11,6 +14,9 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2412_16750_b200 import parallel, synth
+
+LANES = [12, 1, 7, 30, 0, 5, 9, 16, 3]  # includes an empty lane
+SHARED = np.array([8.0, 1.7, 3.0, 1.4, 33.0, 4.0])
 
 
 def _free_port():
@@ -34,70 +40,90 @@ def test_shard_lanes_partition():
                 assert max(sizes) - min(sizes) <= align
 
 
-def _worker(rank, world, port, shared, out_q):
+def _lane_rows(O, w, obs):
+    """Per-lane shared-mode gradient rows [n_lanes, 6] of workload w (oracle, lane by lane)."""
+    rows = np.zeros((w.n_lanes, 6))
+    for l in range(w.n_lanes):
+        if w.lane_offsets[l + 1] == w.lane_offsets[l]:
+            continue
+        sub = synth.lane_subset(w, [l])
+        vi = sub.meta["vehicle_index"]
+        h = O.leader_from_lanes(sub.lane_offsets)
+        P, V = O.rollout(h, sub.length, sub.p0, sub.v0, SHARED, w.K)
+        _, gP = O.loss(P, obs[:, vi], "l1")
+        rows[l] = O.backward(h, sub.length, SHARED, P, V, gP)["g_params"][:, 0]
+    return rows
+
+
+def _worker(rank, world, port, out_q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from oracle import oracle as O
-        w = synth.make_workload("C2", lane_sizes=[12, 1, 7, 30, 5, 9, 16], K=40, seed=17)
+        w = synth.make_workload("C2", lane_sizes=LANES, K=40, seed=17)
         obs = synth.kinematic_obs(w).astype(np.float64)
         l0, l1 = parallel.shard_lanes(w.n_lanes, world, rank)
         sub = synth.lane_subset(w, np.arange(l0, l1))
         vi = sub.meta["vehicle_index"]
-        prm = np.array([8.0, 1.7, 3.0, 1.4, 33.0, 4.0]) if shared else \
-            synth.init_params(sub.n).astype(np.float64)
+        # per-vehicle parameters: the loss is the only collective
+        prm = synth.init_params(sub.n).astype(np.float64)
         h = O.leader_from_lanes(sub.lane_offsets)
         P, V = O.rollout(h, sub.length, sub.p0, sub.v0, prm, w.K)
         L, gP = O.loss(P, obs[:, vi], "l1")
         g = O.backward(h, sub.length, prm, P, V, gP)
         loss = torch.tensor([L], dtype=torch.float64)
-        grads = torch.tensor(g["g_params"][:, 0]) if shared else None
-        parallel.reduce_step(loss, grads)
+        parallel.reduce_loss(loss)
+        # shared parameters: this rank's lane rows -> global rows (exact gather)
+        lane0, total = parallel.lane_offset(l1 - l0)
+        assert (lane0, total) == (l0, w.n_lanes)
+        rows = torch.as_tensor(_lane_rows(O, sub, obs[:, vi]))
+        grows = parallel.gather_lane_rows(rows, lane0, total)
+        n_all = parallel.sum_over_ranks(sub.n)
         # the fused optimizer calls refuse shared parameters across ranks (their in-library
-        # Adam would skip this all-reduce); per-vehicle parameters are fine
+        # Adam would skip the gradient gather); per-vehicle parameters are fine
         import types
         from paper_2412_16750_b200 import idm
         guard = idm.IdmSim._no_sharded_shared
-        if shared:
-            with pytest.raises(idm.IdmError):
-                guard(types.SimpleNamespace(shared_params=True), "fit_step")
-        else:
-            guard(types.SimpleNamespace(shared_params=False), "fit_step")
-        out_q.put((rank, float(loss.item()),
-                   None if grads is None else grads.numpy().copy(),
-                   None if shared else (vi, g["g_params"])))
+        with pytest.raises(idm.IdmError):
+            guard(types.SimpleNamespace(shared_params=True), "fit_step")
+        guard(types.SimpleNamespace(shared_params=False), "fit_step")
+        out_q.put((rank, float(loss.item()), grows.numpy().copy(), vi, g["g_params"], n_all))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("shared", [False, True])
-def test_two_rank_reduce_matches_unsharded(shared):
+@pytest.mark.parametrize("world", [2, 3])
+def test_ranks_reduce_matches_unsharded(world):
     from oracle import oracle as O
     O.build()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, shared, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=120) for _ in procs]
+    res = [q.get(timeout=180) for _ in procs]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     # unsharded reference
-    w = synth.make_workload("C2", lane_sizes=[12, 1, 7, 30, 5, 9, 16], K=40, seed=17)
+    w = synth.make_workload("C2", lane_sizes=LANES, K=40, seed=17)
     obs = synth.kinematic_obs(w).astype(np.float64)
-    prm = np.array([8.0, 1.7, 3.0, 1.4, 33.0, 4.0]) if shared else \
-        synth.init_params(w.n).astype(np.float64)
+    prm = synth.init_params(w.n).astype(np.float64)
     h = O.leader_from_lanes(w.lane_offsets)
     P, V = O.rollout(h, w.length, w.p0, w.v0, prm, w.K)
     L, gP = O.loss(P, obs, "l1")
     g = O.backward(h, w.length, prm, P, V, gP)
-    for rank, loss, grads, per in res:
+    rows = _lane_rows(O, w, obs)
+    Ps, Vs = O.rollout(h, w.length, w.p0, w.v0, SHARED, w.K)
+    _, gPs = O.loss(Ps, obs, "l1")
+    gs = O.backward(h, w.length, SHARED, Ps, Vs, gPs)["g_params"][:, 0]
+    assert np.allclose(rows.sum(axis=0), gs, rtol=1e-12, atol=1e-9)  # rows partition the sum
+    for rank, loss, grows, vi, gp, n_all in res:
         assert abs(loss - L) <= 1e-12 * abs(L)
-        if shared:
-            assert np.allclose(grads, g["g_params"][:, 0], rtol=1e-12, atol=1e-9)
-        else:
-            vi, gp = per
-            # lanes are independent: per-vehicle gradients are shard-invariant, bitwise
-            assert np.array_equal(gp, g["g_params"][:, vi])
+        assert n_all == w.n
+        # the gathered per-lane rows are the unsharded rows bit for bit, on every rank: their
+        # fixed-order sum cannot depend on the number of ranks
+        assert np.array_equal(grows, rows)
+        # lanes are independent: per-vehicle gradients are shard-invariant, bitwise
+        assert np.array_equal(gp, g["g_params"][:, vi])

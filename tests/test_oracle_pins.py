@@ -403,6 +403,41 @@ def test_adjoint_linearity_and_k1(oracle):
     assert g["g_v0"][0] == DT and g["g_p0"][0] == 1.0
 
 
+def test_state_gradient_condition_scales(oracle):
+    """The condition scales of dL/dp0, dL/dv0 (sum of |terms| added into the state adjoint, the
+    analogue of g_abs; SURVEY.md 8(c) parity protocol): closed forms at K = 1 and K = 2, the
+    exact cancellation of a lone vehicle's L = P_2 - P_1 (dL/dp0 = 0 at scale 2), the triangle
+    inequality |g| <= scale on coupled lanes (lane and virtual-leader adjoints), and linearity
+    in the upstream gradient."""
+    lone, ln = np.array([-1], np.int32), np.array([4.0])
+    P, V = oracle.rollout(lone, ln, np.array([0.0]), np.array([10.0]), DEFAULT, 1)
+    g = oracle.backward(lone, ln, DEFAULT, P, V, np.array([[0.0], [1.0]]))
+    assert g["g_p0_abs"][0] == 1.0 and g["g_v0_abs"][0] == DT
+    # L = P_2 - P_1 = dt v_1: p0 cancels exactly; its scale counts both observations
+    P, V = oracle.rollout(lone, ln, np.array([0.0]), np.array([10.0]), DEFAULT, 2)
+    g = oracle.backward(lone, ln, DEFAULT, P, V, np.array([[0.0], [-1.0], [1.0]]))
+    assert g["g_p0"][0] == 0.0 and g["g_p0_abs"][0] == 2.0
+    assert g["g_v0_abs"][0] >= abs(g["g_v0"][0]) > 0.0
+    w = synth.make_workload("C1", lane_sizes=[7, 1, 5], K=60, seed=9)
+    h = oracle.leader_from_lanes(w.lane_offsets)
+    P, V = oracle.rollout(h, w.length, w.p0, w.v0, w.theta_true, w.K)
+    for kind in ("l1", "l2"):
+        _, gP = oracle.loss(P, synth.add_noise(P, 0.3, 4), kind)
+        g = oracle.backward(h, w.length, w.theta_true, P, V, gP)
+        for a, b in (("g_p0", "g_p0_abs"), ("g_v0", "g_v0_abs")):
+            assert np.all(np.abs(g[a]) <= g[b] * (1 + 1e-12))
+        g3 = oracle.backward(h, w.length, w.theta_true, P, V, -3.0 * gP)
+        assert np.allclose(g3["g_p0_abs"], 3 * g["g_p0_abs"], rtol=1e-12)
+        assert np.allclose(g3["g_v0_abs"], 3 * g["g_v0_abs"], rtol=1e-12)
+    dp = np.random.default_rng(2).uniform(5, 40, (w.K, w.n))
+    dv = np.random.default_rng(3).uniform(-2, 2, (w.K, w.n))
+    Pv, Vv = oracle.rollout_vl(w.p0, w.v0, w.theta_true, dp, dv)
+    _, gP = oracle.loss(Pv, synth.add_noise(Pv, 0.3, 5), "l1")
+    g = oracle.backward_vl(w.theta_true, dp, dv, Pv, Vv, gP)
+    for a, b in (("g_p0", "g_p0_abs"), ("g_v0", "g_v0_abs")):
+        assert np.all(np.abs(g[a]) <= g[b] * (1 + 1e-12))
+
+
 def test_shared_parameter_gradient_is_sum_of_per_vehicle(oracle):
     """Shared mode (north_star): with identical per-vehicle parameters, the shared gradient
     equals the sum of the per-vehicle gradients."""
