@@ -130,6 +130,21 @@ size_t idm_workspace_bytes(const idm_desc* d);
 int64_t idm_plan_tiles(const int32_t* lane_offsets, int32_t n_lanes, int64_t n_vehicles,
                        int64_t* tile_start);
 
+/* Initial state of a fit from its observations, the paper's initialisation (PAPER.md:267:
+   "the initial position p(0) and speed v(0) for each trajectory were set to 0 and
+   (Delta P) / Delta t, where Delta P is the distance between the first two data points"; R#13:
+   with lanes, p(0) is the vehicle's own first observation).  obs: DEVICE [(steps+1)][N]
+   step-major positions, NaN = not observed (as idm_loss_grad).  Per vehicle, the first two
+   observed rows t1 < t2 give
+       vel0 = max(0, (obs[t2] - obs[t1]) / ((t2 - t1) dt)),   pos0 = obs[t1] - t1 dt vel0
+   (the first data point carried back to step 0 at that speed: obs[t1] when t1 = 0); one
+   observation: vel0 = 0, pos0 = obs[t1]; none: 0, 0.  pos0, vel0: DEVICE [N] outputs (e.g. the
+   arrays a descriptor will point to).  No handle needed (call before idm_init); ordered on
+   `stream` (cudaStream_t, NULL = legacy); IDM_EINVAL for bad arguments, IDM_ECUDA if the launch
+   fails. */
+int idm_state_from_obs(const float* obs, int64_t n_vehicles, int32_t steps, float dt,
+                       float* pos0, float* vel0, void* stream);
+
 /* Validate the descriptor and input data (finite, v(0) >= 0, lengths >= 0, a_max, a_pref,
    v_targ, delta > 0, lane offsets well formed, every lane fits one lane tile of
    idm_max_lane_vehicles() vehicles, and -- lane mode -- every lane member strictly behind its

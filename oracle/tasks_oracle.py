@@ -3,6 +3,7 @@
 TEST INFRASTRUCTURE ONLY (see oracle/oracle.py).  Pure Python/numpy, written from the paper:
   * nearest time step k_j of each timestamp T_j (PAPER.md:199; SPEC.md:297-302: round half up);
   * Eq. 4 over observation lists, L = sum_j |P_j - P[k_j]| (PAPER.md:201-205);
+  * the fit's initial state from the first two data points (R#13);
   * Table I criteria: Pos. = mean over data points of |P_j - P[k_j]| divided
     by the total trajectory length (spatial P_last - P_first), Acc. = mean / std
     of |a| over all steps, Imp. = fraction of trajectories with any |a| > 10 (strict).
@@ -55,3 +56,28 @@ def acceleration_stats(acc):
 def implausible(acc) -> bool:
     """any |a| exceeding 10 (strict)."""
     return any(abs(x) > 10.0 for x in acc)
+
+
+def state_from_obs(obs, dt):
+    """"the initial position p(0) and speed v(0) for each trajectory were set to
+    0 and (Delta P) / Delta t, where Delta P is the distance between the first two data
+    points".  obs: rows t = 0..K of per-vehicle positions (NaN = not observed).  With lanes the
+    position is the vehicle's own (R#13): p0 = the first data point carried back to step 0 at
+    speed v0 (itself when observed at step 0); v0 clamped at 0 (no backward motion).
+    One data point: v0 = 0; none: (0, 0).  Returns lists (p0, v0)."""
+    n = len(obs[0])
+    p0, v0 = [], []
+    for i in range(n):
+        pts = [(t, float(row[i])) for t, row in enumerate(obs) if math.isfinite(float(row[i]))]
+        if not pts:
+            p0.append(0.0)
+            v0.append(0.0)
+            continue
+        (t1, P1) = pts[0]
+        v = 0.0
+        if len(pts) > 1:
+            (t2, P2) = pts[1]
+            v = max(0.0, (P2 - P1) / ((t2 - t1) * dt))
+        p0.append(P1 - t1 * dt * v)
+        v0.append(v)
+    return p0, v0

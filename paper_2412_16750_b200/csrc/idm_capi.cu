@@ -369,6 +369,17 @@ size_t idm_workspace_bytes(const idm_desc* d) {
 
 int32_t idm_max_lane_vehicles(void) { return kCap; }
 
+int idm_state_from_obs(const float* obs, int64_t n_vehicles, int32_t steps, float dt,
+                       float* pos0, float* vel0, void* stream) {
+    if (!obs || !pos0 || !vel0 || n_vehicles < 1 || steps < 0 || !(dt > 0.f) ||
+        !std::isfinite(dt))
+        return IDM_EINVAL;
+    if (launch_state_from_obs(obs, n_vehicles, steps, dt, pos0, vel0, (cudaStream_t)stream) !=
+        cudaSuccess)
+        return IDM_ECUDA;
+    return IDM_OK;
+}
+
 const char* idm_last_error(const idm_handle* h) { return h ? h->err : kNoHandle; }
 
 int64_t idm_launch_count(const idm_handle* h) { return h ? h->launches : 0; }

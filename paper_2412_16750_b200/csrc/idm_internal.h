@@ -199,6 +199,8 @@ cudaError_t launch_adam_free(float* x, const float* g, float* m, float* v, int64
                              const AdamArgs& hp, cudaStream_t st);
 int64_t vl_blocks(int64_t n);
 cudaError_t launch_fit(const FitArgs& a, int ntiles, bool delta4, int kind, cudaStream_t st);
+cudaError_t launch_state_from_obs(const float* obs, int64_t n, int steps, float dt, float* pos0,
+                                  float* vel0, cudaStream_t st);
 
 // Adam (Kingma & Ba, bias-corrected) + box clamp of one scalar;
 // shared by adam_kernel and the fused backward epilogue so both paths agree bitwise.

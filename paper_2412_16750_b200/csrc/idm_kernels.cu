@@ -938,7 +938,49 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamArgs a) {
     }
 }
 
+// ------------------------------------------------------------------------------ NK6
+// Initial state of a fit from its observations ("p(0) and v(0) ... set to 0 and
+// (Delta P) / Delta t, where Delta P is the distance between the first two data points"; R#13):
+// per vehicle the first two observed rows t1 < t2 of the step-major [(steps+1)][N] array (NaN
+// = missing) give v0 = max(0, (P_t2 - P_t1) / ((t2 - t1) dt)) and p0 = P_t1 - t1 dt v0 (the
+// first data point carried back to step 0 at that speed; = P_t1 when t1 = 0).  One observation:
+// v0 = 0, p0 = P_t1; none: 0, 0.  Coalesced: thread i reads column i row by row.
+__global__ void state_from_obs_kernel(const float* __restrict__ obs, int64_t n, int steps,
+                                      float dt, float* __restrict__ pos0,
+                                      float* __restrict__ vel0) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int t1 = -1, t2 = -1;
+        float o1 = 0.f, o2 = 0.f;
+        for (int t = 0; t <= steps; ++t) {
+            const float o = __ldcs(obs + (int64_t)t * n + i);
+            if (!isfinite(o)) continue;
+            if (t1 < 0) {
+                t1 = t;
+                o1 = o;
+            } else {
+                t2 = t;
+                o2 = o;
+                break;
+            }
+        }
+        float v = 0.f, p = 0.f;
+        if (t2 >= 0) v = fmaxf(0.f, __fdiv_rn(__fsub_rn(o2, o1), __fmul_rn((float)(t2 - t1), dt)));
+        if (t1 >= 0) p = __fsub_rn(o1, __fmul_rn(__fmul_rn((float)t1, dt), v));
+        pos0[i] = p;
+        vel0[i] = v;
+    }
+}
+
 // ------------------------------------------------------------------------------ launchers
+cudaError_t launch_state_from_obs(const float* obs, int64_t n, int steps, float dt, float* pos0,
+                                  float* vel0, cudaStream_t st) {
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    state_from_obs_kernel<<<(int)blocks, 256, 0, st>>>(obs, n, steps, dt, pos0, vel0);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_validate(const ValidateArgs& a, cudaStream_t st) {
     validate_kernel<<<148 * 4, 256, 0, st>>>(a);
     return cudaGetLastError();

@@ -107,6 +107,8 @@ def load_library(path: str | None = None):
     L.idm_forward.argtypes = [vp, i32]
     L.idm_forward_ex.restype = C.c_int
     L.idm_forward_ex.argtypes = [vp, i32, C.c_uint32]
+    L.idm_state_from_obs.restype = C.c_int
+    L.idm_state_from_obs.argtypes = [vp, i64, i32, C.c_float, vp, vp, vp]
     L.idm_reduce_shared.restype = C.c_int
     L.idm_reduce_shared.argtypes = [vp, vp, i64]
     L.idm_loss_grad.restype = C.c_int
@@ -471,6 +473,25 @@ def idm_adam_step(sim: IdmSim, iteration: int, total: int = 500, lr0=0.1, lr1=0.
 def idm_fit_step(sim: IdmSim, obs, kind="l1", iteration=0, total=500, lr0=0.1, lr1=0.01,
                  sync=False):
     return sim.fit_step(obs, kind, iteration, total, lr0, lr1, sync=sync)
+
+
+def idm_state_from_obs(obs: torch.Tensor, dt: float = 0.1, steps: int | None = None,
+                       stream: torch.cuda.Stream | None = None):
+    """(pos0, vel0) device tensors [N] from step-major observations [(K+1), N] (NaN = missing):
+    the paper's initialisation from the first two data points (include/idm.h)."""
+    assert obs.dtype == torch.float32 and obs.is_contiguous() and obs.is_cuda and obs.dim() == 2
+    L = load_library()
+    steps = obs.shape[0] - 1 if steps is None else int(steps)
+    n = obs.shape[1]
+    pos0 = torch.empty(n, dtype=torch.float32, device=obs.device)
+    vel0 = torch.empty(n, dtype=torch.float32, device=obs.device)
+    st = stream or torch.cuda.current_stream(obs.device)
+    with torch.cuda.device(obs.device):
+        rc = L.idm_state_from_obs(_ptr(obs), n, steps, float(dt), _ptr(pos0), _ptr(vel0),
+                                  C.c_void_p(st.cuda_stream))
+    if rc != IDM_OK:
+        raise IdmError(rc, "idm_state_from_obs failed")
+    return pos0, vel0
 
 
 def idm_plan_tiles(lane_offsets) -> "np.ndarray":

@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--iters", type=int, default=1)
     ap.add_argument("--leader", choices=["lane", "virtual"], default="lane")
+    ap.add_argument("--fwd-only", action="store_true",
+                    help="the prediction rollout idm_forward_ex(IDM_FWD_NO_HISTORY) instead")
     args = ap.parse_args()
     w = synth.make_workload(args.config, seed=synth.CONFIGS[args.config]["seed"])
     sim = idm.from_workload(w, w.theta_true, max_steps=w.K, ckpt_every=idm.DEFAULT_CKPT)
@@ -39,7 +41,10 @@ def main():
         sim = idm.from_workload(w, None, max_steps=w.K, ckpt_every=4, virtual_leader=True)
     sim.params.copy_(torch.as_tensor(synth.init_params(w.n), device="cuda"))
     for it in range(args.warmup + args.iters):
-        sim.fit_step(obs, kind="l1", iteration=it, total=500)
+        if args.fwd_only:
+            sim.forward(w.K, history=False)
+        else:
+            sim.fit_step(obs, kind="l1", iteration=it, total=500)
     torch.cuda.synchronize()
     print(f"ok: {args.config} {w.n} vehicles x {w.K} steps, {args.warmup + args.iters} fused iterations")
 

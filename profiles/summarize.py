@@ -1,9 +1,13 @@
 """Summarise an ncu report (.ncu-rep) into the metrics DESIGN.md / bench.py cite.
 
     python profiles/summarize.py gpurun_out/prof_bwd.ncu-rep > profiles/rNN_bwd_summary.txt
+    python profiles/summarize.py gpurun_out/prof.ncu-rep --json profiles/ncu_metrics.json \
+        --units 6e8 --tag fused   # + the per-kernel figures bench.py's roofline reads
 """
 import csv
 import io
+import json
+import os
 import subprocess
 import sys
 from collections import Counter
@@ -26,11 +30,47 @@ def ncu(rep, *args):
     return subprocess.run(["ncu", "-i", rep, *args], capture_output=True, text=True).stdout
 
 
-def main(rep):
+def _num(vals, h, u, key):
+    if key not in h:
+        return None
+    i = h.index(key)
+    try:
+        x = float(vals[i].replace(",", ""))
+    except ValueError:
+        return None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u[i], 1)
+    return x * scale
+
+
+def main(rep, json_out=None, units=None, tag=""):
     rows = list(csv.reader(io.StringIO(ncu(rep, "--page", "raw", "--csv"))))
     h, u = rows[0], rows[1]
+    summary = {}
     for vals in rows[2:]:
-        print(f"kernel: {vals[h.index('Kernel Name')]}")
+        kname = vals[h.index('Kernel Name')]
+        print(f"kernel: {kname}")
+        short = kname.split("<")[0].split("(")[0].split("::")[-1]
+        rec = {
+            "kernel": kname, "source": f"{os.path.basename(rep)} ({tag})",
+            "duration_ns": _num(vals, h, u, "gpu__time_duration.sum"),
+            "dram_bytes": (_num(vals, h, u, "dram__bytes_read.sum") or 0) +
+                          (_num(vals, h, u, "dram__bytes_write.sum") or 0),
+            "issue_active_pct": _num(vals, h, u,
+                                     "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "fma_pipe_pct": _num(vals, h, u,
+                                 "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+            "xu_pipe_pct": _num(vals, h, u,
+                                "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
+            "alu_pipe_pct": _num(vals, h, u,
+                                 "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+            "dram_pct": _num(vals, h, u, "dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+            "registers": _num(vals, h, u, "launch__registers_per_thread"),
+            "warp_instr": _num(vals, h, u, "smsp__inst_executed.sum"),
+        }
+        if units and rec["warp_instr"]:
+            rec["warp_instr_per_unit"] = rec["warp_instr"] * 32 / units
+            rec["dram_bytes_per_unit"] = rec["dram_bytes"] / units
+        summary.setdefault(f"{short}", rec)
         for k in KEYS:
             if k in h:
                 i = h.index(k)
@@ -83,5 +123,20 @@ def main(rep):
         print(f"    {w / tot_s:6.3f} {e:>12d}  {s[:70]}")
 
 
+    if json_out:
+        old = {}
+        if os.path.exists(json_out):
+            with open(json_out) as f:
+                old = json.load(f)
+        for k, v in summary.items():
+            old[f"{tag}_{k}" if tag and tag != "fused" else k] = v
+        with open(json_out, "w") as f:
+            json.dump(old, f, indent=1)
+
+
 if __name__ == "__main__":
-    main(sys.argv[1])
+    a = sys.argv[1:]
+    js = a[a.index("--json") + 1] if "--json" in a else None
+    un = float(a[a.index("--units") + 1]) if "--units" in a else None
+    tg = a[a.index("--tag") + 1] if "--tag" in a else ""
+    main(a[0], js, un, tg)

@@ -56,13 +56,15 @@ def assert_fit_grads(api, fused):
 
 def oracle_grads(oracle, w, params, K, obs, kind, gpu_grad_traj=None):
     """The oracle's rollout, Eq. 4 and adjoint.  For L1 with the GPU's sign pattern given
-    (SURVEY.md 8(c) sign protocol), every sign mismatch must sit within 1e-3 m of the kink."""
+    (SURVEY.md 8(c) sign protocol), every sign mismatch must sit within the position tolerance
+    of the kink (1e-3 m below 10 km)."""
     h = oracle.leader_from_lanes(w.lane_offsets)
     P, V = oracle.rollout(h, w.length, w.p0, w.v0, params, K, w.dt)
     sign = None
     if kind == "l1" and gpu_grad_traj is not None:
         res = sign_mismatch_residual(obs[:K + 1], P, gpu_grad_traj)
-        assert res < 1e-3, f"L1 sign mismatch at residual {res} m"
+        print(f"L1 sign protocol: max residual / position tolerance at mismatches = {res:.3g}")
+        assert res <= 1.0, f"L1 sign mismatch at residual {res} x the position tolerance"
         sign = (-gpu_grad_traj).astype(np.int8)  # GPU sign pattern (dL/dP = -sign)
     L, gP = oracle.loss(P, obs[:K + 1], kind, sign_override=sign)
     g = oracle.backward(h, w.length, params, P, V, gP, w.dt)
@@ -170,10 +172,16 @@ def test_gradients_c3_full_horizon(idm, oracle, kind):
     _, _, _, g = oracle_grads(oracle, w, prm, w.K, obs.astype(np.float64), kind, gt)
     worst, plain = grad_check(sim.grad_params.cpu().numpy(), g["g_params"], g["g_abs"])
     gp = sim.grad_params.cpu().numpy().astype(np.float64)
-    fail = np.abs(gp - g["g_params"]) > 1e-3 * np.abs(g["g_params"]) + 1e-12
-    canc = (np.abs(g["g_params"][fail]) / g["g_abs"][fail]).max() if fail.any() else 0.0
-    print(f"C3 {kind} grad worst/tol = {worst:.3f}, plain pass = {plain:.4f}, max |g|/G_abs "
-          f"among plain failures = {canc:.3g}")
+    print(f"C3 {kind} grad worst/tol = {worst:.3f}, plain pass = {plain:.4f}")
+    for q, name in enumerate(("a_max", "a_pref", "s_min", "T_pref", "v_targ", "delta")):
+        err = np.abs(gp[q] - g["g_params"][q])
+        rel = err / np.maximum(np.abs(g["g_params"][q]), 1e-300)
+        fail = err > 1e-3 * np.abs(g["g_params"][q]) + 1e-12
+        canc = (np.abs(g["g_params"][q][fail]) / g["g_abs"][q][fail]).max() if fail.any() \
+            else float("nan")
+        print(f"  {name}: median rel err {np.median(rel):.2e}, plain pass {1 - fail.mean():.4f},"
+              f" max |g|/G_abs among plain failures {canc:.3g}, max rel err among them "
+              f"{rel[fail].max() if fail.any() else 0:.2e}")
     assert worst <= 1.0
     assert state_grad_check(sim.grad_state0.cpu().numpy(), g, label=f"C3 {kind}") <= 1.0
 
@@ -655,6 +663,7 @@ def test_sparse_reconstruction_lanes(idm, oracle):
     P_o, V_o = oracle.rollout(h, w.length, w.p0, w.v0, prm.astype(np.float64), w.K)
     assert state_violation(Pg, P_o) <= 1.0
     gt = sim.grad_traj.cpu().numpy()
+    assert sign_mismatch_residual(obs, P_o, gt) <= 1.0  # the L1 sign protocol
     g = oracle.backward(h, w.length, prm.astype(np.float64), P_o, V_o, gt.astype(np.float64))
     worst, _ = grad_check(sim.grad_params.cpu().numpy(), g["g_params"], g["g_abs"])
     assert worst <= 1.0
@@ -1169,3 +1178,24 @@ def test_shared_lane_rows(idm, oracle):
     torch.cuda.synchronize()
     assert torch.equal(sim.grad_params, g_first)
     assert np.allclose(sim.grad_params.cpu().numpy()[:, 0], rows.sum(axis=0), rtol=1e-6)
+
+
+def test_state_from_obs_matches_oracle(idm):
+    """idm_state_from_obs (PAPER.md:267 initialisation) against the plain oracle on sparse,
+    irregular NaN-marked observations: first rows at every offset, single observations,
+    unobserved vehicles, decreasing pairs."""
+    from oracle import tasks_oracle as TO
+    rng = np.random.default_rng(3)
+    K, n, dt = 40, 3000, 0.1
+    obs = (rng.uniform(0, 500, n)[None, :] + rng.uniform(-2, 30, n)[None, :] *
+           (np.arange(K + 1)[:, None] * dt)).astype(np.float32)
+    obs[rng.random(obs.shape) < 0.8] = np.nan
+    obs[:, :5] = np.nan                   # never observed
+    obs[:, 5:10] = np.nan
+    obs[7, 5:10] = 12.5                   # observed once
+    p0, v0 = idm.idm_state_from_obs(torch.as_tensor(obs, device="cuda"), dt)
+    torch.cuda.synchronize()
+    po, vo = TO.state_from_obs(obs.astype(np.float64).tolist(), dt)
+    assert state_violation(p0.cpu().numpy(), np.array(po)) <= 1.0
+    assert state_violation(v0.cpu().numpy(), np.array(vo)) <= 1.0
+    assert np.all(v0.cpu().numpy() >= 0) and np.all(p0.cpu().numpy()[:5] == 0)

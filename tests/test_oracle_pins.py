@@ -663,3 +663,20 @@ def test_rollout_converges_to_the_ode_at_first_order(oracle):
     r1, r2 = errs[0] / errs[1], errs[1] / errs[2]
     assert 1.7 < r1 < 2.3 and 1.7 < r2 < 2.3, (errs, r1, r2)
     assert errs[2] < 0.05
+
+
+def test_state_from_obs_worked_values():
+    """PAPER.md:267 initialisation (v(0) = Delta P / Delta t of the first two data points), by
+    hand: vehicle 0 first seen at step 1 (5.0) then step 3 (6.0), dt = 0.5 -> v0 = 1 / 1.0 = 1,
+    p0 = 5 - 0.5 * 1 = 4.5; vehicle 1 at steps 0, 1 -> v0 = 1 / 0.5 = 2, p0 = 0; vehicle 2
+    moving backwards -> v0 clamped to 0 (no backward motion), p0 = its first
+    point; vehicle 3 seen once -> (its point, 0); vehicle 4 never -> (0, 0)."""
+    from oracle import tasks_oracle as TO
+    nan = float("nan")
+    obs = [[nan, 0.0, 7.0, nan, nan],
+           [5.0, 1.0, 6.0, nan, nan],
+           [nan, 2.5, 5.0, 3.0, nan],
+           [6.0, nan, nan, nan, nan]]
+    p0, v0 = TO.state_from_obs(obs, 0.5)
+    assert p0 == [4.5, 0.0, 7.0, 3.0, 0.0]
+    assert v0 == [1.0, 2.0, 0.0, 0.0, 0.0]
