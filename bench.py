@@ -48,6 +48,63 @@ WORKLOAD = "C4"  # the headline configuration (BASELINE.json configs[3]); --conf
 ALG_INSTR = {"fwd": 36.0, "bwd": 114.0}
 PACKED_INSTR = {"fwd": 20.5, "bwd": 44.0, "bwd_fit": 41.0}
 ISSUE_PER_CLK = 148 * 4 * 32  # SMs x schedulers x lanes (thread-instr / clk)
+N_SM = 148
+# Essential operations per vehicle-step by execution pipe (DESIGN.md section 4 "ALU roofline"):
+# the hand count of the step math (core + advance for the forward; core + jac_record +
+# bwd_from_record + the gap rebuild for the backward), equal to the FP32 / MUFU / compare-select
+# instructions in the kernels' SASS loops.  fp32 = FP32 lane operations (an FFMA2 is two);
+# mufu = ex2 / lg2 / rcp; alu = max / select / setp / sign copies.  "bwd_fit": the optimizer-
+# path backward with delta frozen (no dL/d delta, R#1).
+ESSENTIAL = {
+    "fwd": {"fp32": 22.0, "mufu": 5.0, "alu": 5.0},
+    "bwd_fit": {"fp32": 50.0, "mufu": 5.0, "alu": 9.0},
+}
+# Pipe rates per SM per clock, nominal (sm_100: 4 SMSPs x 32 FP32 lanes; XU 16 lanes; ALU 64
+# lanes for FMNMX / FSEL; 4 issue slots x 32 lanes) -- profiles/rNN_pipe_bench.txt holds the
+# measured ones (profiles/pipe_bench.cu), which bench.py uses when present.
+PIPE_NOMINAL = {"fp32": 128.0, "mufu": 16.0, "alu": 64.0, "issue": 128.0}
+
+
+def pipe_rates():
+    """Per-SM-per-clock lane-op rates measured by profiles/pipe_bench.cu on this B200."""
+    path = os.path.join(ROOT, "profiles", "r02_pipe_bench.txt")
+    rates, src = dict(PIPE_NOMINAL), "nominal"
+    try:
+        txt = open(path).read()
+
+        def lane(name):
+            for line in txt.splitlines():
+                if line.startswith(name):
+                    return float(line.split("warp-instr/clk/SM")[1].split()[0])
+            return None
+        r = {"fp32": lane("FFMA2 (packed f32x2)"), "mufu": lane("MUFU.EX2"),
+             "alu": lane("FMNMX"), "issue": lane("FFMA (scalar)")}
+        if all(v for v in r.values()):
+            rates, src = r, "measured (profiles/r02_pipe_bench.txt)"
+    except Exception:
+        pass
+    return rates, src
+
+
+def alu_roofline(kind: str, units: float, seconds: float, clk_mhz: float) -> dict:
+    """Pipe-by-pipe ceiling of a kernel from its essential op counts: the binding pipe is the
+    one needing the most cycles per vehicle-step; achieved / peak are in that pipe's lane-ops."""
+    ess = ESSENTIAL[kind]
+    rates, src = pipe_rates()
+    ops = dict(ess)
+    ops["issue"] = ess["fp32"] / 2 + ess["mufu"] + ess["alu"]  # packed FP32: 2 per slot
+    cyc = {p: ops[p] / rates[p] for p in ops}  # SM cycles per vehicle-step per pipe
+    bind = max(cyc, key=cyc.get)
+    hz = N_SM * clk_mhz * 1e6
+    peak_vs = hz / cyc[bind]
+    achieved_vs = units / seconds
+    return {"binding_pipe": bind, "ops_per_vehicle_step": ops,
+            "pipe_frac": {p: achieved_vs * cyc[p] / hz for p in cyc},
+            "achieved": ops[bind] * achieved_vs / 1e12, "peak": rates[bind] * hz / 1e12,
+            "frac": achieved_vs / peak_vs, "peak_vehicle_steps_per_s": peak_vs,
+            "rates_per_sm_clk": rates, "rates_source": src}
+
+
 # SURVEY.md 8(d) algorithmic HBM bytes per vehicle-step of the method's variants (k = 32 there):
 # forward with the trajectory record 4.5; fwd+bwd through the API 21.0; with the loss inside the
 # kernels (obs read twice) 9.0 -- the variant the fused idm_fit_step implements; single launch 4.2
@@ -546,26 +603,37 @@ def run_ours(args, rank, world, local_rank):
         issue_peak = ISSUE_PER_CLK * sm_mhz_max * 1e6 / 1e12  # Tinstr/s
         kk = "bwd" if dom == "bwd" else "fwd"
         kp = "bwd_fit" if kk == "bwd" else kk  # the headline path is idm_fit_step, delta frozen
-        # essential issue slots of THIS (f32x2-packed) implementation: SURVEY 8(d) addendum
-        achieved = PACKED_INSTR[kp] * n_veh_steps / (kms[dom] * 1e-3) / 1e12
-        frozen = ALG_INSTR[kk] * n_veh_steps / (kms[dom] * 1e-3) / 1e12
+        t_dom = kms[dom] * 1e-3
+        alu = alu_roofline(kp, n_veh_steps, t_dom, sm_mhz_max)
+        frozen = ALG_INSTR[kk] * n_veh_steps / t_dom / 1e12
+        packed = PACKED_INSTR[kp] * n_veh_steps / t_dom / 1e12
         nm = ncu.get(f"{dom}_kernel", {})
-        roofline = {"bound": "alu", "kernel": f"{dom}_kernel (fused path)", "achieved": achieved,
-                    "peak": issue_peak, "unit": "Tinstr/s", "frac": achieved / issue_peak,
+        roofline = {"bound": "alu", "kernel": f"{dom}_kernel (fused path)",
+                    "achieved": alu["achieved"], "peak": alu["peak"],
+                    "unit": f"T {alu['binding_pipe']} lane-ops/s", "frac": alu["frac"],
                     "traffic": nm.get("dram_bytes"),
+                    "binding_pipe": alu["binding_pipe"], "pipe_frac": alu["pipe_frac"],
+                    "ops_per_vehicle_step": alu["ops_per_vehicle_step"],
+                    "rates_per_sm_clk": alu["rates_per_sm_clk"],
+                    "rates_source": alu["rates_source"],
+                    "frac_issue_packed": packed / issue_peak,
                     "frac_survey": frozen / issue_peak,
                     "ncu": {key: nm.get(key) for key in (
                         "issue_active_pct", "fma_pipe_pct", "xu_pipe_pct", "alu_pipe_pct",
-                        "warp_instr_per_unit", "registers", "source")} if nm else None,
-                    "basis": f"{PACKED_INSTR[kp]} essential issue slots per vehicle-step (packed "
-                             f"f32x2 implementation; SURVEY 8(d) addendum) x {n_veh_steps:.3g} "
-                             f"vehicle-steps per launch / CUDA-event launch time; peak = 148 SM "
-                             f"x 4 issue/clk x 32 lanes x {sm_mhz_max:.0f} MHz (MEASURED_PEAKS "
-                             f"sm_max, {peak_src}; issue and pipe rates measured by "
-                             f"profiles/pipe_bench.cu); frac_survey uses SURVEY 8(d)'s frozen "
-                             f"scalar count {ALG_INSTR[kk]:.0f}, which a packed kernel can exceed; "
-                             f"ncu = the kernel's pipe utilisation (profiles/ncu_metrics.json); "
-                             f"traffic = its ncu dram bytes per launch"}
+                        "warp_instr_per_unit", "dram_bytes_per_unit", "registers", "source")}
+                    if nm else None,
+                    "basis": f"essential ops per vehicle-step by pipe (DESIGN.md section 4: "
+                             f"{alu['ops_per_vehicle_step']}) x {n_veh_steps:.3g} vehicle-steps "
+                             f"per launch / CUDA-event launch time; peak = the binding pipe's "
+                             f"lane-op rate per SM per clock ({alu['rates_source']}) x 148 SMs x "
+                             f"{sm_mhz_max:.0f} MHz (MEASURED_PEAKS sm_max, {peak_src}); "
+                             f"frac_issue_packed: {PACKED_INSTR[kp]} packed issue slots per "
+                             f"vehicle-step against 4 issue/clk/SM (round 1's figure); "
+                             f"frac_survey: SURVEY 8(d)'s frozen scalar count "
+                             f"{ALG_INSTR[kk]:.0f} against the issue peak (a packed kernel can "
+                             f"exceed 1); ncu = the kernel's measured pipe utilisation "
+                             f"(profiles/ncu_metrics.json); traffic = its ncu dram bytes per "
+                             f"launch"}
 
     def hbm_of(p, path, survey_key=None):
         ab = alg_bytes(K, k, path)
@@ -591,6 +659,8 @@ def run_ours(args, rank, world, local_rank):
                     "what": "idm_forward_ex(IDM_FWD_NO_HISTORY): the K-step rollout writing P "
                             "(the prediction path)",
                     "hbm": hbm_of(fwd_only, "fwd_only", "fwd"),
+                    "roofline": alu_roofline("fwd", n_veh_steps, fwd_only["ms_per_step"] * 1e-3,
+                                             sm_mhz_max),
                     "with_history": {"value": vsteps / (api["kernel_ms"]["fwd"] * 1e-3),
                                      "ms": api["kernel_ms"]["fwd"],
                                      "what": "idm_forward (P + the state history a backward "

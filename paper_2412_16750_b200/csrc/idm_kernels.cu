@@ -91,16 +91,17 @@ __device__ __forceinline__ RawP dummy_raw() { return RawP{1.f, 1.f, 1.f, 1.f, 1.
 constexpr int kVpt = 2;          // vehicles per thread (one float2 lane pair)
 constexpr int kT = kCap / kVpt;   // 256 threads per CTA
 
-// fixed-order CTA reduction of one double per thread -> *out (deterministic)
+// fixed-order CTA reduction of one double per thread (NT threads) -> *out (deterministic)
+template <int NT = kT>
 __device__ __forceinline__ void block_sum_to(double x, double* out) {
-    __shared__ double red[kT / 32];
+    __shared__ double red[NT / 32];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
     __syncthreads();
     if (threadIdx.x == 0) {
         double y = 0.0;
-        for (int w = 0; w < kT / 32; ++w) y += red[w];
+        for (int w = 0; w < NT / 32; ++w) y += red[w];
         *out = y;
     }
 }
@@ -200,35 +201,63 @@ __device__ __forceinline__ void cp_async_wait() {
 }  // namespace
 
 // ------------------------------------------------------------------------------ NK1
-// One CTA = one lane tile; thread t owns the adjacent local vehicles 2t, 2t + 1 as one float2
-// lane pair (packed f32x2 arithmetic).  Vehicle 2t's leader is 2t + 1 (same thread); vehicle
-// 2t + 1's leader is 2t + 2, thread t + 1's first vehicle, so one speed per thread crosses shared
-// memory per step (one __syncthreads, double-buffered).  A lane head carries the gap +inf, which
-// zeroes its interaction term whatever "leader" speed it reads.
+// One CTA = one lane tile; thread t owns VT = 2 NP adjacent local vehicles VT t .. VT t + VT - 1
+// as NP float2 lane pairs (packed f32x2 arithmetic; NP = 2 by default: 128 threads per tile).
+// Inside the thread a pair's second vehicle leads... its leader is the next pair's first vehicle;
+// the thread's last vehicle's leader is thread t + 1's first vehicle, so one speed per thread
+// crosses shared memory per step (one __syncthreads, double-buffered).  A lane head carries the
+// gap +inf, which zeroes its interaction term whatever "leader" speed it reads.  Per vehicle the
+// arithmetic does not depend on NP (same bits).
 // All `steps` steps run in one launch, in segments of KS steps (compile-time, fully unrolled;
 // the K mod KS tail runs as one predicated segment).  LOSS = 0: record P (idm_forward).
 // LOSS = 1 (L1) / 2 (L2): fused Eq. 4 for idm_fit_step -- observation rows staged two segments
 // ahead (cp.async ring); each step sums Eq. 4 against the fresh positions and, for L1, records
-// dL/dP = -sign(obs - P) as a 4-bit code per thread-step; P and dL/dP are not written.
+// dL/dP = -sign(obs - P) as a 4-bit code per pair-step; P and dL/dP are not written.
 // LOSS = 3: fused iteration whose backward derives Eq. 4 from obs (L2 by default): only the
 // tile history -- speeds, and gap + displacement checkpoints.
 // CK = checkpoint interval (the backward's segment length); the forward's own prefetch
 // segment is KS = max(4, CK) steps, so CK | KS and checkpoints fall at static positions.
 #ifndef IDM_FWD_LOSS_MINB
-#define IDM_FWD_LOSS_MINB 4  // CTAs per SM the fused (LOSS) forward is register-budgeted for
+#define IDM_FWD_LOSS_MINB 4  // CTAs per SM the NP = 1 fused (LOSS) forward is budgeted for
 #endif
+#ifndef IDM_FWD_MINB2
+#define IDM_FWD_MINB2 4  // CTAs (of 128 threads) per SM the NP = 2 forward is budgeted for
+#endif
+// Vehicle pairs per forward thread (1: 256 threads, 2: 128 threads).  Measured at C4
+// (DESIGN.md section 4): NP = 2 runs the fused forward in 1.062 against 1.102 ms and the
+// prediction rollout in 0.797 against 0.820 ms, but the idm_forward that records P and the
+// history in 0.904 against 0.891 ms, so that one keeps NP = 1.
+#ifndef IDM_FWD_NP
+#define IDM_FWD_NP 2
+#endif
+#ifndef IDM_FWD_NP_API
+#define IDM_FWD_NP_API 1
+#endif
+template <int CK, int LOSS, int NP>
+constexpr int fwd_min_blocks() {
+    return NP == 1 ? (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 4)) : (CK > 4 ? 3 : IDM_FWD_MINB2);
+}
+// store NP float2 of one thread (adjacent) as one access: 8 bytes (NP = 1) or 16 (NP = 2)
+template <int NP>
+__device__ __forceinline__ void st_pairs(float2* p, const float2 (&x)[NP]) {
+    if constexpr (NP == 2) __stcs(reinterpret_cast<float4*>(p), make_float4(x[0].x, x[0].y, x[1].x, x[1].y));
+    else __stcs(p, x[0]);
+}
 // HIST = false (LOSS = 0 only): a prediction rollout (idm_forward_ex IDM_FWD_NO_HISTORY) that
 // writes only the P rows -- no speed history or checkpoints, nothing for a backward.
-template <bool D4, bool KAHAN, bool RECV, int LOSS, int CK, bool HIST = true>
-__global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 4)))
+template <bool D4, bool KAHAN, bool RECV, int LOSS, int CK, bool HIST = true,
+          int NP = (LOSS == 0 && HIST ? IDM_FWD_NP_API : IDM_FWD_NP)>
+__global__ void __launch_bounds__(kCap / (2 * NP), (fwd_min_blocks<CK, LOSS, NP>()))
     fwd_kernel(FwdArgs a) {
     static_assert(HIST || LOSS == 0, "the fused forward always feeds a backward");
+    constexpr int VT = 2 * NP;        // vehicles per thread
+    constexpr int kTf = kCap / VT;    // threads per CTA
     constexpr int KS = CK > 4 ? CK : 4;
     // LOSS = 3: the fused iteration whose backward derives Eq. 4 itself (from obs and the
     // rebuilt positions): only the tile history (speeds; gap + displacement checkpoints)
     constexpr bool OBSV = LOSS == 1 || LOSS == 2;  // reads the observations here
     constexpr bool DCK = LOSS == 2 || LOSS == 3;   // displacement checkpoints for the backward
-    __shared__ float xv[2][kT + 1];  // speed of each thread's first vehicle; [kT] = 0 sentinel
+    __shared__ float xv[2][kTf + 1];  // speed of each thread's first vehicle; [kTf] = 0 sentinel
     const int tid = threadIdx.x;
     const int tile = a.tile0 + (int)blockIdx.x;  // launches may cover a chunk of the tiles
     const int64_t base = a.tile_start[tile];
@@ -237,22 +266,26 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     const int64_t N = a.n;
     const int steps = a.steps;
     const int nfull = steps / KS, tail = steps - nfull * KS;
-    const int id0 = 2 * tid;
+    const int id0 = VT * tid;
     const int64_t i0 = base + id0;
-    const bool val[2] = {id0 < n_loc, id0 + 1 < n_loc};
+    bool val[VT];
+#pragma unroll
+    for (int j = 0; j < VT; ++j) val[j] = id0 + j < n_loc;
     if (LOSS && a.tile_ready) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
-
-    auto put = [&](float* row, float2 x) {  // row points at local vehicle 2 tid
-        st_cs_if(row, val[0], x.x);
-        st_cs_if(row + 1, val[1], x.y);
+    auto put = [&](float* row, const float2 (&x)[NP]) {  // row points at local vehicle VT tid
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            st_cs_if(row + 2 * p, val[2 * p], x[p].x);
+            st_cs_if(row + 2 * p + 1, val[2 * p + 1], x[p].y);
+        }
     };
     // out: P row of the current step (LOSS = 0; the fused variant only sums Eq. 4)
     float* orow = LOSS ? nullptr : a.traj + i0;
     float* vrow = RECV ? a.vel_traj + i0 : nullptr;
     // tile-local state history: speed row of every step, (gap, D, compensation) every CK steps
-    float2* vtp = reinterpret_cast<float2*>(a.vt + tile * a.vt_stride) + tid;
-    float2* ckp = reinterpret_cast<float2*>(a.ckt + tile * a.ck_stride) + tid;
+    float2* vtp = reinterpret_cast<float2*>(a.vt + tile * a.vt_stride) + NP * tid;
+    float2* ckp = reinterpret_cast<float2*>(a.ckt + tile * a.ck_stride) + NP * tid;
     constexpr int kR2 = kCap / 2;  // one row in float2 units
     const float* obs = OBSV ? a.obs + i0 : nullptr;
     const float qnan = __int_as_float(0x7fc00000);
@@ -265,11 +298,10 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
 #endif
     constexpr int OR = IDM_FWD_RING;
     __shared__ __align__(16) float obuf[OBSV ? OR : 1][OBSV ? KS : 1][kCap];
-    float2 lseg = f2(0.f);  // loss of this thread's vehicles in this segment (fp32)
+    float2 lseg[NP];  // loss of this thread's vehicles in this segment (fp32)
+#pragma unroll
+    for (int p = 0; p < NP; ++p) lseg[p] = f2(0.f);
     double lacc = 0.0;   // and across segments (fp64)
-    auto ld_obs = [&](const float* o, bool on) {  // absent vehicles observe NaN (= missing)
-        return make_float2(ld_cs_if(o, on && val[0], qnan), ld_cs_if(o + 1, on && val[1], qnan));
-    };
     // segment seg observes rows seg*KS + 1 .. seg*KS + KS; fetches run up to two segments ahead of
     // use, slots rotate 0, 1, 2 (fslot: next fetch, cslot: current use)
     const float* onext = OBSV ? obs + N : nullptr;  // first row of the next fetch
@@ -279,21 +311,25 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
     const bool pair8 = OBSV && ((base | N) & 1) == 0 && ((uintptr_t)a.obs & 7) == 0;
     auto fetch_obs = [&](int seg) {
         const int r0 = seg * KS + 1;
-        float* dst = &obuf[fslot][0][2 * tid];
+        float* dst = &obuf[fslot][0][VT * tid];
         fslot = fslot == OR - 1 ? 0 : fslot + 1;
         if (r0 + KS - 1 <= steps) {  // whole segment inside the rollout (CTA-uniform)
             const float* o = onext;
-            if (pair8) {  // both vehicles in one 8-byte copy (the lone last vehicle: 4 bytes)
+            if (pair8) {  // both vehicles of a pair in one 8-byte copy (a lone last one: 4 bytes)
 #pragma unroll
                 for (int tt = 0; tt < KS; ++tt, o += N) {
-                    cp_async8_if(dst + tt * kCap, o, val[1]);
-                    cp_async4_if(dst + tt * kCap, o, val[0] && !val[1]);
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) {
+                        cp_async8_if(dst + tt * kCap + 2 * p, o + 2 * p, val[2 * p + 1]);
+                        cp_async4_if(dst + tt * kCap + 2 * p, o + 2 * p,
+                                     val[2 * p] && !val[2 * p + 1]);
+                    }
                 }
             } else {
 #pragma unroll
                 for (int tt = 0; tt < KS; ++tt, o += N) {
-                    cp_async4_if(dst + tt * kCap, o, val[0]);
-                    cp_async4_if(dst + tt * kCap + 1, o + 1, val[1]);
+#pragma unroll
+                    for (int j = 0; j < VT; ++j) cp_async4_if(dst + tt * kCap + j, o + j, val[j]);
                 }
             }
             onext = o;
@@ -302,122 +338,166 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
             for (int tt = 0; tt < KS; ++tt) {
                 const bool on = r0 + tt <= steps;
                 const float* o = on ? onext + (int64_t)tt * N : obs;
-                cp_async4_if(dst + tt * kCap, o, on && val[0]);
-                cp_async4_if(dst + tt * kCap + 1, o + 1, on && val[1]);
+#pragma unroll
+                for (int j = 0; j < VT; ++j) cp_async4_if(dst + tt * kCap + j, o + j, on && val[j]);
             }
         }
         cp_async_commit();
     };
-    auto obs_at = [&](int tt) {  // this thread's pair of row seg*KS + 1 + tt (current segment)
-        return *reinterpret_cast<const float2*>(&obuf[cslot][tt][2 * tid]);
+    auto obs_at = [&](int tt, int p) {  // pair p of row seg*KS + 1 + tt (current segment)
+        return *reinterpret_cast<const float2*>(&obuf[cslot][tt][VT * tid + 2 * p]);
     };
     if (OBSV) {
         float* ob = &obuf[0][0][0];
 #pragma unroll
         for (int q = 0; q < OR * KS; ++q) {  // own slots only: no barrier needed
-            if (!val[0]) ob[q * kCap + 2 * tid] = qnan;
-            if (!val[1]) ob[q * kCap + 2 * tid + 1] = qnan;
+#pragma unroll
+            for (int j = 0; j < VT; ++j)
+                if (!val[j]) ob[q * kCap + VT * tid + j] = qnan;
         }
 #pragma unroll
         for (int q = 0; q < OR - 1; ++q) fetch_obs(q);
     }
     // per-vehicle state and constants while the first observation rows are in flight
     const float pinf = __int_as_float(0x7f800000);
-    float sj[2], vj[2], pj[2];
-    VehP Pj[2];
+    float2 s[NP], v[NP], p0[NP], D[NP], cmp[NP];
+    VehPT<float2> P[NP];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const int64_t i = i0 + j;
-        RawP r = dummy_raw();
-        sj[j] = pinf; vj[j] = 0.f; pj[j] = 0.f;  // no leader: gap +inf (see core_dv)
-        if (val[j]) {
-            pj[j] = a.pos0[i];
-            vj[j] = a.vel0[i];
-            if (a.lead[i] != 0) sj[j] = (a.pos0[i + 1] - pj[j]) - a.length[i + 1];
-            r = load_raw(a.params, a.n_par, i);
-            if (D4 && r.delta != 4.f)
-                atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
+    for (int p = 0; p < NP; ++p) {
+        float sj[2], vj[2], pj[2];
+        VehP Pj[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = 2 * p + h;
+            const int64_t i = i0 + j;
+            RawP r = dummy_raw();
+            sj[h] = pinf; vj[h] = 0.f; pj[h] = 0.f;  // no leader: gap +inf (see core_dv)
+            if (val[j]) {
+                pj[h] = a.pos0[i];
+                vj[h] = a.vel0[i];
+                if (a.lead[i] != 0) sj[h] = (a.pos0[i + 1] - pj[h]) - a.length[i + 1];
+                r = load_raw(a.params, a.n_par, i);
+                if (D4 && r.delta != 4.f)
+                    atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
+            }
+            Pj[h] = make_vehp(r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta);
         }
-        Pj[j] = make_vehp(r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta);
+        s[p] = make_float2(sj[0], sj[1]);
+        v[p] = make_float2(vj[0], vj[1]);
+        p0[p] = make_float2(pj[0], pj[1]);
+        P[p] = pack(Pj[0], Pj[1]);
+        D[p] = f2(0.f);
+        cmp[p] = f2(0.f);
     }
-    float2 s = make_float2(sj[0], sj[1]), v = make_float2(vj[0], vj[1]);
-    const float2 p0 = make_float2(pj[0], pj[1]);
-    const VehPT<float2> P = pack(Pj[0], Pj[1]);
-    float2 D = f2(0.f), cmp = f2(0.f);
-    if (tid == 0) { xv[0][kT] = 0.f; xv[1][kT] = 0.f; }
+    if (tid == 0) { xv[0][kTf] = 0.f; xv[1][kTf] = 0.f; }
     // checkpoint rows the consumer reads: the gap (idm_backward); + displacement (fused
     // backward rebuilds positions); + compensation (and that with Kahan)
     auto put_ck = [&] {
         if (!HIST) return;
-        __stcs(ckp, s);
-        if (DCK) __stcs(ckp + kR2, D);
-        if (DCK && KAHAN) __stcs(ckp + 2 * kR2, cmp);
+        st_pairs<NP>(ckp, s);
+        if (DCK) st_pairs<NP>(ckp + kR2, D);
+        if (DCK && KAHAN) st_pairs<NP>(ckp + 2 * kR2, cmp);
     };
-    // fused L1: dL/dP = -sign(obs - P) of the thread's two vehicles as a 4-bit code per step
-    // (bits 0 / 2: r != 0, bits 1 / 3: r < 0), collected in a register and stored as one u16
-    // word per 4 steps (steps 4j .. 4j + 3 -> word j; 64 B per warp)
+    // fused L1: dL/dP = -sign(obs - P) of a pair as a 4-bit code per step (bits 0 / 2: r != 0,
+    // bits 1 / 3: r < 0) at bit 16 p + 4 (t mod 4), collected in a register and stored as one
+    // word per 4 steps (steps 4j .. 4j + 3 -> word j): u16 per pair, so a row holds the pairs'
+    // codes in vehicle order whatever NP (NP = 2 stores the thread's two as one u32)
     static_assert(LOSS != 1 || KS % kSgnSteps == 0, "code words align with segments");
     unsigned short* sgp =
-        LOSS == 1 ? reinterpret_cast<unsigned short*>(a.sgn + tile * a.sg_stride) + tid : nullptr;
+        LOSS == 1 ? reinterpret_cast<unsigned short*>(a.sgn + tile * a.sg_stride) + NP * tid
+                  : nullptr;
     unsigned code = 0;
+    auto put_code = [&] {
+        if constexpr (NP == 2) __stcs(reinterpret_cast<unsigned*>(sgp), code);
+        else __stcs(sgp, (unsigned short)code);
+    };
     // Eq. 4 term of the fused forward at a step t with t mod 4 = ph (compile-time): L2 sums r^2;
     // L1 sums |r| and records -sign(r) of the masked residual r (0 where unobserved), i.e.
     // exactly loss_term<0>'s dL/dP
-    auto loss_step = [&](float2 o, float2 Pv, auto PH) {
+    auto loss_step = [&](const float2 (&o)[NP], const float2 (&Pv)[NP], auto PH) {
         constexpr int ph = decltype(PH)::value;
-        if (LOSS == 2) {
-            (void)loss_term<1>(o, Pv, lseg);
-            return;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            if (LOSS == 2) {
+                (void)loss_term<1>(o[p], Pv[p], lseg[p]);
+                continue;
+            }
+            const float2 rm = vsel(vge(vnabs(o[p]), -3.4e38f), vsub(o[p], Pv[p]), f2(0.f));
+            lseg[p] = vadd(lseg[p], vabs(rm));
+            const unsigned nib = (rm.x != 0.f ? 1u : 0u) | (rm.x < 0.f ? 2u : 0u) |
+                                 (rm.y != 0.f ? 4u : 0u) | (rm.y < 0.f ? 8u : 0u);
+            code |= nib << (16 * p + 4 * ph);
         }
-        const float2 rm = vsel(vge(vnabs(o), -3.4e38f), vsub(o, Pv), f2(0.f));
-        lseg = vadd(lseg, vabs(rm));
-        const unsigned nib = (rm.x != 0.f ? 1u : 0u) | (rm.x < 0.f ? 2u : 0u) |
-                             (rm.y != 0.f ? 4u : 0u) | (rm.y < 0.f ? 8u : 0u);
-        code |= nib << (4 * ph);
-        if (ph == kSgnSteps - 1) {
-            __stcs(sgp, (unsigned short)code);
-            sgp += kT;
+        if (LOSS == 1 && ph == kSgnSteps - 1) {
+            put_code();
+            sgp += kCap / 2;
             code = 0;
         }
     };
-    if (OBSV) loss_step(ld_obs(obs, true), p0, std::integral_constant<int, 0>{});
-    else if (!LOSS) put(orow, p0);
+    if (OBSV) {
+        float2 o0[NP];
+#pragma unroll
+        for (int p = 0; p < NP; ++p)
+            o0[p] = make_float2(ld_cs_if(obs + 2 * p, val[2 * p], qnan),
+                                ld_cs_if(obs + 2 * p + 1, val[2 * p + 1], qnan));
+        loss_step(o0, p0, std::integral_constant<int, 0>{});
+    } else if (!LOSS) {
+        put(orow, p0);
+    }
     if (RECV) put(vrow, v);
-    if (HIST) __stcs(vtp, v);
+    if (HIST) st_pairs<NP>(vtp, v);
     put_ck();
     int par = 0;
     // one synchronous step of the whole tile; o = this step's observations (LOSS)
-    auto step = [&](float2 o, auto PH) {  // PH: (index of the step computed) mod 4
-        xv[par][tid] = v.x;
+    auto step = [&](int tt, auto PH) {  // PH: (index of the step computed) mod 4
+        xv[par][tid] = v[0].x;
         __syncthreads();
-        const float2 vl = make_float2(v.y, xv[par][tid + 1]);
+        float2 vl[NP];
+#pragma unroll
+        for (int p = 0; p < NP; ++p)
+            vl[p] = make_float2(v[p].y, p + 1 < NP ? v[p + 1 < NP ? p + 1 : p].x : xv[par][tid + 1]);
         par ^= 1;
-        if (KAHAN) {  // compensated displacement for long horizons (C3)
-            const float2 y = vfma(v, k.dt, vneg(cmp));
-            const float2 t2 = vadd(D, y);
-            cmp = vsub(vsub(t2, D), y);
-            D = t2;
-        } else {
-            D = vfma(v, k.dt, D);
+        float2 Pv[NP];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            if (KAHAN) {  // compensated displacement for long horizons (C3)
+                const float2 y = vfma(v[p], k.dt, vneg(cmp[p]));
+                const float2 t2 = vadd(D[p], y);
+                cmp[p] = vsub(vsub(t2, D[p]), y);
+                D[p] = t2;
+            } else {
+                D[p] = vfma(v[p], k.dt, D[p]);
+            }
+            fwd_step<D4>(s[p], v[p], vl[p], P[p], k);
+            Pv[p] = vadd(p0[p], D[p]);
         }
-        fwd_step<D4>(s, v, vl, P, k);
         if (!LOSS) orow += N;
         if (RECV) vrow += N;
         vtp += kR2;
-        const float2 Pv = vadd(p0, D);
-        if (OBSV) loss_step(o, Pv, PH);
-        else if (!LOSS) put(orow, Pv);
-        if (HIST) __stcs(vtp, v);
+        if (OBSV) {
+            float2 o[NP];
+#pragma unroll
+            for (int p = 0; p < NP; ++p) o[p] = obs_at(tt, p);
+            loss_step(o, Pv, PH);
+        } else if (!LOSS) {
+            put(orow, Pv);
+        }
+        if (HIST) st_pairs<NP>(vtp, v);
         if (RECV) put(vrow, v);
     };
     // first checkpoint step at which each vehicle's state was non-finite (INT_MAX: none); kept
     // in registers and reported once at the end, no branch or atomic per checkpoint
-    int bad0 = INT_MAX, bad1 = INT_MAX;
+    int bad[VT];
+#pragma unroll
+    for (int j = 0; j < VT; ++j) bad[j] = INT_MAX;
     auto finite2 = [&](int t0) {  // gap: +inf is the no-leader value, only NaN is an error
-        const bool ok0 = !isnan(s.x) && isfinite(v.x) && isfinite(D.x);
-        const bool ok1 = !isnan(s.y) && isfinite(v.y) && isfinite(D.y);
-        bad0 = (!ok0 && bad0 == INT_MAX) ? t0 : bad0;
-        bad1 = (!ok1 && bad1 == INT_MAX) ? t0 : bad1;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const bool ok0 = !isnan(s[p].x) && isfinite(v[p].x) && isfinite(D[p].x);
+            const bool ok1 = !isnan(s[p].y) && isfinite(v[p].y) && isfinite(D[p].y);
+            bad[2 * p] = (!ok0 && bad[2 * p] == INT_MAX) ? t0 : bad[2 * p];
+            bad[2 * p + 1] = (!ok1 && bad[2 * p + 1] == INT_MAX) ? t0 : bad[2 * p + 1];
+        }
     };
     auto checkpoint = [&](int t0) {  // (gap, D, compensation) at step t0 > 0 + finiteness check
         if (HIST) ckp += kCkRows * kR2;
@@ -430,19 +510,23 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
         }
     };
     auto obs_done = [&] { cslot = cslot == OR - 1 ? 0 : cslot + 1; };
+    auto fold_loss = [&] {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            lacc += (double)lseg[p].x + (double)lseg[p].y;
+            lseg[p] = f2(0.f);
+        }
+    };
     for (int seg = 0; seg < nfull; ++seg) {
         const int t0 = seg * KS;
         obs_ready(seg);
         static_for<KS>([&](auto TT) {
             constexpr int tt = decltype(TT)::value;
             if (tt % CK == 0 && (tt > 0 || seg > 0)) checkpoint(t0 + tt);
-            step(OBSV ? obs_at(tt) : f2(0.f), std::integral_constant<int, (tt + 1) % 4>{});
+            step(tt, std::integral_constant<int, (tt + 1) % 4>{});
         });
         obs_done();
-        if (OBSV) {
-            lacc += (double)lseg.x + (double)lseg.y;
-            lseg = f2(0.f);
-        }
+        if (OBSV) fold_loss();
         // refill after the segment's steps (its reads of the refilled slot are long done)
         if (OBSV) fetch_obs(seg + OR - 1);
     }
@@ -452,21 +536,28 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
             constexpr int tt = decltype(TT)::value;
             if (tt < tail) {  // CTA-uniform predicate
                 if (tt % CK == 0 && (tt > 0 || nfull > 0)) checkpoint(nfull * KS + tt);
-                step(OBSV ? obs_at(tt) : f2(0.f), std::integral_constant<int, (tt + 1) % 4>{});
+                step(tt, std::integral_constant<int, (tt + 1) % 4>{});
             }
         });
     }
     if (OBSV) cp_async_wait<0>();  // no copy outlives the CTA
     if (LOSS == 1 && steps % kSgnSteps != kSgnSteps - 1)
-        __stcs(sgp, (unsigned short)code);  // the last, partial code word (holds step K)
+        put_code();  // the last, partial code word (holds step K)
     finite2(steps);
-    if (val[0] && bad0 != INT_MAX) report_nonfinite(a.status, bad0, i0);
-    if (val[1] && bad1 != INT_MAX) report_nonfinite(a.status, bad1, i0 + 1);
+#pragma unroll
+    for (int j = 0; j < VT; ++j)
+        if (val[j] && bad[j] != INT_MAX) report_nonfinite(a.status, bad[j], i0 + j);
     if (a.state_out) {
-        put(a.state_out + i0, vadd(p0, D));
+        float2 pe[NP];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) pe[p] = vadd(p0[p], D[p]);
+        put(a.state_out + i0, pe);
         put(a.state_out + N + i0, v);
     }
-    if (OBSV) block_sum_to(lacc + (double)lseg.x + (double)lseg.y, a.loss_partials + tile);
+    if (OBSV) {
+        fold_loss();
+        block_sum_to<kTf>(lacc, a.loss_partials + tile);
+    }
     if (OBSV && a.loss_out) {  // the step's Eq. 4 loss, summed by the last CTA to finish
         bool mine = false;
         if (tid == 0) {
@@ -475,13 +566,19 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
         }
         if (__syncthreads_or(mine)) {
             __threadfence();
+            // reduce_kernel's order: 256 strided per-thread sums, then a fixed tree (each of
+            // the kTf threads forms VT / 2 of the 256 sums)
+            constexpr int kR = 256;
             double* lred = reinterpret_cast<double*>(&obuf[0][0][0]);  // the ring is idle now
-            double x = 0.0;  // reduce_kernel's order: strided per thread, then a fixed tree
-            for (int r = tid; r < a.n_tiles; r += kT) x += __ldcg(a.loss_partials + r);
-            lred[tid] = x;
+#pragma unroll
+            for (int w = tid; w < kR; w += kTf) {
+                double x = 0.0;
+                for (int r = w; r < a.n_tiles; r += kR) x += __ldcg(a.loss_partials + r);
+                lred[w] = x;
+            }
             __syncthreads();
-            for (int st = kT / 2; st > 0; st >>= 1) {
-                if (tid < st) lred[tid] += lred[tid + st];
+            for (int st = kR / 2; st > 0; st >>= 1) {
+                for (int w = tid; w < st; w += kTf) lred[w] += lred[w + st];
                 __syncthreads();
             }
             if (tid == 0) {
@@ -494,15 +591,19 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
 }
 
 // ------------------------------------------------------------------------------ NK3
-// Per CTA (lane tile, thread t = vehicles 2t, 2t + 1 as in NK1), segments of KS steps from last
-// to first.  The forward stored every vehicle's speed at every step and (gap, displacement,
+// Per CTA (lane tile), segments of KS steps from last to first.  Thread t owns VT = 2 NP
+// adjacent vehicles VT t .. VT t + VT - 1 as NP float2 lane pairs (packed f32x2 arithmetic;
+// NP = 2 by default: 128 threads per 512-vehicle tile, so the per-step exchange, barrier and
+// bookkeeping are paid once per 4 vehicles and every warp carries two independent adjoint
+// chains).  The forward stored every vehicle's speed at every step and (gap, displacement,
 // compensation) at every KS-th step in the tile-local rows, so nothing here is a long serial
 // chain: inside a segment the gaps and displacements follow from the checkpoint by the
 // forward's own one-FMA recurrences (bit-identical), every step's local Jacobian (core +
 // jac_record) depends only on stored state, and the one sequential dependency left is the
-// adjoint itself -- lambda^{t+1} -> lambda^t plus the follower -> leader term F of vehicle
-// 2t + 1, passed to thread t + 1 through shared memory (one barrier per step).  The next
-// segment's rows are prefetched into registers while the current one is swept.
+// adjoint itself -- lambda^{t+1} -> lambda^t plus the follower -> leader term F of the
+// thread's last vehicle, passed to thread t + 1 through shared memory (one barrier per step;
+// inside the thread the terms pass in registers).  Per vehicle the arithmetic and its order do
+// not depend on NP, so every NP gives the same bits.
 //   GOBS = 0:      dL/dP rows from grad_traj (idm_backward after idm_loss_grad);
 //   GOBS = 1:      fused idm_fit_step, L1 -- dL/dP = -sign(obs - P) from the forward's sign
 //                  codes (2 bits per vehicle-step);
@@ -511,12 +612,22 @@ __global__ void __launch_bounds__(kT, (CK > 4 ? 2 : (LOSS ? IDM_FWD_LOSS_MINB : 
 //                  with loss_partials set, this tile's Eq. 4 loss as well (LOSS = 3 forward).
 // Gradient accumulators stay in registers for the whole rollout; ADAM: per-vehicle Adam in the
 // epilogue (idm_fit_step).
-template <bool D4, bool SHARED, bool ADAM, int KS, int GOBS, bool KAHAN>
 #ifndef IDM_BWD_MINB
-#define IDM_BWD_MINB 2  // CTAs per SM the backward is register-budgeted for (128 registers)
+#define IDM_BWD_MINB 2  // CTAs per SM the NP = 1 backward is register-budgeted for (128 regs)
 #endif
-__global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(BwdArgs a) {
-    __shared__ float fx[2][kT + 1];
+#ifndef IDM_BWD_MINB2
+#define IDM_BWD_MINB2 3  // CTAs (of 128 threads) per SM the NP = 2 backward is budgeted for
+#endif
+template <int KS, int NP>
+constexpr int bwd_min_blocks() {
+    return NP == 1 ? (KS <= 4 ? IDM_BWD_MINB : 1) : (KS <= 4 ? IDM_BWD_MINB2 : 1);
+}
+template <bool D4, bool SHARED, bool ADAM, int KS, int GOBS, bool KAHAN, int NP>
+__global__ void __launch_bounds__(kCap / (2 * NP), (bwd_min_blocks<KS, NP>()))
+    bwd_kernel(BwdArgs a) {
+    constexpr int VT = 2 * NP;          // vehicles per thread
+    constexpr int kTb = kCap / VT;      // threads per CTA
+    __shared__ float fx[2][kTb + 1];
     const int tid = threadIdx.x;
     const int tile = a.tile0 + (int)blockIdx.x;  // launches may cover a chunk of the tiles
     const int64_t base = a.tile_start[tile];
@@ -524,12 +635,13 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
     const Consts k = a.k;
     const int64_t N = a.n;
     const int steps = a.steps;
-    const int id0 = 2 * tid;
+    const int id0 = VT * tid;
     const int64_t i0 = base + id0;
-    const bool val[2] = {id0 < n_loc, id0 + 1 < n_loc};
+    bool val[VT];
+#pragma unroll
+    for (int j = 0; j < VT; ++j) val[j] = id0 + j < n_loc;
     const int nseg = (steps + KS - 1) / KS;
     const int tail = steps - (nseg - 1) * KS;  // length of the last segment (1..KS)
-
 
     // Segment rows are staged in shared memory, one to two segments ahead, in a ring of 3
     // buffers (each refill is issued at the end of a segment):
@@ -544,6 +656,7 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
     constexpr int VP = kCap + 4;  // speed row pitch: [kCap] = 0 is the leader read of slot 511
     constexpr bool SGN = GOBS == 1, OBS = GOBS >= 2;
     constexpr int OKIND = GOBS == 3 ? 0 : 1;  // OBS: Eq. 4 as L1 (GOBS 3) or L2 (GOBS 2)
+    constexpr int kSW = kCap / 2;             // u16 sign-code words per tile row (per 4 steps)
     double lacc = 0.0;  // OBS: this thread's Eq. 4 terms (fp32 per segment, fp64 across)
     // fused iteration with delta frozen at 4: dL/d delta is not computed (row 5 written as 0)
     constexpr bool GD = !(D4 && GOBS != 0);
@@ -551,8 +664,9 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
     float* vrow = smem_b;                              // [NB][KS][VP]
     float* ckrow = vrow + NB * KS * VP;                // [NB][3][kCap]
     float* orow = ckrow + NB * kCkRows * kCap;         // [NB][KO][kCap] (dL/dP or obs rows)
-    // SGN: [NB][2][kT] u16 code words (the segment's steps; + the next word, which holds step K
-    // when the last segment is a whole one) and the 16-entry decode table code -> dL/dP pair
+    // SGN: [NB][2][kSW] u16 code words (the segment's steps; + the next word, which holds step
+    // K when the last segment is a whole one) and the 16-entry decode table code -> dL/dP pair.
+    // Word w of a row is the code of vehicles 2w, 2w + 1, so a thread's NP words are adjacent.
     unsigned short* sbuf = reinterpret_cast<unsigned short*>(orow);
     __shared__ float2 glut[16];
     if (SGN && tid < 16) {
@@ -581,13 +695,13 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
             // SGN: code word seg, + word seg + 1 (step K) when the last segment is whole
             const int swords = (seg == nseg - 1 && len == KS) ? 2 : 1;
             const uint32_t bytes = (uint32_t)(len + nckr) * kCap * sizeof(float) +
-                                   (SGN ? (uint32_t)swords * kT * sizeof(unsigned short) : 0u);
+                                   (SGN ? (uint32_t)swords * kSW * sizeof(unsigned short) : 0u);
             mbar_expect_tx(&mbar[b], bytes);
             if (SGN)
-                bulk_g2s(sbuf + b * 2 * kT,
+                bulk_g2s(sbuf + b * 2 * kSW,
                          reinterpret_cast<const unsigned short*>(a.sgn + tile * a.sg_stride) +
-                             (int64_t)seg * kT,
-                         swords * kT * sizeof(unsigned short), &mbar[b]);
+                             (int64_t)seg * kSW,
+                         swords * kSW * sizeof(unsigned short), &mbar[b]);
             const float* src = a.vt + tile * a.vt_stride + t0 * kCap;
             for (int tt = 0; tt < len; ++tt)
                 bulk_g2s(vrow + (b * KS + tt) * VP, src + tt * kCap, kCap * sizeof(float), &mbar[b]);
@@ -597,12 +711,12 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
         }
         if (!SGN) {
             const float* src = (OBS ? a.obs : a.grad_traj) + t0 * N + i0;
-            float* dst = orow + b * KO * kCap + 2 * tid;
+            float* dst = orow + b * KO * kCap + VT * tid;
 #pragma unroll
             for (int tt = 0; tt < KO; ++tt, src += N) {
                 const bool on = tt < len || (OBS && tt == len && seg == nseg - 1);
-                cp_async4(dst + tt * kCap, src, val[0] && on);
-                cp_async4(dst + tt * kCap + 1, src + 1, val[1] && on);
+#pragma unroll
+                for (int j = 0; j < VT; ++j) cp_async4(dst + tt * kCap + j, src + j, val[j] && on);
             }
             cp_async_commit();
         }
@@ -613,32 +727,41 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
     for (int q = 2; q <= NB - 1; ++q)
         if (nseg >= q) fetch(nseg - q, KS);
     // per-vehicle constants while the first two segments' rows are in flight
-    float ldj[2], pj[2];
-    VehP Pj[2];
-    VehA Aj[2];
+    float ldj[VT], pj[VT];
+    VehPT<float2> P[NP];
+    VehAT<float2> B[NP];
+    float2 p0[NP], e[NP], m[NP], u[NP];
+    GradAccT<float2> G[NP];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const int64_t i = i0 + j;
-        RawP r = dummy_raw();
-        ldj[j] = 0.f;
-        pj[j] = 0.f;
-        if (val[j]) {
-            r = load_raw(a.params, a.n_par, i);
-            if (D4 && r.delta != 4.f)
-                atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
-            if (!GOBS) ldj[j] = a.grad_traj[(int64_t)steps * N + i];  // lambda_D^K = dL/dP(K)
-            if (GOBS >= 2) pj[j] = a.pos0[i];
+    for (int p = 0; p < NP; ++p) {
+        VehP Pj[2];
+        VehA Aj[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = 2 * p + h;
+            const int64_t i = i0 + j;
+            RawP r = dummy_raw();
+            ldj[j] = 0.f;
+            pj[j] = 0.f;
+            if (val[j]) {
+                r = load_raw(a.params, a.n_par, i);
+                if (D4 && r.delta != 4.f)
+                    atomicMin(a.status, (unsigned long long)kBadDelta << 32 | (uint64_t)i);
+                if (!GOBS) ldj[j] = a.grad_traj[(int64_t)steps * N + i];  // lambda_D^K = dL/dP(K)
+                if (GOBS >= 2) pj[j] = a.pos0[i];
+            }
+            Pj[h] = make_vehp(r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta);
+            Aj[h] = make_veha(r.a_max, r.a_pref, r.v_targ, r.delta, k);
         }
-        Pj[j] = make_vehp(r.a_max, r.a_pref, r.s_min, r.T, r.v_targ, r.delta);
-        Aj[j] = make_veha(r.a_max, r.a_pref, r.v_targ, r.delta, k);
+        p0[p] = make_float2(pj[2 * p], pj[2 * p + 1]);
+        P[p] = pack(Pj[0], Pj[1]);
+        B[p] = pack(Aj[0], Aj[1]);
+        // scaled adjoint (bwd_from_record): u = dt lambda_v, m = -dt lambda_s, e = dt^2 lambda_D
+        e[p] = vmul(make_float2(ldj[2 * p], ldj[2 * p + 1]), k.dt2);
+        m[p] = f2(0.f);
+        u[p] = f2(0.f);
+        G[p] = GradAccT<float2>{f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
     }
-    const float2 p0 = make_float2(pj[0], pj[1]);
-    const VehPT<float2> P = pack(Pj[0], Pj[1]);
-    const VehAT<float2> B = pack(Aj[0], Aj[1]);
-    // scaled adjoint (bwd_from_record): u = dt lambda_v, m = -dt lambda_s, e = dt^2 lambda_D
-    float2 e = vmul(make_float2(ldj[0], ldj[1]), k.dt2);
-    float2 m = f2(0.f), u = f2(0.f);
-    GradAccT<float2> G = {f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
     if (tid == 0) { fx[0][0] = 0.f; fx[1][0] = 0.f; }  // never written again (slots t+1 >= 1)
     auto segment = [&](const int seg, const int len, auto FULL) {
         constexpr bool kFull = decltype(FULL)::value;
@@ -651,91 +774,123 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
             else if (seg >= 1) cp_async_wait<1>();
             else cp_async_wait<0>();
         }
-        const float* orr = orow + b * KO * kCap + 2 * tid;
-        float2 v[KS], g[KO], vl[KS], sg[KS];
-        const float* vr = vrow + b * KS * VP + 2 * tid;
+        const float* orr = orow + b * KO * kCap + VT * tid;
+        float2 v[KS][NP], g[KO][NP], vl[KS][NP], sg[KS][NP];
+        const float* vr = vrow + b * KS * VP + VT * tid;
 #pragma unroll
         for (int tt = 0; tt < KS; ++tt) {
-            if (kFull || tt < len) {
-                v[tt] = *reinterpret_cast<const float2*>(vr + tt * VP);
-                vl[tt] = make_float2(v[tt].y, vr[tt * VP + 2]);
-            } else {
-                v[tt] = f2(0.f);
-                vl[tt] = f2(0.f);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                if (kFull || tt < len) {
+                    v[tt][p] = *reinterpret_cast<const float2*>(vr + tt * VP + 2 * p);
+                    // the leader of the pair's second vehicle: the next pair's first, or the
+                    // next thread's first vehicle (slot kCap: the 0 sentinel)
+                    vl[tt][p] = make_float2(v[tt][p].y, vr[tt * VP + 2 * p + 2]);
+                } else {
+                    v[tt][p] = f2(0.f);
+                    vl[tt][p] = f2(0.f);
+                }
             }
         }
         unsigned cw0 = 0, cw1 = 0;  // SGN: this thread's code words (steps t0 .. t0 + 4)
         if (SGN) {
             static_assert(!SGN || KS == kSgnSteps, "one code word per segment");
-            cw0 = sbuf[b * 2 * kT + tid];
-            if (seg == nseg - 1 && len == KS) cw1 = sbuf[b * 2 * kT + kT + tid];
+            if (NP == 1) {
+                cw0 = sbuf[b * 2 * kSW + tid];
+                if (seg == nseg - 1 && len == KS) cw1 = sbuf[b * 2 * kSW + kSW + tid];
+            } else {  // NP = 2: the two adjacent u16 words as one u32 (pair p at bit 16 p)
+                cw0 = reinterpret_cast<const unsigned*>(sbuf + b * 2 * kSW)[tid];
+                if (seg == nseg - 1 && len == KS)
+                    cw1 = reinterpret_cast<const unsigned*>(sbuf + b * 2 * kSW + kSW)[tid];
+            }
         }
 #pragma unroll
         for (int tt = 0; tt < KO; ++tt) {
-            if (SGN) {  // -sign(obs - P) of this thread's two vehicles: 4-bit code -> table
-                const unsigned c = ((tt < KS ? cw0 : cw1) >> (4 * (tt % KS))) & 15u;
-                g[tt] = (kFull || tt <= len) ? glut[c] : f2(0.f);
-            } else {
-                g[tt] = (kFull || tt <= len) ? *reinterpret_cast<const float2*>(orr + tt * kCap)
-                                             : f2(0.f);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                if (SGN) {  // -sign(obs - P) of the pair's two vehicles: 4-bit code -> table
+                    const unsigned c = ((tt < KS ? cw0 : cw1) >> (16 * p + 4 * (tt % KS))) & 15u;
+                    g[tt][p] = (kFull || tt <= len) ? glut[c] : f2(0.f);
+                } else {
+                    g[tt][p] = (kFull || tt <= len)
+                                   ? *reinterpret_cast<const float2*>(orr + tt * kCap + 2 * p)
+                                   : f2(0.f);
+                }
             }
         }
         // gaps (and positions) inside the segment: the forward's recurrences from the
         // checkpoint, bitwise
-        const float* cr = ckrow + b * kCkRows * kCap + 2 * tid;
-        float2 s = *reinterpret_cast<const float2*>(cr);
-        float2 D = f2(0.f), cmp = f2(0.f), lsum = f2(0.f);
-        if (OBS) D = *reinterpret_cast<const float2*>(cr + kCap);
-        if (OBS && KAHAN) cmp = *reinterpret_cast<const float2*>(cr + 2 * kCap);
+        const float* cr = ckrow + b * kCkRows * kCap + VT * tid;
 #pragma unroll
-        for (int tt = 0; tt < KO; ++tt) {
-            if (OBS) {
-                // dL/dP at step t0 + tt (the forward's loss term on the same P bits); the
-                // rollout's last step K adds its term to lambda_D^K below.  Each row's Eq. 4
-                // term is counted once: rows t0 .. t0 + len - 1, and row K in the last segment
-                float2 lt = f2(0.f);
-                if (kFull || tt <= len) g[tt] = loss_term<OKIND>(g[tt], vadd(p0, D), lt);
-                if (tt < len || (tt == len && seg == nseg - 1)) lsum = vadd(lsum, lt);
-            }
-            if (tt < KS) {
-                sg[tt] = s;
-                if (kFull || tt < len) {
-                    s = vfma(vsub(v[tt], vl[tt]), -k.dt, s);
-                    if (OBS) {
-                        if (KAHAN) {
-                            const float2 y = vfma(v[tt], k.dt, vneg(cmp));
-                            const float2 t2 = vadd(D, y);
-                            cmp = vsub(vsub(t2, D), y);
-                            D = t2;
-                        } else {
-                            D = vfma(v[tt], k.dt, D);
+        for (int p = 0; p < NP; ++p) {
+            float2 s = *reinterpret_cast<const float2*>(cr + 2 * p);
+            float2 D = f2(0.f), cmp = f2(0.f), lsum = f2(0.f);
+            if (OBS) D = *reinterpret_cast<const float2*>(cr + kCap + 2 * p);
+            if (OBS && KAHAN) cmp = *reinterpret_cast<const float2*>(cr + 2 * kCap + 2 * p);
+#pragma unroll
+            for (int tt = 0; tt < KO; ++tt) {
+                if (OBS) {
+                    // dL/dP at step t0 + tt (the forward's loss term on the same P bits); the
+                    // rollout's last step K adds its term to lambda_D^K below.  Each row's Eq. 4
+                    // term is counted once: rows t0 .. t0 + len - 1, and row K in the last
+                    // segment
+                    float2 lt = f2(0.f);
+                    if (kFull || tt <= len) g[tt][p] = loss_term<OKIND>(g[tt][p], vadd(p0[p], D), lt);
+                    if (tt < len || (tt == len && seg == nseg - 1)) lsum = vadd(lsum, lt);
+                }
+                if (tt < KS) {
+                    sg[tt][p] = s;
+                    if (kFull || tt < len) {
+                        s = vfma(vsub(v[tt][p], vl[tt][p]), -k.dt, s);
+                        if (OBS) {
+                            if (KAHAN) {
+                                const float2 y = vfma(v[tt][p], k.dt, vneg(cmp));
+                                const float2 t2 = vadd(D, y);
+                                cmp = vsub(vsub(t2, D), y);
+                                D = t2;
+                            } else {
+                                D = vfma(v[tt][p], k.dt, D);
+                            }
                         }
                     }
                 }
             }
-        }
-        if (OBS) {  // absent vehicles' slots are zero-filled, not NaN: their terms drop here
-            lacc += (val[0] ? (double)lsum.x : 0.0) + (val[1] ? (double)lsum.y : 0.0);
+            if (OBS) {  // absent vehicles' slots are zero-filled, not NaN: their terms drop here
+                lacc += (val[2 * p] ? (double)lsum.x : 0.0) +
+                        (val[2 * p + 1] ? (double)lsum.y : 0.0);
+            }
         }
         if (GOBS && seg == nseg - 1) {  // lambda_D^K = dL/dP(K) (static selects, no indexing)
 #pragma unroll
             for (int tt = 0; tt < KO; ++tt)
-                if (tt == len) e = vmul(g[tt], k.dt2);
+                if (tt == len)
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) e[p] = vmul(g[tt][p], k.dt2);
         }
-        // reverse sweep t = t0 + len - 1 ... t0; the local Jacobian of the next step down is
-        // independent of the adjoint chain, so the scheduler overlaps it with this one
+        // reverse sweep t = t0 + len - 1 ... t0; the local Jacobians of the next step down are
+        // independent of the adjoint chain, so the scheduler overlaps them with this one
 #pragma unroll
         for (int tt = KS - 1; tt >= 0; --tt) {
             if (kFull || tt < len) {  // CTA-uniform
-                CoreT<float2> c;
-                core<D4>(sg[tt], v[tt], vl[tt], P, k, c);
-                const RecT<float2> R = jac_record<D4, GD>(c, sg[tt], v[tt], P, B, k);
-                const float2 F = bwd_from_record<D4, GD>(R, v[tt], vl[tt], P, B, k, m, u, e, G);
-                fx[par][tid + 1] = F.y;  // vehicle 2t + 1 -> its leader 2t + 2 (thread t + 1)
+                float2 F[NP];
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                    CoreT<float2> c;
+                    core<D4>(sg[tt][p], v[tt][p], vl[tt][p], P[p], k, c);
+                    const RecT<float2> R = jac_record<D4, GD>(c, sg[tt][p], v[tt][p], P[p], B[p], k);
+                    F[p] = bwd_from_record<D4, GD>(R, v[tt][p], vl[tt][p], P[p], B[p], k, m[p],
+                                                   u[p], e[p], G[p]);
+                }
+                // the thread's last vehicle -> its leader, thread t + 1's first vehicle
+                fx[par][tid + 1] = F[NP - 1].y;
+                // in-thread follower terms and lambda_D^t = g^t + lambda_D^{t+1} need no barrier
+#pragma unroll
+                for (int p = 1; p < NP; ++p) u[p] = vadd(u[p], make_float2(F[p - 1].y, F[p].x));
+#pragma unroll
+                for (int p = 0; p < NP; ++p) e[p] = vfma(g[tt][p], k.dt2, e[p]);
                 __syncthreads();
-                // F from the follower: 2t - 1 (thread t - 1) for 2t, 2t (this thread) for 2t + 1
-                u = vadd(u, make_float2(fx[par][tid], F.x));
-                e = vfma(g[tt], k.dt2, e);  // lambda_D^t = g^t + lambda_D^{t+1}
+                // F of the first vehicle's follower: thread t - 1's last vehicle
+                u[0] = vadd(u[0], make_float2(fx[par][tid], F[0].x));
                 par ^= 1;
             }
         }
@@ -748,19 +903,30 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
     if (tail < KS) segment(seg--, tail, std::false_type{});
     for (; seg >= 0; --seg) segment(seg, KS, std::true_type{});
     // dL/dp0_i = lambda_D - lambda_s_i + lambda_s_{follower}; dL/dv0 = lambda_v (unscaled)
-    fx[par][tid + 1] = m.y;
+    fx[par][tid + 1] = m[NP - 1].y;
     __syncthreads();
-    const float2 gp0 = grad_p0(e, m, make_float2(fx[par][tid], m.x), k);
-    const float2 gv0 = grad_v0(u, k);
-
-    // parameter gradients from the factored accumulators
-    unscale_acc(G, k);
-    const float Sj[6][2] = {{G.S1.x, G.S1.y}, {G.S2.x, G.S2.y}, {G.S3.x, G.S3.y},
-                            {G.S4.x, G.S4.y}, {G.S5.x, G.S5.y}, {G.S6.x, G.S6.y}};
-    const float lvj[2] = {gv0.x, gv0.y}, gpj[2] = {gp0.x, gp0.y};
-    float gr[kVpt][6];
+    float gpj[VT], lvj[VT], Sj[6][VT];
 #pragma unroll
-    for (int j = 0; j < kVpt; ++j) {
+    for (int p = 0; p < NP; ++p) {
+        const float mf0 = p == 0 ? fx[par][tid] : m[p - 1].y;
+        const float2 gp0 = grad_p0(e[p], m[p], make_float2(mf0, m[p].x), k);
+        const float2 gv0 = grad_v0(u[p], k);
+        gpj[2 * p] = gp0.x;
+        gpj[2 * p + 1] = gp0.y;
+        lvj[2 * p] = gv0.x;
+        lvj[2 * p + 1] = gv0.y;
+        // parameter gradients from the factored accumulators
+        unscale_acc(G[p], k);
+        const float2 Sp[6] = {G[p].S1, G[p].S2, G[p].S3, G[p].S4, G[p].S5, G[p].S6};
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            Sj[q][2 * p] = Sp[q].x;
+            Sj[q][2 * p + 1] = Sp[q].y;
+        }
+    }
+    float gr[VT][6];
+#pragma unroll
+    for (int j = 0; j < VT; ++j) {
 #pragma unroll
         for (int q = 0; q < 6; ++q) gr[j][q] = 0.f;
         if (!val[j]) continue;
@@ -778,7 +944,7 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
     }
     if (!SHARED) {
 #pragma unroll
-        for (int j = 0; j < kVpt; ++j) {
+        for (int j = 0; j < VT; ++j) {
             if (!val[j]) continue;
             const int64_t i = i0 + j;
             int bq = -1;  // first optimised parameter with a non-finite gradient
@@ -800,19 +966,19 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
         // staging ring is idle after the sweep (the barrier above ordered its last reads).
         double* vg = reinterpret_cast<double*>(smem_b);  // [kCap][6]
 #pragma unroll
-        for (int j = 0; j < kVpt; ++j)
+        for (int j = 0; j < VT; ++j)
 #pragma unroll
             for (int q = 0; q < 6; ++q) vg[(id0 + j) * 6 + q] = (double)gr[j][q];
         __syncthreads();
 #pragma unroll
-        for (int j = 0; j < kVpt; ++j) {
+        for (int j = 0; j < VT; ++j) {
             const int li = id0 + j;
             if (!val[j] || !(li == 0 || a.lead[base + li - 1] == 0)) continue;  // lane starts
             double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            for (int e = li;; ++e) {  // the lane's vehicles up to its head (no leader)
+            for (int ee = li;; ++ee) {  // the lane's vehicles up to its head (no leader)
 #pragma unroll
-                for (int q = 0; q < 6; ++q) acc[q] += vg[e * 6 + q];
-                if (a.lead[base + e] == 0) break;
+                for (int q = 0; q < 6; ++q) acc[q] += vg[ee * 6 + q];
+                if (a.lead[base + ee] == 0) break;
             }
             // lane index: the last l with lane_offsets[l] <= i (empty lanes skipped)
             const int64_t gi = base + li;
@@ -826,7 +992,7 @@ __global__ void __launch_bounds__(kT, (KS <= 4 ? IDM_BWD_MINB : 1)) bwd_kernel(B
             for (int q = 0; q < 6; ++q) a.lane_grads[(int64_t)lo * 6 + q] = acc[q];
         }
     }
-    if (OBS && a.loss_partials) block_sum_to(lacc, a.loss_partials + tile);  // Eq. 4 here
+    if (OBS && a.loss_partials) block_sum_to<kTb>(lacc, a.loss_partials + tile);  // Eq. 4 here
 }
 
 // ------------------------------------------------------------------------------ NK2
@@ -990,7 +1156,8 @@ bool ckpt_supported(int k) { return k == 2 || k == 4 || k == 8; }
 
 template <bool D4, bool KH, int KS>
 static void launch_fwd_k(const FwdArgs& a, int ntiles, const FwdVariant& var, cudaStream_t st) {
-    dim3 g(ntiles), b(kT);
+    dim3 g(ntiles), b(kCap / (2 * IDM_FWD_NP));
+    const dim3 b_api(kCap / (2 * IDM_FWD_NP_API));  // idm_forward with history
     if constexpr (KS == 4) {  // the fused idm_fit_step forward exists for 4-step segments
         if (var.loss == 1) { fwd_kernel<D4, KH, false, 1, KS><<<g, b, 0, st>>>(a); return; }
         if (var.loss == 2) { fwd_kernel<D4, KH, false, 2, KS><<<g, b, 0, st>>>(a); return; }
@@ -1001,8 +1168,8 @@ static void launch_fwd_k(const FwdArgs& a, int ntiles, const FwdVariant& var, cu
         else fwd_kernel<D4, KH, false, 0, 4, false><<<g, b, 0, st>>>(a);
         return;
     }
-    if (var.rec_v) fwd_kernel<D4, KH, true, 0, KS><<<g, b, 0, st>>>(a);
-    else fwd_kernel<D4, KH, false, 0, KS><<<g, b, 0, st>>>(a);
+    if (var.rec_v) fwd_kernel<D4, KH, true, 0, KS><<<g, b_api, 0, st>>>(a);
+    else fwd_kernel<D4, KH, false, 0, KS><<<g, b_api, 0, st>>>(a);
 }
 
 template <bool D4, bool KH>
@@ -1038,20 +1205,26 @@ constexpr size_t bwd_smem_of() {  // ring of NB: speed + checkpoint + dL/dP/obs 
            sizeof(float);
 }
 
+#ifndef IDM_BWD_NP
+#define IDM_BWD_NP 1  // vehicle pairs per backward thread (1: 256 threads, 2: 128 threads; 2 measured 3.7% slower)
+#endif
 template <bool D4, bool SH, bool AD, int KS, int GO, bool KH>
 static cudaError_t launch_bwd_v(const BwdArgs& a, int ntiles, cudaStream_t st,
                                 bool pdl = false) {
+    constexpr int NP = IDM_BWD_NP;
+    constexpr int kTb = kCap / (2 * NP);
     constexpr size_t smem = bwd_smem_of<KS, GO>();
     static std::atomic<unsigned long long> optin{0};  // devices opted in (bit per device)
-    cudaError_t e = smem_optin((const void*)bwd_kernel<D4, SH, AD, KS, GO, KH>, (int)smem, optin);
+    cudaError_t e =
+        smem_optin((const void*)bwd_kernel<D4, SH, AD, KS, GO, KH, NP>, (int)smem, optin);
     if (e != cudaSuccess) return e;
     if (!pdl) {
-        bwd_kernel<D4, SH, AD, KS, GO, KH><<<ntiles, kT, smem, st>>>(a);
+        bwd_kernel<D4, SH, AD, KS, GO, KH, NP><<<ntiles, kTb, smem, st>>>(a);
         return cudaSuccess;  // launch errors: cudaGetLastError in launch_bwd
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ntiles);
-    cfg.blockDim = dim3(kT);
+    cfg.blockDim = dim3(kTb);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -1059,7 +1232,7 @@ static cudaError_t launch_bwd_v(const BwdArgs& a, int ntiles, cudaStream_t st,
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, bwd_kernel<D4, SH, AD, KS, GO, KH>, a);
+    return cudaLaunchKernelEx(&cfg, bwd_kernel<D4, SH, AD, KS, GO, KH, NP>, a);
 }
 
 // API backward (idm_backward): dL/dP rows from grad_traj, Adam by its own kernel
