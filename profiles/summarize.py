@@ -38,7 +38,9 @@ def _num(vals, h, u, key):
         x = float(vals[i].replace(",", ""))
     except ValueError:
         return None
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u[i], 1)
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "ns": 1,
+             "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6, "second": 1e9,
+             "s": 1e9}.get(u[i], 1)
     return x * scale
 
 
@@ -49,7 +51,7 @@ def main(rep, json_out=None, units=None, tag=""):
     for vals in rows[2:]:
         kname = vals[h.index('Kernel Name')]
         print(f"kernel: {kname}")
-        short = kname.split("<")[0].split("(")[0].split("::")[-1]
+        short = kname.split("<")[0].split("(")[0].split("::")[-1].split()[-1]
         rec = {
             "kernel": kname, "source": f"{os.path.basename(rep)} ({tag})",
             "duration_ns": _num(vals, h, u, "gpu__time_duration.sum"),
