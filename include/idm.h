@@ -126,7 +126,8 @@ size_t idm_workspace_bytes(const idm_desc* d);
    consecutive tiles always hold more than that many vehicles.  lane_offsets: HOST [n_lanes+1].
    Writes the n_tiles+1 tile starts (vehicle indices, last = n_vehicles) to tile_start (HOST,
    nullable: count only) and returns n_tiles, or -1 for malformed offsets or a lane longer than
-   a tile. */
+   idm_max_lane_length().  With a lane longer than a tile the plan holds empty padding tiles
+   (equal consecutive starts) so that such lanes start at multiples of the cluster size. */
 int64_t idm_plan_tiles(const int32_t* lane_offsets, int32_t n_lanes, int64_t n_vehicles,
                        int64_t* tile_start);
 
@@ -146,8 +147,8 @@ int idm_state_from_obs(const float* obs, int64_t n_vehicles, int32_t steps, floa
                        float* pos0, float* vel0, void* stream);
 
 /* Validate the descriptor and input data (finite, v(0) >= 0, lengths >= 0, a_max, a_pref,
-   v_targ, delta > 0, lane offsets well formed, every lane fits one lane tile of
-   idm_max_lane_vehicles() vehicles, and -- lane mode -- every lane member strictly behind its
+   v_targ, delta > 0, lane offsets well formed, every lane at most idm_max_lane_length()
+   vehicles, and -- lane mode -- every lane member strictly behind its
    leader: pos0[i+1] - pos0[i] - length[i+1] > 0, the ordering PAPER.md:106 presumes ("the
    vehicle directly ahead"); gaps in (0, eps_gap) are valid and clamped, R#7), build the
    lane -> CTA tile plan and leader flags in the workspace.  IDM_EINVAL on any violation, with
@@ -315,8 +316,15 @@ int idm_check(idm_handle* h);
 /* Number of kernel launches the library issued on this handle since idm_init. */
 int64_t idm_launch_count(const idm_handle* h);
 
-/* Largest lane (vehicles) one lane tile holds. */
+/* Largest lane (vehicles) one lane tile holds (one CTA). */
 int32_t idm_max_lane_vehicles(void);
+
+/* Largest lane (vehicles) supported: idm_max_lane_vehicles() x 8.  A lane longer than one tile
+   runs over a thread-block cluster of consecutive tiles (up to 8, the portable cluster size):
+   the boundary vehicles' leader speeds and adjoint terms cross CTAs through distributed shared
+   memory and every step barrier is cluster-wide.  Such a plan needs ckpt_every == 4, runs
+   every launch in clusters (slower steps), and idm_fit rejects it. */
+int32_t idm_max_lane_length(void);
 
 /* Sticky last error message of h ("" if none; a static message if h is NULL). */
 const char* idm_last_error(const idm_handle* h);

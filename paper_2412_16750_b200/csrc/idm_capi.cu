@@ -19,6 +19,7 @@ struct idm_handle {
     cudaStream_t st;
     int64_t n, n_par;
     int ntiles, nck;
+    int csize;    // > 1: a lane is longer than a tile; every launch runs clusters of csize tiles
     int num_sms;  // of the handle's device
     // workspace carve-outs
     int64_t* tile_start;
@@ -93,17 +94,31 @@ struct Layout {
 
 bool lane_mode(const idm_desc* d) { return d->leader_mode != IDM_LEADER_VIRTUAL; }
 
+constexpr int kMaxCluster = 8;  // portable thread-block cluster size: lanes <= 8 kCap vehicles
+
 int64_t max_tiles_for(const idm_desc* d) {
     if (!lane_mode(d)) return 1;  // virtual leader: independent trajectories, no lane tiles
-    int64_t by_size = 2 * ((d->n_vehicles + kCap - 1) / kCap) + 1;
-    return d->n_lanes < by_size ? d->n_lanes : by_size;
+    const int64_t n = d->n_vehicles;
+    // greedy packing: <= 2N/kCap + 1; each lane longer than a tile (< N/kCap of them) adds at
+    // most 2 (kMaxCluster - 1) empty padding tiles, and the end pads to a cluster multiple
+    int64_t by_size = 2 * ((n + kCap - 1) / kCap) + 1 + 2 * (kMaxCluster - 1) * (n / kCap + 1) +
+                      kMaxCluster;
+    return d->n_lanes + 2 * (kMaxCluster - 1) * (n / kCap + 1) + kMaxCluster < by_size
+               ? d->n_lanes + 2 * (kMaxCluster - 1) * (n / kCap + 1) + kMaxCluster
+               : by_size;
 }
 
 // Lane-tile plan (cold path, host): whole lanes per tile, <= kCap vehicles; greedy, so two
-// consecutive tiles always hold > kCap vehicles (tiles <= 2N/kCap + 1).  Fills tile starts and
-// leader flags (if given); returns the tile count, or -1 with *err set.
+// consecutive tiles always hold > kCap vehicles.  A lane longer than kCap (up to kMaxCluster
+// kCap vehicles) runs over one thread-block cluster of cs consecutive tiles, cs = the longest
+// lane's tile count: it starts at a tile index that is a multiple of cs (empty padding tiles
+// before it), fills full tiles of kCap vehicles (the last one the remainder, then empty ones up
+// to cs), and no other lane shares its tiles; the tile count is padded to a multiple of cs.
+// Every launch of such a plan uses clusters of cs CTAs (csize_out; 1 = no long lane).  Fills
+// tile starts and leader flags (if given); returns the tile count, or -1 with *err set.
 int64_t plan_tiles(const std::vector<int32_t>& off, int32_t n_lanes, int64_t n,
-                   std::vector<int64_t>* tiles, std::vector<uint8_t>* lead, std::string* err) {
+                   std::vector<int64_t>* tiles, std::vector<uint8_t>* lead, std::string* err,
+                   int* csize_out = nullptr) {
     char buf[256];
     if (off[0] != 0 || off.back() != n) {
         std::snprintf(buf, sizeof buf, "lane_offsets must start at 0 and end at N=%lld (got %d..%d)",
@@ -111,8 +126,7 @@ int64_t plan_tiles(const std::vector<int32_t>& off, int32_t n_lanes, int64_t n,
         *err = buf;
         return -1;
     }
-    int64_t count = 1, cur = 0;  // cur: vehicles in the open tile
-    if (tiles) tiles->assign(1, 0);
+    int64_t longest = 0;
     for (int32_t l = 0; l < n_lanes; ++l) {
         const int64_t a = off[l], b = off[l + 1];
         if (b < a) {
@@ -120,25 +134,43 @@ int64_t plan_tiles(const std::vector<int32_t>& off, int32_t n_lanes, int64_t n,
             *err = buf;
             return -1;
         }
-        const int64_t sz = b - a;
-        if (sz == 0) continue;
-        if (sz > kCap) {
+        if (b - a > kMaxCluster * kCap) {
             std::snprintf(buf, sizeof buf,
-                          "lane %d has %lld vehicles; at most %d per lane are supported", l,
-                          (long long)sz, kCap);
+                          "lane %d has %lld vehicles; at most %d per lane are supported (%d "
+                          "tiles of %d in one thread-block cluster)", l, (long long)(b - a),
+                          kMaxCluster * kCap, kMaxCluster, kCap);
             *err = buf;
             return -1;
         }
-        if (cur + sz > kCap) {
-            if (tiles) tiles->push_back(a);
-            ++count;
-            cur = 0;
+        longest = b - a > longest ? b - a : longest;
+    }
+    const int cs = longest > kCap ? (int)((longest + kCap - 1) / kCap) : 1;
+    if (csize_out) *csize_out = cs;
+    std::vector<int64_t> t(1, 0);  // tile starts; the last entry is the open tile
+    int64_t cur = 0;               // vehicles in the open tile
+    for (int32_t l = 0; l < n_lanes; ++l) {
+        const int64_t a = off[l], b = off[l + 1];
+        const int64_t sz = b - a;
+        if (sz == 0) continue;
+        if (sz > kCap) {  // a cluster of its own, starting at a multiple of cs
+            if (cur > 0) t.push_back(a);
+            while ((t.size() - 1) % (size_t)cs != 0) t.push_back(a);  // empty tiles [a, a)
+            for (int c = 1; c < cs; ++c) t.push_back(a + c * (int64_t)kCap < b ? a + c * (int64_t)kCap : b);
+            cur = kCap;  // closed: the next lane opens a new tile
+        } else {
+            if (cur + sz > kCap) {
+                t.push_back(a);
+                cur = 0;
+            }
+            cur += sz;
         }
-        cur += sz;
         if (lead)
             for (int64_t i = a; i + 1 < b; ++i) (*lead)[(size_t)i] = 1;
     }
-    if (tiles) tiles->push_back(n);
+    t.push_back(n);
+    while ((t.size() - 1) % (size_t)cs != 0) t.push_back(n);  // empty tiles [n, n)
+    const int64_t count = (int64_t)t.size() - 1;
+    if (tiles) *tiles = std::move(t);
     return count;
 }
 
@@ -274,6 +306,7 @@ int fused_chunks(const idm_handle* h) {
         return e ? std::atoi(e) : 1;
     }();
     int c = env < 1 ? 1 : (env > 16 ? 16 : env);
+    if (h->csize > 1) return 1;  // chunks would split clusters
     return c > h->ntiles ? h->ntiles : c;
 }
 
@@ -285,7 +318,7 @@ bool use_pdl(const idm_handle* h, int nch) {
         const char* e = std::getenv("IDM_PDL");
         return !(e && e[0] == '0');
     }();
-    return env && nch == 1 && !h->timing;
+    return env && nch == 1 && !h->timing && h->csize <= 1;  // not with clusters (long lanes)
 }
 
 int sync_status(idm_handle* h) {
@@ -368,6 +401,8 @@ size_t idm_workspace_bytes(const idm_desc* d) {
 }
 
 int32_t idm_max_lane_vehicles(void) { return kCap; }
+
+int32_t idm_max_lane_length(void) { return kMaxCluster * kCap; }
 
 int idm_state_from_obs(const float* obs, int64_t n_vehicles, int32_t steps, float dt,
                        float* pos0, float* vel0, void* stream) {
@@ -479,13 +514,19 @@ int idm_init(idm_handle** out, const idm_desc* d) {
                 break;
             }
             std::string perr;
-            nt = plan_tiles(off, d->n_lanes, d->n_vehicles, &tiles, &lead, &perr);
+            nt = plan_tiles(off, d->n_lanes, d->n_vehicles, &tiles, &lead, &perr, &h->csize);
             if (nt < 0) {
                 bail(fail(h, IDM_EINVAL, "%s", perr.c_str()));
                 break;
             }
+            if (h->csize > 1 && d->ckpt_every != 4) {
+                bail(fail(h, IDM_EINVAL, "lanes longer than %d vehicles (thread-block clusters) "
+                                         "need ckpt_every == 4", kCap));
+                break;
+            }
         } else {
             tiles = {0, d->n_vehicles};
+            h->csize = 1;
         }
         if (nt > max_tiles_for(d) || !layout_for(d, nt, &L)) {
             bail(fail(h, IDM_EINVAL, "internal: tile plan exceeds bound"));
@@ -712,6 +753,7 @@ int idm_forward_ex(idm_handle* h, int32_t steps, uint32_t flags) {
     var.rec_v = h->d.vel_traj != nullptr;
     var.loss = 0;
     var.hist = hist;
+    var.csize = h->csize;
     {
         TimedLaunch tl(h, IDM_K_FWD);
         CK(h, launch_fwd(a, h->ntiles, var, h->st));
@@ -787,7 +829,8 @@ int idm_backward(idm_handle* h) {
         CK(h, cudaMemsetAsync(h->lane_grads, 0, sizeof(double) * 6 * (size_t)h->d.n_lanes, h->st));
     {
         TimedLaunch tl(h, IDM_K_BWD);
-        CK(h, launch_bwd(a, h->ntiles, h->delta4, shared, false, 0, false, h->st));
+        CK(h, launch_bwd(a, h->ntiles, h->delta4, shared, false, 0, false, h->st, false,
+                         h->csize));
     }
     h->launches++;
     if (shared) {  // this handle's lanes (one rank: the whole sum; ranks: idm_reduce_shared)
@@ -969,6 +1012,7 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
     var.delta4 = h->delta4;
     var.kahan = steps > 2000;
     var.rec_v = false;
+    var.csize = h->csize;
     // Two schemes, same arithmetic: the forward sums Eq. 4 and records the L1 sign codes (L1
     // default: 2 bits per vehicle-step cross to the backward), or the forward writes only the
     // tile history and the backward derives Eq. 4 from obs and the rebuilt positions (L2
@@ -1030,7 +1074,8 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
         }
         {
             TimedLaunch tl(h, IDM_K_BWD, sb);
-            CK(h, launch_bwd(b, t1 - t0, h->delta4, shared, !shared, gobs, var.kahan, sb, pdl));
+            CK(h, launch_bwd(b, t1 - t0, h->delta4, shared, !shared, gobs, var.kahan, sb, pdl,
+                             h->csize));
         }
         h->launches += 2;
     }
@@ -1142,6 +1187,9 @@ int idm_fit(idm_handle* h, int32_t steps, const float* obs, int32_t kind, int32_
         return fail(h, IDM_EINVAL, "bad loss kind %d", kind);
     if (is_vl(h) || h->d.param_mode != IDM_PARAMS_PER_VEHICLE)
         return fail(h, IDM_EINVAL, "idm_fit supports lane-leader mode with per-vehicle parameters");
+    if (h->csize > 1)
+        return fail(h, IDM_EINVAL, "idm_fit: lanes longer than %d vehicles are not supported (use "
+                                   "idm_fit_step)", kCap);
     if (iters < 1 || iters > kFitMaxIters || iter0 < 0 || iter0 + iters > total_iters)
         return fail(h, IDM_EINVAL, "idm_fit: iterations [%d, %d) outside [0, total_iters=%d) or "
                                    "more than %d per call", iter0, iter0 + iters, total_iters,

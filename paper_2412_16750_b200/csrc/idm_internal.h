@@ -43,6 +43,7 @@ struct FwdVariant {
     bool rec_v;   // record speeds
     int loss;     // 0, or fused Eq. 4 (1 = L1, 2 = L2): read obs, sum the loss (idm_fit_step)
     bool hist = true;  // store the state history for a backward (false: P rows only)
+    int csize = 1;     // > 1: lanes longer than a tile, thread-block clusters of csize tiles
 };
 
 // Lane-mode state history in HBM, TILE-LOCAL layout (internal workspace):
@@ -183,8 +184,9 @@ cudaError_t kernels_configure(int ckpt_every);
 // from obs and the rebuilt positions (gobs != 0: fused idm_fit_step, ckpt_every == 4)
 // pdl: launch as a programmatic dependent of the preceding kernel in the stream (the forward of
 // the same tiles, which signals a.tile_ready)
+// csize > 1: lanes longer than a tile, thread-block clusters of csize tiles (no pdl)
 cudaError_t launch_bwd(const BwdArgs& a, int ntiles, bool delta4, bool shared, bool adam,
-                       int gobs, bool kahan, cudaStream_t st, bool pdl = false);
+                       int gobs, bool kahan, cudaStream_t st, bool pdl = false, int csize = 1);
 bool ckpt_supported(int k);
 cudaError_t launch_loss(const LossArgs& a, int nblocks, cudaStream_t st);
 cudaError_t launch_reduce(const double* partials, int64_t n, int width, double* out, float* out_f,

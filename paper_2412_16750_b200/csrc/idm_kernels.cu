@@ -198,6 +198,42 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
+
+// ------------------------------------------------------------------ thread-block clusters
+// A lane longer than one tile (kCap vehicles) runs as consecutive full tiles of one cluster
+// (idm_capi.cu plan_tiles): CTA r + 1 holds the vehicles ahead of CTA r's, so the leader of CTA
+// r's last vehicle is CTA r + 1's first, read from its shared memory (DSMEM), and every step
+// barrier is cluster-wide.  Tiles of whole lanes inside such a launch do the same with no peer.
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+                 "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared-memory word `p` (a local address) of cluster CTA `rank`
+__device__ __forceinline__ float ld_peer(const float* p, unsigned rank) {
+    uint32_t ra;
+    float v;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(rank));
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
+    return v;
+}
+__device__ __forceinline__ double ld_peer(const double* p, unsigned rank) {
+    uint32_t ra;
+    double v;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(rank));
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
+    return v;
+}
+// the per-step barrier: CTA-wide, or cluster-wide for lanes split over a cluster (CL)
+template <bool CL>
+__device__ __forceinline__ void step_sync() {
+    if constexpr (CL) cluster_sync_all();
+    else __syncthreads();
+}
 }  // namespace
 
 // ------------------------------------------------------------------------------ NK1
@@ -245,7 +281,7 @@ __device__ __forceinline__ void st_pairs(float2* p, const float2 (&x)[NP]) {
 }
 // HIST = false (LOSS = 0 only): a prediction rollout (idm_forward_ex IDM_FWD_NO_HISTORY) that
 // writes only the P rows -- no speed history or checkpoints, nothing for a backward.
-template <bool D4, bool KAHAN, bool RECV, int LOSS, int CK, bool HIST = true,
+template <bool D4, bool KAHAN, bool RECV, int LOSS, int CK, bool HIST = true, bool CL = false,
           int NP = (LOSS == 0 && HIST ? IDM_FWD_NP_API : IDM_FWD_NP)>
 __global__ void __launch_bounds__(kCap / (2 * NP), (fwd_min_blocks<CK, LOSS, NP>()))
     fwd_kernel(FwdArgs a) {
@@ -272,6 +308,10 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (fwd_min_blocks<CK, LOSS, NP>
 #pragma unroll
     for (int j = 0; j < VT; ++j) val[j] = id0 + j < n_loc;
     if (LOSS && a.tile_ready) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // CL: this tile's last vehicle has a leader, the next cluster CTA's first vehicle (a full
+    // tile of a lane longer than a tile)
+    const unsigned crank = CL ? cluster_rank() : 0u;
+    const bool peer_lead = CL && n_loc == kCap && a.lead[base + kCap - 1] != 0;
 
     auto put = [&](float* row, const float2 (&x)[NP]) {  // row points at local vehicle VT tid
 #pragma unroll
@@ -451,11 +491,13 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (fwd_min_blocks<CK, LOSS, NP>
     // one synchronous step of the whole tile; o = this step's observations (LOSS)
     auto step = [&](int tt, auto PH) {  // PH: (index of the step computed) mod 4
         xv[par][tid] = v[0].x;
-        __syncthreads();
+        step_sync<CL>();
+        float nb = xv[par][tid + 1];  // the next thread's first vehicle ([kTf]: sentinel 0)
+        if (CL && peer_lead && tid == kTf - 1) nb = ld_peer(&xv[par][0], crank + 1);
         float2 vl[NP];
 #pragma unroll
         for (int p = 0; p < NP; ++p)
-            vl[p] = make_float2(v[p].y, p + 1 < NP ? v[p + 1 < NP ? p + 1 : p].x : xv[par][tid + 1]);
+            vl[p] = make_float2(v[p].y, p + 1 < NP ? v[p + 1 < NP ? p + 1 : p].x : nb);
         par ^= 1;
         float2 Pv[NP];
 #pragma unroll
@@ -588,6 +630,7 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (fwd_min_blocks<CK, LOSS, NP>
         }
     }
     if (LOSS && a.tile_ready) tile_release(a.tile_ready + tile, a.epoch);
+    if (CL) cluster_sync_all();  // no CTA leaves while a peer may still read its shared memory
 }
 
 // ------------------------------------------------------------------------------ NK3
@@ -622,7 +665,7 @@ template <int KS, int NP>
 constexpr int bwd_min_blocks() {
     return NP == 1 ? (KS <= 4 ? IDM_BWD_MINB : 1) : (KS <= 4 ? IDM_BWD_MINB2 : 1);
 }
-template <bool D4, bool SHARED, bool ADAM, int KS, int GOBS, bool KAHAN, int NP>
+template <bool D4, bool SHARED, bool ADAM, int KS, int GOBS, bool KAHAN, bool CL, int NP>
 __global__ void __launch_bounds__(kCap / (2 * NP), (bwd_min_blocks<KS, NP>()))
     bwd_kernel(BwdArgs a) {
     constexpr int VT = 2 * NP;          // vehicles per thread
@@ -640,6 +683,11 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (bwd_min_blocks<KS, NP>()))
     bool val[VT];
 #pragma unroll
     for (int j = 0; j < VT; ++j) val[j] = id0 + j < n_loc;
+    // CL (a lane longer than a tile over a cluster): the last vehicle's leader is the next CTA's
+    // first vehicle; the first vehicle's follower is the previous CTA's last vehicle
+    const unsigned crank = CL ? cluster_rank() : 0u;
+    const bool peer_lead = CL && n_loc == kCap && a.lead[base + kCap - 1] != 0;
+    const bool peer_follow = CL && base > 0 && n_loc > 0 && a.lead[base - 1] != 0;
     const int nseg = (steps + KS - 1) / KS;
     const int tail = steps - (nseg - 1) * KS;  // length of the last segment (1..KS)
 
@@ -785,7 +833,10 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (bwd_min_blocks<KS, NP>()))
                     v[tt][p] = *reinterpret_cast<const float2*>(vr + tt * VP + 2 * p);
                     // the leader of the pair's second vehicle: the next pair's first, or the
                     // next thread's first vehicle (slot kCap: the 0 sentinel)
-                    vl[tt][p] = make_float2(v[tt][p].y, vr[tt * VP + 2 * p + 2]);
+                    float nb = vr[tt * VP + 2 * p + 2];  // slot kCap: the sentinel 0
+                    if (CL && p == NP - 1 && peer_lead && tid == kTb - 1)
+                        nb = ld_peer(vrow + (b * KS + tt) * VP, crank + 1);
+                    vl[tt][p] = make_float2(v[tt][p].y, nb);
                 } else {
                     v[tt][p] = f2(0.f);
                     vl[tt][p] = f2(0.f);
@@ -888,9 +939,11 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (bwd_min_blocks<KS, NP>()))
                 for (int p = 1; p < NP; ++p) u[p] = vadd(u[p], make_float2(F[p - 1].y, F[p].x));
 #pragma unroll
                 for (int p = 0; p < NP; ++p) e[p] = vfma(g[tt][p], k.dt2, e[p]);
-                __syncthreads();
+                step_sync<CL>();
                 // F of the first vehicle's follower: thread t - 1's last vehicle
-                u[0] = vadd(u[0], make_float2(fx[par][tid], F[0].x));
+                float ff = fx[par][tid];
+                if (CL && peer_follow && tid == 0) ff = ld_peer(&fx[par][kTb], crank - 1);
+                u[0] = vadd(u[0], make_float2(ff, F[0].x));
                 par ^= 1;
             }
         }
@@ -904,11 +957,13 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (bwd_min_blocks<KS, NP>()))
     for (; seg >= 0; --seg) segment(seg, KS, std::true_type{});
     // dL/dp0_i = lambda_D - lambda_s_i + lambda_s_{follower}; dL/dv0 = lambda_v (unscaled)
     fx[par][tid + 1] = m[NP - 1].y;
-    __syncthreads();
+    step_sync<CL>();
+    float mpeer = fx[par][tid];
+    if (CL && peer_follow && tid == 0) mpeer = ld_peer(&fx[par][kTb], crank - 1);
     float gpj[VT], lvj[VT], Sj[6][VT];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-        const float mf0 = p == 0 ? fx[par][tid] : m[p - 1].y;
+        const float mf0 = p == 0 ? mpeer : m[p - 1].y;
         const float2 gp0 = grad_p0(e[p], m[p], make_float2(mf0, m[p].x), k);
         const float2 gv0 = grad_v0(u[p], k);
         gpj[2 * p] = gp0.x;
@@ -969,15 +1024,22 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (bwd_min_blocks<KS, NP>()))
         for (int j = 0; j < VT; ++j)
 #pragma unroll
             for (int q = 0; q < 6; ++q) vg[(id0 + j) * 6 + q] = (double)gr[j][q];
-        __syncthreads();
+        step_sync<CL>();  // CL: a lane's later vehicles sit in the next CTAs' vg
 #pragma unroll
         for (int j = 0; j < VT; ++j) {
             const int li = id0 + j;
-            if (!val[j] || !(li == 0 || a.lead[base + li - 1] == 0)) continue;  // lane starts
+            if (!val[j] || (li == 0 && peer_follow) || !(li == 0 || a.lead[base + li - 1] == 0))
+                continue;  // lane starts (a lane split over CTAs is summed by its first one)
             double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             for (int ee = li;; ++ee) {  // the lane's vehicles up to its head (no leader)
+                if (!CL || ee < kCap) {
 #pragma unroll
-                for (int q = 0; q < 6; ++q) acc[q] += vg[ee * 6 + q];
+                    for (int q = 0; q < 6; ++q) acc[q] += vg[ee * 6 + q];
+                } else {  // the lane continues in cluster CTA crank + ee / kCap
+#pragma unroll
+                    for (int q = 0; q < 6; ++q)
+                        acc[q] += ld_peer(vg + (ee % kCap) * 6 + q, crank + ee / kCap);
+                }
                 if (a.lead[base + ee] == 0) break;
             }
             // lane index: the last l with lane_offsets[l] <= i (empty lanes skipped)
@@ -993,6 +1055,7 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (bwd_min_blocks<KS, NP>()))
         }
     }
     if (OBS && a.loss_partials) block_sum_to<kTb>(lacc, a.loss_partials + tile);  // Eq. 4 here
+    if (CL) cluster_sync_all();  // no CTA leaves while a peer may still read its shared memory
 }
 
 // ------------------------------------------------------------------------------ NK2
@@ -1154,42 +1217,79 @@ cudaError_t launch_validate(const ValidateArgs& a, cudaStream_t st) {
 
 bool ckpt_supported(int k) { return k == 2 || k == 4 || k == 8; }
 
-template <bool D4, bool KH, int KS>
-static void launch_fwd_k(const FwdArgs& a, int ntiles, const FwdVariant& var, cudaStream_t st) {
-    dim3 g(ntiles), b(kCap / (2 * IDM_FWD_NP));
-    const dim3 b_api(kCap / (2 * IDM_FWD_NP_API));  // idm_forward with history
+// One launch: plain <<<>>> unless it needs attributes -- a thread-block cluster of csize CTAs
+// (lanes longer than a tile) and / or programmatic stream serialization (the fused backward).
+template <class A>
+static cudaError_t launch_cfg(void (*kern)(A), const A& a, int grid, int block, size_t smem,
+                              cudaStream_t st, int csize, bool pdl) {
+    if (csize <= 1 && !pdl) {
+        kern<<<grid, block, smem, st>>>(a);
+        return cudaSuccess;  // launch errors: cudaGetLastError in the caller
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (csize > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = (unsigned)csize;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+template <bool D4, bool KH, int KS, bool CL>
+static cudaError_t launch_fwd_k(const FwdArgs& a, int ntiles, const FwdVariant& var,
+                                cudaStream_t st) {
+    const int b = kCap / (2 * IDM_FWD_NP);
+    const int b_api = kCap / (2 * IDM_FWD_NP_API);  // idm_forward with history
+    const int cs = CL ? var.csize : 1;
     if constexpr (KS == 4) {  // the fused idm_fit_step forward exists for 4-step segments
-        if (var.loss == 1) { fwd_kernel<D4, KH, false, 1, KS><<<g, b, 0, st>>>(a); return; }
-        if (var.loss == 2) { fwd_kernel<D4, KH, false, 2, KS><<<g, b, 0, st>>>(a); return; }
-        if (var.loss == 3) { fwd_kernel<D4, KH, false, 3, KS><<<g, b, 0, st>>>(a); return; }
+        if (var.loss == 1) return launch_cfg(fwd_kernel<D4, KH, false, 1, KS, true, CL>, a, ntiles, b, 0, st, cs, false);
+        if (var.loss == 2) return launch_cfg(fwd_kernel<D4, KH, false, 2, KS, true, CL>, a, ntiles, b, 0, st, cs, false);
+        if (var.loss == 3) return launch_cfg(fwd_kernel<D4, KH, false, 3, KS, true, CL>, a, ntiles, b, 0, st, cs, false);
     }
     if (!var.hist) {  // prediction rollout: P rows only (the segment length is immaterial)
-        if (var.rec_v) fwd_kernel<D4, KH, true, 0, 4, false><<<g, b, 0, st>>>(a);
-        else fwd_kernel<D4, KH, false, 0, 4, false><<<g, b, 0, st>>>(a);
-        return;
+        if (var.rec_v) return launch_cfg(fwd_kernel<D4, KH, true, 0, 4, false, CL>, a, ntiles, b, 0, st, cs, false);
+        return launch_cfg(fwd_kernel<D4, KH, false, 0, 4, false, CL>, a, ntiles, b, 0, st, cs, false);
     }
-    if (var.rec_v) fwd_kernel<D4, KH, true, 0, KS><<<g, b_api, 0, st>>>(a);
-    else fwd_kernel<D4, KH, false, 0, KS><<<g, b_api, 0, st>>>(a);
+    if (var.rec_v) return launch_cfg(fwd_kernel<D4, KH, true, 0, KS, true, CL>, a, ntiles, b_api, 0, st, cs, false);
+    return launch_cfg(fwd_kernel<D4, KH, false, 0, KS, true, CL>, a, ntiles, b_api, 0, st, cs, false);
 }
 
 template <bool D4, bool KH>
-static void launch_fwd_dk(const FwdArgs& a, int ntiles, const FwdVariant& var, cudaStream_t st) {
+static cudaError_t launch_fwd_dk(const FwdArgs& a, int ntiles, const FwdVariant& var,
+                                 cudaStream_t st) {
+    if (var.csize > 1)  // lanes split over clusters: 4-step segments only (idm_init checks)
+        return a.ckpt_every == 4 ? launch_fwd_k<D4, KH, 4, true>(a, ntiles, var, st)
+                                 : cudaErrorInvalidValue;
     switch (a.ckpt_every) {
-        case 2: launch_fwd_k<D4, KH, 2>(a, ntiles, var, st); break;
-        case 8: launch_fwd_k<D4, KH, 8>(a, ntiles, var, st); break;
-        default: launch_fwd_k<D4, KH, 4>(a, ntiles, var, st); break;
+        case 2: return launch_fwd_k<D4, KH, 2, false>(a, ntiles, var, st);
+        case 8: return launch_fwd_k<D4, KH, 8, false>(a, ntiles, var, st);
+        default: return launch_fwd_k<D4, KH, 4, false>(a, ntiles, var, st);
     }
 }
 
 cudaError_t launch_fwd(const FwdArgs& a, int ntiles, const FwdVariant& var, cudaStream_t st) {
     if (!ckpt_supported(a.ckpt_every)) return cudaErrorInvalidValue;
-    if (var.delta4) {
-        if (var.kahan) launch_fwd_dk<true, true>(a, ntiles, var, st);
-        else launch_fwd_dk<true, false>(a, ntiles, var, st);
-    } else {
-        if (var.kahan) launch_fwd_dk<false, true>(a, ntiles, var, st);
-        else launch_fwd_dk<false, false>(a, ntiles, var, st);
-    }
+    cudaError_t e;
+    if (var.delta4) e = var.kahan ? launch_fwd_dk<true, true>(a, ntiles, var, st)
+                                  : launch_fwd_dk<true, false>(a, ntiles, var, st);
+    else e = var.kahan ? launch_fwd_dk<false, true>(a, ntiles, var, st)
+                       : launch_fwd_dk<false, false>(a, ntiles, var, st);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -1208,36 +1308,31 @@ constexpr size_t bwd_smem_of() {  // ring of NB: speed + checkpoint + dL/dP/obs 
 #ifndef IDM_BWD_NP
 #define IDM_BWD_NP 1  // vehicle pairs per backward thread (1: 256 threads, 2: 128 threads; 2 measured 3.7% slower)
 #endif
-template <bool D4, bool SH, bool AD, int KS, int GO, bool KH>
-static cudaError_t launch_bwd_v(const BwdArgs& a, int ntiles, cudaStream_t st,
-                                bool pdl = false) {
+template <bool D4, bool SH, bool AD, int KS, int GO, bool KH, bool CL = false>
+static cudaError_t launch_bwd_v(const BwdArgs& a, int ntiles, cudaStream_t st, bool pdl = false,
+                                int csize = 1) {
     constexpr int NP = IDM_BWD_NP;
     constexpr int kTb = kCap / (2 * NP);
     constexpr size_t smem = bwd_smem_of<KS, GO>();
     static std::atomic<unsigned long long> optin{0};  // devices opted in (bit per device)
     cudaError_t e =
-        smem_optin((const void*)bwd_kernel<D4, SH, AD, KS, GO, KH, NP>, (int)smem, optin);
+        smem_optin((const void*)bwd_kernel<D4, SH, AD, KS, GO, KH, CL, NP>, (int)smem, optin);
     if (e != cudaSuccess) return e;
-    if (!pdl) {
-        bwd_kernel<D4, SH, AD, KS, GO, KH, NP><<<ntiles, kTb, smem, st>>>(a);
-        return cudaSuccess;  // launch errors: cudaGetLastError in launch_bwd
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ntiles);
-    cfg.blockDim = dim3(kTb);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, bwd_kernel<D4, SH, AD, KS, GO, KH, NP>, a);
+    return launch_cfg(bwd_kernel<D4, SH, AD, KS, GO, KH, CL, NP>, a, ntiles, kTb, smem, st,
+                      CL ? csize : 1, pdl);
 }
 
 // API backward (idm_backward): dL/dP rows from grad_traj, Adam by its own kernel
 template <bool D4, int KS>
-static cudaError_t launch_bwd_k(const BwdArgs& a, int ntiles, bool shared, cudaStream_t st) {
+static cudaError_t launch_bwd_k(const BwdArgs& a, int ntiles, bool shared, cudaStream_t st,
+                                int csize) {
+    if constexpr (KS == 4) {
+        if (csize > 1) {
+            if (shared) return launch_bwd_v<D4, true, false, KS, 0, false, true>(a, ntiles, st, false, csize);
+            return launch_bwd_v<D4, false, false, KS, 0, false, true>(a, ntiles, st, false, csize);
+        }
+    }
+    if (csize > 1) return cudaErrorInvalidValue;
     if (shared) return launch_bwd_v<D4, true, false, KS, 0, false>(a, ntiles, st);
     return launch_bwd_v<D4, false, false, KS, 0, false>(a, ntiles, st);
 }
@@ -1245,38 +1340,42 @@ static cudaError_t launch_bwd_k(const BwdArgs& a, int ntiles, bool shared, cudaS
 // fused idm_fit_step backward (ckpt_every == 4): dL/dP from obs
 template <bool D4, int GO, bool KH>
 static cudaError_t launch_bwd_obs(const BwdArgs& a, int ntiles, bool shared, cudaStream_t st,
-                                  bool pdl) {
+                                  bool pdl, int csize) {
+    if (csize > 1) {  // no programmatic launch with clusters (idm_capi.cu use_pdl)
+        if (shared) return launch_bwd_v<D4, true, false, 4, GO, KH, true>(a, ntiles, st, false, csize);
+        return launch_bwd_v<D4, false, true, 4, GO, KH, true>(a, ntiles, st, false, csize);
+    }
     if (shared) return launch_bwd_v<D4, true, false, 4, GO, KH>(a, ntiles, st, pdl);
     return launch_bwd_v<D4, false, true, 4, GO, KH>(a, ntiles, st, pdl);
 }
 
 template <bool D4>
 static cudaError_t launch_bwd_d(const BwdArgs& a, int ntiles, bool shared, bool adam, int gobs,
-                                bool kahan, cudaStream_t st, bool pdl) {
+                                bool kahan, cudaStream_t st, bool pdl, int csize) {
     if (gobs) {
         if (a.ckpt_every != 4) return cudaErrorInvalidValue;
         if (gobs == 1)  // sign codes: no positions needed, compensation irrelevant
-            return launch_bwd_obs<D4, 1, false>(a, ntiles, shared, st, pdl);
+            return launch_bwd_obs<D4, 1, false>(a, ntiles, shared, st, pdl, csize);
         if (gobs == 3) {  // L1 re-derived from obs and the rebuilt positions
-            if (kahan) return launch_bwd_obs<D4, 3, true>(a, ntiles, shared, st, pdl);
-            return launch_bwd_obs<D4, 3, false>(a, ntiles, shared, st, pdl);
+            if (kahan) return launch_bwd_obs<D4, 3, true>(a, ntiles, shared, st, pdl, csize);
+            return launch_bwd_obs<D4, 3, false>(a, ntiles, shared, st, pdl, csize);
         }
-        if (kahan) return launch_bwd_obs<D4, 2, true>(a, ntiles, shared, st, pdl);
-        return launch_bwd_obs<D4, 2, false>(a, ntiles, shared, st, pdl);
+        if (kahan) return launch_bwd_obs<D4, 2, true>(a, ntiles, shared, st, pdl, csize);
+        return launch_bwd_obs<D4, 2, false>(a, ntiles, shared, st, pdl, csize);
     }
     if (pdl || adam) return cudaErrorInvalidValue;  // API backward: after the loss kernel, no Adam
     switch (a.ckpt_every) {
-        case 2: return launch_bwd_k<D4, 2>(a, ntiles, shared, st);
-        case 4: return launch_bwd_k<D4, 4>(a, ntiles, shared, st);
-        case 8: return launch_bwd_k<D4, 8>(a, ntiles, shared, st);
+        case 2: return launch_bwd_k<D4, 2>(a, ntiles, shared, st, csize);
+        case 4: return launch_bwd_k<D4, 4>(a, ntiles, shared, st, csize);
+        case 8: return launch_bwd_k<D4, 8>(a, ntiles, shared, st, csize);
         default: return cudaErrorInvalidValue;
     }
 }
 
 cudaError_t launch_bwd(const BwdArgs& a, int ntiles, bool delta4, bool shared, bool adam,
-                       int gobs, bool kahan, cudaStream_t st, bool pdl) {
-    cudaError_t e = delta4 ? launch_bwd_d<true>(a, ntiles, shared, adam, gobs, kahan, st, pdl)
-                           : launch_bwd_d<false>(a, ntiles, shared, adam, gobs, kahan, st, pdl);
+                       int gobs, bool kahan, cudaStream_t st, bool pdl, int csize) {
+    cudaError_t e = delta4 ? launch_bwd_d<true>(a, ntiles, shared, adam, gobs, kahan, st, pdl, csize)
+                           : launch_bwd_d<false>(a, ntiles, shared, adam, gobs, kahan, st, pdl, csize);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

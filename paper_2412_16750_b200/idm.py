@@ -148,6 +148,8 @@ def load_library(path: str | None = None):
     L.idm_launch_count.argtypes = [vp]
     L.idm_max_lane_vehicles.restype = i32
     L.idm_max_lane_vehicles.argtypes = []
+    L.idm_max_lane_length.restype = i32
+    L.idm_max_lane_length.argtypes = []
     L.idm_last_error.restype = C.c_char_p
     L.idm_last_error.argtypes = [vp]
     L.idm_destroy.restype = None
@@ -502,7 +504,8 @@ def idm_plan_tiles(lane_offsets) -> "np.ndarray":
     n_lanes, n = len(off) - 1, int(off[-1])
     nt = lib.idm_plan_tiles(off.ctypes.data, n_lanes, n, None)
     if nt < 0:
-        raise IdmError(IDM_EINVAL, "malformed lane offsets or a lane longer than a tile")
+        raise IdmError(IDM_EINVAL, "malformed lane offsets or a lane longer than "
+                                   "idm_max_lane_length()")
     out = np.zeros(nt + 1, np.int64)
     lib.idm_plan_tiles(off.ctypes.data, n_lanes, n, out.ctypes.data)
     return out

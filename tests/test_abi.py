@@ -115,7 +115,47 @@ def test_tile_plan_properties(lib):
             cur += int(b - a)
         expect.append(n)
         assert tiles.tolist() == expect
+    mx = lib.idm_max_lane_length()
+    assert mx == 8 * cap
     with pytest.raises(idm.IdmError):
-        idm.idm_plan_tiles([0, cap + 1])
+        idm.idm_plan_tiles([0, mx + 1])
     with pytest.raises(idm.IdmError):
         idm.idm_plan_tiles([0, 5, 3])
+
+
+def test_tile_plan_long_lanes(lib):
+    """Lanes longer than a tile (up to idm_max_lane_length()) run over thread-block clusters of
+    cs = ceil(longest / cap) consecutive tiles: every such lane starts at a tile index that is a
+    multiple of cs and fills full tiles of cap vehicles (the last one the remainder, then empty
+    padding tiles); short lanes still pack greedily into whole-lane tiles; the tile count is a
+    multiple of cs; every vehicle is in exactly one tile."""
+    import numpy as np
+    from paper_2412_16750_b200 import idm
+    cap = lib.idm_max_lane_vehicles()
+    for sizes in ([cap + 1], [3, 2 * cap + 5, 7, 0, 100, 3 * cap, 1, cap, 40],
+                  [5] * 300 + [8 * cap] + [5] * 300, [cap + 1, cap + 1, 1]):
+        off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+        tiles = idm.idm_plan_tiles(off)
+        n = int(off[-1])
+        lens = np.diff(tiles)
+        cs = max(1, -(-max(sizes) // cap))
+        assert tiles[0] == 0 and tiles[-1] == n and np.all(lens >= 0) and np.all(lens <= cap)
+        assert len(lens) % cs == 0
+        for a, b in zip(off[:-1], off[1:]):
+            a, b = int(a), int(b)
+            if b - a <= cap:
+                if b > a:  # whole lane inside one tile
+                    t = np.searchsorted(tiles, a, side="right") - 1
+                    assert tiles[t] <= a and b <= tiles[t + 1]
+                continue
+            t = int(np.where(tiles[:-1] == a)[0][-1])  # the first tile of the lane (after pads)
+            assert t % cs == 0
+            nfull = (b - a) // cap
+            for c in range(cs):
+                lo, hi = tiles[t + c], tiles[t + c + 1]
+                if c < nfull:
+                    assert (lo, hi) == (a + c * cap, a + (c + 1) * cap)
+                elif c == nfull:
+                    assert (lo, hi) == (a + c * cap, b)
+                else:
+                    assert lo == hi == b

@@ -483,8 +483,8 @@ def test_error_paths(idm):
     with pytest.raises(idm.IdmError) as e:
         idm.from_workload(w, bad, max_steps=w.K)
     assert e.value.code == idm.IDM_EINVAL
-    cap = idm.load_library().idm_max_lane_vehicles()
-    w2 = synth.make_workload("C1", lane_sizes=[cap + 1], K=5)
+    mx = idm.load_library().idm_max_lane_length()
+    w2 = synth.make_workload("C1", lane_sizes=[mx + 1], K=5)
     with pytest.raises(idm.IdmError) as e:
         idm.from_workload(w2, None, max_steps=5)
     assert e.value.code == idm.IDM_EINVAL
@@ -1199,3 +1199,85 @@ def test_state_from_obs_matches_oracle(idm):
     assert state_violation(p0.cpu().numpy(), np.array(po)) <= 1.0
     assert state_violation(v0.cpu().numpy(), np.array(vo)) <= 1.0
     assert np.all(v0.cpu().numpy() >= 0) and np.all(p0.cpu().numpy()[:5] == 0)
+
+
+# ------------------------------------------------- lanes longer than a tile (clusters)
+LONG_LANES = [40, 513, 7, 1100, 100, 0, 2048, 3, 1, 700]
+
+
+def test_long_lanes_forward_and_gradients(idm, oracle):
+    """Lanes longer than one tile (513 ... 2,048 vehicles, mixed with short and empty lanes) run
+    over thread-block clusters, the boundary vehicles' leader speeds and adjoint terms crossing
+    CTAs through distributed shared memory: states at every step, parameter and state gradients
+    against the fp64 oracle (L1 with the sign protocol), the prediction rollout equal to the
+    recorded one bit for bit."""
+    w = synth.make_workload("C2", lane_sizes=LONG_LANES, K=90, seed=61)
+    obs = oracle_truth_obs(oracle, w)
+    prm = synth.init_params(w.n)
+    r = run_gpu(idm, w, prm, w.K, obs, "l1")
+    P, V = oracle.rollout(oracle.leader_from_lanes(w.lane_offsets), w.length, w.p0, w.v0,
+                          prm.astype(np.float64), w.K)
+    assert state_violation(r["P"], P) <= 1.0
+    assert state_violation(r["V"], V) <= 1.0
+    _, _, _, g = oracle_grads(oracle, w, prm.astype(np.float64), w.K, obs, "l1", r["grad_traj"])
+    worst, plain = grad_check(r["g_params"], g["g_params"], g["g_abs"])
+    print(f"long lanes: param grad worst/tol = {worst:.3f}, plain pass = {plain:.5f}")
+    assert worst <= 1.0
+    assert state_grad_check(r["g_state0"], g, label="long lanes l1") <= 1.0
+    b = idm.from_workload(w, prm, max_steps=w.K, record_velocity=True)
+    b.forward(w.K, history=False)
+    torch.cuda.synchronize()
+    assert np.array_equal(b.traj.cpu().numpy(), r["P"])
+
+
+@pytest.mark.parametrize("kind", ["l1", "l2"])
+def test_long_lanes_fit_step_equals_separate_calls(idm, kind):
+    """The fused iteration over clusters (fused forward with sign codes / the observation-
+    deriving backward with Adam, no programmatic launch) equals the separate calls bit for bit,
+    with missing observations and a partial last segment."""
+    w = synth.make_workload("C2", lane_sizes=LONG_LANES, K=62, seed=62)
+    obs = synth.kinematic_obs(w)
+    obs[np.random.default_rng(62).random(obs.shape) < 0.2] = np.nan
+    o = torch.as_tensor(obs, device="cuda")
+    a = idm.from_workload(w, None, max_steps=w.K)
+    b = idm.from_workload(w, None, max_steps=w.K)
+    for it in range(3):
+        a.forward(w.K)
+        La = a.loss_grad(o, kind=kind)
+        a.backward()
+        gsa = a.grad_state0.clone()
+        ga = a.grad_params.clone()
+        a.adam_step(it)
+        Lb = b.fit_step(o, kind=kind, iteration=it, sync=True)
+        torch.cuda.synchronize()
+        assert abs(La - Lb) <= 1e-6 * abs(La)
+        assert_fit_grads(ga, b.grad_params)
+        assert torch.equal(gsa, b.grad_state0)
+        assert torch.equal(a.params, b.params)
+    with pytest.raises(idm.IdmError):  # the on-chip whole fit keeps lanes inside one tile
+        a.fit(o, iters=2, steps=10)
+
+
+def test_long_lanes_shared_rows(idm, oracle):
+    """Shared mode with lanes over clusters: each long lane's row (summed by its first CTA over
+    the peers' shared memory in vehicle order) is that lane's shared-mode gradient."""
+    sizes = [600, 30, 1500, 0, 5]
+    w = synth.make_workload("C2", lane_sizes=sizes, K=40, seed=63)
+    obs = oracle_truth_obs(oracle, w)
+    prm = np.array([8.0, 1.7, 3.0, 1.4, 33.0, 4.0], np.float32)
+    sim = idm.from_workload(w, prm, max_steps=w.K, shared_params=True)
+    sim.forward(w.K)
+    sim.loss_grad(torch.as_tensor(obs, device="cuda"), kind="l2")
+    sim.backward()
+    torch.cuda.synchronize()
+    rows = sim.lane_grads.cpu().numpy()
+    assert not rows[3].any()
+    for l in (0, 1, 2, 4):
+        sub = synth.lane_subset(w, [l])
+        vi = sub.meta["vehicle_index"]
+        h = oracle.leader_from_lanes(sub.lane_offsets)
+        P, V = oracle.rollout(h, sub.length, sub.p0, sub.v0, prm.astype(np.float64), w.K)
+        _, gP = oracle.loss(P, obs[:, vi], "l2")
+        g = oracle.backward(h, sub.length, prm.astype(np.float64), P, V, gP)
+        worst, _ = grad_check(rows[l], g["g_params"][:, 0], g["g_abs"][:, 0])
+        assert worst <= 1.0, l
