@@ -373,6 +373,8 @@ CONFIG_DESC = {
     "C4": WORKLOAD_DESC,
     "C5": "C5: Waymo-shaped, 100k scenes x 4-12 lanes x 1+Bin(7,0.2) vehicles (~1.9M), K=10 "
           "history fit",
+    "C4L": "C4L (not a BASELINE config): 2,000 lanes x 1,000 vehicles = 2M, K=300 -- lanes "
+           "longer than a tile, each over a 2-CTA thread-block cluster",
 }
 
 
@@ -726,7 +728,7 @@ def main():
                     help="seconds of oracle work for --impl reference")
     ap.add_argument("--leader", choices=["lane", "virtual"], default="lane",
                     help="lane leader (default) or the paper's virtual-leader fit (PAPER.md:208)")
-    ap.add_argument("--config", choices=["C1", "C2", "C3", "C4", "C5"], default="C4",
+    ap.add_argument("--config", choices=["C1", "C2", "C3", "C4", "C5", "C4L"], default="C4",
                     help="BASELINE.json configuration (C4 = the headline)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
                     help="N > 1: strong (default; the 2M vehicles split over the ranks) or weak")

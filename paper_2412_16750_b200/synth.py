@@ -52,6 +52,9 @@ CONFIGS = {
     "C3": dict(lanes=6, per_lane=333, K=27000, seed=3),
     "C4": dict(lanes=20000, per_lane=100, K=300, seed=4),
     "C5": dict(scenes=100000, K=10, seed=5),
+    # not a BASELINE.json config: C4's 2M vehicles in 2,000 lanes of 1,000 (each over a 2-CTA
+    # thread-block cluster), to measure the long-lane path against C4's whole-lane tiles
+    "C4L": dict(lanes=2000, per_lane=1000, K=300, seed=4),
 }
 
 
