@@ -116,9 +116,12 @@ int64_t max_tiles_for(const idm_desc* d) {
 // to cs), and no other lane shares its tiles; the tile count is padded to a multiple of cs.
 // Every launch of such a plan uses clusters of cs CTAs (csize_out; 1 = no long lane).  Fills
 // tile starts and leader flags (if given); returns the tile count, or -1 with *err set.
+// chunk (a multiple of 4, <= kCap): lanes longer than chunk are split into tiles of chunk
+// vehicles (kCap: only lanes that do not fit a tile; smaller: latency-bound shapes spread over
+// more SMs, see split_chunk_for).
 int64_t plan_tiles(const std::vector<int32_t>& off, int32_t n_lanes, int64_t n,
                    std::vector<int64_t>* tiles, std::vector<uint8_t>* lead, std::string* err,
-                   int* csize_out = nullptr) {
+                   int* csize_out = nullptr, int64_t chunk = kCap) {
     char buf[256];
     if (off[0] != 0 || off.back() != n) {
         std::snprintf(buf, sizeof buf, "lane_offsets must start at 0 and end at N=%lld (got %d..%d)",
@@ -134,17 +137,17 @@ int64_t plan_tiles(const std::vector<int32_t>& off, int32_t n_lanes, int64_t n,
             *err = buf;
             return -1;
         }
-        if (b - a > kMaxCluster * kCap) {
+        if (b - a > kMaxCluster * chunk) {
             std::snprintf(buf, sizeof buf,
-                          "lane %d has %lld vehicles; at most %d per lane are supported (%d "
-                          "tiles of %d in one thread-block cluster)", l, (long long)(b - a),
-                          kMaxCluster * kCap, kMaxCluster, kCap);
+                          "lane %d has %lld vehicles; at most %lld per lane are supported (%d "
+                          "tiles of %lld in one thread-block cluster)", l, (long long)(b - a),
+                          (long long)(kMaxCluster * chunk), kMaxCluster, (long long)chunk);
             *err = buf;
             return -1;
         }
         longest = b - a > longest ? b - a : longest;
     }
-    const int cs = longest > kCap ? (int)((longest + kCap - 1) / kCap) : 1;
+    const int cs = longest > chunk ? (int)((longest + chunk - 1) / chunk) : 1;
     if (csize_out) *csize_out = cs;
     std::vector<int64_t> t(1, 0);  // tile starts; the last entry is the open tile
     int64_t cur = 0;               // vehicles in the open tile
@@ -152,10 +155,10 @@ int64_t plan_tiles(const std::vector<int32_t>& off, int32_t n_lanes, int64_t n,
         const int64_t a = off[l], b = off[l + 1];
         const int64_t sz = b - a;
         if (sz == 0) continue;
-        if (sz > kCap) {  // a cluster of its own, starting at a multiple of cs
+        if (sz > chunk) {  // a cluster of its own, starting at a multiple of cs
             if (cur > 0) t.push_back(a);
             while ((t.size() - 1) % (size_t)cs != 0) t.push_back(a);  // empty tiles [a, a)
-            for (int c = 1; c < cs; ++c) t.push_back(a + c * (int64_t)kCap < b ? a + c * (int64_t)kCap : b);
+            for (int c = 1; c < cs; ++c) t.push_back(a + c * chunk < b ? a + c * chunk : b);
             cur = kCap;  // closed: the next lane opens a new tile
         } else {
             if (cur + sz > kCap) {
@@ -174,6 +177,35 @@ int64_t plan_tiles(const std::vector<int32_t>& off, int32_t n_lanes, int64_t n,
     return count;
 }
 
+// Split chunk of the lane plan.  A latency-bound shape -- few tiles and a long horizon, e.g.
+// C3's 6 lanes of 333 vehicles over 27,000 steps on 148 SMs -- steps at the pace of one CTA's
+// per-step chain, so its lanes can be spread over thread-block clusters of smaller tiles
+// (IDM_SPLIT_LANES=auto | <vehicles per tile> | 0 = off, the default).
+int64_t split_chunk_for(const std::vector<int32_t>& off, int32_t n_lanes, int64_t n,
+                        int32_t max_steps, int num_sms) {
+    const char* e = std::getenv("IDM_SPLIT_LANES");
+    if (!e || e[0] == '0' || e[0] == 0) return kCap;
+    int64_t longest = 0;
+    for (int32_t l = 0; l < n_lanes; ++l)
+        longest = off[l + 1] - off[l] > longest ? off[l + 1] - off[l] : longest;
+    int64_t chunk;
+    if (std::strcmp(e, "auto") == 0) {
+        std::string err;
+        const int64_t nt = plan_tiles(off, n_lanes, n, nullptr, nullptr, &err);
+        if (nt < 0 || 4 * nt > num_sms || max_steps < 1000 || longest <= 8) return kCap;
+        int64_t c = num_sms / nt;
+        c = c > kMaxCluster ? kMaxCluster : (c < 1 ? 1 : c);
+        chunk = (longest + c - 1) / c;
+    } else {
+        chunk = std::atoll(e);
+    }
+    chunk = (chunk + 3) / 4 * 4;  // tiles of a split lane hold a multiple of 4 vehicles
+    if (chunk < 4) chunk = 4;
+    if (chunk > kCap) chunk = kCap;
+    if (longest > kMaxCluster * chunk) chunk = kCap;  // the lane would need a larger cluster
+    return chunk;
+}
+
 // Tile count of the descriptor's lane plan (reads lane_offsets), or the bound if unreadable.
 int64_t tiles_of(const idm_desc* d) {
     if (!d || !d->lane_offsets || d->n_lanes < 1) return -1;
@@ -185,7 +217,12 @@ int64_t tiles_of(const idm_desc* d) {
         return -1;
     }
     std::string err;
-    return plan_tiles(off, d->n_lanes, d->n_vehicles, nullptr, nullptr, &err);
+    int num_sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaGetLastError();
+    return plan_tiles(off, d->n_lanes, d->n_vehicles, nullptr, nullptr, &err, nullptr,
+                      split_chunk_for(off, d->n_lanes, d->n_vehicles, d->max_steps, num_sms));
 }
 
 // ntiles: the plan's tile count (< 0: size for the bound max_tiles_for)
@@ -514,7 +551,14 @@ int idm_init(idm_handle** out, const idm_desc* d) {
                 break;
             }
             std::string perr;
-            nt = plan_tiles(off, d->n_lanes, d->n_vehicles, &tiles, &lead, &perr, &h->csize);
+            int num_sms = 148, dv = 0;
+            if (cudaGetDevice(&dv) == cudaSuccess)
+                cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dv);
+            cudaGetLastError();
+            const int64_t chunk =
+                split_chunk_for(off, d->n_lanes, d->n_vehicles, d->max_steps, num_sms);
+            nt = plan_tiles(off, d->n_lanes, d->n_vehicles, &tiles, &lead, &perr, &h->csize,
+                            chunk);
             if (nt < 0) {
                 bail(fail(h, IDM_EINVAL, "%s", perr.c_str()));
                 break;
@@ -528,7 +572,7 @@ int idm_init(idm_handle** out, const idm_desc* d) {
             tiles = {0, d->n_vehicles};
             h->csize = 1;
         }
-        if (nt > max_tiles_for(d) || !layout_for(d, nt, &L)) {
+        if (!layout_for(d, nt, &L)) {
             bail(fail(h, IDM_EINVAL, "internal: tile plan exceeds bound"));
             break;
         }

@@ -308,10 +308,11 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (fwd_min_blocks<CK, LOSS, NP>
 #pragma unroll
     for (int j = 0; j < VT; ++j) val[j] = id0 + j < n_loc;
     if (LOSS && a.tile_ready) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    // CL: this tile's last vehicle has a leader, the next cluster CTA's first vehicle (a full
-    // tile of a lane longer than a tile)
+    // CL: this tile's last vehicle has a leader, the next cluster CTA's first vehicle (a lane
+    // split over a cluster; the planner keeps such tiles a multiple of 4 vehicles, so the last
+    // vehicle is the last one of thread n_loc / VT - 1)
     const unsigned crank = CL ? cluster_rank() : 0u;
-    const bool peer_lead = CL && n_loc == kCap && a.lead[base + kCap - 1] != 0;
+    const bool peer_lead = CL && n_loc > 0 && n_loc % VT == 0 && a.lead[base + n_loc - 1] != 0;
 
     auto put = [&](float* row, const float2 (&x)[NP]) {  // row points at local vehicle VT tid
 #pragma unroll
@@ -493,7 +494,7 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (fwd_min_blocks<CK, LOSS, NP>
         xv[par][tid] = v[0].x;
         step_sync<CL>();
         float nb = xv[par][tid + 1];  // the next thread's first vehicle ([kTf]: sentinel 0)
-        if (CL && peer_lead && tid == kTf - 1) nb = ld_peer(&xv[par][0], crank + 1);
+        if (CL && peer_lead && tid == n_loc / VT - 1) nb = ld_peer(&xv[par][0], crank + 1);
         float2 vl[NP];
 #pragma unroll
         for (int p = 0; p < NP; ++p)
@@ -686,8 +687,10 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (bwd_min_blocks<KS, NP>()))
     // CL (a lane longer than a tile over a cluster): the last vehicle's leader is the next CTA's
     // first vehicle; the first vehicle's follower is the previous CTA's last vehicle
     const unsigned crank = CL ? cluster_rank() : 0u;
-    const bool peer_lead = CL && n_loc == kCap && a.lead[base + kCap - 1] != 0;
+    const bool peer_lead = CL && n_loc > 0 && n_loc % VT == 0 && a.lead[base + n_loc - 1] != 0;
     const bool peer_follow = CL && base > 0 && n_loc > 0 && a.lead[base - 1] != 0;
+    // the previous CTA's last vehicle writes its term to its fx[par][n_prev / VT]
+    const int pslot = peer_follow ? (int)(base - a.tile_start[tile - 1]) / VT : 0;
     const int nseg = (steps + KS - 1) / KS;
     const int tail = steps - (nseg - 1) * KS;  // length of the last segment (1..KS)
 
@@ -834,7 +837,7 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (bwd_min_blocks<KS, NP>()))
                     // the leader of the pair's second vehicle: the next pair's first, or the
                     // next thread's first vehicle (slot kCap: the 0 sentinel)
                     float nb = vr[tt * VP + 2 * p + 2];  // slot kCap: the sentinel 0
-                    if (CL && p == NP - 1 && peer_lead && tid == kTb - 1)
+                    if (CL && p == NP - 1 && peer_lead && tid == n_loc / VT - 1)
                         nb = ld_peer(vrow + (b * KS + tt) * VP, crank + 1);
                     vl[tt][p] = make_float2(v[tt][p].y, nb);
                 } else {
@@ -942,7 +945,7 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (bwd_min_blocks<KS, NP>()))
                 step_sync<CL>();
                 // F of the first vehicle's follower: thread t - 1's last vehicle
                 float ff = fx[par][tid];
-                if (CL && peer_follow && tid == 0) ff = ld_peer(&fx[par][kTb], crank - 1);
+                if (CL && peer_follow && tid == 0) ff = ld_peer(&fx[par][pslot], crank - 1);
                 u[0] = vadd(u[0], make_float2(ff, F[0].x));
                 par ^= 1;
             }
@@ -959,7 +962,7 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (bwd_min_blocks<KS, NP>()))
     fx[par][tid + 1] = m[NP - 1].y;
     step_sync<CL>();
     float mpeer = fx[par][tid];
-    if (CL && peer_follow && tid == 0) mpeer = ld_peer(&fx[par][kTb], crank - 1);
+    if (CL && peer_follow && tid == 0) mpeer = ld_peer(&fx[par][pslot], crank - 1);
     float gpj[VT], lvj[VT], Sj[6][VT];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
@@ -1031,16 +1034,23 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (bwd_min_blocks<KS, NP>()))
             if (!val[j] || (li == 0 && peer_follow) || !(li == 0 || a.lead[base + li - 1] == 0))
                 continue;  // lane starts (a lane split over CTAs is summed by its first one)
             double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            for (int ee = li;; ++ee) {  // the lane's vehicles up to its head (no leader)
-                if (!CL || ee < kCap) {
-#pragma unroll
-                    for (int q = 0; q < 6; ++q) acc[q] += vg[ee * 6 + q];
-                } else {  // the lane continues in cluster CTA crank + ee / kCap
-#pragma unroll
-                    for (int q = 0; q < 6; ++q)
-                        acc[q] += ld_peer(vg + (ee % kCap) * 6 + q, crank + ee / kCap);
+            // the lane's vehicles up to its head (no leader); a lane split over a cluster
+            // continues in CTAs crank + c, whose vehicles start at tile_start[tile + c]
+            int c = 0, e = li, nc = n_loc;
+            for (int64_t gi = base + li;; ++gi, ++e) {
+                if (CL && e == nc) {
+                    ++c;
+                    e = 0;
+                    nc = (int)(a.tile_start[tile + c + 1] - a.tile_start[tile + c]);
                 }
-                if (a.lead[base + ee] == 0) break;
+                if (!CL || c == 0) {
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) acc[q] += vg[e * 6 + q];
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) acc[q] += ld_peer(vg + e * 6 + q, crank + c);
+                }
+                if (a.lead[gi] == 0) break;
             }
             // lane index: the last l with lane_offsets[l] <= i (empty lanes skipped)
             const int64_t gi = base + li;

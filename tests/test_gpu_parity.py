@@ -1281,3 +1281,29 @@ def test_long_lanes_shared_rows(idm, oracle):
         g = oracle.backward(h, sub.length, prm.astype(np.float64), P, V, gP)
         worst, _ = grad_check(rows[l], g["g_params"][:, 0], g["g_abs"][:, 0])
         assert worst <= 1.0, l
+
+
+@pytest.mark.parametrize("chunk", ["44", "auto", "100"])
+def test_split_lanes_equal_whole_lanes(idm, monkeypatch, chunk):
+    """Latency-bound shapes may spread each lane over a thread-block cluster of smaller tiles
+    (IDM_SPLIT_LANES): the per-vehicle arithmetic is unchanged, so the forward, the adjoint and
+    the fused iteration give the whole-lane tiles' results bit for bit (C3-shaped, 6 x 333
+    vehicles, 1,200 steps with compensated displacement)."""
+    w = synth.make_workload("C3", lane_sizes=[333] * 6, K=1200, seed=3)
+    obs = synth.kinematic_obs(w)
+    obs[np.random.default_rng(3).random(obs.shape) < 0.1] = np.nan
+    o = torch.as_tensor(obs, device="cuda")
+    runs = []
+    for split in ("0", chunk):
+        monkeypatch.setenv("IDM_SPLIT_LANES", split)
+        a = idm.from_workload(w, w.theta_true, max_steps=w.K, record_velocity=True)
+        a.forward(w.K)
+        a.loss_grad(o, kind="l1")
+        a.backward()
+        b = idm.from_workload(w, None, max_steps=w.K)
+        b.fit_step(o, kind="l2", iteration=0, sync=True)
+        torch.cuda.synchronize()
+        runs.append([t.clone() for t in (a.traj, a.vel_traj, a.grad_params, a.grad_state0,
+                                         b.params, b.grad_params, b.grad_state0)])
+    for x, y in zip(*runs):
+        assert torch.equal(x, y)
