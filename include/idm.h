@@ -242,19 +242,24 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
                  int32_t kind, int32_t iter, int32_t total_iters, float lr0, float lr1,
                  double* loss_dev, double* loss_host);
 
-/* Whole fit in one launch for short horizons (Waymo-shaped prediction histories of 10 steps,
-   PAPER.md:218, :329-331): iterations iter0 .. iter0+iters-1 of exactly idm_fit_step(steps,
-   obs, kind, it, total_iters, lr0, lr1) -- parameters, Adam moments and gradients (incl. the
-   zero delta row of a frozen delta) come out bit-identical -- with the state history, observations and Adam moments of each lane tile
-   kept on chip (no HBM traffic between iterations).  steps <= idm_fit_max_steps(); lane-leader
-   mode with per-vehicle parameters; iters <= 4096 per call; grad_traj is not written.  The
-   loss of the last iteration (same Eq. 4, summed in a different fixed order) goes to
-   *loss_dev / *loss_host. */
+/* Whole fit in one launch (NEXT-4): iterations iter0 .. iter0+iters-1 of exactly
+   idm_fit_step(steps, obs, kind, it, total_iters, lr0, lr1) -- parameters, Adam moments and
+   gradients (incl. the zero delta row of a frozen delta) come out bit-identical.  Lane tiles are
+   independent across iterations (tile j's next forward needs only the parameters its own
+   backward updated), so each CTA runs its tile's whole fit with no grid-wide synchronisation:
+     steps <= idm_fit_max_steps(): state history, observations and Adam moments on chip (Waymo-
+       shaped prediction histories of 10 steps);
+     longer horizons: per iteration the fused forward (Eq. 4 in-kernel) then the backward with
+       Adam, the state history through memory (written and re-read by the same CTA; needs
+       ckpt_every == 4).
+   Lane-leader mode with per-vehicle parameters and lanes within one tile; iters <= 4096 per
+   call; traj / grad_traj are not written.  The loss of the last iteration (same Eq. 4, summed in
+   a different fixed order) goes to *loss_dev / *loss_host. */
 int idm_fit(idm_handle* h, int32_t steps, const float* obs, int32_t kind, int32_t iter0,
             int32_t iters, int32_t total_iters, float lr0, float lr1, double* loss_dev,
             double* loss_host);
 
-/* Largest horizon idm_fit accepts. */
+/* Largest horizon of idm_fit's on-chip variant (longer ones run the long-horizon kernel). */
 int32_t idm_fit_max_steps(void);
 
 /* Iterations iter0 .. iter0+iters-1 of idm_fit_step(steps, obs, kind, it, total_iters, lr0, lr1)

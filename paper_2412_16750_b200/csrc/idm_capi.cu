@@ -1223,9 +1223,12 @@ int idm_fit(idm_handle* h, int32_t steps, const float* obs, int32_t kind, int32_
             double* loss_host) {
     if (!h) return IDM_EINVAL;
     OnDevice on_dev(h);
-    if (steps < 1 || steps > h->d.max_steps || steps > kFitMaxSteps)
-        return fail(h, IDM_EINVAL, "idm_fit: steps=%d outside [1, min(max_steps, %d)]", steps,
-                    kFitMaxSteps);
+    if (steps < 1 || steps > h->d.max_steps)
+        return fail(h, IDM_EINVAL, "idm_fit: steps=%d outside [1, max_steps=%d]", steps,
+                    h->d.max_steps);
+    const bool on_chip = steps <= kFitMaxSteps;  // else the long-horizon kernel (NEXT-4)
+    if (!on_chip && h->d.ckpt_every != 4)
+        return fail(h, IDM_EINVAL, "idm_fit beyond %d steps needs ckpt_every == 4", kFitMaxSteps);
     if (!obs) return fail(h, IDM_EINVAL, "obs is NULL");
     if (kind != IDM_LOSS_L1 && kind != IDM_LOSS_L2)
         return fail(h, IDM_EINVAL, "bad loss kind %d", kind);
@@ -1250,6 +1253,50 @@ int idm_fit(idm_handle* h, int32_t steps, const float* obs, int32_t kind, int32_
     CK(h, cudaMemcpyAsync(h->adam_table, h->adam_table_host, sizeof(float) * 2 * iters,
                           cudaMemcpyHostToDevice, h->st));
     AdamArgs ad = make_adam(h, iter0, total_iters, lr0, lr1);
+    if (!on_chip) {
+        // every iteration in one launch, each CTA its tile's whole fit (fit_long_kernel): the
+        // arguments of idm_fit_step's two kernels, without the programmatic handoff
+        FwdArgs f = fwd_args(h, steps);
+        f.obs = obs;
+        f.kind = kind;
+        f.loss_partials = h->loss_partials;
+        if (kind == IDM_LOSS_L1) {  // the forward's last CTA sums the last iteration's loss
+            f.loss_out = h->loss_scalar;
+            f.done_count = h->done_count;
+            f.n_tiles = h->ntiles;
+        }
+        BwdArgs b = bwd_args(h, steps);
+        b.obs = obs;
+        b.pos0 = h->d.pos0;
+        b.adam = ad;
+        if (kind == IDM_LOSS_L2) b.loss_partials = h->loss_partials;
+        FitLongArgs fl;
+        fl.iters = iters;
+        fl.adam_table = h->adam_table;
+        {
+            TimedLaunch tl(h, IDM_K_FWD);
+            CK(h, launch_fit_long(f, b, fl, h->ntiles, h->delta4, steps > 2000, kind, h->st));
+        }
+        h->launches++;
+        if (kind == IDM_LOSS_L2) {
+            TimedLaunch tl(h, IDM_K_REDUCE);
+            CK(h, launch_reduce(h->loss_partials, h->ntiles, 1, h->loss_scalar, nullptr, h->st));
+            h->launches++;
+        }
+        h->steps = steps;
+        h->stage = 0;
+        if (loss_dev)
+            CK(h, cudaMemcpyAsync(loss_dev, h->loss_scalar, sizeof(double),
+                                  cudaMemcpyDeviceToDevice, h->st));
+        if (loss_host) {
+            CK(h, cudaMemcpyAsync(&h->pinned[0], h->loss_scalar, sizeof(double),
+                                  cudaMemcpyDeviceToHost, h->st));
+            int st2 = sync_status(h);
+            *loss_host = h->pinned[0];
+            if (st2 != IDM_OK) return st2;
+        }
+        return IDM_OK;
+    }
     FitArgs a;
     a.tile_start = h->tile_start;
     a.lead = h->lead;

@@ -168,6 +168,12 @@ struct FitArgs {
     unsigned long long* status;
 };
 
+// every iteration of a long-horizon fit in one launch (fit_long_kernel)
+struct FitLongArgs {
+    int iters;
+    const float* adam_table;  // [iters][2] (step_size, sqrt_bc2) of each iteration
+};
+
 struct LossArgs {
     const float *traj, *obs;
     const uint8_t* mask;
@@ -201,6 +207,8 @@ cudaError_t launch_adam_free(float* x, const float* g, float* m, float* v, int64
                              const AdamArgs& hp, cudaStream_t st);
 int64_t vl_blocks(int64_t n);
 cudaError_t launch_fit(const FitArgs& a, int ntiles, bool delta4, int kind, cudaStream_t st);
+cudaError_t launch_fit_long(const FwdArgs& af, const BwdArgs& ab, const FitLongArgs& fl,
+                            int ntiles, bool delta4, bool kahan, int kind, cudaStream_t st);
 cudaError_t launch_state_from_obs(const float* obs, int64_t n, int steps, float dt, float* pos0,
                                   float* vel0, cudaStream_t st);
 

@@ -281,10 +281,10 @@ __device__ __forceinline__ void st_pairs(float2* p, const float2 (&x)[NP]) {
 }
 // HIST = false (LOSS = 0 only): a prediction rollout (idm_forward_ex IDM_FWD_NO_HISTORY) that
 // writes only the P rows -- no speed history or checkpoints, nothing for a backward.
-template <bool D4, bool KAHAN, bool RECV, int LOSS, int CK, bool HIST = true, bool CL = false,
-          int NP = (LOSS == 0 && HIST ? IDM_FWD_NP_API : IDM_FWD_NP)>
-__global__ void __launch_bounds__(kCap / (2 * NP), (fwd_min_blocks<CK, LOSS, NP>()))
-    fwd_kernel(FwdArgs a) {
+// The forward of lane tile a.tile0 + blockIdx.x (the body of fwd_kernel, and the forward phase
+// of fit_long_kernel).
+template <bool D4, bool KAHAN, bool RECV, int LOSS, int CK, bool HIST, bool CL, int NP>
+__device__ __forceinline__ void fwd_tile(FwdArgs a) {
     static_assert(HIST || LOSS == 0, "the fused forward always feeds a backward");
     constexpr int VT = 2 * NP;        // vehicles per thread
     constexpr int kTf = kCap / VT;    // threads per CTA
@@ -634,6 +634,13 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (fwd_min_blocks<CK, LOSS, NP>
     if (CL) cluster_sync_all();  // no CTA leaves while a peer may still read its shared memory
 }
 
+template <bool D4, bool KAHAN, bool RECV, int LOSS, int CK, bool HIST = true, bool CL = false,
+          int NP = (LOSS == 0 && HIST ? IDM_FWD_NP_API : IDM_FWD_NP)>
+__global__ void __launch_bounds__(kCap / (2 * NP), (fwd_min_blocks<CK, LOSS, NP>()))
+    fwd_kernel(FwdArgs a) {
+    fwd_tile<D4, KAHAN, RECV, LOSS, CK, HIST, CL, NP>(a);
+}
+
 // ------------------------------------------------------------------------------ NK3
 // Per CTA (lane tile), segments of KS steps from last to first.  Thread t owns VT = 2 NP
 // adjacent vehicles VT t .. VT t + VT - 1 as NP float2 lane pairs (packed f32x2 arithmetic;
@@ -666,9 +673,10 @@ template <int KS, int NP>
 constexpr int bwd_min_blocks() {
     return NP == 1 ? (KS <= 4 ? IDM_BWD_MINB : 1) : (KS <= 4 ? IDM_BWD_MINB2 : 1);
 }
+// The backward of lane tile a.tile0 + blockIdx.x (the body of bwd_kernel, and the backward phase
+// of fit_long_kernel).
 template <bool D4, bool SHARED, bool ADAM, int KS, int GOBS, bool KAHAN, bool CL, int NP>
-__global__ void __launch_bounds__(kCap / (2 * NP), (bwd_min_blocks<KS, NP>()))
-    bwd_kernel(BwdArgs a) {
+__device__ __forceinline__ void bwd_tile(BwdArgs a) {
     constexpr int VT = 2 * NP;          // vehicles per thread
     constexpr int kTb = kCap / VT;      // threads per CTA
     __shared__ float fx[2][kTb + 1];
@@ -1068,6 +1076,12 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (bwd_min_blocks<KS, NP>()))
     if (CL) cluster_sync_all();  // no CTA leaves while a peer may still read its shared memory
 }
 
+template <bool D4, bool SHARED, bool ADAM, int KS, int GOBS, bool KAHAN, bool CL, int NP>
+__global__ void __launch_bounds__(kCap / (2 * NP), (bwd_min_blocks<KS, NP>()))
+    bwd_kernel(BwdArgs a) {
+    bwd_tile<D4, SHARED, ADAM, KS, GOBS, KAHAN, CL, NP>(a);
+}
+
 // ------------------------------------------------------------------------------ NK2
 // Eq. 4 over the flat [(steps+1) * N] arrays.  Fixed grid + fixed per-thread element order +
 // fixed tree => bitwise deterministic partial sums.
@@ -1211,6 +1225,86 @@ __global__ void state_from_obs_kernel(const float* __restrict__ obs, int64_t n, 
     }
 }
 
+template <int KS, int GOBS>
+constexpr size_t bwd_smem_of() {  // ring of NB: speed + checkpoint + dL/dP/obs (or sign) rows
+    return (size_t)IDM_BWD_RING *
+           (KS * (kCap + 4) + kCkRows * kCap +
+            (GOBS == 1 ? kCap / 2 : (GOBS ? KS + 1 : KS) * kCap)) *
+           sizeof(float);
+}
+
+// ------------------------------------------------------------------------------ NK7
+// NEXT-4, any horizon: iterations it0 .. it0 + iters - 1 of the fused iteration in ONE launch.
+// Lane tiles are independent across iterations too -- tile j's next forward needs only tile
+// j's parameters, which its own backward's Adam epilogue wrote -- so each CTA runs its tile's
+// whole fit: fused forward (Eq. 4 in-kernel), then the backward with Adam, iters times, with
+// no grid-wide synchronisation.  The state history still goes through memory (K = 300 does not
+// fit on chip), but it is re-read by the same CTA right after it was
+// written, and the two resident CTAs of an SM drift into different phases, so the HBM-bound
+// forward of one overlaps the FP32-bound backward of the other.  Same device code and the same
+// per-vehicle order as idm_fit_step (fwd_tile / bwd_tile, one vehicle pair per thread in both):
+// parameters, moments and gradients are bit-identical to the loop of idm_fit_step calls.
+//   L1 (KIND 0): forward with sign codes (LOSS 1) -> backward from the codes (GOBS 1);
+//   L2 (KIND 1): history-only forward (LOSS 3) -> backward deriving Eq. 4 from obs (GOBS 2).
+// The Eq. 4 loss of the last iteration: L1 summed by the forward's last CTA, L2 as per-tile
+// partials from the backward (reduce_kernel after the launch).
+template <bool D4, bool KAHAN, int KIND>
+__global__ void __launch_bounds__(kT, 2) fit_long_kernel(FwdArgs af, BwdArgs ab, FitLongArgs fl) {
+    double* const loss_out = af.loss_out;
+    double* const bwd_partials = ab.loss_partials;
+    for (int it = 0; it < fl.iters; ++it) {
+        const bool last = it + 1 == fl.iters;
+        if (KIND == 0) {
+            af.loss_out = last ? loss_out : nullptr;  // the last CTA sums the last iteration's
+            fwd_tile<D4, KAHAN, false, 1, 4, true, false, 1>(af);
+        } else {
+            fwd_tile<D4, KAHAN, false, 3, 4, true, false, 1>(af);
+        }
+        // the tile's history (this CTA's generic stores) -> the backward's bulk copies (async
+        // proxy, issued by thread 0): every store visible, then the proxy fence
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+        ab.adam.step_size = fl.adam_table[2 * it];
+        ab.adam.sqrt_bc2 = fl.adam_table[2 * it + 1];
+        if (KIND == 0) {
+            bwd_tile<D4, false, true, 4, 1, false, false, 1>(ab);
+        } else {
+            ab.loss_partials = last ? bwd_partials : nullptr;
+            bwd_tile<D4, false, true, 4, 2, KAHAN, false, 1>(ab);
+        }
+        // the Adam epilogue's parameters are the next forward's inputs; the backward's last
+        // staging reads are done before the next forward overwrites the history
+        __syncthreads();
+    }
+}
+
+template <bool D4, bool KH, int KIND>
+static cudaError_t launch_fit_long_v(const FwdArgs& af, const BwdArgs& ab, const FitLongArgs& fl,
+                                     int ntiles, cudaStream_t st) {
+    constexpr size_t smem = bwd_smem_of<4, KIND == 0 ? 1 : 2>();
+    static std::atomic<unsigned long long> optin{0};
+    cudaError_t e = smem_optin((const void*)fit_long_kernel<D4, KH, KIND>, (int)smem, optin);
+    if (e != cudaSuccess) return e;
+    fit_long_kernel<D4, KH, KIND><<<ntiles, kT, smem, st>>>(af, ab, fl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fit_long(const FwdArgs& af, const BwdArgs& ab, const FitLongArgs& fl,
+                            int ntiles, bool delta4, bool kahan, int kind, cudaStream_t st) {
+    if (af.ckpt_every != 4 || ab.ckpt_every != 4) return cudaErrorInvalidValue;
+    if (delta4) {
+        if (kahan) return kind == 0 ? launch_fit_long_v<true, true, 0>(af, ab, fl, ntiles, st)
+                                    : launch_fit_long_v<true, true, 1>(af, ab, fl, ntiles, st);
+        return kind == 0 ? launch_fit_long_v<true, false, 0>(af, ab, fl, ntiles, st)
+                         : launch_fit_long_v<true, false, 1>(af, ab, fl, ntiles, st);
+    }
+    if (kahan) return kind == 0 ? launch_fit_long_v<false, true, 0>(af, ab, fl, ntiles, st)
+                                : launch_fit_long_v<false, true, 1>(af, ab, fl, ntiles, st);
+    return kind == 0 ? launch_fit_long_v<false, false, 0>(af, ab, fl, ntiles, st)
+                     : launch_fit_long_v<false, false, 1>(af, ab, fl, ntiles, st);
+}
+
 // ------------------------------------------------------------------------------ launchers
 cudaError_t launch_state_from_obs(const float* obs, int64_t n, int steps, float dt, float* pos0,
                                   float* vel0, cudaStream_t st) {
@@ -1307,13 +1401,6 @@ cudaError_t kernels_configure(int ckpt_every) {
     return ckpt_supported(ckpt_every) ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <int KS, int GOBS>
-constexpr size_t bwd_smem_of() {  // ring of NB: speed + checkpoint + dL/dP/obs (or sign) rows
-    return (size_t)IDM_BWD_RING *
-           (KS * (kCap + 4) + kCkRows * kCap +
-            (GOBS == 1 ? kCap / 2 : (GOBS ? KS + 1 : KS) * kCap)) *
-           sizeof(float);
-}
 
 #ifndef IDM_BWD_NP
 #define IDM_BWD_NP 1  // vehicle pairs per backward thread (1: 256 threads, 2: 128 threads; 2 measured 3.7% slower)

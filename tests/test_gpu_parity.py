@@ -972,8 +972,8 @@ def test_whole_fit_equals_fit_step_loop(idm, kind):
     Lc = c.fit_step(obs, kind=kind, iteration=19, total=500, sync=True)
     assert abs(Lb - Lc) <= 1e-6 * Lc
     kmax = idm.load_library().idm_fit_max_steps()
-    d = idm.from_workload(w, None, max_steps=kmax + 1)
-    with pytest.raises(idm.IdmError):  # horizon beyond the on-chip limit
+    d = idm.from_workload(w, None, max_steps=kmax + 1, ckpt_every=2)
+    with pytest.raises(idm.IdmError):  # beyond the on-chip horizon the long kernel needs k = 4
         d.fit(torch.zeros(kmax + 2, w.n, device="cuda"), iters=2, steps=kmax + 1)
 
 
@@ -1307,3 +1307,35 @@ def test_split_lanes_equal_whole_lanes(idm, monkeypatch, chunk):
                                          b.params, b.grad_params, b.grad_state0)])
     for x, y in zip(*runs):
         assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("kind,K", [("l1", 90), ("l2", 90), ("l1", 93), ("l2", 2503)])
+def test_whole_fit_long_horizon_equals_fit_step_loop(idm, kind, K):
+    """idm_fit beyond the on-chip horizon (NEXT-4: every iteration in one launch, each CTA its
+    tile's whole fit, the history through memory) == the idm_fit_step loop bit for bit in
+    parameters, Adam moments, gradients and dL/dp0, dL/dv0; ragged multi-tile lanes, missing
+    observations, a partial last segment, and a compensated (> 2,000-step) horizon."""
+    cap = idm.load_library().idm_max_lane_vehicles()
+    sizes = [100] * 12 + [1, 7, cap, 3] if K < 1000 else [60, 60, 5]
+    w = synth.make_workload("C2", lane_sizes=sizes, K=K, seed=70 + K)
+    obs = synth.kinematic_obs(w)
+    obs[np.random.default_rng(K).random(obs.shape) < 0.15] = np.nan
+    o = torch.as_tensor(obs, device="cuda")
+    iters = 4 if K < 1000 else 2
+    a = idm.from_workload(w, None, max_steps=w.K)
+    b = idm.from_workload(w, None, max_steps=w.K)
+    for it in range(iters):
+        La = a.fit_step(o, kind=kind, iteration=it, total=500, sync=True)
+    Lb = b.fit(o, iters=iters, kind=kind, iter0=0, total=500, sync=True)
+    torch.cuda.synchronize()
+    assert torch.equal(a.params, b.params)
+    assert torch.equal(a.adam_m, b.adam_m) and torch.equal(a.adam_v, b.adam_v)
+    assert torch.equal(a.grad_params, b.grad_params)
+    assert torch.equal(a.grad_state0, b.grad_state0)
+    assert abs(La - Lb) <= 1e-6 * abs(La)
+    # and a second call continues the schedule
+    Lc = b.fit(o, iters=2, kind=kind, iter0=iters, total=500, sync=True)
+    for it in range(iters, iters + 2):
+        La = a.fit_step(o, kind=kind, iteration=it, total=500, sync=True)
+    torch.cuda.synchronize()
+    assert torch.equal(a.params, b.params) and abs(La - Lc) <= 1e-6 * abs(La)
