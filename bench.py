@@ -505,12 +505,12 @@ def run_ours(args, rank, world, local_rank):
         on_chip = K <= idm.load_library().idm_fit_max_steps()
         n_it = 500 if on_chip else args.whole_iters
         reset(sim)
-        sim.fit(obs, iters=min(10, n_it), total=500)
+        sim.fit(obs, iters=min(10, n_it), kind=args.loss, total=500)
         torch.cuda.synchronize()
         reset(sim)
         e0, e1 = _events(torch)
         e0.record(sim.stream)
-        sim.fit(obs, iters=n_it, total=500)
+        sim.fit(obs, iters=n_it, kind=args.loss, total=500)
         e1.record(sim.stream)
         torch.cuda.synchronize()
         t_fit = parallel.max_over_ranks(e0.elapsed_time(e1), dev)
