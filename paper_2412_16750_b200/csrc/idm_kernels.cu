@@ -191,6 +191,13 @@ __device__ __forceinline__ void cp_async8_if(float* dst, const float* src, bool 
                  "l"(src), "r"((int)on)
                  : "memory");
 }
+// 16-byte cp.async bypassing L1 (streamed rows), issued only when `on` (16-byte aligned)
+__device__ __forceinline__ void cp_async16_if(float* dst, const float* src, bool on) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n"
+                 " @q cp.async.cg.shared.global [%0], [%1], 16;\n}" ::"r"(smem_u32(dst)),
+                 "l"(src), "r"((int)on)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() {
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -348,15 +355,22 @@ __device__ __forceinline__ void fwd_tile(FwdArgs a) {
     const float* onext = OBSV ? obs + N : nullptr;  // first row of the next fetch
     int fslot = 0, cslot = 0;
     // pairs are 8-byte aligned in every row when the tile starts at an even vehicle, N is even
-    // and the array is 8-byte aligned (CTA-uniform)
+    // and the array is 8-byte aligned (CTA-uniform); a thread's 4 vehicles (NP = 2) are one
+    // 16-byte block when the start and N are multiples of 4 and the array is 16-byte aligned
     const bool pair8 = OBSV && ((base | N) & 1) == 0 && ((uintptr_t)a.obs & 7) == 0;
+    const bool quad16 = OBSV && NP == 2 && ((base | N) & 3) == 0 && ((uintptr_t)a.obs & 15) == 0;
     auto fetch_obs = [&](int seg) {
         const int r0 = seg * KS + 1;
         float* dst = &obuf[fslot][0][VT * tid];
         fslot = fslot == OR - 1 ? 0 : fslot + 1;
         if (r0 + KS - 1 <= steps) {  // whole segment inside the rollout (CTA-uniform)
             const float* o = onext;
-            if (pair8) {  // both vehicles of a pair in one 8-byte copy (a lone last one: 4 bytes)
+            if (quad16 && val[VT - 1]) {  // the thread's 4 vehicles in one 16-byte copy (a
+                                          // partial last thread takes the pair copies below)
+#pragma unroll
+                for (int tt = 0; tt < KS; ++tt, o += N) cp_async16_if(dst + tt * kCap, o, true);
+            } else if (pair8) {  // both vehicles of a pair in one 8-byte copy (a lone last one: 4
+                                 // bytes)
 #pragma unroll
                 for (int tt = 0; tt < KS; ++tt, o += N) {
 #pragma unroll

@@ -362,8 +362,9 @@ class IdmSim:
     def fit(self, obs: torch.Tensor, iters: int, kind: str = "l1", iter0: int = 0,
             total: int = 500, lr0: float = 0.1, lr1: float = 0.01, steps: int | None = None,
             sync: bool = False):
-        """`iters` fused iterations in ONE launch (idm_fit; horizons <= idm_fit_max_steps()):
-        bit-identical to calling fit_step for iterations iter0 .. iter0+iters-1."""
+        """`iters` fused iterations in ONE launch (idm_fit: on chip for horizons <=
+        idm_fit_max_steps(), else each CTA runs its lane tile's whole fit with the history
+        through memory): bit-identical to calling fit_step for iterations iter0 .. iter0+iters-1."""
         self._no_sharded_shared("fit")
         steps = self.max_steps if steps is None else int(steps)
         assert obs.dtype == torch.float32 and obs.is_contiguous() and obs.device == self.device
