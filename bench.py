@@ -227,9 +227,14 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- workload
-def make_rank_workload(rank: int, world: int, scaling: str):
+def make_rank_workload(rank: int, world: int, scaling: str, shard=None):
     """strong: the 2M-vehicle C4 workload split in contiguous whole-lane shards;
-    weak: every rank its own C4-sized workload (seed per rank)."""
+    weak: every rank its own C4-sized workload (seed per rank).  shard = (r, n): one process
+    runs shard r of an n-way strong split (an estimate of the per-GPU work at n GPUs)."""
+    if shard is not None:
+        full = synth.make_workload(WORKLOAD)
+        l0, l1 = parallel.shard_lanes(full.n_lanes, shard[1], shard[0])
+        return synth.lane_subset(full, np.arange(l0, l1))
     if scaling == "weak" or world == 1:
         return synth.make_workload(WORKLOAD, seed=synth.CONFIGS[WORKLOAD]["seed"] + 1000 * rank)
     full = synth.make_workload(WORKLOAD)
@@ -399,7 +404,8 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     scaling = args.scaling or ("strong" if world > 1 else "weak")
-    w = make_rank_workload(rank, world, scaling)
+    shard = tuple(int(x) for x in args.shard.split("/")) if args.shard else None
+    w = make_rank_workload(rank, world, scaling, shard)
     vl = args.leader == "virtual"
     K, k = w.K, (4 if vl else (args.ckpt or idm.DEFAULT_CKPT))
     n_total = parallel.sum_over_ranks(w.n)
@@ -682,6 +688,7 @@ def run_ours(args, rank, world, local_rank):
                                                 "vehicle fitted alone with free per-step "
                                                 "(dp, dv) leaves" if vl else ""),
                    "vehicles_total": n_total, "vehicles_rank0": w.n, "K": K,
+                   "shard": args.shard,
                    "ckpt_every": k, "loss": args.loss,
                    "path": "idm_fit_step (fused fwd+Eq.4 / bwd+Adam)",
                    "parallelism": f"lane-sharded x{world} ({scaling})",
@@ -743,6 +750,9 @@ def main():
     ap.add_argument("--vl-also", type=int, default=1,
                     help="N = 1: also measure the virtual-leader fit step (secondary field)")
     ap.add_argument("--ckpt", type=int, default=None, help="checkpoint interval k")
+    ap.add_argument("--shard", default=None,
+                    help="r/n: run only shard r of an n-way strong split on this one GPU (the "
+                         "per-GPU work at n GPUs; an estimate, not a multi-GPU measurement)")
     ap.add_argument("--loss", choices=["l1", "l2"], default="l1",
                     help="Eq. 4 as the paper's L1 (headline) or the smooth L2 variant")
     ap.add_argument("--e2e", type=int, default=8, help="end-to-end steps (0 = skip)")
