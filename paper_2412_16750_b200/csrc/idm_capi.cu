@@ -119,11 +119,9 @@ int64_t max_tiles_for(const idm_desc* d) {
 // chunk (a multiple of 4, <= kCap): lanes longer than chunk are split into tiles of chunk
 // vehicles (kCap: only lanes that do not fit a tile; smaller: latency-bound shapes spread over
 // more SMs, see split_chunk_for).
-// target > 0 (no lane longer than chunk): about `target` tiles of equal vehicle counts (each
-// still <= kCap, whole lanes) instead of the greedy packing -- see balance_target_for.
 int64_t plan_tiles(const std::vector<int32_t>& off, int32_t n_lanes, int64_t n,
                    std::vector<int64_t>* tiles, std::vector<uint8_t>* lead, std::string* err,
-                   int* csize_out = nullptr, int64_t chunk = kCap, int64_t target = 0) {
+                   int* csize_out = nullptr, int64_t chunk = kCap) {
     char buf[256];
     if (off[0] != 0 || off.back() != n) {
         std::snprintf(buf, sizeof buf, "lane_offsets must start at 0 and end at N=%lld (got %d..%d)",
@@ -163,10 +161,7 @@ int64_t plan_tiles(const std::vector<int32_t>& off, int32_t n_lanes, int64_t n,
             for (int c = 1; c < cs; ++c) t.push_back(a + c * chunk < b ? a + c * chunk : b);
             cur = kCap;  // closed: the next lane opens a new tile
         } else {
-            // balanced: a new tile once this lane starts past the current tile's share
-            const bool past = cs == 1 && target > 0 && cur > 0 &&
-                              (double)a >= (double)t.size() * (double)n / (double)target;
-            if (cur + sz > kCap || past) {
+            if (cur + sz > kCap) {
                 t.push_back(a);
                 cur = 0;
             }
@@ -211,21 +206,6 @@ int64_t split_chunk_for(const std::vector<int32_t>& off, int32_t n_lanes, int64_
     return chunk;
 }
 
-// Balanced tile count.  The greedy plan's last wave of CTAs is partly empty; with few waves
-// (a strong-scaling shard: C4 / 8 = 500 tiles on 296 backward slots) that tail costs up to a
-// third of a wave.  IDM_TILE_BALANCE=1 rounds the tile count up to whole waves of the
-// backward's residency (2 CTAs per SM) and spreads the vehicles evenly.
-int64_t balance_target_for(const std::vector<int32_t>& off, int32_t n_lanes, int64_t n,
-                           int num_sms) {
-    const char* e = std::getenv("IDM_TILE_BALANCE");
-    if (!e || e[0] != '1') return 0;
-    std::string err;
-    const int64_t g = plan_tiles(off, n_lanes, n, nullptr, nullptr, &err);
-    const int64_t slots = 2 * (int64_t)num_sms;
-    if (g <= 0 || g % slots == 0 || g > 16 * slots) return 0;
-    return (g + slots - 1) / slots * slots;
-}
-
 // Tile count of the descriptor's lane plan (reads lane_offsets), or the bound if unreadable.
 int64_t tiles_of(const idm_desc* d) {
     if (!d || !d->lane_offsets || d->n_lanes < 1) return -1;
@@ -242,8 +222,7 @@ int64_t tiles_of(const idm_desc* d) {
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaGetLastError();
     return plan_tiles(off, d->n_lanes, d->n_vehicles, nullptr, nullptr, &err, nullptr,
-                      split_chunk_for(off, d->n_lanes, d->n_vehicles, d->max_steps, num_sms),
-                      balance_target_for(off, d->n_lanes, d->n_vehicles, num_sms));
+                      split_chunk_for(off, d->n_lanes, d->n_vehicles, d->max_steps, num_sms));
 }
 
 // ntiles: the plan's tile count (< 0: size for the bound max_tiles_for)
@@ -579,7 +558,7 @@ int idm_init(idm_handle** out, const idm_desc* d) {
             const int64_t chunk =
                 split_chunk_for(off, d->n_lanes, d->n_vehicles, d->max_steps, num_sms);
             nt = plan_tiles(off, d->n_lanes, d->n_vehicles, &tiles, &lead, &perr, &h->csize,
-                            chunk, balance_target_for(off, d->n_lanes, d->n_vehicles, num_sms));
+                            chunk);
             if (nt < 0) {
                 bail(fail(h, IDM_EINVAL, "%s", perr.c_str()));
                 break;
