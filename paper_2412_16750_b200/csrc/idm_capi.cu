@@ -1066,7 +1066,9 @@ int idm_fit_step(idm_handle* h, int32_t steps, const float* obs, const uint8_t* 
         const char* e = std::getenv("IDM_FUSED_OBS_BWD");
         return e ? (e[0] == '1' ? 1 : 0) : -1;
     }();
-    const bool obs_bwd = obs_env >= 0 ? obs_env == 1 : kind == 1;
+    // lanes over clusters: always the history-only forward (its observation-staging variants
+    // are not built with the cluster channel, idm_kernels.cu launch_fwd_k)
+    const bool obs_bwd = h->csize > 1 || (obs_env >= 0 ? obs_env == 1 : kind == 1);
     var.loss = obs_bwd ? 3 : 1 + kind;
     const int gobs = obs_bwd ? (kind == 0 ? 3 : 2) : 1 + kind;
     h->steps = steps;

@@ -241,6 +241,48 @@ __device__ __forceinline__ void step_sync() {
     if constexpr (CL) cluster_sync_all();
     else __syncthreads();
 }
+
+// One-way per-step message channel between neighbouring cluster CTAs (the boundary vehicle's
+// value of each step).  A cluster-wide barrier per step compiles to a GPU-scope MEMBAR (each
+// thread waits for its streaming history stores) plus an L1 invalidate; instead the producer
+// pushes the value with st.async into the consumer CTA's slot, completing on the consumer's
+// mbarrier (no fence), and a cluster barrier every kChanQ messages bounds how far the producer
+// may run ahead (flow control: a slot is rewritten only in the next window, after its reader
+// passed the barrier).  The buffer sits at the same shared offset in every CTA of the kernel.
+constexpr int kChanQ = 32;
+struct ChanBuf {
+    uint64_t bar[kChanQ];  // consumer-side: one completion (4 bytes + 1 arrival) per window
+    float val[kChanQ];
+};
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, unsigned rank) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(rank));
+    return ra;
+}
+// consumer thread: initialise and arm every slot for the first window (call before the
+// cluster barrier that precedes the first send)
+__device__ __forceinline__ void chan_init(ChanBuf& c) {
+    for (int q = 0; q < kChanQ; ++q) mbar_init(&c.bar[q], 1);
+    mbar_fence_init();
+    for (int q = 0; q < kChanQ; ++q) mbar_expect_tx(&c.bar[q], 4);
+}
+// producer thread: message seq into cluster CTA `rank`'s channel
+__device__ __forceinline__ void chan_send(ChanBuf& c, unsigned rank, int seq, float v) {
+    const int q = seq % kChanQ;
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+            mapa_u32(&c.val[q], rank)),
+        "r"(__float_as_uint(v)), "r"(mapa_u32(&c.bar[q], rank))
+        : "memory");
+}
+// consumer thread: wait for message seq, read it, re-arm its slot for the next window
+__device__ __forceinline__ float chan_recv(ChanBuf& c, int seq) {
+    const int q = seq % kChanQ;
+    mbar_wait(&c.bar[q], (uint32_t)(seq / kChanQ) & 1u);
+    const float v = c.val[q];
+    mbar_expect_tx(&c.bar[q], 4);
+    return v;
+}
 }  // namespace
 
 // ------------------------------------------------------------------------------ NK1
@@ -320,6 +362,15 @@ __device__ __forceinline__ void fwd_tile(FwdArgs a) {
     // vehicle is the last one of thread n_loc / VT - 1)
     const unsigned crank = CL ? cluster_rank() : 0u;
     const bool peer_lead = CL && n_loc > 0 && n_loc % VT == 0 && a.lead[base + n_loc - 1] != 0;
+    // ... and this tile's first vehicle is the previous CTA's last vehicle's leader
+    const bool peer_follow = CL && base > 0 && n_loc > 0 && a.lead[base - 1] != 0;
+    const int reader = peer_lead ? n_loc / VT - 1 : -1;  // the thread of the last vehicle
+    // CL: the leader speed of the last vehicle arrives by a message channel each step
+    __shared__ std::conditional_t<CL, ChanBuf, char> chanV;
+    if constexpr (CL) {
+        if (tid == reader) chan_init(chanV);
+        cluster_sync_all();  // every channel armed before the first message
+    }
 
     auto put = [&](float* row, const float2 (&x)[NP]) {  // row points at local vehicle VT tid
 #pragma unroll
@@ -504,11 +555,16 @@ __device__ __forceinline__ void fwd_tile(FwdArgs a) {
     put_ck();
     int par = 0;
     // one synchronous step of the whole tile; o = this step's observations (LOSS)
-    auto step = [&](int tt, auto PH) {  // PH: (index of the step computed) mod 4
+    auto step = [&](int t, int tt, auto PH) {  // t = t0 + tt; PH: (index of the step computed) mod 4
         xv[par][tid] = v[0].x;
-        step_sync<CL>();
+        if constexpr (CL) {  // the first vehicle's speed to the previous CTA's last vehicle
+            if (peer_follow && tid == 0) chan_send(chanV, crank - 1, t, v[0].x);
+        }
+        __syncthreads();
         float nb = xv[par][tid + 1];  // the next thread's first vehicle ([kTf]: sentinel 0)
-        if (CL && peer_lead && tid == n_loc / VT - 1) nb = ld_peer(&xv[par][0], crank + 1);
+        if constexpr (CL) {
+            if (tid == reader) nb = chan_recv(chanV, t);
+        }
         float2 vl[NP];
 #pragma unroll
         for (int p = 0; p < NP; ++p)
@@ -580,8 +636,10 @@ __device__ __forceinline__ void fwd_tile(FwdArgs a) {
         static_for<KS>([&](auto TT) {
             constexpr int tt = decltype(TT)::value;
             if (tt % CK == 0 && (tt > 0 || seg > 0)) checkpoint(t0 + tt);
-            step(tt, std::integral_constant<int, (tt + 1) % 4>{});
+            step(t0 + tt, tt, std::integral_constant<int, (tt + 1) % 4>{});
         });
+        // CL: the channel's flow-control window (kChanQ steps, a multiple of KS)
+        if (CL && (t0 + KS) % kChanQ == 0) cluster_sync_all();
         obs_done();
         if (OBSV) fold_loss();
         // refill after the segment's steps (its reads of the refilled slot are long done)
@@ -593,7 +651,7 @@ __device__ __forceinline__ void fwd_tile(FwdArgs a) {
             constexpr int tt = decltype(TT)::value;
             if (tt < tail) {  // CTA-uniform predicate
                 if (tt % CK == 0 && (tt > 0 || nfull > 0)) checkpoint(nfull * KS + tt);
-                step(tt, std::integral_constant<int, (tt + 1) % 4>{});
+                step(nfull * KS + tt, tt, std::integral_constant<int, (tt + 1) % 4>{});
             }
         });
     }
@@ -713,6 +771,9 @@ __device__ __forceinline__ void bwd_tile(BwdArgs a) {
     const bool peer_follow = CL && base > 0 && n_loc > 0 && a.lead[base - 1] != 0;
     // the previous CTA's last vehicle writes its term to its fx[par][n_prev / VT]
     const int pslot = peer_follow ? (int)(base - a.tile_start[tile - 1]) / VT : 0;
+    const int reader = peer_lead ? n_loc / VT - 1 : -1;  // the thread of the last vehicle
+    // CL: the follower -> leader adjoint term crosses to the next CTA by a message channel
+    __shared__ std::conditional_t<CL, ChanBuf, char> chanF;
     const int nseg = (steps + KS - 1) / KS;
     const int tail = steps - (nseg - 1) * KS;  // length of the last segment (1..KS)
 
@@ -756,7 +817,12 @@ __device__ __forceinline__ void bwd_tile(BwdArgs a) {
         if (GOBS && a.tile_ready) tile_acquire(a.tile_ready + tile, a.epoch, a.steps);
     }
     if (tid < NB * KS) vrow[tid * VP + kCap] = 0.f;
-    __syncthreads();
+    if constexpr (CL) {
+        if (peer_follow && tid == 0) chan_init(chanF);
+        cluster_sync_all();  // every channel armed before the first message
+    } else {
+        __syncthreads();
+    }
     uint32_t phase = 0;  // bit q: parity of buffer q's next completion
     auto fetch = [&](int seg, int len) {
         const int b = seg % NB;
@@ -767,7 +833,12 @@ __device__ __forceinline__ void bwd_tile(BwdArgs a) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             // SGN: code word seg, + word seg + 1 (step K) when the last segment is whole
             const int swords = (seg == nseg - 1 && len == KS) ? 2 : 1;
-            const uint32_t bytes = (uint32_t)(len + nckr) * kCap * sizeof(float) +
+            // CL: the last vehicle's leader is the next tile's first vehicle: the speed row
+            // holds this tile's n_loc vehicles, then 16 bytes of the next tile's row (slot n_loc,
+            // where the last vehicle reads its leader; 16-byte aligned: n_loc is a multiple of 4)
+            const uint32_t vrow_b = (uint32_t)(peer_lead ? n_loc : kCap) * sizeof(float);
+            const uint32_t bytes = (uint32_t)len * (vrow_b + (peer_lead ? 16u : 0u)) +
+                                   (uint32_t)nckr * kCap * sizeof(float) +
                                    (SGN ? (uint32_t)swords * kSW * sizeof(unsigned short) : 0u);
             mbar_expect_tx(&mbar[b], bytes);
             if (SGN)
@@ -776,8 +847,12 @@ __device__ __forceinline__ void bwd_tile(BwdArgs a) {
                              (int64_t)seg * kSW,
                          swords * kSW * sizeof(unsigned short), &mbar[b]);
             const float* src = a.vt + tile * a.vt_stride + t0 * kCap;
-            for (int tt = 0; tt < len; ++tt)
-                bulk_g2s(vrow + (b * KS + tt) * VP, src + tt * kCap, kCap * sizeof(float), &mbar[b]);
+            for (int tt = 0; tt < len; ++tt) {
+                bulk_g2s(vrow + (b * KS + tt) * VP, src + tt * kCap, vrow_b, &mbar[b]);
+                if (CL && peer_lead)
+                    bulk_g2s(vrow + (b * KS + tt) * VP + n_loc, src + a.vt_stride + tt * kCap, 16u,
+                             &mbar[b]);
+            }
             bulk_g2s(ckrow + b * kCkRows * kCap,
                      a.ckt + tile * a.ck_stride + (int64_t)seg * kCkRows * kCap,
                      nckr * kCap * sizeof(float), &mbar[b]);
@@ -857,11 +932,9 @@ __device__ __forceinline__ void bwd_tile(BwdArgs a) {
                 if (kFull || tt < len) {
                     v[tt][p] = *reinterpret_cast<const float2*>(vr + tt * VP + 2 * p);
                     // the leader of the pair's second vehicle: the next pair's first, or the
-                    // next thread's first vehicle (slot kCap: the 0 sentinel)
-                    float nb = vr[tt * VP + 2 * p + 2];  // slot kCap: the sentinel 0
-                    if (CL && p == NP - 1 && peer_lead && tid == n_loc / VT - 1)
-                        nb = ld_peer(vrow + (b * KS + tt) * VP, crank + 1);
-                    vl[tt][p] = make_float2(v[tt][p].y, nb);
+                    // next thread's first vehicle (slot kCap: the 0 sentinel; CL: slot n_loc
+                    // holds the next tile's first vehicle)
+                    vl[tt][p] = make_float2(v[tt][p].y, vr[tt * VP + 2 * p + 2]);
                 } else {
                     v[tt][p] = f2(0.f);
                     vl[tt][p] = f2(0.f);
@@ -959,15 +1032,24 @@ __device__ __forceinline__ void bwd_tile(BwdArgs a) {
                 }
                 // the thread's last vehicle -> its leader, thread t + 1's first vehicle
                 fx[par][tid + 1] = F[NP - 1].y;
+                // CL: message seq of the reverse sweep (steps done before this one)
+                const int seq = steps - 1 - (seg * KS + tt);
+                (void)seq;
+                if constexpr (CL) {  // the tile's last vehicle -> the next CTA's first
+                    if (tid == reader) chan_send(chanF, crank + 1, seq, F[NP - 1].y);
+                }
                 // in-thread follower terms and lambda_D^t = g^t + lambda_D^{t+1} need no barrier
 #pragma unroll
                 for (int p = 1; p < NP; ++p) u[p] = vadd(u[p], make_float2(F[p - 1].y, F[p].x));
 #pragma unroll
                 for (int p = 0; p < NP; ++p) e[p] = vfma(g[tt][p], k.dt2, e[p]);
-                step_sync<CL>();
+                __syncthreads();
                 // F of the first vehicle's follower: thread t - 1's last vehicle
                 float ff = fx[par][tid];
-                if (CL && peer_follow && tid == 0) ff = ld_peer(&fx[par][pslot], crank - 1);
+                if constexpr (CL) {
+                    if (peer_follow && tid == 0) ff = chan_recv(chanF, seq);
+                    if (seq % kChanQ == kChanQ - 1) cluster_sync_all();  // flow-control window
+                }
                 u[0] = vadd(u[0], make_float2(ff, F[0].x));
                 par ^= 1;
             }
@@ -1375,8 +1457,14 @@ static cudaError_t launch_fwd_k(const FwdArgs& a, int ntiles, const FwdVariant& 
     const int b_api = kCap / (2 * IDM_FWD_NP_API);  // idm_forward with history
     const int cs = CL ? var.csize : 1;
     if constexpr (KS == 4) {  // the fused idm_fit_step forward exists for 4-step segments
-        if (var.loss == 1) return launch_cfg(fwd_kernel<D4, KH, false, 1, KS, true, CL>, a, ntiles, b, 0, st, cs, false);
-        if (var.loss == 2) return launch_cfg(fwd_kernel<D4, KH, false, 2, KS, true, CL>, a, ntiles, b, 0, st, cs, false);
+        // (with clusters only the history-only variant: ptxas 12.9 crashes on the observation-
+        // staging ones combined with the cluster message channel; the host uses LOSS 3 there)
+        if constexpr (!CL) {
+            if (var.loss == 1) return launch_cfg(fwd_kernel<D4, KH, false, 1, KS, true, CL>, a, ntiles, b, 0, st, cs, false);
+            if (var.loss == 2) return launch_cfg(fwd_kernel<D4, KH, false, 2, KS, true, CL>, a, ntiles, b, 0, st, cs, false);
+        } else {
+            if (var.loss == 1 || var.loss == 2) return cudaErrorInvalidValue;
+        }
         if (var.loss == 3) return launch_cfg(fwd_kernel<D4, KH, false, 3, KS, true, CL>, a, ntiles, b, 0, st, cs, false);
     }
     if (!var.hist) {  // prediction rollout: P rows only (the segment length is immaterial)
