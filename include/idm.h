@@ -114,10 +114,12 @@ typedef struct {
                                     Nullable: then kept in the workspace */
 } idm_desc;
 
-/* Bytes of device workspace idm_init needs for this descriptor: the lane-mode state history
-   (every vehicle's speed at every step and (gap, displacement) every ckpt_every steps, in a
-   tile-local layout sized for the worst-case tile count, about 2 (max_steps + 1) N floats),
-   the lane-tile plan, leader flags, reduction partials, status word.
+/* Bytes of device workspace idm_init needs for this descriptor (reads lane_offsets to plan the
+   tiles): lane mode -- the state history (every vehicle's speed at every step and (gap,
+   displacement) every ckpt_every steps, in a tile-local layout sized for the plan's tile count,
+   about (max_steps + 1) N floats), the L1 sign codes; virtual-leader mode -- speed and
+   displacement checkpoints; both -- the lane-tile plan, leader flags, reduction partials,
+   per-lane shared-gradient rows (shared mode without desc.lane_grads), status word.
    Returns 0 if the descriptor is malformed. */
 size_t idm_workspace_bytes(const idm_desc* d);
 
