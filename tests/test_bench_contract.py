@@ -23,3 +23,14 @@ def test_reference_arm_json_line():
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+def test_multi_gpu_request_fails_loudly_without_gpus():
+    """`bench.py --gpus 2` outside torchrun launches its own ranks -- or, with fewer GPUs than
+    ranks, exits non-zero with the reason (never a silent single-rank run)."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--steps", "1", "--warmup", "0"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT,
+                         env={k: v for k, v in os.environ.items() if k != "WORLD_SIZE"})
+    assert out.returncode != 0
+    assert "needs 2 GPUs" in (out.stderr + out.stdout)
