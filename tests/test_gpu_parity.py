@@ -1254,8 +1254,27 @@ def test_long_lanes_fit_step_equals_separate_calls(idm, kind):
         assert_fit_grads(ga, b.grad_params)
         assert torch.equal(gsa, b.grad_state0)
         assert torch.equal(a.params, b.params)
-    with pytest.raises(idm.IdmError):  # the on-chip whole fit keeps lanes inside one tile
+    with pytest.raises(idm.IdmError):  # the whole fit keeps lanes inside one tile
         a.fit(o, iters=2, steps=10)
+    # the iteration loop as one CUDA graph (cluster launches captured) continues bit for bit
+    c = idm.from_workload(w, None, max_steps=w.K)
+    c.fit_steps(o, iters=3, kind=kind, iter0=0, total=500)
+    torch.cuda.synchronize()
+    assert torch.equal(c.params, b.params) and torch.equal(c.grad_state0, b.grad_state0)
+    # shared parameters over clusters: the fused iteration equals the separate calls
+    prm = np.array([8.0, 1.7, 3.0, 1.4, 33.0, 4.0], np.float32)
+    sa = idm.from_workload(w, prm, max_steps=w.K, shared_params=True)
+    sb = idm.from_workload(w, prm, max_steps=w.K, shared_params=True)
+    for it in range(2):
+        sa.forward(w.K)
+        sa.loss_grad(o, kind=kind)
+        sa.backward()
+        sa.adam_step(it)
+        sb.fit_step(o, kind=kind, iteration=it)
+        torch.cuda.synchronize()
+        assert torch.equal(sa.lane_grads, sb.lane_grads)
+        assert_fit_grads(sa.grad_params, sb.grad_params)
+        assert torch.equal(sa.params, sb.params)
 
 
 def test_long_lanes_shared_rows(idm, oracle):
