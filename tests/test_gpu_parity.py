@@ -531,15 +531,14 @@ def test_virtual_leader_forward_and_gradients(idm, oracle):
                             vl_dp=dp, vl_dv=dv)
     sim.forward(w.K)
     P_o, V_o = oracle.rollout_vl(w.p0, w.v0, prm.astype(np.float64), dp, dv)
-    obs = (P_o + np.random.default_rng(1).normal(0, 0.3, P_o.shape)).astype(np.float32)
+    # residuals of a few metres: L2's dL/dP = -2 (obs - P) then does not amplify the fp32 /
+    # fp64 trajectory difference (a 0.3 m residual would, up to 3e-3 relative)
+    obs = (P_o + np.random.default_rng(1).normal(0, 3.0, P_o.shape)).astype(np.float32)
     sim.loss_grad(torch.as_tensor(obs, device="cuda"), kind="l2")
     sim.backward()
     torch.cuda.synchronize()
     assert state_violation(sim.traj.cpu().numpy(), P_o) <= 1.0
-    # the backward is linear in dL/dP: give the oracle the GPU's upstream gradient so the
-    # check isolates the adjoint (an L2 residual of 0.3 m makes dL/dP sensitive to the 1e-4
-    # relative position tolerance)
-    gP = sim.grad_traj.cpu().numpy().astype(np.float64)
+    _, gP = oracle.loss(P_o, obs.astype(np.float64), "l2")  # the oracle's own dL/dP
     g = oracle.backward_vl(prm.astype(np.float64), dp, dv, P_o, V_o, gP)
     worst, _ = grad_check(sim.grad_params.cpu().numpy(), g["g_params"], g["g_abs"])
     assert worst <= 1.0
@@ -554,30 +553,29 @@ def test_virtual_leader_forward_and_gradients(idm, oracle):
 def test_virtual_leader_c4_full_size_sampled(idm, oracle):
     """Virtual-leader mode at the C4 geometry bench.py --leader virtual times (2M trajectories,
     K = 300, the paper's leaf initialisation Delta p = 10, Delta v = 0): trajectories fit alone,
-    so 2,000 sampled trajectories are exactly the oracle's problem.  Positions, parameter and
-    leaf gradients of those against the fp64 oracle (the GPU's dL/dP given, as above)."""
+    so 2,000 sampled trajectories are exactly the oracle's problem.  They are observed (the
+    oracle's truth rollout with theta_true and the leaves at their initial values, plus
+    N(0, 3^2)); every other vehicle is unobserved (NaN).  Positions, parameter, leaf and state
+    gradients of the sampled ones against the fp64 oracle with its own dL/dP."""
     w = synth.make_workload("C4")
-    lane = idm.from_workload(w, w.theta_true, max_steps=w.K)
-    lane.forward(w.K)
-    gen = torch.Generator(device="cuda").manual_seed(5)
-    obs = lane.traj.clone()
-    obs[1:].add_(torch.randn(obs[1:].shape, device="cuda", generator=gen), alpha=0.3)
-    lane.close()
-    del lane
+    vi = np.sort(np.random.default_rng(1).choice(w.n, 2000, replace=False))
+    dp = np.full((w.K, vi.size), idm.VL_INIT[0])
+    dv = np.full((w.K, vi.size), idm.VL_INIT[1])
+    P_t, _ = oracle.rollout_vl(w.p0[vi], w.v0[vi], w.theta_true[:, vi].astype(np.float64), dp, dv)
+    o_s = (P_t + np.random.default_rng(5).normal(0, 3.0, P_t.shape)).astype(np.float32)
+    obs = torch.full((w.K + 1, w.n), float("nan"), dtype=torch.float32, device="cuda")
+    idx = torch.as_tensor(vi, device="cuda")
+    obs.index_copy_(1, idx, torch.as_tensor(o_s, device="cuda"))
     prm = synth.init_params(w.n)
     sim = idm.from_workload(w, prm, max_steps=w.K, ckpt_every=4, virtual_leader=True)
     sim.forward(w.K)
     sim.loss_grad(obs, kind="l2")
     sim.backward()
     torch.cuda.synchronize()
-    vi = np.sort(np.random.default_rng(1).choice(w.n, 2000, replace=False))
-    idx = torch.as_tensor(vi, device="cuda")
-    dp = np.full((w.K, vi.size), idm.VL_INIT[0])
-    dv = np.full((w.K, vi.size), idm.VL_INIT[1])
     p = prm[:, vi].astype(np.float64)
     P_o, V_o = oracle.rollout_vl(w.p0[vi], w.v0[vi], p, dp, dv)
     assert state_violation(sim.traj.index_select(1, idx).cpu().numpy(), P_o) <= 1.0
-    gP = sim.grad_traj.index_select(1, idx).cpu().numpy().astype(np.float64)
+    _, gP = oracle.loss(P_o, o_s.astype(np.float64), "l2")  # the oracle's own dL/dP
     g = oracle.backward_vl(p, dp, dv, P_o, V_o, gP)
     worst, plain = grad_check(sim.grad_params.index_select(1, idx).cpu().numpy(), g["g_params"],
                               g["g_abs"])
@@ -734,7 +732,7 @@ def test_general_delta_and_delta_optimised(idm, oracle, fused):
     """delta != 4 (the general x^delta = 2^(delta log2 x) kernels) and delta optimised by
     Adam (opt_mask bit 5): gradients against the oracle, then one Adam step."""
     w = synth.make_workload("C2", lane_sizes=[40] * 8 + [3, 1], K=70, seed=17)
-    obs = oracle_truth_obs(oracle, w)
+    obs = oracle_truth_obs(oracle, w, sigma=3.0)  # L2 residuals of metres (see the VL test)
     prm = synth.init_params(w.n)
     prm[5] = np.random.default_rng(0).uniform(2.5, 6.0, w.n).astype(np.float32)
     sim = idm.from_workload(w, prm, max_steps=w.K, opt_mask=0x3F, record_velocity=True)
@@ -750,8 +748,8 @@ def test_general_delta_and_delta_optimised(idm, oracle, fused):
     P, V = oracle.rollout(h, w.length, w.p0, w.v0, prm.astype(np.float64), w.K)
     if not fused:
         assert state_violation(sim.traj.cpu().numpy(), P) <= 1.0
-    g = oracle.backward(h, w.length, prm.astype(np.float64), P, V,
-                        sim.grad_traj[:w.K + 1].cpu().numpy().astype(np.float64))
+    _, gP = oracle.loss(P, obs.astype(np.float64), "l2")  # the oracle's own dL/dP
+    g = oracle.backward(h, w.length, prm.astype(np.float64), P, V, gP)
     worst, _ = grad_check(sim.grad_params.cpu().numpy(), g["g_params"], g["g_abs"])
     assert worst <= 1.0
     if not fused:
@@ -782,8 +780,8 @@ def test_degenerate_starts(idm, oracle):
     assert state_violation(sim.traj.cpu().numpy(), P) <= 1.0
     assert state_violation(sim.vel_traj.cpu().numpy(), V) <= 1.0
     assert sim.vel_traj.cpu().numpy().min() >= 0.0
-    g = oracle.backward(h, length, prm.astype(np.float64), P, V,
-                        sim.grad_traj.cpu().numpy().astype(np.float64))
+    _, gP = oracle.loss(P, obs.astype(np.float64), "l2")  # the oracle's own dL/dP (= -1)
+    g = oracle.backward(h, length, prm.astype(np.float64), P, V, gP)
     worst, _ = grad_check(sim.grad_params.cpu().numpy(), g["g_params"], g["g_abs"])
     assert worst <= 1.0
 
