@@ -167,7 +167,7 @@ def test_gradients_c3_full_horizon(idm, oracle, kind):
     sim.loss_grad(torch.as_tensor(obs, device="cuda"), kind=kind)
     sim.backward()
     torch.cuda.synchronize()
-    prm = sim.params.cpu().numpy().astype(np.float64)
+    prm = synth.init_params(w.n).astype(np.float64)
     gt = sim.grad_traj.cpu().numpy().astype(np.float64)
     _, _, _, g = oracle_grads(oracle, w, prm, w.K, obs.astype(np.float64), kind, gt)
     worst, plain = grad_check(sim.grad_params.cpu().numpy(), g["g_params"], g["g_abs"])
@@ -308,6 +308,10 @@ def test_gradients_c4_subset(idm, oracle):
 
 # ---------------------------------------------------------------------- Adam / fit
 def test_adam_step_matches_oracle(idm, oracle):
+    """idm_adam_step (Adam, the linear lr schedule and the box clamp)
+    against the oracle's Adam on the same seeded gradients (written into grad_params after a
+    backward, so the call order holds; the generator is the only source of both inputs), five
+    iterations, parameters within 2e-6; delta frozen."""
     w = synth.make_workload("C2", lane_sizes=[100] * 20, K=60, seed=3)
     obs = oracle_truth_obs(oracle, w)
     prm = synth.init_params(w.n)
@@ -316,16 +320,16 @@ def test_adam_step_matches_oracle(idm, oracle):
     m1 = np.zeros_like(x)
     m2 = np.zeros_like(x)
     pm = oracle.param_mask(0x1F, w.n)
+    rng = np.random.default_rng(3)
     for it in range(5):
         sim.forward(w.K)
         sim.loss_grad(torch.as_tensor(obs, device="cuda"), kind="l1")
         sim.backward()
-        torch.cuda.synchronize()
-        g = sim.grad_params.cpu().numpy().astype(np.float64)
-        x_before = sim.params.cpu().numpy().astype(np.float64)
-        assert np.allclose(x_before, x, rtol=1e-5, atol=1e-6)
-        x = x_before.copy()
-        oracle.adam_step(x, g, m1, m2, it + 1, oracle.lr(it, 500, 0.1, 0.01), mask=pm)
+        g = (rng.standard_normal(x.shape) * rng.choice([1e-3, 1.0, 50.0], x.shape)).astype(
+            np.float32)
+        sim.grad_params.copy_(torch.as_tensor(g, device="cuda"))
+        oracle.adam_step(x, g.astype(np.float64), m1, m2, it + 1,
+                         oracle.lr(it, 500, 0.1, 0.01), mask=pm)
         oracle.project(x)
         sim.adam_step(it, 500, 0.1, 0.01)
         torch.cuda.synchronize()
@@ -1012,7 +1016,7 @@ def test_whole_fit_c5_full_size_sampled(idm, oracle, kind):
     w = synth.make_workload("C5")
     obs = synth.kinematic_obs(w, sigma=0.1)
     sim = idm.from_workload(w, None, max_steps=w.K)
-    prm = sim.params.cpu().numpy().astype(np.float64)
+    prm = synth.init_params(w.n).astype(np.float64)
     sim.fit(torch.as_tensor(obs, device="cuda"), iters=1, kind=kind, total=500)
     torch.cuda.synchronize()
     lanes = np.sort(np.random.default_rng(2).choice(w.n_lanes, 400, replace=False))
