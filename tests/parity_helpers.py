@@ -74,3 +74,11 @@ def sign_mismatch_residual(obs, P_ora, gpu_grad_traj):
         return 0.0
     tol = np.maximum(STATE_REL * np.abs(P_ora), STATE_ABS)
     return float((np.abs(r) / tol)[mism].max())
+
+
+def near_kink_vehicles(V, dt=0.1, a_min=-10.0, tol=1e-4):
+    """Vehicles whose (oracle) speed comes within `tol` m/s of the a_lb tie v = dt |a_min|
+    at some step (R#5: a_lb = max(-v/dt, a_min) switches branch there, so its derivative jumps;
+    SURVEY.md 8(c) parity protocol: such vehicles are reported separately, not failed)."""
+    V = np.asarray(V, np.float64)
+    return np.where((np.abs(V[:-1] - dt * abs(a_min)) < tol).any(axis=0))[0]

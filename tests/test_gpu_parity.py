@@ -556,11 +556,19 @@ def test_virtual_leader_forward_and_gradients(idm, oracle):
 
 def test_virtual_leader_c4_full_size_sampled(idm, oracle):
     """Virtual-leader mode at the C4 geometry bench.py --leader virtual times (2M trajectories,
-    K = 300, the paper's leaf initialisation Delta p = 10, Delta v = 0): trajectories fit alone,
-    so 2,000 sampled trajectories are exactly the oracle's problem.  They are observed (the
-    oracle's truth rollout with theta_true and the leaves at their initial values, plus
-    N(0, 3^2)); every other vehicle is unobserved (NaN).  Positions, parameter, leaf and state
-    gradients of the sampled ones against the fp64 oracle with its own dL/dP."""
+    K = 300, the paper's leaf initialisation Delta p = 10, Delta v = 0, the paper's L1 loss):
+    trajectories fit alone, so 2,000 sampled trajectories are exactly the oracle's problem.
+    They are observed (the oracle's truth rollout with theta_true and the leaves at their
+    initial values, plus N(0, 3^2)); every other vehicle is unobserved (NaN).  Positions, then
+    parameter, leaf and state gradients of the sampled ones against the fp64 oracle under the
+    L1 sign protocol.
+
+    Not L2 at this size: its dL/dP = 2 (P - obs) carries the fp32 position rounding (here up
+    to 4e-4 m after 300 steps at 3.6 km) straight into a gradient that is a small difference
+    of large terms -- dL/da_max = -1.0 out of sum_k |dL/dP_k| |dP_k/da_max| ~ 230 -- so the
+    oracle's own dL/dP moves it by 0.4 %; fed the dL/dP of the GPU's trajectory the oracle
+    agrees to 2e-4 (measured, profiles/r02_pytest.log).  L2 with the oracle's own dL/dP is
+    checked where that ratio is small (test_virtual_leader_forward_and_gradients)."""
     w = synth.make_workload("C4")
     vi = np.sort(np.random.default_rng(1).choice(w.n, 2000, replace=False))
     dp = np.full((w.K, vi.size), idm.VL_INIT[0])
@@ -573,13 +581,17 @@ def test_virtual_leader_c4_full_size_sampled(idm, oracle):
     prm = synth.init_params(w.n)
     sim = idm.from_workload(w, prm, max_steps=w.K, ckpt_every=4, virtual_leader=True)
     sim.forward(w.K)
-    sim.loss_grad(obs, kind="l2")
+    sim.loss_grad(obs, kind="l1")
     sim.backward()
     torch.cuda.synchronize()
     p = prm[:, vi].astype(np.float64)
     P_o, V_o = oracle.rollout_vl(w.p0[vi], w.v0[vi], p, dp, dv)
     assert state_violation(sim.traj.index_select(1, idx).cpu().numpy(), P_o) <= 1.0
-    _, gP = oracle.loss(P_o, o_s.astype(np.float64), "l2")  # the oracle's own dL/dP
+    gt = sim.grad_traj.index_select(1, idx).cpu().numpy()
+    res = sign_mismatch_residual(o_s, P_o, gt)
+    print(f"VL C4 L1 sign protocol: max residual / position tolerance at mismatches = {res:.3g}")
+    assert res <= 1.0
+    _, gP = oracle.loss(P_o, o_s.astype(np.float64), "l1", sign_override=(-gt).astype(np.int8))
     g = oracle.backward_vl(p, dp, dv, P_o, V_o, gP)
     worst, plain = grad_check(sim.grad_params.index_select(1, idx).cpu().numpy(), g["g_params"],
                               g["g_abs"])
@@ -1274,7 +1286,10 @@ def test_long_lanes_fit_step_equals_separate_calls(idm, kind):
         sa.adam_step(it)
         sb.fit_step(o, kind=kind, iteration=it)
         torch.cuda.synchronize()
-        assert torch.equal(sa.lane_grads, sb.lane_grads)
+        # per-lane rows equal, except dL/d delta, which the fused iteration does not compute
+        # for a frozen delta (column 5 = 0, include/idm.h)
+        assert torch.equal(sa.lane_grads[:, :5], sb.lane_grads[:, :5])
+        assert torch.count_nonzero(sb.lane_grads[:, 5]) == 0
         assert_fit_grads(sa.grad_params, sb.grad_params)
         assert torch.equal(sa.params, sb.params)
 
