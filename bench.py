@@ -111,6 +111,9 @@ def alu_roofline(kind: str, units: float, seconds: float, clk_mhz: float) -> dic
 SURVEY_BYTES = {"fwd": 4.5, "api": 21.0, "fused": 9.0, "single_launch": 4.2}
 
 
+GAP_CK = 8  # the gap row of every 8th checkpoint is stored (csrc/idm_internal.h kGapCk)
+
+
 def alg_bytes(K: int, k: int, path: str) -> dict:
     """HBM bytes per vehicle-step each kernel of this implementation moves by design
     (DESIGN.md section 4): the method's bytes plus the speed history the design stores."""
@@ -128,27 +131,30 @@ def alg_bytes(K: int, k: int, path: str) -> dict:
             "bwd": 8.0 + 4.0 + 8.0 + 4.0 / k + (24 + 24 + 8) / K,
             "adam": 2 * 28.0 + 6 * 28.0 / K,
         }
-    # lane mode: the forward stores the speed history (4 B) and the gap checkpoint (4 B / k;
-    # + displacement on the fused path); the backward reads them back instead of recomputing
+    # lane mode: the forward stores the speed history (4 B), the gap of every GAP_CK-th
+    # checkpoint (4 B / (GAP_CK k)) and the final gap (4 B / K), + displacement checkpoints
+    # (4 B / k) on the fused L2 path; the backward reads them back instead of recomputing
+    gk = GAP_CK * k
     if path == "api":
         return {
-            "fwd": 8.0 + 4.0 / k + (4 * 4 + 24 + 1) / K,        # P + speed rows, gap ckpt, loads
+            "fwd": 8.0 + 4.0 / gk + (4 * 4 + 24 + 1 + 4) / K,   # P + speed rows, gap ckpt, loads
             "loss": 12.0,                                       # read P, obs; write dL/dP
-            "bwd": 8.0 + 4.0 / k + (24 + 24 + 8 + 1) / K,       # speed + dL/dP rows, ckpt, params
+            "bwd": 8.0 + 4.0 / gk + (24 + 24 + 8 + 1 + 4) / K,  # speed + dL/dP rows, ckpt, params
             "adam": 6 * 28.0 / K,                               # x, g, m, v in; x, m, v out
         }
     if path == "fwd_only":  # prediction rollout (IDM_FWD_NO_HISTORY): P rows only
         return {"fwd": 4.0 + (4 * 4 + 24 + 1) / K}
     if path == "fused_l2":  # the forward sums Eq. 4; the backward re-derives dL/dP from obs
         return {
-            "fwd": 4.0 + 4.0 + 8.0 / k + (4 * 4 + 24 + 1) / K,  # obs in; speeds, gap + D out
-            "bwd": 4.0 + 4.0 + 8.0 / k + (24 + 1 + 4 + 24 + 8 + 6 * 20) / K,  # + obs, p0
+            "fwd": 4.0 + 4.0 + 4.0 / k + 4.0 / gk + (4 * 4 + 24 + 1 + 4) / K,  # obs in; speeds,
+            # gap + D out
+            "bwd": 4.0 + 4.0 + 4.0 / k + 4.0 / gk + (24 + 1 + 4 + 4 + 24 + 8 + 6 * 20) / K,
         }
     # fused L1 (the headline): the forward sums Eq. 4 and records -sign(obs - P) as 2 bits
     return {
-        "fwd": 4.0 + 4.0 + 4.0 / k + 0.25 + (4 * 4 + 24 + 1) / K,  # obs in; speeds, gap, bits out
-        # speed rows, sign bits, gap checkpoint; params, Adam (x, m, v in and out), grads out
-        "bwd": 4.0 + 0.25 + 4.0 / k + (24 + 1 + 24 + 8 + 6 * 20) / K,
+        "fwd": 4.0 + 4.0 + 4.0 / gk + 0.25 + (4 * 4 + 24 + 1 + 4) / K,  # obs in; speeds, gaps,
+        # bits out; speed rows, sign bits, gaps; params, Adam (x, m, v in and out), grads out
+        "bwd": 4.0 + 0.25 + 4.0 / gk + (24 + 1 + 4 + 24 + 8 + 6 * 20) / K,
     }
 
 

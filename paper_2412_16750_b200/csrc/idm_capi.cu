@@ -239,7 +239,7 @@ bool layout_for(const idm_desc* d, int64_t ntiles, Layout* L) {
     L->lead = off; off += align256((size_t)n);
     // lane mode only: tile-local state history (idm_internal.h), sized for the plan's tiles
     L->vt_stride = lane ? (int64_t)(d->max_steps + 1) * kCap : 0;
-    L->ck_stride = lane ? nck * kCkRows * kCap : 0;
+    L->ck_stride = lane ? (nck + 1) * kCkRows * kCap : 0;  // + the final gap's row (kGapCk)
     L->sg_stride = lane ? sgn_words_per_tile(d->max_steps) : 0;
     L->vt = off; if (lane) off += align256(sizeof(float) * ((size_t)(mt * L->vt_stride) + 64));
     L->ckt = off; off += align256(sizeof(float) * (size_t)(mt * L->ck_stride));

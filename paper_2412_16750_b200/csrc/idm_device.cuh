@@ -128,10 +128,10 @@ template <class T> using Mask = typename MaskOf<T>::type;
 // ------------------------------------------------------------------ per-vehicle constants
 // Forward constants of one vehicle (hoisted out of the time loop), base-2 scaled:
 //   s_opt log2e = sm2 + v (T2 + dv c2)          (Eq. 1)
-//   a_raw log2e = am2 (1 - w) - amln2 qr^2      (Eq. 2, qr = s*_opt log2e / dp)
+//   a_raw log2e = am2 (1 - w - ln2^2 qr^2)     (Eq. 2, qr = s*_opt log2e / dp)
 template <class T>
 struct VehPT {
-    T sm2, T2, c2, ivt, am2, amln2, delta;
+    T sm2, T2, c2, ivt, am2, delta;
 };
 using VehP = VehPT<float>;
 
@@ -145,7 +145,6 @@ __device__ __forceinline__ VehP make_vehp(float a_max, float a_pref, float s_min
     p.c2 = c * kLog2e;
     p.ivt = rcp(v_targ);
     p.am2 = a_max * kLog2e;
-    p.amln2 = a_max * kLn2;
     p.delta = delta;
     return p;
 }
@@ -153,15 +152,14 @@ __device__ __forceinline__ VehP make_vehp(float a_max, float a_pref, float s_min
 __device__ __forceinline__ VehPT<float2> pack(const VehP& a, const VehP& b) {
     return VehPT<float2>{make_float2(a.sm2, b.sm2),     make_float2(a.T2, b.T2),
                          make_float2(a.c2, b.c2),       make_float2(a.ivt, b.ivt),
-                         make_float2(a.am2, b.am2),     make_float2(a.amln2, b.amln2),
-                         make_float2(a.delta, b.delta)};
+                         make_float2(a.am2, b.am2),     make_float2(a.delta, b.delta)};
 }
 
 // Everything one step computes from (s, v, v_leader) before the state update; shared by the
 // forward update and the adjoint so both see the same values.
 template <class T>
 struct CoreT {
-    T x, x2, w, dv, c12, s_opt2, es, ones, ss2, idp, qr, inter2, t1, vda, z2, ea, onea, lx,
+    T x, x2, w, dv, c12, s_opt2, es, ones, ss2, idp, qr, inter2, t1, r1, vda, z2, ea, onea, lx,
         vlb2;
 };
 using Core = CoreT<float>;
@@ -197,7 +195,8 @@ __device__ __forceinline__ void core_dv(T s, T v, T dv, const VehPT<T>& p, const
     c.qr = vmul(c.ss2, c.idp);                                 // (s*/Delta p) log2 e
     c.inter2 = vmul(c.qr, c.qr);
     c.t1 = vsub(1.f, c.w);
-    const T a_raw2 = vfma(vneg(p.amln2), c.inter2, vmul(p.am2, c.t1));
+    c.r1 = vfma(c.inter2, -kLn2Sq, c.t1);                      // 1 - w - r^2 (r = s*/Delta p)
+    const T a_raw2 = vmul(p.am2, c.r1);                        // a_max (1 - w - r^2) log2 e
     c.vda = vadd(v, k.dt_amin);                                // v + dt a_min
     c.vlb2 = vmul(v, k.ninv_dt2);                              // (-v / dt) log2 e
     const T a_lb2 = vmax(c.vlb2, k.a_min2);                    // a_lb = max(-v/dt, a_min)
@@ -340,7 +339,6 @@ __device__ __forceinline__ RecT<T> jac_record(const CoreT<T>& c, T s, T v, const
     const T sig_s = vadd(hs, 0.5f);                                  // d s*/d s_opt
     const T ha = vcopysign(vfma(c.ones, rp, splat<T>(-0.5f)), c.z2);
     const T sig_a = vadd(ha, 0.5f);                                  // d a*/d a_raw
-    const T omsa = vsub(0.5f, ha);                                   // d a*/d a_lb
     const T As = vmul(vmul(b.Kb, c.qr), c.idp);                     // (d a_raw/d s*) ln2 dt
     const T sAs = vmul(sig_a, As);
     RecT<T> R;
@@ -352,16 +350,16 @@ __device__ __forceinline__ RecT<T> jac_record(const CoreT<T>& c, T s, T v, const
     if (D4) xm1 = vmul(c.x2, c.x);
     else xm1 = vsel(vgt(c.x, 0.f), vmul(c.w, rcp(c.x)), splat<T>(0.f));
     // 1 + dt d a*/d v at fixed leader speed: free term + s_opt term (T + (dv + v) c; c2 = c
-    // log2 e meets beta's ln 2) + a_lb branch (R#5: dt (1 - sigma_a)(-1/dt)); the 1 of the
-    // adjoint's lambda_v^{t+1} term rides in the FMA of the free term (one op fewer per step)
-    const T Jv = vfma(R.beta, vfma(v, p.c2, c.c12),
-                      vfma(vmul(sig_a, b.ndvt), xm1, splat<T>(1.f)));
+    // log2 e meets beta's ln 2) + a_lb branch (R#5: dt (1 - sigma_a)(-1/dt)).  The 1 of the
+    // adjoint's lambda_v^{t+1} term rides in the FMA of the free term, and on the a_lb = -v/dt
+    // branch 1 - (1 - sigma_a) = sigma_a replaces it (a select instead of two adds)
     const Mask<T> lb_act = vgt(c.vlb2, k.a_min2);                    // a_lb = -v/dt branch
-    R.Jv = vsel(lb_act, vsub(Jv, omsa), Jv);
+    R.Jv = vfma(R.beta, vfma(v, p.c2, c.c12),
+                vfma(vmul(sig_a, b.ndvt), xm1, vsel(lb_act, sig_a, splat<T>(1.f))));
     // d a*/d Delta p = sig_a (d a_raw/d s*)(-qr ln2) (log2 units): -dt^2 times it is sAs qr
     R.Js = vsel(vge(s, k.eps), vmul(sAs, c.qr), splat<T>(0.f));
     // log2 x (x = 0: w = 0 makes w log2 x = 0 with log2 of the smallest normal)
-    R.r1 = vfma(c.inter2, -kLn2Sq, c.t1);
+    R.r1 = c.r1;
     if (GD) {
         const T lx = D4 ? lg2(vmax(c.x, 1.17549435e-38f)) : c.lx;
         R.r2 = vmul(c.w, lx);
@@ -449,7 +447,7 @@ __device__ __forceinline__ void bwd_vl(const CoreT<T>& c, T dp, T v, const VehPT
     gdv = vmul(vneg(qbv), b.nc);                                // d s_opt/d dv = v c
     lv = vfma(lD, k.dt, vfma(q, Jv, lv));
     const T lx = D4 ? lg2(vmax(c.x, 1.17549435e-38f)) : c.lx;
-    g.S1 = vfma(qa, vfma(c.inter2, -kLn2Sq, c.t1), g.S1);
+    g.S1 = vfma(qa, c.r1, g.S1);
     g.S2 = vfma(qbv, c.dv, g.S2);
     g.S3 = vadd(g.S3, qb);
     g.S4 = vadd(g.S4, qbv);

@@ -121,12 +121,19 @@ __global__ void __launch_bounds__(kFT, 2) fit_kernel(FitArgs a) {
         // scaled adjoint as bwd_kernel: u = dt lambda_v, m = -dt lambda_s, e = dt^2 lambda_D
         float2 m = f2(0.f), u = f2(0.f), e = vmul(gg[K * kFT + tid], k.dt2);  // lambda_D^K = dL/dP(K)
         GradAccT<float2> G = {f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
+        // gaps as bwd_kernel sees them: the reverse recurrence from the final gap s_K, exact at
+        // the first step of each 4-step segment with a gap checkpoint row (gap_row)
+        constexpr int kSeg = 4;  // the fused backward's segment (ckpt_every)
+        float2 sn = s;           // s_K
 #pragma unroll
         for (int t = KM - 1; t >= 0; --t) {
             if (t < K) {
                 const float2 vv = hv[t * (kFT + 1) + tid];
                 const float2 vl = make_float2(vv.y, hv[t * (kFT + 1) + tid + 1].x);
-                const float2 sv = sg[t * kFT + tid];
+                const float2 sv = (t % kSeg == 0 && gap_row(t / kSeg))
+                                      ? sg[t * kFT + tid]
+                                      : vfma(vsub(vv, vl), k.dt, sn);
+                sn = sv;
                 CoreT<float2> c;
                 core<D4>(sv, vv, vl, P, k, c);
                 const RecT<float2> R = jac_record<D4, !D4>(c, sv, vv, P, B, k);

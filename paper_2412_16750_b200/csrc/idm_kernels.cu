@@ -498,9 +498,9 @@ __device__ __forceinline__ void fwd_tile(FwdArgs a) {
     if (tid == 0) { xv[0][kTf] = 0.f; xv[1][kTf] = 0.f; }
     // checkpoint rows the consumer reads: the gap (idm_backward); + displacement (fused
     // backward rebuilds positions); + compensation (and that with Kahan)
-    auto put_ck = [&] {
+    auto put_ck = [&](int j) {  // checkpoint j (step j CK)
         if (!HIST) return;
-        st_pairs<NP>(ckp, s);
+        if (gap_row(j)) st_pairs<NP>(ckp, s);
         if (DCK) st_pairs<NP>(ckp + kR2, D);
         if (DCK && KAHAN) st_pairs<NP>(ckp + 2 * kR2, cmp);
     };
@@ -552,7 +552,7 @@ __device__ __forceinline__ void fwd_tile(FwdArgs a) {
     }
     if (RECV) put(vrow, v);
     if (HIST) st_pairs<NP>(vtp, v);
-    put_ck();
+    put_ck(0);
     int par = 0;
     // one synchronous step of the whole tile; o = this step's observations (LOSS)
     auto step = [&](int t, int tt, auto PH) {  // t = t0 + tt; PH: (index of the step computed) mod 4
@@ -614,7 +614,7 @@ __device__ __forceinline__ void fwd_tile(FwdArgs a) {
     };
     auto checkpoint = [&](int t0) {  // (gap, D, compensation) at step t0 > 0 + finiteness check
         if (HIST) ckp += kCkRows * kR2;
-        put_ck();
+        put_ck(t0 / CK);
         finite2(t0);
     };
     auto obs_ready = [&](int seg) {
@@ -658,6 +658,11 @@ __device__ __forceinline__ void fwd_tile(FwdArgs a) {
     if (OBSV) cp_async_wait<0>();  // no copy outlives the CTA
     if (LOSS == 1 && steps % kSgnSteps != kSgnSteps - 1)
         put_code();  // the last, partial code word (holds step K)
+    if (HIST)  // the final gap s_K: the backward's reverse gap recurrence starts from it
+        st_pairs<NP>(reinterpret_cast<float2*>(a.ckt + tile * a.ck_stride +
+                                               (int64_t)((steps + CK - 1) / CK) * kCkRows * kCap) +
+                         NP * tid,
+                     s);
     finite2(steps);
 #pragma unroll
     for (int j = 0; j < VT; ++j)
@@ -837,8 +842,10 @@ __device__ __forceinline__ void bwd_tile(BwdArgs a) {
             // holds this tile's n_loc vehicles, then 16 bytes of the next tile's row (slot n_loc,
             // where the last vehicle reads its leader; 16-byte aligned: n_loc is a multiple of 4)
             const uint32_t vrow_b = (uint32_t)(peer_lead ? n_loc : kCap) * sizeof(float);
+            // checkpoint rows: the gap row only where the forward wrote it (gap_row)
+            const int ck0 = gap_row(seg) ? 0 : 1;
             const uint32_t bytes = (uint32_t)len * (vrow_b + (peer_lead ? 16u : 0u)) +
-                                   (uint32_t)nckr * kCap * sizeof(float) +
+                                   (uint32_t)(nckr - ck0) * kCap * sizeof(float) +
                                    (SGN ? (uint32_t)swords * kSW * sizeof(unsigned short) : 0u);
             mbar_expect_tx(&mbar[b], bytes);
             if (SGN)
@@ -853,9 +860,10 @@ __device__ __forceinline__ void bwd_tile(BwdArgs a) {
                     bulk_g2s(vrow + (b * KS + tt) * VP + n_loc, src + a.vt_stride + tt * kCap, 16u,
                              &mbar[b]);
             }
-            bulk_g2s(ckrow + b * kCkRows * kCap,
-                     a.ckt + tile * a.ck_stride + (int64_t)seg * kCkRows * kCap,
-                     nckr * kCap * sizeof(float), &mbar[b]);
+            if (nckr > ck0)
+                bulk_g2s(ckrow + (b * kCkRows + ck0) * kCap,
+                         a.ckt + tile * a.ck_stride + ((int64_t)seg * kCkRows + ck0) * kCap,
+                         (nckr - ck0) * kCap * sizeof(float), &mbar[b]);
         }
         if (!SGN) {
             const float* src = (OBS ? a.obs : a.grad_traj) + t0 * N + i0;
@@ -878,7 +886,7 @@ __device__ __forceinline__ void bwd_tile(BwdArgs a) {
     float ldj[VT], pj[VT];
     VehPT<float2> P[NP];
     VehAT<float2> B[NP];
-    float2 p0[NP], e[NP], m[NP], u[NP];
+    float2 p0[NP], e[NP], m[NP], u[NP], sc[NP];
     GradAccT<float2> G[NP];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
@@ -908,6 +916,11 @@ __device__ __forceinline__ void bwd_tile(BwdArgs a) {
         e[p] = vmul(make_float2(ldj[2 * p], ldj[2 * p + 1]), k.dt2);
         m[p] = f2(0.f);
         u[p] = f2(0.f);
+        // the final gap s_K (written by the forward one row past the last segment's; L2 load:
+        // after the handoff / the whole-fit barrier, an L1 line of an earlier iteration is stale)
+        sc[p] = __ldcg(reinterpret_cast<const float2*>(a.ckt + tile * a.ck_stride +
+                                                       (int64_t)nseg * kCkRows * kCap) +
+                       NP * tid + p);
         G[p] = GradAccT<float2>{f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
     }
     if (tid == 0) { fx[0][0] = 0.f; fx[1][0] = 0.f; }  // never written again (slots t+1 >= 1)
@@ -967,12 +980,13 @@ __device__ __forceinline__ void bwd_tile(BwdArgs a) {
                 }
             }
         }
-        // gaps (and positions) inside the segment: the forward's recurrences from the
-        // checkpoint, bitwise
+        // positions inside the segment (OBS): the forward's recurrence from the checkpoint,
+        // bitwise; gaps: the reverse recurrence from the later segment's first gap sc (s_K for
+        // the last), the segment's first gap replaced by the exact row where there is one
         const float* cr = ckrow + b * kCkRows * kCap + VT * tid;
+        const bool ck_gap = gap_row(seg);  // CTA-uniform
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-            float2 s = *reinterpret_cast<const float2*>(cr + 2 * p);
             float2 D = f2(0.f), cmp = f2(0.f), lsum = f2(0.f);
             if (OBS) D = *reinterpret_cast<const float2*>(cr + kCap + 2 * p);
             if (OBS && KAHAN) cmp = *reinterpret_cast<const float2*>(cr + 2 * kCap + 2 * p);
@@ -988,9 +1002,7 @@ __device__ __forceinline__ void bwd_tile(BwdArgs a) {
                     if (tt < len || (tt == len && seg == nseg - 1)) lsum = vadd(lsum, lt);
                 }
                 if (tt < KS) {
-                    sg[tt][p] = s;
                     if (kFull || tt < len) {
-                        s = vfma(vsub(v[tt][p], vl[tt][p]), -k.dt, s);
                         if (OBS) {
                             if (KAHAN) {
                                 const float2 y = vfma(v[tt][p], k.dt, vneg(cmp));
@@ -1008,6 +1020,14 @@ __device__ __forceinline__ void bwd_tile(BwdArgs a) {
                 lacc += (val[2 * p] ? (double)lsum.x : 0.0) +
                         (val[2 * p + 1] ? (double)lsum.y : 0.0);
             }
+            float2 sr = sc[p];  // s_t = s_{t+1} + dt (v_t - v_h,t), t = t0 + len - 1 .. t0
+#pragma unroll
+            for (int tt = KS - 1; tt >= 0; --tt) {
+                if (kFull || tt < len) sr = vfma(vsub(v[tt][p], vl[tt][p]), k.dt, sr);
+                sg[tt][p] = sr;
+            }
+            if (ck_gap) sg[0][p] = *reinterpret_cast<const float2*>(cr + 2 * p);
+            sc[p] = sg[0][p];  // this segment's first gap, for the segment before it
         }
         if (GOBS && seg == nseg - 1) {  // lambda_D^K = dL/dP(K) (static selects, no indexing)
 #pragma unroll
