@@ -15,6 +15,7 @@
 // vehicle 2t's leader is in the thread and 2t + 1's is thread t + 1's first vehicle (one
 // shared-memory word and one barrier per step).  Segments are KS steps (compile-time,
 // unrolled).  Lane-mode state history and its layout: idm_internal.h, DESIGN.md section 3.
+#include <cstdlib>
 #include <climits>
 #include <cstdint>
 #include <type_traits>
@@ -1439,9 +1440,27 @@ bool ckpt_supported(int k) { return k == 2 || k == 4 || k == 8; }
 
 // One launch: plain <<<>>> unless it needs attributes -- a thread-block cluster of csize CTAs
 // (lanes longer than a tile) and / or programmatic stream serialization (the fused backward).
+// IDM_SMEM_PAD=<bytes> (measurement only): extra dynamic shared memory
+// on every forward / backward launch, which caps the resident CTAs per SM -- the occupancy an
+// on-chip state history would leave (the on-chip-history experiment of NEXT-4).
+static size_t smem_pad() {
+    static const size_t pad = [] {
+        const char* e = std::getenv("IDM_SMEM_PAD");
+        return e ? (size_t)std::strtoull(e, nullptr, 10) : (size_t)0;
+    }();
+    return pad;
+}
+
 template <class A>
 static cudaError_t launch_cfg(void (*kern)(A), const A& a, int grid, int block, size_t smem,
                               cudaStream_t st, int csize, bool pdl) {
+    if (const size_t pad = smem_pad()) {
+        smem += pad;
+        const cudaError_t e = cudaFuncSetAttribute((const void*)kern,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)smem);
+        if (e != cudaSuccess) return e;
+    }
     if (csize <= 1 && !pdl) {
         kern<<<grid, block, smem, st>>>(a);
         return cudaSuccess;  // launch errors: cudaGetLastError in the caller

@@ -20,7 +20,7 @@ def main(path):
         rows.append((short, name, float(r["Metric Value"].replace(",", ""))))
     ours = {"fwd_kernel", "bwd_kernel", "loss_kernel", "reduce_kernel", "adam_kernel",
             "validate_kernel", "fit_kernel", "vl_fwd_kernel", "vl_bwd_kernel", "adam_free_kernel",
-            "state_from_obs_kernel"}
+            "state_from_obs_kernel", "fit_long_kernel"}
     tot = defaultdict(float)
     cnt = defaultdict(int)
     for short, name, ns in rows:
