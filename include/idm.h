@@ -163,8 +163,8 @@ int idm_init(idm_handle** out, const idm_desc* d);
 
 /* Simulate `steps` (1..max_steps) synchronous steps from (pos0, vel0) (Eqs. 1-3, Sec. III-B/C,
    PAPER.md:106-152): one fused launch, state in registers; traj rows 0..steps (and vel_traj,
-   state_out if given); the workspace gets every vehicle's speed at every step and its gap every
-   ckpt_every steps, which idm_backward reads back.
+   state_out if given); the workspace gets every vehicle's speed at every step, its gap every
+   8 ckpt_every steps and its final gap, which idm_backward reads back.
    Non-finite states are detected at checkpoints and reported by the next synchronizing call. */
 int idm_forward(idm_handle* h, int32_t steps);
 
@@ -192,7 +192,8 @@ int idm_loss_grad(idm_handle* h, const float* obs, const uint8_t* mask, int32_t 
    simulator that PAPER.md:134 makes "differentiable" and PAPER.md:227 obtains by autograd:
    the full coupled BPTT of Eqs. 1-3 with the Sec. III-C bounds (leader states included,
    R#23), given dL/dP from idm_loss_grad (Eq. 4).  Per lane tile it rebuilds
-   each checkpoint segment's gaps from the stored speeds on chip and sweeps it backwards.
+   each checkpoint segment's gaps from the stored speeds on chip (backwards from the final gap,
+   re-anchored on the stored gap every 8 segments) and sweeps it backwards.
    Writes
      grad_params  [6][n_par]  dL/d(a_max, a_pref, s_min, T_pref, v_targ, delta), row 5 = the
                   true dL/d delta on this call (the fused optimizer calls write 0 there when

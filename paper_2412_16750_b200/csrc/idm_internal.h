@@ -48,8 +48,9 @@ struct FwdVariant {
 
 // Lane-mode state history in HBM, TILE-LOCAL layout (internal workspace):
 //   vt  [tile][max_steps + 1][kCap]     speed of every vehicle slot at every step
-//   ckt [tile][nck][3][kCap]            (gap, displacement, Kahan compensation) at every
-//                                       ckpt_every-th step
+//   ckt [tile][nck + 1][3][kCap]        (gap, displacement, Kahan compensation) at every
+//                                       ckpt_every-th step (the gap only where gap_row(), the
+//                                       final gap s_K in row nck's gap slot; see kGapCk)
 // A tile's rows are kCap floats apart (compile-time), so a thread's vehicle pair is one
 // aligned 8-byte access at an immediate offset, and slots past the tile's vehicles are
 // private padding (stores need no predicate).
