@@ -170,8 +170,8 @@ using Core = CoreT<float>;
 // A vehicle without a leader (lane head, or an empty slot of a tile) carries the gap s = +inf:
 // 1/Delta p = rcp(inf) = 0 makes the interaction term and every derivative through it vanish
 // exactly, and s + dt (v_h - v) stays +inf.
-// Explicit _rn intrinsics: the forward kernel and the backward recompute produce bitwise
-// identical states.
+// Explicit _rn intrinsics: every kernel that evaluates a step on the same state (the lane,
+// on-chip-fit and virtual-leader forwards and backwards) gets the same bits.
 template <bool D4, class T>
 __device__ __forceinline__ void core_dv(T s, T v, T dv, const VehPT<T>& p, const Consts& k,
                                         CoreT<T>& c) {

@@ -726,8 +726,9 @@ __global__ void __launch_bounds__(kCap / (2 * NP), (fwd_min_blocks<CK, LOSS, NP>
 // bookkeeping are paid once per 4 vehicles and every warp carries two independent adjoint
 // chains).  The forward stored every vehicle's speed at every step and (gap, displacement,
 // compensation) at every KS-th step in the tile-local rows, so nothing here is a long serial
-// chain: inside a segment the gaps and displacements follow from the checkpoint by the
-// forward's own one-FMA recurrences (bit-identical), every step's local Jacobian (core +
+// chain: inside a segment the displacements follow from the checkpoint by the forward's own
+// one-FMA recurrence (bit-identical) and the gaps from the later segment's by the reverse one
+// (re-anchored on the stored gap every kGapCk segments), every step's local Jacobian (core +
 // jac_record) depends only on stored state, and the one sequential dependency left is the
 // adjoint itself -- lambda^{t+1} -> lambda^t plus the follower -> leader term F of the
 // thread's last vehicle, passed to thread t + 1 through shared memory (one barrier per step;
