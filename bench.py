@@ -46,7 +46,7 @@ WORKLOAD = "C4"  # the headline configuration (BASELINE.json configs[3]); --conf
 # multiply-adds issue as one f32x2 instruction (SURVEY 8(d) addendum).  "bwd_fit": the
 # optimizer-path backward with delta frozen at 4 (no dL/d delta, R#1).
 ALG_INSTR = {"fwd": 36.0, "bwd": 114.0}
-PACKED_INSTR = {"fwd": 20.5, "bwd": 40.0, "bwd_fit": 37.0}
+PACKED_INSTR = {"fwd": 20.5, "bwd": 41.0, "bwd_fit": 38.0}
 ISSUE_PER_CLK = 148 * 4 * 32  # SMs x schedulers x lanes (thread-instr / clk)
 N_SM = 148
 # Essential operations per vehicle-step by execution pipe (DESIGN.md section 4 "ALU roofline"):
@@ -57,7 +57,7 @@ N_SM = 148
 # path backward with delta frozen (no dL/d delta, R#1).
 ESSENTIAL = {
     "fwd": {"fp32": 22.0, "mufu": 5.0, "alu": 5.0},
-    "bwd_fit": {"fp32": 46.0, "mufu": 5.0, "alu": 9.0},
+    "bwd_fit": {"fp32": 48.0, "mufu": 5.0, "alu": 9.0},
 }
 # Pipe rates per SM per clock, nominal (sm_100: 4 SMSPs x 32 FP32 lanes; XU 16 lanes; ALU 64
 # lanes for FMNMX / FSEL; 4 issue slots x 32 lanes) -- profiles/rNN_pipe_bench.txt holds the

@@ -128,10 +128,10 @@ template <class T> using Mask = typename MaskOf<T>::type;
 // ------------------------------------------------------------------ per-vehicle constants
 // Forward constants of one vehicle (hoisted out of the time loop), base-2 scaled:
 //   s_opt log2e = sm2 + v (T2 + dv c2)          (Eq. 1)
-//   a_raw log2e = am2 (1 - w - ln2^2 qr^2)     (Eq. 2, qr = s*_opt log2e / dp)
+//   a_raw log2e = am2 (1 - w) - amln2 qr^2      (Eq. 2, qr = s*_opt log2e / dp)
 template <class T>
 struct VehPT {
-    T sm2, T2, c2, ivt, am2, delta;
+    T sm2, T2, c2, ivt, am2, amln2, delta;
 };
 using VehP = VehPT<float>;
 
@@ -145,6 +145,7 @@ __device__ __forceinline__ VehP make_vehp(float a_max, float a_pref, float s_min
     p.c2 = c * kLog2e;
     p.ivt = rcp(v_targ);
     p.am2 = a_max * kLog2e;
+    p.amln2 = a_max * kLn2;
     p.delta = delta;
     return p;
 }
@@ -152,7 +153,8 @@ __device__ __forceinline__ VehP make_vehp(float a_max, float a_pref, float s_min
 __device__ __forceinline__ VehPT<float2> pack(const VehP& a, const VehP& b) {
     return VehPT<float2>{make_float2(a.sm2, b.sm2),     make_float2(a.T2, b.T2),
                          make_float2(a.c2, b.c2),       make_float2(a.ivt, b.ivt),
-                         make_float2(a.am2, b.am2),     make_float2(a.delta, b.delta)};
+                         make_float2(a.am2, b.am2),     make_float2(a.amln2, b.amln2),
+                         make_float2(a.delta, b.delta)};
 }
 
 // Everything one step computes from (s, v, v_leader) before the state update; shared by the
@@ -190,16 +192,19 @@ __device__ __forceinline__ void core_dv(T s, T v, T dv, const VehPT<T>& p, const
     c.s_opt2 = vfma(v, c.c12, p.sm2);                          // s_opt log2 e
     c.es = ex2(vnabs(c.s_opt2));
     c.ones = vadd(c.es, 1.f);
-    c.ss2 = vadd(vmax(c.s_opt2, 0.f), lg2(c.ones));            // softplus(s_opt) log2 e
     c.idp = rcp(vmax(s, k.eps));                               // 1 / Delta p (0: no leader)
+    c.ss2 = vadd(vmax(c.s_opt2, 0.f), lg2(c.ones));            // softplus(s_opt) log2 e
     c.qr = vmul(c.ss2, c.idp);                                 // (s*/Delta p) log2 e
     c.inter2 = vmul(c.qr, c.qr);
     c.t1 = vsub(1.f, c.w);
-    c.r1 = vfma(c.inter2, -kLn2Sq, c.t1);                      // 1 - w - r^2 (r = s*/Delta p)
-    const T a_raw2 = vmul(p.am2, c.r1);                        // a_max (1 - w - r^2) log2 e
+    c.r1 = vfma(c.inter2, -kLn2Sq, c.t1);                      // 1 - w - r^2 (backward only)
     c.vda = vadd(v, k.dt_amin);                                // v + dt a_min
     c.vlb2 = vmul(v, k.ninv_dt2);                              // (-v / dt) log2 e
     const T a_lb2 = vmax(c.vlb2, k.a_min2);                    // a_lb = max(-v/dt, a_min)
+    // a_raw from (1 - w) and r^2 directly, not as a_max r1: r1 is off the forward's serial
+    // chain (it feeds only the backward's dL/da_max), so the step's latency is one op shorter
+    // (step 23)
+    const T a_raw2 = vfma(vneg(p.amln2), c.inter2, vmul(p.am2, c.t1));
     c.z2 = vsub(a_raw2, a_lb2);                                // (a - a_lb) log2 e
     c.ea = ex2(vnabs(c.z2));
     c.onea = vadd(c.ea, 1.f);
