@@ -755,7 +755,7 @@ constexpr int bwd_min_blocks() {
 // The backward of lane tile a.tile0 + blockIdx.x (the body of bwd_kernel, and the backward phase
 // of fit_long_kernel).
 template <bool D4, bool SHARED, bool ADAM, int KS, int GOBS, bool KAHAN, bool CL, int NP>
-__device__ __forceinline__ void bwd_tile(BwdArgs a) {
+__device__ __forceinline__ void bwd_tile(const BwdArgs& a) {
     constexpr int VT = 2 * NP;          // vehicles per thread
     constexpr int kTb = kCap / VT;      // threads per CTA
     __shared__ float fx[2][kTb + 1];
@@ -1196,8 +1196,17 @@ __device__ __forceinline__ void bwd_tile(BwdArgs a) {
 
 template <bool D4, bool SHARED, bool ADAM, int KS, int GOBS, bool KAHAN, bool CL, int NP>
 __global__ void __launch_bounds__(kCap / (2 * NP), (bwd_min_blocks<KS, NP>()))
-    bwd_kernel(BwdArgs a) {
-    bwd_tile<D4, SHARED, ADAM, KS, GOBS, KAHAN, CL, NP>(a);
+    bwd_kernel(const __grid_constant__ BwdArgs a) {
+    // How the argument block reaches the body changes the code around the staging: the
+    // single-CTA observation variants read it in place (L2 fused backward 2.00 -> 1.82 ms), the
+    // others from a copy (fused L1 backward 1.48 -> 1.42 ms, C4L 3.61 -> 3.57 ms; same-box A/B,
+    // DESIGN.md section 4)
+    if constexpr (GOBS >= 2 && !CL) {
+        bwd_tile<D4, SHARED, ADAM, KS, GOBS, KAHAN, CL, NP>(a);
+    } else {
+        const BwdArgs c = a;
+        bwd_tile<D4, SHARED, ADAM, KS, GOBS, KAHAN, CL, NP>(c);
+    }
 }
 
 // ------------------------------------------------------------------------------ NK2
