@@ -277,22 +277,44 @@ def _oracle_inputs(full, lanes, K):
     return w.n * K, st, obs
 
 
-def oracle_step(lanes: int, K: int, threads: int, seed: int = 99):
-    """The fp64 oracle as it stands (oracle.fit_iteration: rollout, Eq. 4 L1, adjoint, Adam) on
-    the first `lanes` lanes of the workload, one full step, over `threads` host threads: whole
-    lanes per task (the adjoint scatters into leaders, so lanes are the unit of parallelism;
-    the C oracle releases the GIL).  Inputs are prepared before the timed region.
-    Returns (vehicle-steps, seconds)."""
-    from oracle import oracle as O
-    full = synth.make_workload(WORKLOAD, seed=seed)
+_FULL_WORKLOADS = {}
+
+
+def _full_workload():
+    """The configuration's synthetic workload, drawn once per process (2M vehicles at C4)."""
+    key = (WORKLOAD, synth.CONFIGS[WORKLOAD]["seed"])
+    if key not in _FULL_WORKLOADS:
+        _FULL_WORKLOADS[key] = synth.make_workload(WORKLOAD, seed=key[1])
+    return _FULL_WORKLOADS[key]
+
+
+def oracle_prepare(lanes: int, K: int, threads: int, lane0: int = 0):
+    """Inputs of the oracle's fit on `lanes` consecutive lanes of the workload from lane `lane0`,
+    split into whole-lane tasks for `threads` host threads (the adjoint scatters into leaders,
+    so lanes are the unit of parallelism)."""
+    full = _full_workload()
     lanes = min(lanes, full.n_lanes)
-    chunks = [c for c in np.array_split(np.arange(lanes), max(1, 4 * threads)) if len(c)]
-    work = [_oracle_inputs(full, c, K) for c in chunks]
+    lane0 = lane0 % (full.n_lanes - lanes + 1)
+    idx = np.arange(lane0, lane0 + lanes)
+    chunks = [c for c in np.array_split(idx, max(1, 4 * threads)) if len(c)]
+    return [_oracle_inputs(full, c, K) for c in chunks]
+
+
+def oracle_run(work, threads: int, it: int = 0):
+    """One step of the fp64 oracle as it stands (oracle.fit_iteration: rollout, Eq. 4 L1,
+    adjoint, Adam iteration `it`) over prepared inputs on `threads` host threads (the C oracle
+    releases the GIL).  Returns (vehicle-steps, seconds)."""
+    from oracle import oracle as O
     t0 = time.perf_counter()
     with cf.ThreadPoolExecutor(max_workers=threads) as ex:
-        list(ex.map(lambda x: O.fit_iteration(x[1], x[2], 0), work))
+        list(ex.map(lambda x: O.fit_iteration(x[1], x[2], it), work))
     dt = time.perf_counter() - t0
     return sum(x[0] for x in work), dt
+
+
+def oracle_step(lanes: int, K: int, threads: int, lane0: int = 0):
+    """oracle_prepare + one oracle_run (inputs prepared before the timed region)."""
+    return oracle_run(oracle_prepare(lanes, K, threads, lane0), threads)
 
 
 def oracle_c1_fit_seconds() -> float:
@@ -348,16 +370,20 @@ def run_reference(args, rank, world):
     per_step = args.ref_budget / max(1, args.steps + args.warmup)
     lanes = int(max(1, min(synth.CONFIGS[WORKLOAD].get("lanes", 10 ** 9),
                            per_step * 0.8 * cores / per_lane_core)))
-    for _ in range(args.warmup):
-        oracle_step(lanes, K, cores)
+    # the sample's inputs once; each step is one more iteration of its fit (as the GPU arm
+    # iterates on resident inputs)
+    work = oracle_prepare(lanes, K, cores)
+    for it in range(args.warmup):
+        oracle_run(work, cores, it)
     tot_vs, tot_t = 0, 0.0
     for i in range(args.steps):
-        vs, t = oracle_step(lanes, K, cores, seed=100 + i)
+        vs, t = oracle_run(work, cores, args.warmup + i)
         tot_vs += vs
         tot_t += t
     value = tot_vs / tot_t
-    sample = (f"first {lanes} lanes x {K} steps of {WORKLOAD} per step (rollout + Eq.4 L1 + "
-              f"adjoint + Adam, fp64), whole lanes over {cores} host threads ({cpu_model()})")
+    sample = (f"first {lanes} lanes x {K} steps of {WORKLOAD}, one fit iteration per step "
+              f"(rollout + Eq.4 L1 + adjoint + Adam, fp64), whole lanes over {cores} host "
+              f"threads ({cpu_model()})")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "vehicle-steps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
